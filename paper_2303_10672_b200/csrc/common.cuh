@@ -1,0 +1,51 @@
+// Shared device helpers: error checking, ordered-double atomics, block
+// reductions.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "model.hpp"
+
+namespace pvi_b200 {
+
+#define PVI_CUDA(call)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      ::pvi_b200::fail(PVI_ERR_DEVICE, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                           " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+__host__ __device__ inline int ipos(int x) { return x > 0 ? x : 0; }
+
+// Order-preserving map from double to u64 so that atomicMax/atomicMin on
+// the key are max/min on the value (NaNs never reach here: the non-finite
+// scan reports them separately).
+__device__ __forceinline__ unsigned long long dkey(double x) {
+  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+__host__ __device__ inline double dkey_inv(unsigned long long k) {
+  const unsigned long long u = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double(static_cast<long long>(u));
+#else
+  double d;
+  __builtin_memcpy(&d, &u, 8);
+  return d;
+#endif
+}
+
+// Per-sweep statistics reduced on the device: max and min of the
+// convergence statistic, and the first non-finite state.
+struct SweepStats {
+  unsigned long long max_key;
+  unsigned long long min_key;
+  unsigned long long first_bad;  // UINT64_MAX when none
+  unsigned long long pad;
+};
+
+}  // namespace pvi_b200

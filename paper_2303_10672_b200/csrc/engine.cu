@@ -1,0 +1,657 @@
+// Host engine: device residency of the model tables, the value-iteration
+// driver (run_value_iteration, vi.hpp:162-291), single-sweep entry points
+// and the PVI1 checkpoint format (checkpoint.cpp).  The driver keeps V and
+// its history on the device; per sweep the host reads back one 32-byte
+// statistics record (max/min of the convergence statistic and the first
+// non-finite state), so the only host round trip is that flag.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "vi_kernels.cuh"
+
+namespace pvi_b200 {
+
+// ---------------------------------------------------------------------------
+// Device residency
+
+namespace {
+
+template <typename U>
+const U* upload(DeviceCopy& dc, const std::vector<U>& host) {
+  if (host.empty()) return nullptr;
+  void* p = nullptr;
+  PVI_CUDA(cudaMalloc(&p, host.size() * sizeof(U)));
+  PVI_CUDA(cudaMemcpy(p, host.data(), host.size() * sizeof(U), cudaMemcpyHostToDevice));
+  dc.allocations.push_back(p);
+  return static_cast<const U*>(p);
+}
+
+}  // namespace
+
+Model::~Model() {
+  int prev = -1;
+  cudaGetDevice(&prev);
+  for (auto& kv : dev) {
+    cudaSetDevice(kv.first);
+    for (void* p : kv.second->allocations) cudaFree(p);
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+const DevModel& Model::device_view(int device) const {
+  std::lock_guard<std::mutex> lock(dev_mutex);
+  auto it = dev.find(device);
+  if (it != dev.end()) return it->second->dm;
+  auto dc = std::make_unique<DeviceCopy>();
+  DevModel& d = dc->dm;
+  d.scenario = scenario;
+  d.n_digits = static_cast<int>(space.radix.size());
+  d.n_states = space.count;
+  d.n_actions = n_actions;
+  for (int i = 0; i < d.n_digits; ++i) {
+    d.weight[i] = space.weight[i];
+    d.radix[i] = space.radix[i];
+  }
+  switch (scenario) {
+    case PVI_SCENARIO_A:
+      d.a_m = pa.useful_life;
+      d.a_lead = pa.lead_time;
+      d.a_lifo = pa.issuing != 0;
+      d.a_max_order = pa.max_order;
+      d.a_dmax = pa.max_demand;
+      d.a_cv = pa.unit_cost;
+      d.a_ch = pa.holding_cost;
+      d.a_cs = pa.shortage_cost;
+      d.a_cw = pa.wastage_cost;
+      d.a_pmf = upload(*dc, a_pmf);
+      d.a_cdf = upload(*dc, a_cdf);
+      break;
+    case PVI_SCENARIO_B:
+      d.b_m = pb.useful_life;
+      d.b_na = b_na;
+      d.b_nb = b_nb;
+      d.b_cap_a = b_cap_a;
+      d.b_cap_b = b_cap_b;
+      d.b_dn = b_dmax + 1;
+      d.b_len_a = static_cast<int>(b_pmf_a.size());
+      d.b_len_b = static_cast<int>(b_pmf_b.size());
+      d.b_cva = pb.unit_cost_a;
+      d.b_cvb = pb.unit_cost_b;
+      d.b_cra = pb.revenue_a;
+      d.b_crb = pb.revenue_b;
+      d.b_rho = pb.substitution_prob;
+      d.b_mu_a = pb.demand_mean_a;
+      d.b_mu_b = pb.demand_mean_b;
+      d.b_pmf_a = upload(*dc, b_pmf_a);
+      d.b_pmf_b = upload(*dc, b_pmf_b);
+      d.b_sf_a = upload(*dc, b_sf_a);
+      d.b_sf_b = upload(*dc, b_sf_b);
+      d.b_pz = upload(*dc, b_pz);
+      d.b_pz_cum = upload(*dc, b_pz_cum);
+      d.b_cdf_a = upload(*dc, b_cdf_a);
+      d.b_cdf_b = upload(*dc, b_cdf_b);
+      d.b_lane_order = upload(*dc, b_lane_order);
+      d.b_tile = static_cast<int>(b_lane_order.size());
+      break;
+    case PVI_SCENARIO_C:
+      d.c_m = pc.useful_life;
+      d.c_max_order = pc.max_order;
+      d.c_dmax = pc.max_demand;
+      d.c_n_comp = c_n_comp;
+      d.c_cf = pc.fixed_order_cost;
+      d.c_ch = pc.holding_cost;
+      d.c_cs = pc.shortage_cost;
+      d.c_cw = pc.wastage_cost;
+      d.c_pmf = upload(*dc, c_pmf);
+      d.c_cdf = upload(*dc, c_cdf);
+      d.c_comp = upload(*dc, c_comp);
+      d.c_ids = upload(*dc, c_ids);
+      d.c_probs = upload(*dc, c_probs);
+      d.c_offsets = upload(*dc, c_offsets);
+      d.c_receipt = upload(*dc, c_receipt);
+      break;
+    default:
+      d.t_outcomes = n_outcomes;
+      d.t_next = upload(*dc, t_next);
+      d.t_reward = upload(*dc, t_reward);
+      d.t_prob = upload(*dc, t_prob);
+      break;
+  }
+  const DevModel& out = dc->dm;
+  dev.emplace(device, std::move(dc));
+  return out;
+}
+
+int select_device(int requested) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    fail(PVI_ERR_DEVICE, "no CUDA device available (pvi_b200 has no CPU fallback)");
+  }
+  int dev = requested;
+  if (dev < 0) PVI_CUDA(cudaGetDevice(&dev));
+  if (dev >= count) fail(PVI_ERR_DEVICE, "CUDA device ordinal out of range");
+  PVI_CUDA(cudaSetDevice(dev));
+  return dev;
+}
+
+// ---------------------------------------------------------------------------
+// Small RAII helpers
+
+struct DevBuf {
+  void* p = nullptr;
+  DevBuf() = default;
+  explicit DevBuf(std::size_t bytes) {
+    if (bytes) PVI_CUDA(cudaMalloc(&p, bytes));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <typename U>
+  U* as() const {
+    return static_cast<U*>(p);
+  }
+};
+
+struct Stream {
+  cudaStream_t s = nullptr;
+  Stream() { PVI_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~Stream() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+struct PinnedStats {
+  SweepStats* h = nullptr;
+  PinnedStats() { PVI_CUDA(cudaMallocHost(&h, sizeof(SweepStats))); }
+  ~PinnedStats() {
+    if (h) cudaFreeHost(h);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Checkpoints (checkpoint.hpp:24-35): "PVI1" | iteration u64 LE |
+// fingerprint[32] | count u64 LE | count x f64 LE; temp file + rename.
+
+void save_checkpoint(const std::string& path, const double* values, std::uint64_t count,
+                     std::uint64_t iteration, const std::uint8_t fp[32]) {
+  const std::string tmp = path + ".tmp";
+  {
+    std::ofstream out(tmp, std::ios::binary | std::ios::trunc);
+    if (!out) fail(PVI_ERR_IO, "cannot open checkpoint file for writing: " + tmp);
+    unsigned char header[52];
+    std::memcpy(header, "PVI1", 4);
+    for (int i = 0; i < 8; ++i) header[4 + i] = static_cast<unsigned char>(iteration >> (8 * i));
+    std::memcpy(header + 12, fp, 32);
+    for (int i = 0; i < 8; ++i) header[44 + i] = static_cast<unsigned char>(count >> (8 * i));
+    out.write(reinterpret_cast<const char*>(header), sizeof(header));
+    // x86-64 and the device are little-endian: the payload is the raw bits.
+    out.write(reinterpret_cast<const char*>(values), static_cast<std::streamsize>(count * 8));
+    if (!out) fail(PVI_ERR_IO, "failed writing checkpoint: " + tmp);
+  }
+  std::error_code ec;
+  std::filesystem::rename(tmp, path, ec);
+  if (ec) fail(PVI_ERR_IO, "failed to move checkpoint into place: " + ec.message());
+}
+
+void load_checkpoint(const std::string& path, const std::uint8_t* expected, double* values,
+                     std::uint64_t capacity, std::uint64_t* count, std::uint64_t* iteration,
+                     std::uint8_t fp[32]) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) fail(PVI_ERR_IO, "cannot open checkpoint file: " + path);
+  unsigned char header[52];
+  in.read(reinterpret_cast<char*>(header), sizeof(header));
+  if (!in || std::memcmp(header, "PVI1", 4) != 0)
+    fail(PVI_ERR_FORMAT, "not a checkpoint file (bad magic): " + path);
+  std::uint64_t it = 0, n = 0;
+  for (int i = 0; i < 8; ++i) it |= static_cast<std::uint64_t>(header[4 + i]) << (8 * i);
+  for (int i = 0; i < 8; ++i) n |= static_cast<std::uint64_t>(header[44 + i]) << (8 * i);
+  if (fp) std::memcpy(fp, header + 12, 32);
+  if (count) *count = n;
+  if (iteration) *iteration = it;
+  if (expected && std::memcmp(expected, header + 12, 32) != 0) {
+    fail(PVI_ERR_FINGERPRINT, "checkpoint fingerprint " + hex32(header + 12) +
+                                  " does not match model fingerprint " + hex32(expected));
+  }
+  if (!values) {
+    // Still validate the payload length.
+    in.seekg(0, std::ios::end);
+    const auto size = static_cast<std::uint64_t>(in.tellg());
+    if (size < 52 + 8 * n) fail(PVI_ERR_FORMAT, "checkpoint truncated: " + path);
+    return;
+  }
+  if (n > capacity) fail(PVI_ERR_FORMAT, "checkpoint larger than the destination buffer");
+  in.read(reinterpret_cast<char*>(values), static_cast<std::streamsize>(n * 8));
+  if (!in) fail(PVI_ERR_FORMAT, "checkpoint truncated: " + path);
+}
+
+std::string hex32(const std::uint8_t* fp) {
+  static const char* digits = "0123456789abcdef";
+  std::string s;
+  for (int i = 0; i < 32; ++i) {
+    s.push_back(digits[fp[i] >> 4]);
+    s.push_back(digits[fp[i] & 15]);
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// Initial values (vi.hpp:197-200): f64 on the device.
+
+void initial_values_device(const Model& m, const DevModel& dm, double* out, cudaStream_t stream) {
+  const std::uint64_t n = m.space.count;
+  switch (m.scenario) {
+    case PVI_SCENARIO_B:
+      launch_initial_b(dm, out, n, stream);
+      break;
+    case PVI_TABULAR:
+      PVI_CUDA(cudaMemcpyAsync(out, m.t_initial.data(), n * 8, cudaMemcpyHostToDevice, stream));
+      break;
+    default:
+      PVI_CUDA(cudaMemsetAsync(out, 0, n * 8, stream));
+  }
+}
+
+void initial_values_host(const Model& m, double* out) {
+  const int device = select_device(-1);
+  const DevModel& dm = m.device_view(device);
+  const std::uint64_t n = m.space.count;
+  Stream stream;
+  DevBuf d(n * sizeof(double));
+  initial_values_device(m, dm, d.as<double>(), stream.s);
+  PVI_CUDA(cudaMemcpyAsync(out, d.p, n * 8, cudaMemcpyDeviceToHost, stream.s));
+  PVI_CUDA(cudaStreamSynchronize(stream.s));
+}
+
+// ---------------------------------------------------------------------------
+// Value iteration driver (vi.hpp:162-291)
+
+namespace {
+
+bool evaluate_test(int test, double hi, double lo, double epsilon, std::uint64_t iteration) {
+  switch (test) {
+    case PVI_TEST_VALUE_SPAN:
+      return std::max(0.0, hi) < epsilon;
+    case PVI_TEST_CHANGE_SPAN:
+      return hi - lo < epsilon;
+    default:
+      if (iteration < 7) return false;
+      return hi - lo <= 2.0 * epsilon * std::min(std::abs(hi), std::abs(lo));
+  }
+}
+
+template <typename T>
+void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_values,
+                std::uint64_t resume_iteration, const std::uint8_t* resume_fp, double* out_values,
+                std::uint32_t* out_policy, pvi_vi_stats* stats) {
+  const auto t_start = std::chrono::steady_clock::now();
+  const std::uint64_t n = m.space.count;
+  if (n > cfg.max_states)
+    fail(PVI_ERR_CAPACITY, "value iteration requires " + std::to_string(n) +
+                               " states, exceeding the configured capacity of " +
+                               std::to_string(cfg.max_states), n);
+  if (n == 0) fail(PVI_ERR_PARAMETER, "value iteration: empty state space");
+  const double gamma = cfg.has_gamma ? cfg.gamma : m.gamma;
+  const int test = cfg.convergence_test >= 0 ? cfg.convergence_test : m.default_test;
+  std::uint8_t fp[32];
+  sha256(m.fingerprint.data(), m.fingerprint.size(), fp);
+
+  const int device = select_device(cfg.device);
+  const DevModel& dm = m.device_view(device);
+  Stream stream;
+  Scratch scratch;
+  PinnedStats pstats;
+  DevBuf dstats(sizeof(SweepStats));
+
+  const int hist_cap = test == PVI_TEST_PERIODIC_SPAN ? 8 : 2;
+  std::vector<std::unique_ptr<DevBuf>> ring;
+  for (int i = 0; i < hist_cap; ++i) ring.push_back(std::make_unique<DevBuf>(n * sizeof(T)));
+  std::vector<int> order;  // slots oldest..newest
+  std::uint64_t iteration = 0;
+  {
+    DevBuf v0(n * sizeof(double));
+    if (resume_values) {
+      if (resume_fp && std::memcmp(resume_fp, fp, 32) != 0)
+        fail(PVI_ERR_FINGERPRINT, "resume checkpoint fingerprint " + hex32(resume_fp) +
+                                      " does not match model fingerprint " + hex32(fp));
+      PVI_CUDA(cudaMemcpyAsync(v0.p, resume_values, n * 8, cudaMemcpyHostToDevice, stream.s));
+      iteration = resume_iteration;
+    } else {
+      initial_values_device(m, dm, v0.as<double>(), stream.s);
+    }
+    launch_cast_from_f64<T>(v0.as<double>(), ring[0]->as<T>(), n, stream.s);
+    order.push_back(0);
+  }
+
+  const bool ckpt = cfg.checkpoint_every > 0 && cfg.checkpoint_path && cfg.checkpoint_path[0];
+  std::vector<double> host_wide;
+  std::unique_ptr<DevBuf> wide;
+  auto write_checkpoint = [&](const T* dv, std::uint64_t iter) {
+    if (!ckpt) return;
+    if (!wide) {
+      wide = std::make_unique<DevBuf>(n * sizeof(double));
+      host_wide.resize(n);
+    }
+    launch_widen<T>(dv, wide->as<double>(), n, stream.s);
+    PVI_CUDA(cudaMemcpyAsync(host_wide.data(), wide->p, n * 8, cudaMemcpyDeviceToHost, stream.s));
+    PVI_CUDA(cudaStreamSynchronize(stream.s));
+    save_checkpoint(cfg.checkpoint_path, host_wide.data(), n, iter, fp);
+  };
+  if (ckpt && !resume_values) write_checkpoint(ring[order.back()]->as<T>(), iteration);
+
+  cudaEvent_t ev0, ev1;
+  PVI_CUDA(cudaEventCreate(&ev0));
+  PVI_CUDA(cudaEventCreate(&ev1));
+  double sweep_ms = 0.0;
+  std::uint64_t sweeps = 0;
+  double last_hi = 0.0, last_lo = 0.0;
+
+  bool converged = false;
+  const std::uint64_t start_iteration = iteration;
+  while (true) {
+    if (cfg.fixed_iterations > 0) {
+      if (iteration >= cfg.fixed_iterations) {
+        converged = true;
+        break;
+      }
+    } else if (iteration >= start_iteration + cfg.max_iterations) {
+      break;
+    }
+    ++iteration;
+    const int prev_slot = order.back();
+    int next_slot;
+    if (static_cast<int>(order.size()) < hist_cap) {
+      next_slot = static_cast<int>(order.size());
+    } else {
+      next_slot = order.front();
+      order.erase(order.begin());
+    }
+    const int hist_after = static_cast<int>(order.size()) + 1;
+    const bool want_test = cfg.fixed_iterations == 0 && hist_after >= hist_cap;
+
+    SweepArgs<T> a;
+    a.v = ring[prev_slot]->as<T>();
+    a.vout = ring[next_slot]->as<T>();
+    a.lo = 0;
+    a.hi = n;
+    a.gamma = gamma;
+    a.fa.test = want_test ? test : -1;
+    a.fa.gamma = gamma;
+    a.fa.stats = dstats.as<SweepStats>();
+    if (want_test && test == PVI_TEST_PERIODIC_SPAN) {
+      // previous vectors oldest..newest, excluding the slot being written
+      a.fa.n_hist = static_cast<int>(order.size());
+      for (int k = 0; k < a.fa.n_hist; ++k) a.fa.hist[k] = ring[order[k]]->p;
+    }
+    PVI_CUDA(cudaEventRecord(ev0, stream.s));
+    launch_sweep<T>(m, dm, a, scratch, stream.s);
+    PVI_CUDA(cudaEventRecord(ev1, stream.s));
+    PVI_CUDA(cudaMemcpyAsync(pstats.h, dstats.p, sizeof(SweepStats), cudaMemcpyDeviceToHost, stream.s));
+    PVI_CUDA(cudaStreamSynchronize(stream.s));
+    float ms = 0.f;
+    PVI_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    sweep_ms += ms;
+    ++sweeps;
+    order.push_back(next_slot);
+
+    if (pstats.h->first_bad != ~0ull)
+      fail(PVI_ERR_DIVERGENCE, "non-finite value for state " + std::to_string(pstats.h->first_bad) +
+                                   " at iteration " + std::to_string(iteration), iteration);
+    if (want_test) {
+      last_hi = dkey_inv(pstats.h->max_key);
+      last_lo = test == PVI_TEST_VALUE_SPAN ? 0.0 : dkey_inv(pstats.h->min_key);
+      converged = evaluate_test(test, last_hi, last_lo, cfg.epsilon, iteration);
+    }
+    if (ckpt && iteration % cfg.checkpoint_every == 0)
+      write_checkpoint(ring[order.back()]->as<T>(), iteration);
+    if (converged) break;
+  }
+
+  // Policy extraction (vi.hpp:267-280): one more argmax sweep.
+  const T* vfinal = ring[order.back()]->as<T>();
+  DevBuf policy(n * sizeof(std::uint32_t));
+  {
+    SweepArgs<T> a;
+    a.v = vfinal;
+    a.act = policy.as<std::uint32_t>();
+    a.lo = 0;
+    a.hi = n;
+    a.gamma = gamma;
+    PVI_CUDA(cudaEventRecord(ev0, stream.s));
+    launch_sweep<T>(m, dm, a, scratch, stream.s);
+    PVI_CUDA(cudaEventRecord(ev1, stream.s));
+    PVI_CUDA(cudaStreamSynchronize(stream.s));
+    float ms = 0.f;
+    PVI_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    sweep_ms += ms;
+    ++sweeps;
+  }
+  if (out_values) {
+    DevBuf w(n * sizeof(double));
+    launch_widen<T>(vfinal, w.as<double>(), n, stream.s);
+    PVI_CUDA(cudaMemcpyAsync(out_values, w.p, n * 8, cudaMemcpyDeviceToHost, stream.s));
+    PVI_CUDA(cudaStreamSynchronize(stream.s));
+  }
+  if (out_policy) {
+    PVI_CUDA(cudaMemcpyAsync(out_policy, policy.p, n * 4, cudaMemcpyDeviceToHost, stream.s));
+    PVI_CUDA(cudaStreamSynchronize(stream.s));
+  }
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  if (stats) {
+    stats->iterations = iteration;
+    stats->converged = converged ? 1 : 0;
+    stats->wall_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    stats->sweep_seconds = sweep_ms * 1e-3;
+    stats->sweeps = sweeps;
+    stats->span_lo = last_lo;
+    stats->span_hi = last_hi;
+    stats->terms_per_sweep = m.terms_per_sweep();
+  }
+}
+
+}  // namespace
+
+void vi_solve(const Model& m, const pvi_vi_config& cfg, const double* resume_values,
+              std::uint64_t resume_iteration, const std::uint8_t* resume_fp, double* out_values,
+              std::uint32_t* out_policy, pvi_vi_stats* stats) {
+  if (!(cfg.epsilon > 0.0)) fail(PVI_ERR_PARAMETER, "value iteration: epsilon must be > 0");
+  if (cfg.precision == 1)
+    solve_impl<float>(m, cfg, resume_values, resume_iteration, resume_fp, out_values, out_policy, stats);
+  else
+    solve_impl<double>(m, cfg, resume_values, resume_iteration, resume_fp, out_values, out_policy, stats);
+}
+
+// ---------------------------------------------------------------------------
+// Single sweeps with host buffers
+
+namespace {
+
+template <typename T>
+void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t lo,
+                 std::uint64_t hi, void* out_values, std::uint32_t* out_actions, void* out_q) {
+  const std::uint64_t n = m.space.count;
+  if (lo > hi || hi > n) fail(PVI_ERR_PARAMETER, "state range out of bounds");
+  const int device = select_device(-1);
+  const DevModel& dm = m.device_view(device);
+  Stream stream;
+  Scratch scratch;
+  DevBuf v(n * sizeof(T));
+  PVI_CUDA(cudaMemcpyAsync(v.p, values, n * sizeof(T), cudaMemcpyHostToDevice, stream.s));
+  const std::uint64_t nr = hi - lo;
+  DevBuf vo(out_values ? nr * sizeof(T) : 0);
+  DevBuf ao(out_actions ? nr * sizeof(std::uint32_t) : 0);
+  DevBuf qo(out_q ? nr * m.n_actions * sizeof(T) : 0);
+  SweepArgs<T> a;
+  a.v = v.as<T>();
+  a.vout = vo.as<T>();
+  a.act = ao.as<std::uint32_t>();
+  a.qout = qo.as<T>();
+  a.lo = lo;
+  a.hi = hi;
+  a.out_off = lo;
+  a.gamma = gamma;
+  a.want_values = out_values || out_actions;
+  launch_sweep<T>(m, dm, a, scratch, stream.s);
+  if (out_values) PVI_CUDA(cudaMemcpyAsync(out_values, vo.p, nr * sizeof(T), cudaMemcpyDeviceToHost, stream.s));
+  if (out_actions) PVI_CUDA(cudaMemcpyAsync(out_actions, ao.p, nr * 4, cudaMemcpyDeviceToHost, stream.s));
+  if (out_q) PVI_CUDA(cudaMemcpyAsync(out_q, qo.p, nr * m.n_actions * sizeof(T), cudaMemcpyDeviceToHost, stream.s));
+  PVI_CUDA(cudaStreamSynchronize(stream.s));
+}
+
+}  // namespace
+
+void vi_backup(const Model& m, int precision, double gamma, const void* values, std::uint64_t lo,
+               std::uint64_t hi, void* out_values, std::uint32_t* out_actions, void* out_q) {
+  if (precision == 1)
+    backup_impl<float>(m, gamma, values, lo, hi, out_values, out_actions, out_q);
+  else
+    backup_impl<double>(m, gamma, values, lo, hi, out_values, out_actions, out_q);
+}
+
+// ---------------------------------------------------------------------------
+// check_convergence over explicit host history (vi.hpp:107-158)
+
+namespace {
+template <typename T>
+bool check_impl(const Model& m, int test, const void* const* history, int n_hist, double gamma,
+                double epsilon, std::uint64_t iteration) {
+  const int need = test == PVI_TEST_PERIODIC_SPAN ? 8 : 2;
+  if (n_hist < need)
+    fail(PVI_ERR_CONTRACT, "convergence test needs " + std::to_string(need) +
+                               " value vectors, got " + std::to_string(n_hist));
+  if (test == PVI_TEST_PERIODIC_SPAN && iteration < 7) return false;
+  const std::uint64_t n = m.space.count;
+  select_device(-1);
+  Stream stream;
+  const int used = test == PVI_TEST_PERIODIC_SPAN ? 8 : 2;
+  std::vector<std::unique_ptr<DevBuf>> bufs;
+  for (int k = 0; k < used; ++k) {
+    bufs.push_back(std::make_unique<DevBuf>(n * sizeof(T)));
+    PVI_CUDA(cudaMemcpyAsync(bufs.back()->p, history[n_hist - used + k], n * sizeof(T),
+                             cudaMemcpyHostToDevice, stream.s));
+  }
+  DevBuf dstats(sizeof(SweepStats));
+  PinnedStats ps;
+  FinalizeArgs fa;
+  fa.test = test;
+  fa.gamma = gamma;
+  fa.stats = dstats.as<SweepStats>();
+  fa.n_hist = used - 1;
+  for (int k = 0; k < used - 1; ++k) fa.hist[k] = bufs[k]->p;
+  launch_stats<T>(bufs[used - 1]->as<T>(), bufs[used - 2]->as<T>(), n, fa, stream.s);
+  PVI_CUDA(cudaMemcpyAsync(ps.h, dstats.p, sizeof(SweepStats), cudaMemcpyDeviceToHost, stream.s));
+  PVI_CUDA(cudaStreamSynchronize(stream.s));
+  const double hi = dkey_inv(ps.h->max_key);
+  const double lo = test == PVI_TEST_VALUE_SPAN ? 0.0 : dkey_inv(ps.h->min_key);
+  return evaluate_test(test, hi, lo, epsilon, iteration);
+}
+}  // namespace
+
+bool check_convergence(const Model& m, int precision, int test, const void* const* history,
+                       int n_hist, double gamma, double epsilon, std::uint64_t iteration) {
+  if (precision == 1) return check_impl<float>(m, test, history, n_hist, gamma, epsilon, iteration);
+  return check_impl<double>(m, test, history, n_hist, gamma, epsilon, iteration);
+}
+
+// ---------------------------------------------------------------------------
+// Device-resident sweep of one shard (multi-GPU driver)
+
+namespace {
+__global__ void k_stats_to_doubles(const SweepStats* st, double* out) {
+  const SweepStats s = *st;
+  out[0] = s.max_key == 0ull ? -1.7976931348623157e308 : dkey_inv(s.max_key);
+  out[1] = s.min_key == ~0ull ? -1.7976931348623157e308 : -dkey_inv(s.min_key);
+  out[2] = s.first_bad == ~0ull ? -1.7976931348623157e308 : -static_cast<double>(s.first_bad);
+  out[3] = 0.0;
+}
+
+template <typename T>
+void sweep_device_impl(const Model& m, double gamma, const void* vprev, void* vnext,
+                       std::uint32_t* act, std::uint64_t lo, std::uint64_t hi, int test,
+                       const void* const* hist, int n_hist, int want_stats, double* stats,
+                       cudaStream_t stream) {
+  int device = 0;
+  PVI_CUDA(cudaGetDevice(&device));
+  const DevModel& dm = m.device_view(device);
+  static thread_local Scratch scratch;
+  static thread_local DevBuf* dstats = nullptr;
+  if (!dstats) dstats = new DevBuf(sizeof(SweepStats));
+  SweepArgs<T> a;
+  a.v = static_cast<const T*>(vprev);
+  a.vout = static_cast<T*>(vnext);
+  a.act = act;
+  a.lo = lo;
+  a.hi = hi;
+  a.out_off = 0;
+  a.gamma = gamma;
+  a.want_values = true;
+  if (want_stats && stats) {
+    a.fa.stats = dstats->as<SweepStats>();
+    a.fa.test = test;
+    a.fa.gamma = gamma;
+    if (test == PVI_TEST_PERIODIC_SPAN) {
+      if (n_hist < 7 || !hist) fail(PVI_ERR_CONTRACT, "periodic span needs 7 previous vectors");
+      a.fa.n_hist = 7;
+      for (int k = 0; k < 7; ++k) a.fa.hist[k] = hist[n_hist - 7 + k];
+    }
+  }
+  launch_sweep<T>(m, dm, a, scratch, stream);
+  if (want_stats && stats) k_stats_to_doubles<<<1, 1, 0, stream>>>(dstats->as<SweepStats>(), stats);
+  PVI_CUDA(cudaGetLastError());
+}
+}  // namespace
+
+void vi_sweep_device(const Model& m, int precision, double gamma, const void* vprev, void* vnext,
+                     std::uint32_t* act, std::uint64_t lo, std::uint64_t hi, int test,
+                     const void* const* hist, int n_hist, int want_stats, double* stats,
+                     void* stream) {
+  if (lo > hi || hi > m.space.count) fail(PVI_ERR_PARAMETER, "state range out of bounds");
+  auto st = static_cast<cudaStream_t>(stream);
+  if (precision == 1)
+    sweep_device_impl<float>(m, gamma, vprev, vnext, act, lo, hi, test, hist, n_hist, want_stats, stats, st);
+  else
+    sweep_device_impl<double>(m, gamma, vprev, vnext, act, lo, hi, test, hist, n_hist, want_stats, stats, st);
+}
+
+// ---------------------------------------------------------------------------
+// Cost-weighted contiguous partition
+
+void partition(const Model& m, int parts, std::uint64_t* bounds) {
+  if (parts < 1) fail(PVI_ERR_PARAMETER, "partition: parts must be >= 1");
+  const std::uint64_t n = m.space.count;
+  const std::uint64_t tile = std::max<std::uint64_t>(1, m.tile_states());
+  const std::uint64_t n_tiles = (n + tile - 1) / tile;
+  std::vector<double> cost(n_tiles, 0.0);
+  if (m.scenario == PVI_SCENARIO_B) {
+    for (std::uint64_t s = 0; s < n; ++s) cost[s / tile] += m.state_cost(s);
+  } else {
+    for (std::uint64_t t = 0; t < n_tiles; ++t)
+      cost[t] = static_cast<double>(std::min(n, (t + 1) * tile) - t * tile);
+  }
+  double total = 0.0;
+  for (double c : cost) total += c;
+  bounds[0] = 0;
+  double acc = 0.0;
+  std::uint64_t t = 0;
+  for (int p = 1; p < parts; ++p) {
+    const double target = total * p / parts;
+    while (t < n_tiles && acc + cost[t] * 0.5 < target) acc += cost[t++];
+    bounds[p] = std::min(n, t * tile);
+  }
+  bounds[parts] = n;
+  for (int p = 1; p <= parts; ++p) bounds[p] = std::max(bounds[p], bounds[p - 1]);
+}
+
+}  // namespace pvi_b200

@@ -1,0 +1,42 @@
+// Host engine entry points behind the C ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include "model.hpp"
+
+namespace pvi_b200 {
+
+int select_device(int requested);
+std::string hex32(const std::uint8_t* fp);
+
+void vi_solve(const Model& m, const pvi_vi_config& cfg, const double* resume_values,
+              std::uint64_t resume_iteration, const std::uint8_t* resume_fp, double* out_values,
+              std::uint32_t* out_policy, pvi_vi_stats* stats);
+void vi_backup(const Model& m, int precision, double gamma, const void* values, std::uint64_t lo,
+               std::uint64_t hi, void* out_values, std::uint32_t* out_actions, void* out_q);
+bool check_convergence(const Model& m, int precision, int test, const void* const* history,
+                       int n_hist, double gamma, double epsilon, std::uint64_t iteration);
+void vi_sweep_device(const Model& m, int precision, double gamma, const void* vprev, void* vnext,
+                     std::uint32_t* act, std::uint64_t lo, std::uint64_t hi, int test,
+                     const void* const* hist, int n_hist, int want_stats, double* stats,
+                     void* stream);
+void partition(const Model& m, int parts, std::uint64_t* bounds);
+void initial_values_host(const Model& m, double* out);
+
+void save_checkpoint(const std::string& path, const double* values, std::uint64_t count,
+                     std::uint64_t iteration, const std::uint8_t fp[32]);
+void load_checkpoint(const std::string& path, const std::uint8_t* expected, double* values,
+                     std::uint64_t capacity, std::uint64_t* count, std::uint64_t* iteration,
+                     std::uint8_t fp[32]);
+
+// Simulation (sim_kernels.cu)
+void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_policies,
+                  const pvi_rollout_config& cfg, pvi_rollout_summary* per_rollout,
+                  pvi_evaluation* evals);
+void philox_block_device(const std::uint32_t ctr[4], const std::uint32_t key[2], std::uint32_t out[4]);
+void rollout_draws_device(std::uint64_t seed, std::uint64_t rollout, std::uint32_t day, int n,
+                          std::uint64_t* out);
+
+}  // namespace pvi_b200

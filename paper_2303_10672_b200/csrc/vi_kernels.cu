@@ -1,0 +1,758 @@
+// Bellman-sweep kernels (K1-A/B/C, tabular), the fused finalize +
+// convergence reduction (K2), policy extraction (K3, the same kernels with
+// the action output enabled) and Scenario B's initial value (K4).
+//
+// Exactness: the whole library is compiled with -fmad=false, and every
+// per-(state, action) accumulation visits its terms in the reference's
+// order with the reference's expression tree (cited per kernel).  The
+// device therefore reproduces the reference CPU solver's value vectors bit
+// for bit in both f64 and f32 modes (tests/test_gpu_parity.py).
+//
+// Layout in HBM: V is a flat |S| array of T in mixed-radix index order
+// (digit 0 most significant, tuple_space.hpp:12-13), exactly the
+// reference's; Scenario B/C partial maxima live in an (action-chunk x
+// state) scratch array so the cross-chunk argmax stays in action order.
+
+#include <cfloat>
+
+#include "common.cuh"
+#include "vi_kernels.cuh"
+
+namespace pvi_b200 {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// K2: block reduction of the convergence statistic + non-finite scan.
+
+template <typename T>
+__device__ __forceinline__ void state_stat(const FinalizeArgs& fa, std::uint64_t s, T vnew,
+                                           const T* __restrict__ vprev, double& smax,
+                                           double& smin, unsigned long long& bad) {
+  const double cur = static_cast<double>(vnew);
+  if (!isfinite(cur)) bad = s < bad ? s : bad;
+  if (fa.test < 0) return;
+  double stat;
+  if (fa.test == PVI_TEST_PERIODIC_SPAN) {
+    // vi.hpp:136-156: D(s) = sum_{j=0..6} gamma^j (V_{i-j} - V_{i-j-1}).
+    double vals[8];
+    vals[7] = cur;
+    for (int k = 1; k <= 7; ++k)
+      vals[7 - k] = static_cast<double>(static_cast<const T*>(fa.hist[fa.n_hist - k])[s]);
+    double acc = 0.0, w = 1.0;
+    for (int j = 0; j <= 6; ++j) {
+      acc += w * (vals[7 - j] - vals[6 - j]);
+      w *= fa.gamma;
+    }
+    stat = acc;
+  } else {
+    const double d = cur - static_cast<double>(vprev[s]);  // vi.hpp:118-133
+    stat = fa.test == PVI_TEST_VALUE_SPAN ? fabs(d) : d;
+  }
+  smax = fmax(smax, stat);
+  smin = fmin(smin, stat);
+}
+
+__device__ __forceinline__ void reduce_stats(double smax, double smin, unsigned long long bad,
+                                             SweepStats* st) {
+  if (st == nullptr) return;
+  for (int o = 16; o > 0; o >>= 1) {
+    smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+    smin = fmin(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+    const unsigned long long ob = __shfl_xor_sync(0xffffffffu, bad, o);
+    bad = ob < bad ? ob : bad;
+  }
+  __shared__ double r_max[32], r_min[32];
+  __shared__ unsigned long long r_bad[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = (blockDim.x + 31) >> 5;
+  if (lane == 0) {
+    r_max[warp] = smax;
+    r_min[warp] = smin;
+    r_bad[warp] = bad;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    smax = lane < nwarps ? r_max[lane] : -DBL_MAX;
+    smin = lane < nwarps ? r_min[lane] : DBL_MAX;
+    bad = lane < nwarps ? r_bad[lane] : ~0ull;
+    for (int o = 16; o > 0; o >>= 1) {
+      smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+      smin = fmin(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+      const unsigned long long ob = __shfl_xor_sync(0xffffffffu, bad, o);
+      bad = ob < bad ? ob : bad;
+    }
+    if (lane == 0) {
+      if (smax != -DBL_MAX) atomicMax(&st->max_key, dkey(smax));
+      if (smin != DBL_MAX) atomicMin(&st->min_key, dkey(smin));
+      if (bad != ~0ull) atomicMin(&st->first_bad, bad);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FIFO / LIFO ageing of a stock profile x[1..m] (scenario_a.cpp:18-40,
+// scenario_b.cpp:18-26).  Writes next[1..m-1]; returns units expiring.
+
+__device__ __forceinline__ int age_fifo(const int* x, int m, int demand, int* next) {
+  const int expired = ipos(x[1] - demand);
+  int prefix = 0;
+  for (int j = 1; j <= m - 1; ++j) {
+    prefix += x[j];
+    next[j] = ipos(x[j + 1] - ipos(demand - prefix));
+  }
+  return expired;
+}
+
+__device__ __forceinline__ int age_lifo(const int* x, int m, int demand, int* next) {
+  int suffix = 0;
+  for (int j = 2; j <= m; ++j) suffix += x[j];
+  const int expired = ipos(x[1] - ipos(demand - suffix));
+  for (int j = 1; j <= m - 1; ++j) {
+    suffix -= x[j + 1];
+    next[j] = ipos(x[j + 1] - ipos(demand - suffix));
+  }
+  return expired;
+}
+
+__device__ __forceinline__ void decode(const DevModel& dm, std::uint64_t s, int* st) {
+  for (int i = 0; i < dm.n_digits; ++i) {
+    st[i] = static_cast<int>(s / dm.weight[i]);
+    s %= dm.weight[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1-A: one thread per state, all actions in registers, the demand pmf in
+// shared memory.  Term order and expression follow
+// ScenarioA::q_row_impl (scenario_a.cpp:104-146): d outer, a inner,
+// term = T(p * (r_sd - C_v*a + gamma*V[base + a*W0])), accumulated in T.
+
+template <typename T, int NA>
+__global__ void __launch_bounds__(256) k_sweep_a(DevModel dm, const T* __restrict__ V,
+                                                 T* __restrict__ vout, std::uint32_t* __restrict__ act,
+                                                 T* __restrict__ qout, std::uint64_t lo,
+                                                 std::uint64_t hi, std::uint64_t out_off,
+                                                 double gamma, FinalizeArgs fa) {
+  extern __shared__ double s_pmf[];
+  const int dn = dm.a_dmax + 1;
+  for (int i = threadIdx.x; i < dn; i += blockDim.x) s_pmf[i] = dm.a_pmf[i];
+  __syncthreads();
+
+  const std::uint64_t s = lo + static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double smax = -DBL_MAX, smin = DBL_MAX;
+  unsigned long long bad = ~0ull;
+  if (s < hi) {
+    const int m = dm.a_m, lead = dm.a_lead, na = static_cast<int>(dm.n_actions);
+    int st[kMaxDigits];
+    decode(dm, s, st);
+    int x[14], aged[14];
+    int xt = 0;
+    for (int j = 1; j <= m; ++j) {
+      x[j] = st[lead - 1 + m - j];
+      xt += x[j];
+    }
+    std::uint64_t base_static = 0;
+    for (int k = 1; k <= lead - 2; ++k) base_static += st[k - 1] * dm.weight[k];
+    if (lead >= 2) base_static += st[lead - 2] * dm.weight[lead - 1];
+    const std::uint64_t w0 = dm.weight[0];
+
+    T q[NA];
+    double cva[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      q[a] = T(0);
+      cva[a] = dm.a_cv * a;
+    }
+    for (int d = 0; d < dn; ++d) {
+      const double p = s_pmf[d];
+      const int expired = dm.a_lifo ? age_lifo(x, m, d, aged) : age_fifo(x, m, d, aged);
+      std::uint64_t base = base_static;
+      for (int j = 1; j <= m - 1; ++j) base += aged[j] * dm.weight[lead + m - 1 - j];
+      const double reward_sd = -dm.a_ch * ipos(xt - d - expired) - dm.a_cs * ipos(d - xt) -
+                               dm.a_cw * expired;
+      const T* vb = V + base;
+#pragma unroll
+      for (int a = 0; a < NA; ++a) {
+        if (a < na) {
+          const double v = static_cast<double>(vb[a * w0]);
+          q[a] += static_cast<T>(p * (reward_sd - cva[a] + gamma * v));
+        }
+      }
+    }
+    T best = q[0];
+    std::uint32_t besta = 0;
+#pragma unroll
+    for (int a = 1; a < NA; ++a) {
+      if (a < na && q[a] > best) {
+        best = q[a];
+        besta = a;
+      }
+    }
+    if (qout) {
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+        if (a < na) qout[(s - lo) * na + a] = q[a];
+    }
+    if (vout) vout[s - out_off] = best;
+    if (act) act[s - out_off] = besta;
+    state_stat<T>(fa, s, best, V, smax, smin, bad);
+  }
+  reduce_stats(smax, smin, bad, fa.stats);
+}
+
+// ---------------------------------------------------------------------------
+// K1-B: one thread per (state, order_a); the order_b row in registers.
+// A block is one tile of states sharing every digit except the two least
+// significant (b_lane_order sorts the tile by their stock sum so lanes of a
+// warp share loop trip counts and V cache lines) times one order_a.
+// Term order and expression follow ScenarioB::q_row_impl
+// (scenario_b.cpp:262-321): h_a outer, h_b inner, p == 0 skipped,
+// term = T(p * (head - C_v^b*o_b + gamma*V[...])), accumulated in T.
+
+template <typename T, int NB>
+__global__ void __launch_bounds__(256) k_sweep_b(DevModel dm, const T* __restrict__ V,
+                                                 T* __restrict__ part_v,
+                                                 std::uint8_t* __restrict__ part_a,
+                                                 T* __restrict__ qout, std::uint64_t lo,
+                                                 std::uint64_t hi, std::uint64_t tile0,
+                                                 double gamma) {
+  extern __shared__ double smem[];
+  double* s_pmf_a = smem;
+  double* s_pmf_b = s_pmf_a + dm.b_len_a;
+  double* s_sf_a = s_pmf_b + dm.b_len_b;
+  double* s_sf_b = s_sf_a + dm.b_len_a + 1;
+  double* s_pz = s_sf_b + dm.b_len_b + 1;
+  const int pz_len = (dm.b_cap_b + 1) * dm.b_dn;
+  double* s_pz_cum = s_pz + pz_len;
+  for (int i = threadIdx.x; i < dm.b_len_a; i += blockDim.x) s_pmf_a[i] = dm.b_pmf_a[i];
+  for (int i = threadIdx.x; i < dm.b_len_b; i += blockDim.x) s_pmf_b[i] = dm.b_pmf_b[i];
+  for (int i = threadIdx.x; i <= dm.b_len_a; i += blockDim.x) s_sf_a[i] = dm.b_sf_a[i];
+  for (int i = threadIdx.x; i <= dm.b_len_b; i += blockDim.x) s_sf_b[i] = dm.b_sf_b[i];
+  for (int i = threadIdx.x; i < pz_len; i += blockDim.x) {
+    s_pz[i] = dm.b_pz[i];
+    s_pz_cum[i] = dm.b_pz_cum[i];
+  }
+  __syncthreads();
+
+  const int t = threadIdx.x;
+  if (t >= dm.b_tile) return;
+  const std::uint64_t s =
+      (tile0 + blockIdx.x) * static_cast<std::uint64_t>(dm.b_tile) + dm.b_lane_order[t];
+  if (s < lo || s >= hi) return;
+  const int oa = blockIdx.y;
+  const int m = dm.b_m, nb = dm.b_nb;
+  int st[kMaxDigits];
+  decode(dm, s, st);
+  int xa[10], xb[10], aged[10];
+  int ia = 0, ib = 0;
+  for (int j = 1; j <= m; ++j) {
+    xa[j] = st[m - j];
+    xb[j] = st[2 * m - j];
+    ia += xa[j];
+    ib += xb[j];
+  }
+  const std::uint64_t wa = dm.weight[0];
+  const std::uint64_t wb = dm.weight[m];
+  const double cva_oa = dm.b_cva * oa;
+  double cvb[NB];
+  T q[NB];
+#pragma unroll
+  for (int ob = 0; ob < NB; ++ob) {
+    cvb[ob] = dm.b_cvb * ob;
+    q[ob] = T(0);
+  }
+  const int dnp = dm.b_dn;
+  const int ha_hi = min(ia, dm.b_cap_a);
+  const int hb_hi = min(ib, dm.b_cap_b);
+  for (int ha = 0; ha <= ha_hi; ++ha) {
+    age_fifo(xa, m, ha, aged);
+    std::uint64_t base_a = oa * wa;
+    for (int j = 1; j <= m - 1; ++j) base_a += aged[j] * dm.weight[m - j];
+    const double revenue_a = dm.b_cra * ha;
+    const bool a_int = ha < ia;
+    for (int hb = 0; hb <= hb_hi; ++hb) {
+      // issued_probability (scenario_b.cpp:168-176)
+      double p;
+      if (a_int)
+        p = hb < ib ? s_pmf_a[ha] * s_pmf_b[hb] : s_pz[ib * dnp + ha] * s_sf_b[ib];
+      else
+        p = hb < ib ? s_sf_a[ia] * s_pmf_b[hb] : (1.0 - s_pz_cum[ib * dnp + ia]) * s_sf_b[ib];
+      if (p == 0.0) continue;
+      age_fifo(xb, m, hb, aged);
+      std::uint64_t base = base_a;
+      for (int j = 1; j <= m - 1; ++j) base += aged[j] * dm.weight[2 * m - j];
+      const double revenue = revenue_a + dm.b_crb * hb;
+      const double head = revenue - cva_oa;
+      const T* va = V + base;
+#pragma unroll
+      for (int ob = 0; ob < NB; ++ob) {
+        if (ob < nb) {
+          const double v = static_cast<double>(va[ob * wb]);
+          q[ob] += static_cast<T>(p * (head - cvb[ob] + gamma * v));
+        }
+      }
+    }
+  }
+  T best = q[0];
+  int bo = 0;
+#pragma unroll
+  for (int ob = 1; ob < NB; ++ob)
+    if (ob < nb && q[ob] > best) {
+      best = q[ob];
+      bo = ob;
+    }
+  const std::uint64_t nr = hi - lo;
+  if (part_v) {
+    part_v[oa * nr + (s - lo)] = best;
+    part_a[oa * nr + (s - lo)] = static_cast<std::uint8_t>(bo);
+  }
+  if (qout) {
+    const std::uint64_t row = (s - lo) * dm.n_actions + static_cast<std::uint64_t>(oa) * nb;
+#pragma unroll
+    for (int ob = 0; ob < NB; ++ob)
+      if (ob < nb) qout[row + ob] = q[ob];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1-C: one thread per (state, order); the demand dimension unrolled into
+// DN register accumulators.  Blocks run heaviest order first.  Term order
+// and expression follow ScenarioC::q_row_impl (scenario_c.cpp:223-302):
+// for each d, inner_d = sum over compositions c (ascending) of
+// p_c * (r + gamma*V[idx]); q = T(sum_d p_d * inner_d); all in double.
+// Iterating c outer and d inner keeps every inner_d's own order, and lets
+// one composition's prefix sums serve all DN demands.  The reward is read
+// from two exact tables: RA[total-d+D] = (fixed - C_h*(total-d)^+) -
+// C_s*(d-total)^+ and CW[w] = C_w*w, reproducing the reference's
+// left-to-right evaluation.
+
+template <int M, int DN>
+struct CAcc {
+  double v[DN > 0 ? DN : 1];
+};
+
+template <typename T, int M, int DN>
+__global__ void __launch_bounds__(128) k_sweep_c(DevModel dm, const T* __restrict__ V,
+                                                 T* __restrict__ part_v, T* __restrict__ qout,
+                                                 std::uint64_t lo, std::uint64_t hi,
+                                                 double gamma) {
+  extern __shared__ double smem[];
+  const int cap = dm.c_max_order;
+  const int dmax = dm.c_dmax;
+  const int n_ra = M * cap + dmax + 1;
+  double* s_ra = smem;
+  double* s_cw = s_ra + n_ra;
+  const int na = static_cast<int>(dm.n_actions);
+  const int a = na - 1 - static_cast<int>(blockIdx.y);
+  const double fixed = a > 0 ? -dm.c_cf : 0.0;
+  for (int k = threadIdx.x; k < n_ra; k += blockDim.x) {
+    const int diff = k - dmax;  // total - d
+    s_ra[k] = fixed - dm.c_ch * ipos(diff) - dm.c_cs * ipos(-diff);
+  }
+  for (int k = threadIdx.x; k <= cap; k += blockDim.x) s_cw[k] = dm.c_cw * k;
+  __syncthreads();
+
+  const std::uint64_t s = lo + static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= hi) return;
+  int st[kMaxDigits];
+  decode(dm, s, st);
+  const int tau = st[0];
+  int x[M + 1];
+#pragma unroll
+  for (int j = 1; j <= M - 1; ++j) x[j] = st[M - j];
+  const std::uint64_t tau_base = static_cast<std::uint64_t>((tau + 1) % 7) * dm.weight[0];
+  std::uint64_t w[M + 1];
+#pragma unroll
+  for (int k = 1; k < M; ++k) w[k] = dm.weight[k];
+
+  double inner[DN];
+#pragma unroll
+  for (int d = 0; d < DN; ++d) inner[d] = 0.0;
+
+  const std::uint32_t off = dm.c_offsets[a];
+  const std::uint32_t n_c = dm.c_offsets[a + 1] - off;
+  for (std::uint32_t c = 0; c < n_c; ++c) {
+    const std::uint32_t id = __ldg(dm.c_ids + off + c);
+    const double prob = __ldg(dm.c_probs + off + c);
+    const std::int8_t* yt = dm.c_comp + static_cast<std::size_t>(id) * M;
+    int sp[M + 1], z[M + 1];
+    int prefix = 0;
+#pragma unroll
+    for (int j = 1; j <= M - 1; ++j) {
+      z[j] = min(x[j] + static_cast<int>(yt[M - j]), cap);
+      prefix += z[j];
+      sp[j] = prefix;
+    }
+    const int fresh = yt[0];
+    const int total = prefix + fresh;
+    const int z1 = z[1];
+#pragma unroll
+    for (int d = 0; d < DN; ++d) {
+      std::uint64_t idx = tau_base;
+#pragma unroll
+      for (int j = 1; j <= M - 2; ++j) {
+        const int e = d > sp[j] ? d - sp[j] : 0;
+        int nxj = z[j + 1] - e;
+        if (nxj < 0) nxj = 0;
+        idx += static_cast<std::uint64_t>(nxj) * w[M - j];
+      }
+      const int e_last = d > sp[M - 1] ? d - sp[M - 1] : 0;
+      int nx1 = fresh - e_last;
+      if (nx1 < 0) nx1 = 0;
+      idx += static_cast<std::uint64_t>(nx1) * w[1];
+      const double reward = s_ra[total - d + dmax] - s_cw[ipos(z1 - d)];
+      inner[d] += prob * (reward + gamma * static_cast<double>(V[idx]));
+    }
+  }
+  const double* pmf = dm.c_pmf + tau * (dmax + 1);
+  double acc = 0.0;
+#pragma unroll
+  for (int d = 0; d < DN; ++d) acc += __ldg(pmf + d) * inner[d];
+  const T qa = static_cast<T>(acc);
+  const std::uint64_t nr = hi - lo;
+  if (part_v) part_v[static_cast<std::uint64_t>(a) * nr + (s - lo)] = qa;
+  if (qout) qout[(s - lo) * na + a] = qa;
+}
+
+// Generic Scenario C kernel for any (m, D_max): one thread per
+// (state, order, demand), so no demand-indexed register array is needed.
+// Writes inner_d into `inner_out` ((a, d, state) layout); k_reduce_c then
+// folds the demands in order.
+template <typename T>
+__global__ void __launch_bounds__(128) k_sweep_c_generic(DevModel dm, const T* __restrict__ V,
+                                                         double* __restrict__ inner_out,
+                                                         std::uint64_t lo, std::uint64_t hi,
+                                                         double gamma) {
+  const int m = dm.c_m, cap = dm.c_max_order, dmax = dm.c_dmax;
+  const int na = static_cast<int>(dm.n_actions);
+  const int a = na - 1 - static_cast<int>(blockIdx.y);
+  const int d = blockIdx.z;
+  const std::uint64_t s = lo + static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= hi) return;
+  const double fixed = a > 0 ? -dm.c_cf : 0.0;
+  int st[kMaxDigits];
+  decode(dm, s, st);
+  const int tau = st[0];
+  int x[14];
+  for (int j = 1; j <= m - 1; ++j) x[j] = st[m - j];
+  const std::uint64_t tau_base = static_cast<std::uint64_t>((tau + 1) % 7) * dm.weight[0];
+  const std::uint32_t off = dm.c_offsets[a];
+  const std::uint32_t n_c = dm.c_offsets[a + 1] - off;
+  double inner = 0.0;
+  for (std::uint32_t c = 0; c < n_c; ++c) {
+    const std::uint32_t id = dm.c_ids[off + c];
+    const double prob = dm.c_probs[off + c];
+    const std::int8_t* yt = dm.c_comp + static_cast<std::size_t>(id) * m;
+    int sp[14], z[14];
+    int prefix = 0;
+    for (int j = 1; j <= m - 1; ++j) {
+      z[j] = min(x[j] + static_cast<int>(yt[m - j]), cap);
+      prefix += z[j];
+      sp[j] = prefix;
+    }
+    const int fresh = yt[0];
+    const int total = prefix + fresh;
+    std::uint64_t idx = tau_base;
+    for (int j = 1; j <= m - 2; ++j) {
+      const int e = d > sp[j] ? d - sp[j] : 0;
+      int nxj = z[j + 1] - e;
+      if (nxj < 0) nxj = 0;
+      idx += static_cast<std::uint64_t>(nxj) * dm.weight[m - j];
+    }
+    const int e_last = d > sp[m - 1] ? d - sp[m - 1] : 0;
+    int nx1 = fresh - e_last;
+    if (nx1 < 0) nx1 = 0;
+    idx += static_cast<std::uint64_t>(nx1) * dm.weight[1];
+    const double reward = fixed - dm.c_ch * ipos(total - d) - dm.c_cs * ipos(d - total) -
+                          dm.c_cw * ipos(z[1] - d);
+    inner += prob * (reward + gamma * static_cast<double>(V[idx]));
+  }
+  const std::uint64_t nr = hi - lo;
+  inner_out[(static_cast<std::uint64_t>(a) * (dmax + 1) + d) * nr + (s - lo)] = inner;
+}
+
+template <typename T>
+__global__ void k_reduce_c(DevModel dm, const double* __restrict__ inner, T* __restrict__ part_v,
+                           T* __restrict__ qout, std::uint64_t lo, std::uint64_t hi) {
+  const std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const std::uint64_t nr = hi - lo;
+  if (i >= nr) return;
+  const int a = blockIdx.y;
+  const int dn = dm.c_dmax + 1;
+  const int tau = static_cast<int>((lo + i) / dm.weight[0]);
+  const double* pmf = dm.c_pmf + tau * dn;
+  double acc = 0.0;
+  for (int d = 0; d < dn; ++d) acc += pmf[d] * inner[(static_cast<std::uint64_t>(a) * dn + d) * nr + i];
+  const T qa = static_cast<T>(acc);
+  if (part_v) part_v[static_cast<std::uint64_t>(a) * nr + i] = qa;
+  if (qout) qout[i * dm.n_actions + a] = qa;
+}
+
+// ---------------------------------------------------------------------------
+// Tabular (tests/support/tabular_mdp.hpp:88-99): one thread per state.
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_sweep_tab(DevModel dm, const T* __restrict__ V,
+                                                   T* __restrict__ vout,
+                                                   std::uint32_t* __restrict__ act,
+                                                   T* __restrict__ qout, std::uint64_t lo,
+                                                   std::uint64_t hi, std::uint64_t out_off,
+                                                   double gamma, FinalizeArgs fa) {
+  const std::uint64_t s = lo + static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double smax = -DBL_MAX, smin = DBL_MAX;
+  unsigned long long bad = ~0ull;
+  if (s < hi) {
+    const std::uint32_t na = dm.n_actions;
+    const std::uint64_t no = dm.t_outcomes;
+    T best = T(0);
+    std::uint32_t besta = 0;
+    for (std::uint32_t a = 0; a < na; ++a) {
+      T acc = T(0);
+      const std::uint64_t base = (s * na + a) * no;
+      for (std::uint64_t w = 0; w < no; ++w)
+        acc += static_cast<T>(dm.t_prob[base + w] *
+                              (dm.t_reward[base + w] + gamma * static_cast<double>(V[dm.t_next[base + w]])));
+      if (qout) qout[(s - lo) * na + a] = acc;
+      if (a == 0 || acc > best) {
+        best = acc;
+        besta = a;
+      }
+    }
+    if (vout) vout[s - out_off] = best;
+    if (act) act[s - out_off] = besta;
+    state_stat<T>(fa, s, best, V, smax, smin, bad);
+  }
+  reduce_stats(smax, smin, bad, fa.stats);
+}
+
+// ---------------------------------------------------------------------------
+// Finalize over action chunks (B: chunk = order_a with a within-chunk
+// argmax; C: chunk = one order): first maximum in action order, then the
+// fused convergence statistic.
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_finalize(const T* __restrict__ part_v,
+                                                  const std::uint8_t* __restrict__ part_a,
+                                                  int n_chunks, int chunk_width,
+                                                  const T* __restrict__ V, T* __restrict__ vout,
+                                                  std::uint32_t* __restrict__ act, std::uint64_t lo,
+                                                  std::uint64_t hi, std::uint64_t out_off,
+                                                  FinalizeArgs fa) {
+  const std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const std::uint64_t nr = hi - lo;
+  double smax = -DBL_MAX, smin = DBL_MAX;
+  unsigned long long bad = ~0ull;
+  if (i < nr) {
+    const std::uint64_t s = lo + i;
+    T best = part_v[i];
+    std::uint32_t arg = part_a ? part_a[i] : 0;
+    for (int c = 1; c < n_chunks; ++c) {
+      const T v = part_v[static_cast<std::uint64_t>(c) * nr + i];
+      if (v > best) {
+        best = v;
+        arg = static_cast<std::uint32_t>(c) * chunk_width +
+              (part_a ? part_a[static_cast<std::uint64_t>(c) * nr + i] : 0);
+      }
+    }
+    if (vout) vout[s - out_off] = best;
+    if (act) act[s - out_off] = arg;
+    state_stat<T>(fa, s, best, V, smax, smin, bad);
+  }
+  reduce_stats(smax, smin, bad, fa.stats);
+}
+
+// Statistic over explicit vectors (pvi_check_convergence).
+template <typename T>
+__global__ void __launch_bounds__(256) k_stats(const T* __restrict__ vnew, const T* __restrict__ vprev,
+                                               std::uint64_t n, FinalizeArgs fa) {
+  const std::uint64_t s = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double smax = -DBL_MAX, smin = DBL_MAX;
+  unsigned long long bad = ~0ull;
+  if (s < n) state_stat<T>(fa, s, vnew[s], vprev, smax, smin, bad);
+  reduce_stats(smax, smin, bad, fa.stats);
+}
+
+// ---------------------------------------------------------------------------
+// K4: ScenarioB::initial_value (scenario_b.cpp:178-192), one thread per state.
+__global__ void __launch_bounds__(256) k_initial_b(DevModel dm, double* __restrict__ out,
+                                                   std::uint64_t n) {
+  const std::uint64_t s = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int m = dm.b_m;
+  int st[kMaxDigits];
+  decode(dm, s, st);
+  int ia = 0, ib = 0;
+  for (int i = 0; i < m; ++i) ia += st[i];
+  for (int i = m; i < 2 * m; ++i) ib += st[i];
+  const int dn = dm.b_dn;
+  double expected = 0.0;
+  for (int ha = 0; ha <= ia; ++ha)
+    for (int hb = 0; hb <= ib; ++hb) {
+      double p;
+      if (ha < ia)
+        p = hb < ib ? dm.b_pmf_a[ha] * dm.b_pmf_b[hb] : dm.b_pz[ib * dn + ha] * dm.b_sf_b[ib];
+      else
+        p = hb < ib ? dm.b_sf_a[ia] * dm.b_pmf_b[hb] : (1.0 - dm.b_pz_cum[ib * dn + ia]) * dm.b_sf_b[ib];
+      expected += p * (dm.b_cra * ha + dm.b_crb * hb);
+    }
+  out[s] = expected;
+}
+
+template <typename T>
+__global__ void k_cast_from_f64(const double* __restrict__ in, T* __restrict__ out, std::uint64_t n) {
+  const std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = static_cast<T>(in[i]);
+}
+
+template <typename T>
+__global__ void k_widen_to_f64(const T* __restrict__ in, double* __restrict__ out, std::uint64_t n) {
+  const std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = static_cast<double>(in[i]);
+}
+
+__global__ void k_init_stats(SweepStats* st) {
+  st->max_key = 0ull;
+  st->min_key = ~0ull;
+  st->first_bad = ~0ull;
+  st->pad = 0;
+}
+
+inline unsigned grid_for(std::uint64_t n, unsigned block) {
+  return static_cast<unsigned>((n + block - 1) / block);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Launchers
+
+template <typename T>
+void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
+                  Scratch& scratch, cudaStream_t stream) {
+  const std::uint64_t lo = a.lo, hi = a.hi, nr = hi - lo;
+  if (nr == 0) return;
+  FinalizeArgs fa = a.fa;
+  if (fa.stats) k_init_stats<<<1, 1, 0, stream>>>(fa.stats);
+  switch (model.scenario) {
+    case PVI_SCENARIO_A: {
+      const unsigned block = 256;
+      const std::size_t sm = (dm.a_dmax + 1) * sizeof(double);
+      const int na = static_cast<int>(dm.n_actions);
+      if (na <= 16)
+        k_sweep_a<T, 16><<<grid_for(nr, block), block, sm, stream>>>(dm, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
+      else if (na <= 32)
+        k_sweep_a<T, 32><<<grid_for(nr, block), block, sm, stream>>>(dm, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
+      else if (na <= 64)
+        k_sweep_a<T, 64><<<grid_for(nr, block), block, sm, stream>>>(dm, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
+      else
+        fail(PVI_ERR_PARAMETER, "scenario a: max_order > 63 is not supported by the device kernel");
+      break;
+    }
+    case PVI_TABULAR: {
+      const unsigned block = 256;
+      k_sweep_tab<T><<<grid_for(nr, block), block, 0, stream>>>(dm, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
+      break;
+    }
+    case PVI_SCENARIO_B: {
+      const int tile = dm.b_tile;
+      const std::uint64_t t0 = lo / tile, t1 = (hi + tile - 1) / tile;
+      const unsigned block = static_cast<unsigned>((tile + 31) / 32 * 32);
+      if (block > 1024) fail(PVI_ERR_PARAMETER, "scenario b: order cap too large for the device tile");
+      const std::size_t sm = sizeof(double) * (2 * (dm.b_len_a + dm.b_len_b + 1) +
+                                               2 * static_cast<std::size_t>(dm.b_cap_b + 1) * dm.b_dn);
+      T* pv = a.want_values ? scratch.get<T>(0, static_cast<std::size_t>(dm.b_na) * nr, stream) : nullptr;
+      std::uint8_t* pa = a.want_values ? scratch.get<std::uint8_t>(1, static_cast<std::size_t>(dm.b_na) * nr, stream) : nullptr;
+      const dim3 grid(static_cast<unsigned>(t1 - t0), static_cast<unsigned>(dm.b_na));
+      static bool attr_set[2] = {false, false};
+      (void)attr_set;
+      cudaFuncSetAttribute(k_sweep_b<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_sweep_b<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (dm.b_nb <= 16)
+        k_sweep_b<T, 16><<<grid, block, sm, stream>>>(dm, a.v, pv, pa, a.qout, lo, hi, t0, a.gamma);
+      else if (dm.b_nb <= 32)
+        k_sweep_b<T, 32><<<grid, block, sm, stream>>>(dm, a.v, pv, pa, a.qout, lo, hi, t0, a.gamma);
+      else
+        fail(PVI_ERR_PARAMETER, "scenario b: max_order_b > 31 is not supported by the device kernel");
+      PVI_CUDA(cudaGetLastError());
+      if (a.want_values)
+        k_finalize<T><<<grid_for(nr, 256), 256, 0, stream>>>(pv, pa, dm.b_na, dm.b_nb, a.v, a.vout, a.act, lo, hi, a.out_off, fa);
+      break;
+    }
+    case PVI_SCENARIO_C: {
+      const int na = static_cast<int>(dm.n_actions);
+      T* pv = a.want_values ? scratch.get<T>(0, static_cast<std::size_t>(na) * nr, stream) : nullptr;
+      const int dn = dm.c_dmax + 1;
+      const unsigned block = 128;
+      const dim3 grid(grid_for(nr, block), static_cast<unsigned>(na));
+      const std::size_t sm = sizeof(double) * (dm.c_m * dm.c_max_order + dm.c_dmax + 1 + dm.c_max_order + 1);
+      bool done = false;
+#define PVI_C_CASE(MM)                                                                      \
+  if (!done && dm.c_m == MM && dn == 21) {                                                  \
+    cudaFuncSetAttribute(k_sweep_c<T, MM, 21>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         100 * 1024);                                                       \
+    k_sweep_c<T, MM, 21><<<grid, block, sm, stream>>>(dm, a.v, pv, a.qout, lo, hi, a.gamma); \
+    done = true;                                                                            \
+  }
+      PVI_C_CASE(2)
+      PVI_C_CASE(3)
+      PVI_C_CASE(4)
+      PVI_C_CASE(5)
+      PVI_C_CASE(6)
+      PVI_C_CASE(7)
+      PVI_C_CASE(8)
+#undef PVI_C_CASE
+      if (!done) {
+        double* inner = scratch.get<double>(2, static_cast<std::size_t>(na) * dn * nr, stream);
+        const dim3 g3(grid_for(nr, block), static_cast<unsigned>(na), static_cast<unsigned>(dn));
+        k_sweep_c_generic<T><<<g3, block, 0, stream>>>(dm, a.v, inner, lo, hi, a.gamma);
+        PVI_CUDA(cudaGetLastError());
+        const dim3 g2(grid_for(nr, 256), static_cast<unsigned>(na));
+        k_reduce_c<T><<<g2, 256, 0, stream>>>(dm, inner, pv, a.qout, lo, hi);
+      }
+      PVI_CUDA(cudaGetLastError());
+      if (a.want_values)
+        k_finalize<T><<<grid_for(nr, 256), 256, 0, stream>>>(pv, nullptr, na, 1, a.v, a.vout, a.act, lo, hi, a.out_off, fa);
+      break;
+    }
+    default:
+      fail(PVI_ERR_PARAMETER, "unknown scenario");
+  }
+  PVI_CUDA(cudaGetLastError());
+}
+
+template <typename T>
+void launch_stats(const T* vnew, const T* vprev, std::uint64_t n, const FinalizeArgs& fa,
+                  cudaStream_t stream) {
+  k_init_stats<<<1, 1, 0, stream>>>(fa.stats);
+  k_stats<T><<<grid_for(n, 256), 256, 0, stream>>>(vnew, vprev, n, fa);
+  PVI_CUDA(cudaGetLastError());
+}
+
+void launch_initial_b(const DevModel& dm, double* out, std::uint64_t n, cudaStream_t stream) {
+  k_initial_b<<<grid_for(n, 256), 256, 0, stream>>>(dm, out, n);
+  PVI_CUDA(cudaGetLastError());
+}
+
+template <typename T>
+void launch_cast_from_f64(const double* in, T* out, std::uint64_t n, cudaStream_t stream) {
+  k_cast_from_f64<T><<<grid_for(n, 256), 256, 0, stream>>>(in, out, n);
+  PVI_CUDA(cudaGetLastError());
+}
+
+template <typename T>
+void launch_widen(const T* in, double* out, std::uint64_t n, cudaStream_t stream) {
+  k_widen_to_f64<T><<<grid_for(n, 256), 256, 0, stream>>>(in, out, n);
+  PVI_CUDA(cudaGetLastError());
+}
+
+template void launch_sweep<double>(const Model&, const DevModel&, const SweepArgs<double>&, Scratch&, cudaStream_t);
+template void launch_sweep<float>(const Model&, const DevModel&, const SweepArgs<float>&, Scratch&, cudaStream_t);
+template void launch_stats<double>(const double*, const double*, std::uint64_t, const FinalizeArgs&, cudaStream_t);
+template void launch_stats<float>(const float*, const float*, std::uint64_t, const FinalizeArgs&, cudaStream_t);
+template void launch_cast_from_f64<double>(const double*, double*, std::uint64_t, cudaStream_t);
+template void launch_cast_from_f64<float>(const double*, float*, std::uint64_t, cudaStream_t);
+template void launch_widen<double>(const double*, double*, std::uint64_t, cudaStream_t);
+template void launch_widen<float>(const float*, double*, std::uint64_t, cudaStream_t);
+
+}  // namespace pvi_b200

@@ -1,0 +1,75 @@
+// Launch interface of the value-iteration kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+#include "model.hpp"
+
+namespace pvi_b200 {
+
+// Arguments of the fused finalize / convergence reduction.
+struct FinalizeArgs {
+  int test = -1;                 // -1: only the non-finite scan
+  int n_hist = 0;                // previous vectors available in hist (periodic span: >= 7)
+  const void* hist[8] = {};      // device pointers, oldest..newest (newest = V_prev)
+  double gamma = 0.0;
+  SweepStats* stats = nullptr;   // device; nullptr disables the reduction
+};
+
+template <typename T>
+struct SweepArgs {
+  const T* v = nullptr;          // V_prev, |S| entries (device)
+  T* vout = nullptr;             // indexed by s - out_off
+  std::uint32_t* act = nullptr;  // indexed by s - out_off
+  T* qout = nullptr;             // (hi-lo) x |A| Q values, or nullptr
+  std::uint64_t lo = 0, hi = 0, out_off = 0;
+  double gamma = 0.0;
+  bool want_values = true;       // false: Q rows only (B/C skip the partial buffers)
+  FinalizeArgs fa;
+};
+
+// Grow-only device scratch buffers, keyed by slot.
+struct Scratch {
+  std::vector<void*> ptr;
+  std::vector<std::size_t> bytes;
+  template <typename U>
+  U* get(int slot, std::size_t count, cudaStream_t stream) {
+    if (static_cast<int>(ptr.size()) <= slot) {
+      ptr.resize(slot + 1, nullptr);
+      bytes.resize(slot + 1, 0);
+    }
+    const std::size_t need = count * sizeof(U);
+    if (bytes[slot] < need) {
+      if (ptr[slot]) {
+        cudaStreamSynchronize(stream);
+        cudaFree(ptr[slot]);
+      }
+      ptr[slot] = nullptr;
+      PVI_CUDA(cudaMalloc(&ptr[slot], need));
+      bytes[slot] = need;
+    }
+    return static_cast<U*>(ptr[slot]);
+  }
+  ~Scratch() {
+    for (void* p : ptr)
+      if (p) cudaFree(p);
+  }
+};
+
+template <typename T>
+void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a, Scratch& scratch,
+                  cudaStream_t stream);
+template <typename T>
+void launch_stats(const T* vnew, const T* vprev, std::uint64_t n, const FinalizeArgs& fa,
+                  cudaStream_t stream);
+void launch_initial_b(const DevModel& dm, double* out, std::uint64_t n, cudaStream_t stream);
+template <typename T>
+void launch_cast_from_f64(const double* in, T* out, std::uint64_t n, cudaStream_t stream);
+template <typename T>
+void launch_widen(const T* in, double* out, std::uint64_t n, cudaStream_t stream);
+
+}  // namespace pvi_b200
