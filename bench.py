@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark: Bellman evaluations per second of the B200 value-iteration
+sweep (BASELINE.json metric), plus wall time to converge.
+
+Workload (N=1 and every N): one synchronous Jacobi sweep of the >16M-state
+scenario, Hendrix two-product b/m3/exp1 (16,777,216 states x 256 actions,
+2.372e12 reference backup terms per sweep), f64, with the fused convergence
+reduction.  A "step" is one full sweep over all states with V resident in
+HBM; at N>1 each rank sweeps its cost-weighted state shard and the shards
+are all-gathered over NCCL.  The sweep is the same at every N, so scaling
+is "strong".  The unit of work is one reference backup term
+(state, action, outcome) exactly as the reference enumerates it
+(SURVEY §8d), so evals/s is comparable with the CPU reference arm.
+
+  python bench.py [--gpus N --steps K --warmup W]            # our arm
+  python bench.py --impl reference [--steps K --warmup W]     # reference CPU arm
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_TERM = {"f64": 8, "f32": 4}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="b/m3/exp1")
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--no-solve", action="store_true", help="skip the time-to-converge solve")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of reference CPU work")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+
+def init_dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# work model (SURVEY §8d closed forms, per state)
+
+
+def state_terms(model, lo: int, hi: int) -> float:
+    """Reference backup terms of states [lo, hi)."""
+    sc = model.scenario()
+    n = hi - lo
+    if sc != "b":
+        return model.terms_per_sweep() * n / model.state_count()
+    m = (model.state_arity()) // 2
+    na = model.info.max_order_a + 1
+    nb = model.info.max_order_b + 1
+    s = np.arange(lo, hi, dtype=np.int64)
+    ia = np.zeros(n, np.int64)
+    ib = np.zeros(n, np.int64)
+    rem = s.copy()
+    radices = [na] * m + [nb] * m
+    weights = [int(np.prod(radices[i + 1:])) for i in range(2 * m)]
+    for i in range(2 * m):
+        d = rem // weights[i]
+        rem = rem % weights[i]
+        if i < m:
+            ia += d
+        else:
+            ib += d
+    return float(np.sum((ia + 1) * (ib + 1), dtype=np.float64)) * model.action_count()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md clocks line)
+
+
+class Clocks:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref = the unmodified reference, compiled here)
+
+
+def cpu_sample_plan(model, budget_s: float, calib_rate: float):
+    """Contiguous state ranges spread over the space, sized to ~budget_s of CPU work."""
+    n = model.state_count()
+    if model.scenario() == "b":
+        group = int(model.info.max_order_b + 1) ** ((model.state_arity()) // 2)
+    else:
+        group = max(1, n // 4096)
+    n_groups = max(1, n // group)
+    per_group = model.terms_per_sweep() / n_groups  # mean group size
+    want = max(1, int(budget_s * calib_rate / max(per_group, 1.0)))
+    want = min(want, n_groups)
+    stride = max(1, n_groups // want)
+    return [(g * group, min(n, (g + 1) * group)) for g in range(0, n_groups, stride)][:want]
+
+
+def run_cpu_reference(model, preset: str, precision: str, budget_s: float, V: np.ndarray,
+                      offset: int = 0):
+    """Time the reference's bellman_backup_batch (threads = all host cores) on a bounded
+    sample; returns (terms/s, seconds, terms, description, threads)."""
+    from oracle import refbind as R
+    threads = os.cpu_count() or 1
+    # calibrate with one small range
+    plan = cpu_sample_plan(model, budget_s, 3e9)
+    lo, hi = plan[len(plan) // 2]
+    _, _, secs = R.backup_range(preset, V, lo, hi, f32=precision == "f32", threads=threads)
+    rate = state_terms(model, lo, hi) / max(secs, 1e-6)
+    plan = cpu_sample_plan(model, budget_s, rate)
+    if offset:
+        plan = plan[offset % len(plan):] + plan[:offset % len(plan)]
+    terms = 0.0
+    total = 0.0
+    used = 0
+    for lo, hi in plan:
+        _, _, secs = R.backup_range(preset, V, lo, hi, f32=precision == "f32", threads=threads)
+        total += secs
+        terms += state_terms(model, lo, hi)
+        used += hi - lo
+        if total > budget_s * 1.5:
+            break
+    desc = (f"reference bellman_backup_batch over {used} of {model.state_count()} states "
+            f"({terms:.3e} terms) in contiguous tiles spread across the space")
+    return terms / total, total, terms, desc, threads
+
+
+# ---------------------------------------------------------------------------
+# arms
+
+
+def reference_arm(args, world, rank):
+    import paper_2303_10672_b200 as P
+    from oracle import refbind as R
+    if rank != 0:
+        return
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libpvi_ref.so was not built (needs /root/reference)"}))
+        return
+    model = P.make_preset(args.workload)
+    V = R.initial_values(args.workload)
+    step_budget = 4.0
+    rates = []
+    times = []
+    for k in range(args.warmup + args.steps):
+        rate, secs, terms, desc, threads = run_cpu_reference(model, args.workload, args.precision,
+                                                             step_budget, V, offset=k)
+        if k >= args.warmup:
+            rates.append(rate)
+            times.append(secs)
+    value = float(sum(r * t for r, t in zip(rates, times)) / sum(times))
+    line = {
+        "metric": "bellman_evals_per_sec", "value": value, "unit": "evals/s",
+        "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * model.terms_per_sweep() / value,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": args.precision, "data": "synthetic (deterministic preset tables; V = initial value)",
+        "config": workload_config(model, args, world),
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference",
+                         "sample": desc + f"; {step_budget:.0f} s per step"},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+
+
+def workload_config(model, args, world):
+    return {"workload": f"{args.workload} Bellman sweep ({model.state_count():,} states, "
+                        f"{model.action_count()} actions, {args.precision})",
+            "preset": args.workload, "states": model.state_count(),
+            "actions": model.action_count(), "terms_per_sweep": model.terms_per_sweep(),
+            "l2_flush": "256 MiB write between timed steps (V is 128 MiB, partials 2.4 GB)",
+            "parallelism": f"state-shards x{world} (cost-weighted, NCCL all-gather)"}
+
+
+def ours_arm(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+    import paper_2303_10672_b200 as P
+    from paper_2303_10672_b200.sharded import ShardedValueIteration
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    model = P.make_preset(args.workload)
+    n = model.state_count()
+    cfg = P.ViConfig(precision=args.precision)
+    solver = ShardedValueIteration(model, cfg)
+    dt = torch.float32 if args.precision == "f32" else torch.float64
+    v0 = model.initial_values()
+    vprev = torch.as_tensor(v0, device="cuda").to(dt)
+    vnext = torch.empty_like(vprev)
+    stats = torch.empty(4, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    test = model.default_convergence_test()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        solver.step(vprev, vnext, stats, test)
+    barrier()
+
+    clocks = Clocks(local)
+    clocks.start()
+    P.profile_enable(True)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    for k in range(args.steps):
+        flush.zero_()
+        starts[k].record()
+        solver.step(vprev, vnext, stats, test)
+        ends[k].record()
+    barrier()
+    kernel_ms, k_launches, all_launches = P.profile_read()
+    P.profile_enable(False)
+    clk = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+    total_ms = float(total_ms.item())
+    terms = model.terms_per_sweep()
+    value = terms * args.steps / (total_ms * 1e-3)
+
+    # roofline of the dominant kernel (K1 backup) on this rank
+    shard_terms = state_terms(model, solver.lo, solver.hi)
+    bpt = BYTES_PER_TERM[args.precision]
+    achieved_gbs = bpt * shard_terms * k_launches / (kernel_ms * 1e-3) / 1e9 if kernel_ms else 0.0
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
+            tj = json.load(f)
+            if tj.get("workload") == args.workload and tj.get("precision") == args.precision:
+                traffic = tj.get("dram_bytes_per_launch")
+    except OSError:
+        pass
+    roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+                "frac": achieved_gbs / peak, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)" if peaks else
+                "fallback 6650 GB/s (B200_PROFILING.md)",
+                "algorithmic_bytes": f"{bpt} B (one V[next] gather) per reference term; "
+                                     f"{shard_terms:.4e} terms per launch",
+                "kernel_ms_per_launch": kernel_ms / max(k_launches, 1),
+                "kernel_share_of_step": (kernel_ms / max(sum(step_ms), 1e-9)),
+                "fp64_pipe_note": "V (128 MiB) is L2/L1-resident across the 141k reuses per "
+                                  "element, so the gather roofline is an upper bound on bytes, "
+                                  "not the binding limit; see DESIGN.md"}
+
+    line = {"metric": "bellman_evals_per_sec", "value": value, "unit": "evals/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": args.precision,
+            "data": "synthetic (deterministic preset tables; V = initial value)",
+            "config": workload_config(model, args, world), "clocks": clk,
+            "gpu_launches": int(all_launches), "roofline": roofline}
+
+    # e2e: the reference-facing call with HOST buffers, copies inside the timing
+    if not args.no_e2e:
+        vh = np.ascontiguousarray(v0.astype(np.float32 if args.precision == "f32" else np.float64))
+        P.bellman_backup_batch(model, vh, solver.lo, solver.hi, precision=args.precision)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            P.bellman_backup_batch(model, vh, solver.lo, solver.hi, precision=args.precision)
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        line["e2e"] = {"value": terms * args.steps / float(el.item()), "unit": "evals/s",
+                       "h2d_bytes_per_step": int(vh.nbytes),
+                       "d2h_bytes_per_step": int((solver.hi - solver.lo) * (vh.itemsize + 4)),
+                       "call": "pvi_vi_backup (bellman_backup_batch) over the rank's shard, "
+                               "host V in, host V' + argmax out"}
+
+    # wall time to converge (the second half of the BASELINE metric)
+    if not args.no_solve:
+        barrier()
+        res = solver.solve()
+        line["solve"] = {"preset": args.workload, "iterations": res.iterations,
+                         "converged": res.converged, "wall_seconds": res.wall_seconds,
+                         "sweep_seconds": res.sweep_seconds,
+                         "checkpoints": "off (the reference cmd_solve writes one per sweep)"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import refbind as R
+        if R.available():
+            rate, secs, sterms, desc, threads = run_cpu_reference(model, args.workload,
+                                                                  args.precision,
+                                                                  args.cpu_budget, v0)
+            line["cpu_baseline"] = {"value": rate, "unit": "evals/s", "cores": threads,
+                                    "kind": "reference", "sample": desc,
+                                    "seconds": secs}
+            if "solve" in line:
+                line["cpu_baseline"]["extrapolated_solve_seconds"] = (
+                    line["solve"]["iterations"] + 1) * terms / rate
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    world, rank, local = init_dist()
+    if args.impl == "reference":
+        reference_arm(args, world, rank)
+    else:
+        ours_arm(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

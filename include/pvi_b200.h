@@ -294,6 +294,15 @@ int pvi_sim_evaluate(const pvi_model* m, const pvi_policy* policies, uint32_t n_
 int pvi_philox_block(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 int pvi_rollout_draws(uint64_t base_seed, uint64_t rollout, uint32_t day, int n, uint64_t* out);
 
+/* ---- measurement hook (bench.py) ----------------------------------------
+ * While enabled, every launch of a main backup kernel (K1) is bracketed by
+ * CUDA events on the stream it runs on, and every kernel the VI path
+ * launches is counted.  Read returns the summed K1 milliseconds, the K1
+ * launch count and the total launch count since the last enable/read, and
+ * resets them (it synchronises on the recorded events). */
+int pvi_profile_enable(int on);
+int pvi_profile_read(double* kernel_ms, uint64_t* kernel_launches, uint64_t* all_launches);
+
 /* ---- checkpoints (checkpoint.hpp:24-35) --------------------------------- */
 int pvi_checkpoint_save(const char* path, const double* values, uint64_t count, uint64_t iteration,
                         const uint8_t fingerprint[32], char* err, size_t errlen);

@@ -136,6 +136,8 @@ SIGNATURES = {
     "pvi_checkpoint_save": (C.c_int, [C.c_char_p, _vp, C.c_uint64, C.c_uint64, _vp] + _E),
     "pvi_checkpoint_load": (C.c_int, [C.c_char_p, _vp, _vp, C.c_uint64, _vp, _vp, _vp] + _E),
     "pvi_sha256": (C.c_int, [_vp, C.c_size_t, _vp]),
+    "pvi_profile_enable": (C.c_int, [C.c_int]),
+    "pvi_profile_read": (C.c_int, [_vp, _vp, _vp]),
 }
 
 _lib = None

@@ -367,6 +367,14 @@ int pvi_checkpoint_load(const char* path, const uint8_t* expected_fingerprint, d
   });
 }
 
+int pvi_profile_enable(int on) {
+  return guarded(nullptr, 0, nullptr, [&] { profile_enable(on != 0); });
+}
+
+int pvi_profile_read(double* kernel_ms, uint64_t* kernel_launches, uint64_t* all_launches) {
+  return guarded(nullptr, 0, nullptr, [&] { profile_read(kernel_ms, kernel_launches, all_launches); });
+}
+
 int pvi_sha256(const void* data, size_t len, uint8_t out[32]) {
   return guarded(nullptr, 0, nullptr, [&] { sha256(data, len, out); });
 }

@@ -23,6 +23,8 @@ void vi_sweep_device(const Model& m, int precision, double gamma, const void* vp
                      const void* const* hist, int n_hist, int want_stats, double* stats,
                      void* stream);
 void partition(const Model& m, int parts, std::uint64_t* bounds);
+void profile_enable(bool on);
+void profile_read(double* ms, std::uint64_t* main_launches, std::uint64_t* all_launches);
 void initial_values_host(const Model& m, double* out);
 
 void save_checkpoint(const std::string& path, const double* values, std::uint64_t count,

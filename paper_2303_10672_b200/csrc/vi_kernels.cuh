@@ -66,6 +66,8 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
 template <typename T>
 void launch_stats(const T* vnew, const T* vprev, std::uint64_t n, const FinalizeArgs& fa,
                   cudaStream_t stream);
+void profile_enable(bool on);
+void profile_read(double* ms, std::uint64_t* main_launches, std::uint64_t* all_launches);
 void launch_initial_b(const DevModel& dm, double* out, std::uint64_t n, cudaStream_t stream);
 template <typename T>
 void launch_cast_from_f64(const double* in, T* out, std::uint64_t n, cudaStream_t stream);

@@ -390,8 +390,9 @@ def run_value_iteration(model: Model, config: Optional[ViConfig] = None,
                         resume: Optional[Checkpoint] = None) -> ViResult:
     config = config or ViConfig()
     n = model.state_count()
-    values = np.zeros(n, np.float64)
-    policy = np.zeros(n, np.uint32)
+    fits = n <= config.max_states  # else the C side raises CapacityError first
+    values = np.zeros(n, np.float64) if fits else None
+    policy = np.zeros(n, np.uint32) if fits else None
     st = L.ViStats()
     ev = C.c_uint64()
     err = _err_buf()
@@ -415,6 +416,39 @@ def run_value_iteration(model: Model, config: Optional[ViConfig] = None,
 
 def _dtype(precision: str):
     return np.float32 if precision == "f32" else np.float64
+
+
+def sweep_device(model: Model, precision: str, gamma: float, vprev_ptr: int, vnext_ptr: int,
+                 actions_ptr: Optional[int], lo: int, hi: int, test: Optional[str] = None,
+                 hist_ptrs: Sequence[int] = (), stats_ptr: Optional[int] = None,
+                 stream_ptr: Optional[int] = None):
+    """One device-resident sweep of states [lo, hi) (pvi_vi_sweep_device).
+
+    Pointers are raw device addresses (e.g. torch.Tensor.data_ptr()); the
+    launch is asynchronous on `stream_ptr` (a cudaStream_t, e.g.
+    torch.cuda.current_stream().cuda_stream)."""
+    t = -1 if test is None else _TEST_NAMES[test]
+    hist = (C.c_void_p * max(1, len(hist_ptrs)))(*[int(p) for p in hist_ptrs])
+    err = _err_buf()
+    _raise(L.load().pvi_vi_sweep_device(model.handle, int(precision == "f32"), gamma,
+                                        C.c_void_p(vprev_ptr), C.c_void_p(vnext_ptr),
+                                        None if actions_ptr is None else C.c_void_p(actions_ptr),
+                                        lo, hi, t, hist, len(hist_ptrs),
+                                        int(stats_ptr is not None),
+                                        None if stats_ptr is None else C.c_void_p(stats_ptr),
+                                        None if stream_ptr is None else C.c_void_p(stream_ptr),
+                                        err, len(err)), err)
+
+
+def profile_enable(on: bool = True):
+    _raise(L.load().pvi_profile_enable(int(on)), None)
+
+
+def profile_read():
+    """(K1 milliseconds, K1 launches, all VI-path kernel launches) since enable/read."""
+    ms, k, a = C.c_double(), C.c_uint64(), C.c_uint64()
+    _raise(L.load().pvi_profile_read(C.byref(ms), C.byref(k), C.byref(a)), None)
+    return ms.value, k.value, a.value
 
 
 def bellman_backup_batch(model: Model, values, lo: int, hi: int, gamma: Optional[float] = None,

@@ -1,0 +1,204 @@
+"""Multi-GPU value iteration: one process per GPU over torch.distributed.
+
+The state space is split into contiguous, cost-weighted shards
+(pvi_partition; Scenario B's per-state work is (I_a+1)(I_b+1), so equal
+counts would leave the 8-GPU load at 1.30x the mean).  Every
+rank holds a full replica of V_prev, backs up its own slice, and the slices
+are exchanged with one NCCL all-gather per sweep; the convergence
+statistic of each slice (max, -min, first non-finite state) is combined with
+one 4-double MAX all-reduce.  Max and min are exact, so the convergence
+decision, the iteration count and the value vector are identical to the
+single-GPU run (and to the reference).
+
+The per-slice sweep is injectable so the host logic (partition, exchange,
+reduction, history window, convergence) runs under `gloo` on CPU in tests;
+the default sweep is the device kernel through pvi_vi_sweep_device.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+from typing import Callable, List, Optional
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import pvi as P
+
+NEG_INF = -1.7976931348623157e308
+
+SweepFn = Callable[..., None]
+
+
+def evaluate_test(test: int, hi: float, lo: float, epsilon: float, iteration: int) -> bool:
+    """check_convergence's decision from the reduced statistic (vi.hpp:107-158)."""
+    if test == P.VALUE_SPAN:
+        return max(0.0, hi) < epsilon
+    if test == P.CHANGE_SPAN:
+        return hi - lo < epsilon
+    if iteration < 7:
+        return False
+    return hi - lo <= 2.0 * epsilon * min(abs(hi), abs(lo))
+
+
+def device_sweep(model: P.Model, precision: str, gamma: float):
+    def sweep(vprev: torch.Tensor, vnext: torch.Tensor, actions: Optional[torch.Tensor],
+              lo: int, hi: int, test: Optional[int], hist: List[torch.Tensor],
+              stats: Optional[torch.Tensor]):
+        names = {0: "value_span", 1: "change_span", 2: "periodic_span"}
+        P.sweep_device(model, precision, gamma, vprev.data_ptr(), vnext.data_ptr(),
+                       None if actions is None else actions.data_ptr(), lo, hi,
+                       None if test is None else names[test], [h.data_ptr() for h in hist],
+                       None if stats is None else stats.data_ptr(),
+                       torch.cuda.current_stream().cuda_stream)
+    return sweep
+
+
+@dataclass
+class ShardedResult:
+    values: np.ndarray
+    policy: np.ndarray
+    iterations: int
+    converged: bool
+    wall_seconds: float
+    sweep_seconds: float
+    bounds: list
+
+
+class ShardedValueIteration:
+    """run_value_iteration (vi.hpp:162-291) over `world` ranks."""
+
+    def __init__(self, model: P.Model, config: Optional[P.ViConfig] = None,
+                 device: Optional[torch.device] = None, sweep: Optional[SweepFn] = None,
+                 group=None):
+        self.model = model
+        self.cfg = config or P.ViConfig()
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.device = device or (torch.device("cuda", torch.cuda.current_device())
+                                 if torch.cuda.is_available() else torch.device("cpu"))
+        self.n = model.state_count()
+        self.bounds = [int(b) for b in model.partition(self.world)]
+        self.lo, self.hi = self.bounds[self.rank], self.bounds[self.rank + 1]
+        self.maxlen = max(self.bounds[r + 1] - self.bounds[r] for r in range(self.world))
+        self.dtype = torch.float32 if self.cfg.precision == "f32" else torch.float64
+        self.gamma = self.cfg.gamma if self.cfg.gamma is not None else model.discount()
+        self.test = (model.default_convergence_test() if self.cfg.convergence_test is None
+                     else P._TEST_NAMES[self.cfg.convergence_test])
+        self.sweep = sweep or device_sweep(model, self.cfg.precision, self.gamma)
+        self.hist_cap = 8 if self.test == P.PERIODIC_SPAN else 2
+        self._send = torch.empty(self.maxlen, dtype=self.dtype, device=self.device)
+        self._recv = torch.empty(self.maxlen * self.world, dtype=self.dtype, device=self.device)
+
+    # -- collectives ---------------------------------------------------------
+    def exchange(self, v: torch.Tensor, send=None, recv=None):
+        """All-gather every rank's slice of `v` into every replica."""
+        if self.world == 1:
+            return
+        send = self._send if send is None else send
+        recv = self._recv if recv is None else recv
+        ln = self.hi - self.lo
+        send[:ln].copy_(v[self.lo:self.hi])
+        dist.all_gather_into_tensor(recv, send, group=self.group)
+        for r in range(self.world):
+            a, b = self.bounds[r], self.bounds[r + 1]
+            if r != self.rank and b > a:
+                v[a:b].copy_(recv[r * self.maxlen:r * self.maxlen + (b - a)])
+
+    def reduce_stats(self, stats: torch.Tensor):
+        if self.world > 1:
+            dist.all_reduce(stats, op=dist.ReduceOp.MAX, group=self.group)
+
+    # -- one sweep (bench step) ---------------------------------------------
+    def step(self, vprev: torch.Tensor, vnext: torch.Tensor, stats: Optional[torch.Tensor] = None,
+             test: Optional[int] = None):
+        self.sweep(vprev, vnext, None, self.lo, self.hi, test, [], stats)
+        if stats is not None:
+            self.reduce_stats(stats)
+        self.exchange(vnext)
+
+    # -- full solve ----------------------------------------------------------
+    def solve(self, resume: Optional[P.Checkpoint] = None) -> ShardedResult:
+        t0 = time.perf_counter()
+        cfg, n = self.cfg, self.n
+        if n > cfg.max_states:
+            raise P.CapacityError(f"value iteration requires {n} states, exceeding the "
+                                  f"configured capacity of {cfg.max_states}", n)
+        if not cfg.epsilon > 0:
+            raise P.ParameterError("value iteration: epsilon must be > 0")
+        ring = [torch.empty(n, dtype=self.dtype, device=self.device) for _ in range(self.hist_cap)]
+        if resume is not None:
+            if resume.fingerprint != self.model.fingerprint():
+                raise P.FingerprintMismatch("resume checkpoint fingerprint does not match model")
+            v0 = resume.values
+            iteration = resume.iteration
+        else:
+            v0 = self._initial_values()
+            iteration = 0
+        ring[0].copy_(torch.as_tensor(v0, dtype=torch.float64).to(self.dtype))
+        order = [0]
+        stats = torch.empty(4, dtype=torch.float64, device=self.device)
+        sweep_s = 0.0
+        converged = False
+        start = iteration
+        ckpt = cfg.checkpoint_every > 0 and bool(cfg.checkpoint_path)
+        fp = self.model.fingerprint()
+        if ckpt and resume is None and self.rank == 0:
+            P.save_checkpoint(cfg.checkpoint_path, ring[0].double().cpu().numpy(), iteration, fp)
+        while True:
+            if cfg.fixed_iterations > 0:
+                if iteration >= cfg.fixed_iterations:
+                    converged = True
+                    break
+            elif iteration >= start + cfg.max_iterations:
+                break
+            iteration += 1
+            prev = order[-1]
+            if len(order) < self.hist_cap:
+                nxt = len(order)
+            else:
+                nxt = order.pop(0)
+            want = cfg.fixed_iterations == 0 and len(order) + 1 >= self.hist_cap
+            hist = [ring[k] for k in order] if (want and self.test == P.PERIODIC_SPAN) else []
+            ts = time.perf_counter()
+            self.sweep(ring[prev], ring[nxt], None, self.lo, self.hi,
+                       self.test if want else None, hist, stats)
+            self.reduce_stats(stats)
+            self.exchange(ring[nxt])
+            st = stats.cpu().numpy()  # the one host round trip per sweep
+            sweep_s += time.perf_counter() - ts
+            order.append(nxt)
+            if st[2] > NEG_INF:
+                bad = int(-st[2])
+                raise P.NumericDivergence(f"non-finite value for state {bad} at iteration "
+                                          f"{iteration}", iteration)
+            if want:
+                hi = st[0]
+                lo = 0.0 if self.test == P.VALUE_SPAN else -st[1]
+                converged = bool(evaluate_test(self.test, float(hi), float(lo), cfg.epsilon, iteration))
+            if ckpt and iteration % cfg.checkpoint_every == 0 and self.rank == 0:
+                P.save_checkpoint(cfg.checkpoint_path, ring[order[-1]].double().cpu().numpy(),
+                                  iteration, fp)
+            if converged:
+                break
+        vfinal = ring[order[-1]]
+        actions = torch.zeros(n, dtype=torch.int32, device=self.device)
+        self.sweep(vfinal, ring[order[0]] if len(order) > 1 else torch.empty_like(vfinal),
+                   actions, self.lo, self.hi, None, [], None)
+        self.exchange(actions, send=torch.empty(self.maxlen, dtype=torch.int32, device=self.device),
+                      recv=torch.empty(self.maxlen * self.world, dtype=torch.int32,
+                                       device=self.device))
+        values = vfinal.double().cpu().numpy()
+        policy = actions.cpu().numpy().astype(np.uint32)
+        return ShardedResult(values, policy, iteration, converged, time.perf_counter() - t0,
+                             sweep_s, self.bounds)
+
+    def _initial_values(self) -> np.ndarray:
+        if self.device.type == "cuda":
+            return self.model.initial_values()
+        from_fn = getattr(self.sweep, "initial_values", None)
+        if from_fn is None:
+            raise P.DeviceError("initial values need the device (or a sweep providing them)")
+        return from_fn()
