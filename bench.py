@@ -262,6 +262,9 @@ def ours_arm(args, world, rank, local):
     stats = torch.empty(4, dtype=torch.float64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     test = model.default_convergence_test()
+    # the periodic-span statistic (Scenario C) reads the 7 previous vectors
+    hist = ([torch.empty_like(vprev).copy_(vprev) for _ in range(6)] + [vprev]
+            if test == P.PERIODIC_SPAN else [])
 
     def barrier():
         if world > 1:
@@ -269,7 +272,7 @@ def ours_arm(args, world, rank, local):
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        solver.step(vprev, vnext, stats, test)
+        solver.step(vprev, vnext, stats, test, hist)
     barrier()
 
     clocks = Clocks(local)
@@ -281,7 +284,7 @@ def ours_arm(args, world, rank, local):
     for k in range(args.steps):
         flush.zero_()
         starts[k].record()
-        solver.step(vprev, vnext, stats, test)
+        solver.step(vprev, vnext, stats, test, hist)
         ends[k].record()
     barrier()
     kernel_ms, k_launches, all_launches = P.profile_read()

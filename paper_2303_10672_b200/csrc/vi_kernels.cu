@@ -323,20 +323,33 @@ __global__ void __launch_bounds__(256) k_sweep_b(DevModel dm, const T* __restric
 // becomes an immediate load offset, and the per-term work is exactly one
 // L1-resident gather plus the reference's five f64 operations.  Same term
 // order and expression as k_sweep_b, hence the same bits.
+// Read-only gather that the compiler may not move or drop.
+__device__ __forceinline__ double ldg_keep(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ldg_keep(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
 template <int M, int NB>
 struct BGeo {
   static constexpr int pow(int b, int e) { return e == 0 ? 1 : b * pow(b, e - 1); }
   static constexpr int WB = pow(NB, M - 1);
 };
 
-template <typename T, int M, int NB>
-__global__ void __launch_bounds__(256, 2) k_sweep_b_geo(DevModel dm, const T* __restrict__ V,
+template <typename T, int M, int NB, int NCH>
+__global__ void __launch_bounds__(256, NCH == 1 ? 2 : 3) k_sweep_b_geo(DevModel dm, const T* __restrict__ V,
                                                         T* __restrict__ part_v,
                                                         std::uint8_t* __restrict__ part_a,
                                                         T* __restrict__ qout, std::uint64_t lo,
                                                         std::uint64_t hi, std::uint64_t tile0,
                                                         double gamma) {
   constexpr int WB = BGeo<M, NB>::WB;
+  constexpr int OBC = NB / NCH;  // order_b values per thread
   extern __shared__ double smem[];
   double* s_pmf_a = smem;
   double* s_pmf_b = s_pmf_a + dm.b_len_a;
@@ -353,7 +366,8 @@ __global__ void __launch_bounds__(256, 2) k_sweep_b_geo(DevModel dm, const T* __
   const std::uint64_t s =
       (tile0 + blockIdx.x) * static_cast<std::uint64_t>(dm.b_tile) + dm.b_lane_order[t];
   if (s < lo || s >= hi) return;
-  const int oa = blockIdx.y;
+  const int oa = blockIdx.y / NCH;
+  const int ob0 = (blockIdx.y % NCH) * OBC;
   // decode: digits 0..M-1 are product A (radix na), M..2M-1 product B (radix NB)
   int xa[M + 1], xb[M + 1];
   int ia = 0, ib = 0;
@@ -378,11 +392,11 @@ __global__ void __launch_bounds__(256, 2) k_sweep_b_geo(DevModel dm, const T* __
   for (int j = 1; j <= M - 1; ++j) wa_digit[j] = static_cast<std::uint32_t>(dm.weight[M - j]);
   const std::uint32_t oa_base = static_cast<std::uint32_t>(oa * dm.weight[0]);
   const double cva_oa = dm.b_cva * oa;
-  double cvb[NB];
-  T q[NB];
+  double cvb[OBC];
+  T q[OBC];
 #pragma unroll
-  for (int ob = 0; ob < NB; ++ob) {
-    cvb[ob] = dm.b_cvb * ob;
+  for (int ob = 0; ob < OBC; ++ob) {
+    cvb[ob] = dm.b_cvb * (ob0 + ob);
     asm volatile("" : "+d"(cvb[ob]));  // keep in registers, do not rematerialise
     q[ob] = T(0);
   }
@@ -425,9 +439,9 @@ __global__ void __launch_bounds__(256, 2) k_sweep_b_geo(DevModel dm, const T* __
       }
       const double revenue = revenue_a + crb * hb;
       const double head = revenue - cva_oa;
-      const T* va = V + base;
+      const T* va = V + base + ob0 * WB;
 #pragma unroll
-      for (int ob = 0; ob < NB; ++ob) {
+      for (int ob = 0; ob < OBC; ++ob) {
         const double v = static_cast<double>(__ldg(va + ob * WB));
         q[ob] += static_cast<T>(p * (head - cvb[ob] + gamma * v));
       }
@@ -436,20 +450,20 @@ __global__ void __launch_bounds__(256, 2) k_sweep_b_geo(DevModel dm, const T* __
   T best = q[0];
   int bo = 0;
 #pragma unroll
-  for (int ob = 1; ob < NB; ++ob)
+  for (int ob = 1; ob < OBC; ++ob)
     if (q[ob] > best) {
       best = q[ob];
       bo = ob;
     }
   const std::uint64_t nr = hi - lo;
   if (part_v) {
-    part_v[oa * nr + (s - lo)] = best;
-    part_a[oa * nr + (s - lo)] = static_cast<std::uint8_t>(bo);
+    part_v[blockIdx.y * nr + (s - lo)] = best;
+    part_a[blockIdx.y * nr + (s - lo)] = static_cast<std::uint8_t>(bo);
   }
   if (qout) {
-    const std::uint64_t row = (s - lo) * dm.n_actions + static_cast<std::uint64_t>(oa) * NB;
+    const std::uint64_t row = (s - lo) * dm.n_actions + static_cast<std::uint64_t>(oa) * NB + ob0;
 #pragma unroll
-    for (int ob = 0; ob < NB; ++ob) qout[row + ob] = q[ob];
+    for (int ob = 0; ob < OBC; ++ob) qout[row + ob] = q[ob];
   }
 }
 
@@ -465,11 +479,6 @@ __global__ void __launch_bounds__(256, 2) k_sweep_b_geo(DevModel dm, const T* __
 // C_s*(d-total)^+ and CW[w] = C_w*w, reproducing the reference's
 // left-to-right evaluation.
 
-template <int M, int DN>
-struct CAcc {
-  double v[DN > 0 ? DN : 1];
-};
-
 template <typename T, int M, int DN>
 __global__ void __launch_bounds__(128) k_sweep_c(DevModel dm, const T* __restrict__ V,
                                                  T* __restrict__ part_v, T* __restrict__ qout,
@@ -477,10 +486,10 @@ __global__ void __launch_bounds__(128) k_sweep_c(DevModel dm, const T* __restric
                                                  double gamma) {
   extern __shared__ double smem[];
   const int cap = dm.c_max_order;
-  const int dmax = dm.c_dmax;
+  constexpr int dmax = DN - 1;
   const int n_ra = M * cap + dmax + 1;
-  double* s_ra = smem;
-  double* s_cw = s_ra + n_ra;
+  double* s_ra = smem;            // RA[total - d + D]
+  double* s_cw = s_ra + n_ra;     // CWX[z1 - d + D] = C_w * (z1 - d)^+
   const int na = static_cast<int>(dm.n_actions);
   const int a = na - 1 - static_cast<int>(blockIdx.y);
   const double fixed = a > 0 ? -dm.c_cf : 0.0;
@@ -488,21 +497,30 @@ __global__ void __launch_bounds__(128) k_sweep_c(DevModel dm, const T* __restric
     const int diff = k - dmax;  // total - d
     s_ra[k] = fixed - dm.c_ch * ipos(diff) - dm.c_cs * ipos(-diff);
   }
-  for (int k = threadIdx.x; k <= cap; k += blockDim.x) s_cw[k] = dm.c_cw * k;
+  for (int k = threadIdx.x; k <= dmax + cap; k += blockDim.x) s_cw[k] = dm.c_cw * ipos(k - dmax);
   __syncthreads();
 
   const std::uint64_t s = lo + static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= hi) return;
-  int st[kMaxDigits];
-  decode(dm, s, st);
-  const int tau = st[0];
+  // decode (digit 0 = weekday, digits 1..M-1 = x_{M-1} .. x_1, radix A_max+1)
   int x[M + 1];
+  int tau;
+  std::uint32_t w[M + 1];
+  {
+    const std::uint32_t r = static_cast<std::uint32_t>(cap + 1);
+    std::uint32_t rem = static_cast<std::uint32_t>(s);
+    std::uint32_t wk = 1;
 #pragma unroll
-  for (int j = 1; j <= M - 1; ++j) x[j] = st[M - j];
-  const std::uint64_t tau_base = static_cast<std::uint64_t>((tau + 1) % 7) * dm.weight[0];
-  std::uint64_t w[M + 1];
-#pragma unroll
-  for (int k = 1; k < M; ++k) w[k] = dm.weight[k];
+    for (int j = 1; j <= M - 1; ++j) {  // x_j is digit M-j, weight r^(j-1)
+      x[j] = static_cast<int>(rem % r);
+      rem /= r;
+      w[M - j] = wk;
+      wk *= r;
+    }
+    tau = static_cast<int>(rem);
+    w[0] = wk;
+  }
+  const std::uint32_t tau_base = static_cast<std::uint32_t>((tau + 1) % 7) * w[0];
 
   double inner[DN];
 #pragma unroll
@@ -514,6 +532,7 @@ __global__ void __launch_bounds__(128) k_sweep_c(DevModel dm, const T* __restric
     const std::uint32_t id = __ldg(dm.c_ids + off + c);
     const double prob = __ldg(dm.c_probs + off + c);
     const std::int8_t* yt = dm.c_comp + static_cast<std::size_t>(id) * M;
+    // post-delivery profile z_j = min(x_j + y_j, cap), prefix sums sp_j
     int sp[M + 1], z[M + 1];
     int prefix = 0;
 #pragma unroll
@@ -524,26 +543,22 @@ __global__ void __launch_bounds__(128) k_sweep_c(DevModel dm, const T* __restric
     }
     const int fresh = yt[0];
     const int total = prefix + fresh;
-    const int z1 = z[1];
+    const double* ra_row = s_ra + total + dmax;  // ra_row[-d] = RA[total - d + D]
+    const double* cw_row = s_cw + z[1] + dmax;   // cw_row[-d] = C_w * (z1 - d)^+
 #pragma unroll
     for (int d = 0; d < DN; ++d) {
-      std::uint64_t idx = tau_base;
+      // next-state digits: nx_j = clamp(sp_{j+1} - d, 0, z_{j+1}) (== the
+      // reference's max(z_{j+1} - max(d - sp_j, 0), 0)), fresh: clamp(total - d, 0, y_M)
+      std::uint32_t idx = tau_base;
 #pragma unroll
-      for (int j = 1; j <= M - 2; ++j) {
-        const int e = d > sp[j] ? d - sp[j] : 0;
-        int nxj = z[j + 1] - e;
-        if (nxj < 0) nxj = 0;
-        idx += static_cast<std::uint64_t>(nxj) * w[M - j];
-      }
-      const int e_last = d > sp[M - 1] ? d - sp[M - 1] : 0;
-      int nx1 = fresh - e_last;
-      if (nx1 < 0) nx1 = 0;
-      idx += static_cast<std::uint64_t>(nx1) * w[1];
-      const double reward = s_ra[total - d + dmax] - s_cw[ipos(z1 - d)];
-      inner[d] += prob * (reward + gamma * static_cast<double>(V[idx]));
+      for (int j = 1; j <= M - 2; ++j)
+        idx += static_cast<std::uint32_t>(max(min(sp[j + 1] - d, z[j + 1]), 0)) * w[M - j];
+      idx += static_cast<std::uint32_t>(max(min(total - d, fresh), 0)) * w[1];
+      const double reward = ra_row[-d] - cw_row[-d];
+      inner[d] += prob * (reward + gamma * static_cast<double>(__ldg(V + idx)));
     }
   }
-  const double* pmf = dm.c_pmf + tau * (dmax + 1);
+  const double* pmf = dm.c_pmf + tau * DN;
   double acc = 0.0;
 #pragma unroll
   for (int d = 0; d < DN; ++d) acc += __ldg(pmf + d) * inner[d];
@@ -875,6 +890,7 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
       T* pv = a.want_values ? scratch.get<T>(0, static_cast<std::size_t>(dm.b_na) * nr, stream) : nullptr;
       std::uint8_t* pa = a.want_values ? scratch.get<std::uint8_t>(1, static_cast<std::size_t>(dm.b_na) * nr, stream) : nullptr;
       const dim3 grid(static_cast<unsigned>(t1 - t0), static_cast<unsigned>(dm.b_na));
+      int n_chunks = dm.b_na, chunk_width = dm.b_nb;
       static bool attr_set[2] = {false, false};
       (void)attr_set;
       cudaFuncSetAttribute(k_sweep_b<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -884,20 +900,28 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
       MainKernelScope prof(stream);
       const std::size_t sm_geo = sizeof(double) * (2 * (dm.b_len_a + dm.b_len_b + 1));
       bool done = false;
-#define PVI_B_GEO(MM, NNB)                                                                    \
+      // Two order_b chunks per (state, order_a) when NB is even: half the
+      // accumulators per thread -> 3 CTAs/SM instead of 2 (K1-B).
+#define PVI_B_GEO(MM, NNB, NCH)                                                               \
   if (!done && dm.b_m == MM && dm.b_nb == NNB) {                                              \
-    k_sweep_b_geo<T, MM, NNB><<<grid, block, sm_geo, stream>>>(dm, a.v, pv, pa, a.qout, lo, hi, \
-                                                               t0, a.gamma);                  \
+    const dim3 g2(grid.x, grid.y * NCH);                                                      \
+    T* pv2 = a.want_values ? scratch.get<T>(0, static_cast<std::size_t>(dm.b_na) * NCH * nr, stream) : nullptr; \
+    std::uint8_t* pa2 = a.want_values ? scratch.get<std::uint8_t>(1, static_cast<std::size_t>(dm.b_na) * NCH * nr, stream) : nullptr; \
+    k_sweep_b_geo<T, MM, NNB, NCH><<<g2, block, sm_geo, stream>>>(dm, a.v, pv2, pa2, a.qout, lo, hi, t0, a.gamma); \
+    pv = pv2;                                                                                 \
+    pa = pa2;                                                                                 \
+    n_chunks = dm.b_na * NCH;                                                                 \
+    chunk_width = NNB / NCH;                                                                  \
     done = true;                                                                              \
   }
-      PVI_B_GEO(3, 16)
-      PVI_B_GEO(3, 14)
-      PVI_B_GEO(3, 10)
-      PVI_B_GEO(3, 5)
-      PVI_B_GEO(2, 11)
-      PVI_B_GEO(2, 7)
-      PVI_B_GEO(2, 13)
-      PVI_B_GEO(2, 14)
+      PVI_B_GEO(3, 16, 1)
+      PVI_B_GEO(3, 14, 1)
+      PVI_B_GEO(3, 10, 1)
+      PVI_B_GEO(3, 5, 1)
+      PVI_B_GEO(2, 11, 1)
+      PVI_B_GEO(2, 7, 1)
+      PVI_B_GEO(2, 13, 1)
+      PVI_B_GEO(2, 14, 1)
 #undef PVI_B_GEO
       if (done) {
       } else if (dm.b_nb <= 16)
@@ -909,7 +933,7 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
       }
       PVI_CUDA(cudaGetLastError());
       if (a.want_values)
-        k_finalize<T><<<grid_for(nr, 256), 256, 0, stream>>>(pv, pa, dm.b_na, dm.b_nb, a.v, a.vout, a.act, lo, hi, a.out_off, fa);
+        k_finalize<T><<<grid_for(nr, 256), 256, 0, stream>>>(pv, pa, n_chunks, chunk_width, a.v, a.vout, a.act, lo, hi, a.out_off, fa);
       break;
     }
     case PVI_SCENARIO_C: {
@@ -918,7 +942,7 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
       const int dn = dm.c_dmax + 1;
       const unsigned block = 128;
       const dim3 grid(grid_for(nr, block), static_cast<unsigned>(na));
-      const std::size_t sm = sizeof(double) * (dm.c_m * dm.c_max_order + dm.c_dmax + 1 + dm.c_max_order + 1);
+      const std::size_t sm = sizeof(double) * (dm.c_m * dm.c_max_order + 2 * (dm.c_dmax + 1) + dm.c_max_order);
       bool done = false;
       count_launches(a.want_values ? 2 : 1);
       MainKernelScope prof(stream);

@@ -113,8 +113,10 @@ class ShardedValueIteration:
 
     # -- one sweep (bench step) ---------------------------------------------
     def step(self, vprev: torch.Tensor, vnext: torch.Tensor, stats: Optional[torch.Tensor] = None,
-             test: Optional[int] = None):
-        self.sweep(vprev, vnext, None, self.lo, self.hi, test, [], stats)
+             test: Optional[int] = None, hist: List[torch.Tensor] = ()):
+        """One sweep + exchange.  `hist` holds the 7 previous vectors
+        (oldest..newest, newest = vprev) when test is the periodic span."""
+        self.sweep(vprev, vnext, None, self.lo, self.hi, test, list(hist), stats)
         if stats is not None:
             self.reduce_stats(stats)
         self.exchange(vnext)
