@@ -289,6 +289,42 @@ int pvi_sim_evaluate(const pvi_model* m, const pvi_policy* policies, uint32_t n_
                      const pvi_rollout_config* cfg, pvi_rollout_summary* per_rollout,
                      pvi_evaluation* evals, char* err, size_t errlen);
 
+/* ---- simulation optimisation (simopt.hpp, runner.cpp:352-403) ----------
+ * The reference's grid search / generational GA (simopt.cpp:22-161), run on
+ * the host exactly as the reference runs it (std::mt19937_64 and the
+ * libstdc++ distributions, so the search trajectory is the reference's),
+ * with each generation's fresh candidates scored in ONE batched device
+ * evaluation (pvi_sim_evaluate) instead of one evaluate_policy per candidate. */
+typedef struct {
+  int sampler;                 /* 0 auto (grid if 1-D, else GA), 1 grid, 2 GA */
+  int population;              /* 50 */
+  int max_generations;         /* 100 */
+  int patience;                /* 5 */
+  double crossover_rate;       /* 0.9 */
+  double mutation_rate;        /* 0 = 1/dimension */
+  uint64_t seed;               /* GA seed, 1 */
+  int rollouts_per_candidate;  /* 4000 */
+  int horizon_days;            /* 365 */
+  int warmup_days;             /* 100 */
+  uint64_t base_seed;          /* eval.base_seed, 42 */
+  int device;                  /* -1 = current */
+} pvi_simopt_config;
+
+void pvi_simopt_config_defaults(pvi_simopt_config* c);
+
+/* One logged candidate (ScoredCandidate, simopt.hpp:39-44). */
+typedef struct {
+  int generation;
+  int values[14];
+  double mean, sd;
+} pvi_scored_candidate;
+
+/* best: dimension ints; log: up to log_capacity entries (n_logged gets the
+ * full count); device_seconds: time inside the batched device evaluations. */
+int pvi_simopt(const pvi_model* m, const pvi_simopt_config* cfg, int* best, double* best_mean,
+               double* best_sd, int* generations, pvi_scored_candidate* log, int log_capacity,
+               int* n_logged, int* dimension, double* device_seconds, char* err, size_t errlen);
+
 /* Philox4x32-10 block and RolloutRng draws evaluated ON THE DEVICE
  * (rng.hpp:15-60), for known-answer tests. */
 int pvi_philox_block(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);

@@ -88,6 +88,19 @@ class EvaluationC(C.Structure):
                 ("products", C.c_int), ("n_rollouts", C.c_int)]
 
 
+class SimoptConfigC(C.Structure):
+    _fields_ = [("sampler", C.c_int), ("population", C.c_int), ("max_generations", C.c_int),
+                ("patience", C.c_int), ("crossover_rate", C.c_double),
+                ("mutation_rate", C.c_double), ("seed", C.c_uint64),
+                ("rollouts_per_candidate", C.c_int), ("horizon_days", C.c_int),
+                ("warmup_days", C.c_int), ("base_seed", C.c_uint64), ("device", C.c_int)]
+
+
+class ScoredCandidateC(C.Structure):
+    _fields_ = [("generation", C.c_int), ("values", C.c_int * 14), ("mean", C.c_double),
+                ("sd", C.c_double)]
+
+
 class PolicyC(C.Structure):
     _fields_ = [("kind", C.c_int), ("table", C.POINTER(C.c_uint32)),
                 ("params", C.c_int * 14), ("n_params", C.c_int)]
@@ -136,6 +149,8 @@ SIGNATURES = {
     "pvi_checkpoint_save": (C.c_int, [C.c_char_p, _vp, C.c_uint64, C.c_uint64, _vp] + _E),
     "pvi_checkpoint_load": (C.c_int, [C.c_char_p, _vp, _vp, C.c_uint64, _vp, _vp, _vp] + _E),
     "pvi_sha256": (C.c_int, [_vp, C.c_size_t, _vp]),
+    "pvi_simopt_config_defaults": (None, [_vp]),
+    "pvi_simopt": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp] + _E),
     "pvi_profile_enable": (C.c_int, [C.c_int]),
     "pvi_profile_read": (C.c_int, [_vp, _vp, _vp]),
 }

@@ -342,6 +342,38 @@ int pvi_sim_evaluate(const pvi_model* m, const pvi_policy* policies, uint32_t n_
   });
 }
 
+void pvi_simopt_config_defaults(pvi_simopt_config* c) {
+  *c = pvi_simopt_config{};
+  c->sampler = 0;
+  c->population = 50;
+  c->max_generations = 100;
+  c->patience = 5;
+  c->crossover_rate = 0.9;
+  c->mutation_rate = 0.0;
+  c->seed = 1;
+  c->rollouts_per_candidate = 4000;
+  c->horizon_days = 365;
+  c->warmup_days = 100;
+  c->base_seed = 42;
+  c->device = -1;
+}
+
+int pvi_simopt(const pvi_model* m, const pvi_simopt_config* cfg, int* best, double* best_mean,
+               double* best_sd, int* generations, pvi_scored_candidate* log, int log_capacity,
+               int* n_logged, int* dimension, double* device_seconds, char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if (!best || !best_mean || !best_sd || !generations || !n_logged)
+      fail(PVI_ERR_PARAMETER, "null argument");
+    pvi_simopt_config c;
+    if (cfg)
+      c = *cfg;
+    else
+      pvi_simopt_config_defaults(&c);
+    simopt_run(M(m), c, best, best_mean, best_sd, generations, log, log ? log_capacity : 0, n_logged,
+               dimension, device_seconds);
+  });
+}
+
 int pvi_philox_block(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
   return guarded(nullptr, 0, nullptr, [&] { philox_block_device(ctr, key, out); });
 }

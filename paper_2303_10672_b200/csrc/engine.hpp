@@ -37,6 +37,9 @@ void load_checkpoint(const std::string& path, const std::uint8_t* expected, doub
 void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_policies,
                   const pvi_rollout_config& cfg, pvi_rollout_summary* per_rollout,
                   pvi_evaluation* evals);
+void simopt_run(const Model& m, const pvi_simopt_config& cfg, int* best, double* best_mean,
+                double* best_sd, int* generations, pvi_scored_candidate* log, int log_capacity,
+                int* n_logged, int* dimension, double* device_seconds);
 void philox_block_device(const std::uint32_t ctr[4], const std::uint32_t key[2], std::uint32_t out[4]);
 void rollout_draws_device(std::uint64_t seed, std::uint64_t rollout, std::uint32_t day, int n,
                           std::uint64_t* out);

@@ -635,6 +635,50 @@ def evaluate_policy(model: Model, policy: Policy, config: RolloutConfig) -> Eval
     return evaluate_policies(model, [policy], config)[0][0]
 
 
+@dataclass
+class SimoptResult:
+    best: list
+    best_mean: float
+    best_sd: float
+    generations: int
+    log: list            # (generation, values, mean, sd) per evaluated candidate, in order
+    device_seconds: float
+    wall_seconds: float
+
+
+def simopt(model: Model, sampler: str = "auto", population: int = 50, max_generations: int = 100,
+           patience: int = 5, crossover_rate: float = 0.9, mutation_rate: float = 0.0,
+           seed: int = 1, rollouts_per_candidate: int = 4000, horizon_days: int = 365,
+           warmup_days: int = 100, base_seed: int = 42, device: int = -1,
+           log_capacity: int = 20000) -> SimoptResult:
+    """cmd_simopt's search (runner.cpp:352-403): grid (1-D) or GA, batched on the GPU."""
+    import time
+    c = L.SimoptConfigC()
+    lib = L.load()
+    lib.pvi_simopt_config_defaults(C.byref(c))
+    c.sampler = {"auto": 0, "grid": 1, "ga": 2}[sampler]
+    c.population, c.max_generations, c.patience = population, max_generations, patience
+    c.crossover_rate, c.mutation_rate, c.seed = crossover_rate, mutation_rate, seed
+    c.rollouts_per_candidate, c.horizon_days, c.warmup_days = (rollouts_per_candidate,
+                                                              horizon_days, warmup_days)
+    c.base_seed, c.device = base_seed, device
+    best = (C.c_int * 14)()
+    bm, bsd, dev_s = C.c_double(), C.c_double(), C.c_double()
+    gens, nlog, dim = C.c_int(), C.c_int(), C.c_int()
+    logs = (L.ScoredCandidateC * log_capacity)()
+    err = _err_buf()
+    t0 = time.perf_counter()
+    _raise(lib.pvi_simopt(model.handle, C.byref(c), best, C.byref(bm), C.byref(bsd),
+                          C.byref(gens), logs, log_capacity, C.byref(nlog), C.byref(dim),
+                          C.byref(dev_s), err, len(err)), err)
+    wall = time.perf_counter() - t0
+    d = dim.value
+    entries = [(logs[i].generation, list(logs[i].values[:d]), logs[i].mean, logs[i].sd)
+               for i in range(min(nlog.value, log_capacity))]
+    return SimoptResult(list(best[:d]), bm.value, bsd.value, gens.value, entries, dev_s.value,
+                        wall)
+
+
 def philox_block(ctr, key) -> np.ndarray:
     c = np.ascontiguousarray(ctr, np.uint32)
     k = np.ascontiguousarray(key, np.uint32)

@@ -132,5 +132,26 @@ def main():
     print(f"wrote {len(out)} arrays")
 
 
+def simopt_golden():
+    """cmd_simopt trajectories (runner.cpp:352-403) with 4096 rollouts per
+    candidate, eval seed 42, GA seed 1."""
+    out = {}
+    for preset in ["a/m2/exp1", "b/m2/exp1", "c/m3/exp1"]:
+        r = R.simopt(preset, rollouts=4096, eval_seed=42, ga_seed=1)
+        dim = {"a": 1, "b": 2, "c": 14}[preset[0]]
+        n = r["n_logged"]
+        out[f"simopt|{preset}|best"] = r["best"][:dim].astype(np.int64)
+        out[f"simopt|{preset}|meta"] = np.array([r["generations"], n], np.int64)
+        out[f"simopt|{preset}|score"] = np.array([r["mean"], r["sd"]])
+        out[f"simopt|{preset}|log_values"] = r["log_values"][:n * dim].reshape(n, dim).astype(np.int64)
+        out[f"simopt|{preset}|log_scores"] = r["log_scores"][:n]
+        out[f"simopt|{preset}|ref_wall"] = np.array([r["wall"]])
+        print(preset, r["best"][:dim], r["mean"], r["generations"], n, r["wall"])
+    np.savez_compressed(os.path.join(HERE, "simopt_golden.npz"), **out)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "simopt":
+        simopt_golden()
+    else:
+        main()
