@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="b/m3/exp1")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--algorithm", default="exact", choices=["exact", "factored"])
     ap.add_argument("--no-solve", action="store_true", help="skip the time-to-converge solve")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -251,7 +252,7 @@ def ours_arm(args, world, rank, local):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    model = P.make_preset(args.workload)
+    model = P.make_preset(args.workload).set_algorithm(args.algorithm)
     n = model.state_count()
     cfg = P.ViConfig(precision=args.precision)
     solver = ShardedValueIteration(model, cfg)

@@ -177,7 +177,18 @@ typedef struct {
   uint64_t max_states;       /* capacity gate, 200'000'000 */
   int device;                /* CUDA ordinal, -1 = current */
   int sweeps_per_sync;       /* >1: speculative multi-sweep launches between host syncs (0/1 = 1) */
+  int algorithm;             /* -1: the model's (pvi_model_set_algorithm), else pvi_algorithm */
 } pvi_vi_config;
+
+/* Backup algorithm.  EXACT reproduces the reference's per-term expression
+ * and summation order (bit-identical results).  FACTORED (Scenario B only;
+ * others fall back to EXACT) contracts the separable issued-pair law first,
+ * doing ~16x fewer operations per sweep; results agree with the reference to
+ * rounding (the north-star 1e-9 contract), not bit for bit. */
+typedef enum { PVI_ALGO_EXACT = 0, PVI_ALGO_FACTORED = 1 } pvi_algorithm;
+/* Default algorithm of every sweep on this model (pvi_vi_backup, pvi_q_rows,
+ * pvi_vi_sweep_device, and pvi_vi_solve with algorithm = -1). */
+int pvi_model_set_algorithm(pvi_model* m, int algorithm);
 
 void pvi_vi_config_defaults(pvi_vi_config* c);
 

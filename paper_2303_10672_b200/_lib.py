@@ -60,7 +60,8 @@ class ViConfigC(C.Structure):
                 ("max_iterations", C.c_uint64), ("fixed_iterations", C.c_uint64),
                 ("checkpoint_every", C.c_uint64), ("checkpoint_path", C.c_char_p),
                 ("precision", C.c_int), ("convergence_test", C.c_int),
-                ("max_states", C.c_uint64), ("device", C.c_int), ("sweeps_per_sync", C.c_int)]
+                ("max_states", C.c_uint64), ("device", C.c_int), ("sweeps_per_sync", C.c_int),
+                ("algorithm", C.c_int)]
 
 
 class ViStats(C.Structure):
@@ -132,6 +133,7 @@ SIGNATURES = {
     "pvi_model_outcome_probability": (C.c_int, [_vp, C.c_uint64, C.c_uint32, C.c_uint64, _vp]),
     "pvi_model_initial_values": (C.c_int, [_vp, _vp] + _E),
     "pvi_vi_config_defaults": (None, [_vp]),
+    "pvi_model_set_algorithm": (C.c_int, [_vp, C.c_int]),
     "pvi_vi_solve": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _vp, _vp, _vp, _vp, _vp] + _E),
     "pvi_vi_backup": (C.c_int, [_vp, C.c_int, C.c_double, _vp, C.c_uint64, C.c_uint64, _vp,
                                 _vp] + _E),

@@ -265,6 +265,16 @@ void pvi_vi_config_defaults(pvi_vi_config* c) {
   c->max_states = 200000000ull;
   c->device = -1;
   c->sweeps_per_sync = 1;
+  c->algorithm = -1;
+}
+
+int pvi_model_set_algorithm(pvi_model* m, int algorithm) {
+  return guarded(nullptr, 0, nullptr, [&] {
+    if (!m || !m->impl) fail(PVI_ERR_PARAMETER, "null model");
+    if (algorithm != PVI_ALGO_EXACT && algorithm != PVI_ALGO_FACTORED)
+      fail(PVI_ERR_PARAMETER, "unknown algorithm");
+    m->impl->algorithm = algorithm;
+  });
 }
 
 int pvi_vi_solve(const pvi_model* m, const pvi_vi_config* cfg, const double* resume_values,

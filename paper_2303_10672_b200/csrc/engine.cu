@@ -130,6 +130,12 @@ const DevModel& Model::device_view(int device) const {
   return out;
 }
 
+DeviceCopy& Model::device_copy(int device) const {
+  device_view(device);
+  std::lock_guard<std::mutex> lock(dev_mutex);
+  return *dev.at(device);
+}
+
 int select_device(int requested) {
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
@@ -303,6 +309,7 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
   if (n == 0) fail(PVI_ERR_PARAMETER, "value iteration: empty state space");
   const double gamma = cfg.has_gamma ? cfg.gamma : m.gamma;
   const int test = cfg.convergence_test >= 0 ? cfg.convergence_test : m.default_test;
+  const int algo = cfg.algorithm >= 0 ? cfg.algorithm : m.algorithm;
   std::uint8_t fp[32];
   sha256(m.fingerprint.data(), m.fingerprint.size(), fp);
 
@@ -385,6 +392,7 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
     a.lo = 0;
     a.hi = n;
     a.gamma = gamma;
+    a.algorithm = algo;
     a.fa.test = want_test ? test : -1;
     a.fa.gamma = gamma;
     a.fa.stats = dstats.as<SweepStats>();
@@ -427,6 +435,7 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
     a.lo = 0;
     a.hi = n;
     a.gamma = gamma;
+    a.algorithm = algo;
     PVI_CUDA(cudaEventRecord(ev0, stream.s));
     launch_sweep<T>(m, dm, a, scratch, stream.s);
     PVI_CUDA(cudaEventRecord(ev1, stream.s));
@@ -502,6 +511,7 @@ void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t
   a.hi = hi;
   a.out_off = lo;
   a.gamma = gamma;
+  a.algorithm = m.algorithm;
   a.want_values = out_values || out_actions;
   launch_sweep<T>(m, dm, a, scratch, stream.s);
   if (out_values) PVI_CUDA(cudaMemcpyAsync(out_values, vo.p, nr * sizeof(T), cudaMemcpyDeviceToHost, stream.s));
@@ -596,6 +606,7 @@ void sweep_device_impl(const Model& m, double gamma, const void* vprev, void* vn
   a.hi = hi;
   a.out_off = 0;
   a.gamma = gamma;
+  a.algorithm = m.algorithm;
   a.want_values = true;
   if (want_stats && stats) {
     a.fa.stats = dstats->as<SweepStats>();

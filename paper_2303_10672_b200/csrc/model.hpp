@@ -92,6 +92,12 @@ struct DevModel {
 struct DeviceCopy {
   DevModel dm{};
   std::vector<void*> allocations;
+  // Scenario B factored sweep: per-state expected revenue and total issued
+  // probability (V-independent, built once), and the A / B digit-block
+  // orders sorted by stock so warps share loop trip counts.
+  double* b_erpt = nullptr;
+  std::uint16_t* b_order_a = nullptr;
+  std::uint16_t* b_order_b = nullptr;
 };
 
 struct Model {
@@ -123,12 +129,14 @@ struct Model {
   std::vector<double> t_reward, t_prob, t_initial;
 
   std::string fingerprint;  // fingerprint_material()
+  int algorithm = PVI_ALGO_EXACT;  // engine option, not part of the model's identity
 
   mutable std::mutex dev_mutex;
   mutable std::map<int, std::unique_ptr<DeviceCopy>> dev;
 
   ~Model();
   const DevModel& device_view(int device) const;  // uploads on first use
+  DeviceCopy& device_copy(int device) const;      // device_view's backing record
   double terms_per_sweep() const;
   double state_cost(std::uint64_t s) const;  // relative backup cost of one state
   std::uint64_t tile_states() const;         // partition alignment

@@ -13,6 +13,7 @@
 // reference's; Scenario B/C partial maxima live in an (action-chunk x
 // state) scratch array so the cross-chunk argmax stays in action order.
 
+#include <algorithm>
 #include <cfloat>
 #include <mutex>
 #include <utility>
@@ -468,6 +469,214 @@ __global__ void __launch_bounds__(256, NCH == 1 ? 2 : 3) k_sweep_b_geo(DevModel 
 }
 
 // ---------------------------------------------------------------------------
+// K1-B factored ("algorithm = factored"; not the reference's summation order,
+// parity contract 1e-9 relative instead of bits).
+//
+// The issued-pair law is separable away from product B's stock-out row:
+// p(h_a,h_b) = alpha(h_a) pmf_b(h_b) for h_b < I_b, with alpha = pmf_a (h_a < I_a)
+// or sf_a(I_a); and p(h_a, I_b) = g(h_a) sf_b(I_b), g = pz(I_b, .) or
+// 1 - pz_cum(I_b, I_a) (scenario_b.cpp:168-176).  With r = (o_a, aged A
+// digits) and bp = aged B digits, V[next] = V[r, o_b, bp], and B(x_b, I_b) = 0:
+//
+//   Q(s,o_a,o_b) = ER(s) - (C_v^a o_a + C_v^b o_b) PT(s)
+//                + gamma [ sum_ha alpha(ha) W[x_b][r(ha)][o_b]
+//                          + sf_b(I_b) sum_ha g(ha) V[r(ha), o_b, 0] ]
+//   W[x_b][r][o_b] = sum_{h_b < I_b} pmf_b(h_b) V[r, o_b, B(x_b, h_b)]
+//
+// ER = sum p (C_r^a h_a + C_r^b h_b) and PT = sum p are V-independent.  Stage 1
+// (k_b_fact_w) builds W with one CTA per r (the r-slab of V staged in shared
+// memory); stage 2 (k_b_fact_q) one CTA per (x_b, o_a) with W[x_b][o_a, .][.]
+// and V[o_a, ., ., 0] in shared memory.  A sweep is ~1.5e11 FMAs instead of the
+// reference's 2.4e12 terms x 5 operations.
+
+__global__ void __launch_bounds__(256) k_b_erpt(DevModel dm, double* __restrict__ erpt,
+                                                std::uint64_t n) {
+  const std::uint64_t s = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int m = dm.b_m;
+  int st[kMaxDigits];
+  decode(dm, s, st);
+  int ia = 0, ib = 0;
+  for (int i = 0; i < m; ++i) ia += st[i];
+  for (int i = m; i < 2 * m; ++i) ib += st[i];
+  const int dn = dm.b_dn;
+  double er = 0.0, pt = 0.0;
+  for (int ha = 0; ha <= ia; ++ha)
+    for (int hb = 0; hb <= ib; ++hb) {
+      double p;
+      if (ha < ia)
+        p = hb < ib ? dm.b_pmf_a[ha] * dm.b_pmf_b[hb] : dm.b_pz[ib * dn + ha] * dm.b_sf_b[ib];
+      else
+        p = hb < ib ? dm.b_sf_a[ia] * dm.b_pmf_b[hb] : (1.0 - dm.b_pz_cum[ib * dn + ia]) * dm.b_sf_b[ib];
+      er += p * (dm.b_cra * ha + dm.b_crb * hb);
+      pt += p;
+    }
+  erpt[s] = er;
+  erpt[n + s] = pt;
+}
+
+// Stage 1: W[x_b][r][o_b].  grid.x = r (na^M values), threads stride over x_b.
+template <typename T, int M, int NBX>
+__global__ void __launch_bounds__(256) k_b_fact_w(DevModel dm, const T* __restrict__ V,
+                                                  double* __restrict__ W,
+                                                  double* __restrict__ v0t,
+                                                  const std::uint16_t* __restrict__ order_b,
+                                                  int n_xb, int n_bp, int n_r) {
+  extern __shared__ double slab[];  // [bp][ob], row stride nb|1
+  const int nb = dm.b_nb;
+  const int stride = nb | 1;
+  const int r = blockIdx.x;
+  const std::uint64_t base = static_cast<std::uint64_t>(r) * n_xb;  // r * nb^M
+  for (int i = threadIdx.x; i < nb * n_bp; i += blockDim.x) {
+    const int ob = i / n_bp, bp = i % n_bp;
+    slab[bp * stride + ob] = static_cast<double>(V[base + static_cast<std::uint64_t>(ob) * n_bp + bp]);
+  }
+  __syncthreads();
+  if (threadIdx.x < nb) v0t[static_cast<std::size_t>(r) * nb + threadIdx.x] = slab[threadIdx.x];
+  __shared__ double s_pmf_b[128];
+  for (int i = threadIdx.x; i < 128 && i < dm.b_len_b; i += blockDim.x) s_pmf_b[i] = dm.b_pmf_b[i];
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_xb; t += blockDim.x) {
+    const int xbi = order_b[t];
+    int xb[M + 1];
+    int ib = 0;
+    {
+      int rem = xbi;
+#pragma unroll
+      for (int j = 1; j <= M; ++j) {
+        xb[j] = rem % nb;
+        rem /= nb;
+        ib += xb[j];
+      }
+    }
+    double acc[NBX];
+#pragma unroll
+    for (int ob = 0; ob < NBX; ++ob) acc[ob] = 0.0;
+    for (int hb = 0; hb < ib; ++hb) {
+      int bp = 0, prefix = 0, w = 1;
+#pragma unroll
+      for (int j = 1; j <= M - 1; ++j) {
+        prefix += xb[j];
+        bp += ipos(xb[j + 1] - ipos(hb - prefix)) * w;
+        w *= nb;
+      }
+      const double pw = hb < 128 ? s_pmf_b[hb] : dm.b_pmf_b[hb];
+      const double* row = slab + bp * stride;
+#pragma unroll
+      for (int ob = 0; ob < NBX; ++ob)
+        if (ob < nb) acc[ob] = fma(pw, row[ob], acc[ob]);
+    }
+    double* out = W + (static_cast<std::size_t>(xbi) * n_r + r) * nb;
+#pragma unroll
+    for (int ob = 0; ob < NBX; ++ob)
+      if (ob < nb) out[ob] = acc[ob];
+  }
+}
+
+// Stage 2: Q for states [lo, hi).  grid = (x_b, o_a), threads stride over x_a.
+template <typename T, int M, int NBX>
+__global__ void __launch_bounds__(256) k_b_fact_q(DevModel dm, const double* __restrict__ W,
+                                                  const double* __restrict__ v0t,
+                                                  const double* __restrict__ erpt,
+                                                  const std::uint16_t* __restrict__ order_a,
+                                                  T* __restrict__ part_v,
+                                                  std::uint8_t* __restrict__ part_a,
+                                                  T* __restrict__ qout, std::uint64_t lo,
+                                                  std::uint64_t hi, double gamma, int n_xa,
+                                                  int n_xb, int n_ap, int n_r) {
+  extern __shared__ double sm[];
+  const int nb = dm.b_nb, na = dm.b_na;
+  const int stride = nb | 1;
+  double* w_sl = sm;                        // [ap][ob]
+  double* v0_sl = sm + n_ap * stride;       // [ap][ob]
+  const int xbi = blockIdx.x;
+  const int oa = blockIdx.y;
+  const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
+  for (int i = threadIdx.x; i < n_ap * nb; i += blockDim.x) {
+    const int ap = i / nb, ob = i % nb;
+    w_sl[ap * stride + ob] = W[(static_cast<std::size_t>(xbi) * n_r + r0 + ap) * nb + ob];
+    v0_sl[ap * stride + ob] = v0t[(r0 + ap) * nb + ob];
+  }
+  __syncthreads();
+  int xb[M + 1];
+  int ib = 0;
+  {
+    int rem = xbi;
+#pragma unroll
+    for (int j = 1; j <= M; ++j) {
+      xb[j] = rem % nb;
+      rem /= nb;
+      ib += xb[j];
+    }
+  }
+  const double sfb = dm.b_sf_b[ib];
+  const int dnp = dm.b_dn;
+  const double* pz_row = dm.b_pz + ib * dnp;
+  const std::uint64_t n = dm.n_states;
+  const std::uint64_t nr = hi - lo;
+  const double cva_oa = dm.b_cva * oa;
+  for (int t = threadIdx.x; t < n_xa; t += blockDim.x) {
+    const int xai = order_a[t];
+    const std::uint64_t s = static_cast<std::uint64_t>(xai) * n_xb + xbi;
+    if (s < lo || s >= hi) continue;
+    int xa[M + 1];
+    int ia = 0;
+    {
+      int rem = xai;
+#pragma unroll
+      for (int j = 1; j <= M; ++j) {
+        xa[j] = rem % na;
+        rem /= na;
+        ia += xa[j];
+      }
+    }
+    double acc1[NBX], acc2[NBX];
+#pragma unroll
+    for (int ob = 0; ob < NBX; ++ob) acc1[ob] = acc2[ob] = 0.0;
+    for (int ha = 0; ha <= ia; ++ha) {
+      int ap = 0, prefix = 0, w = 1;
+#pragma unroll
+      for (int j = 1; j <= M - 1; ++j) {
+        prefix += xa[j];
+        ap += ipos(xa[j + 1] - ipos(ha - prefix)) * w;
+        w *= na;
+      }
+      const bool interior = ha < ia;
+      const double al = interior ? __ldg(dm.b_pmf_a + ha) : __ldg(dm.b_sf_a + ia);
+      const double g = interior ? __ldg(pz_row + ha) : 1.0 - __ldg(dm.b_pz_cum + ib * dnp + ia);
+      const double* wr = w_sl + ap * stride;
+      const double* vr = v0_sl + ap * stride;
+#pragma unroll
+      for (int ob = 0; ob < NBX; ++ob)
+        if (ob < nb) {
+          acc1[ob] = fma(al, wr[ob], acc1[ob]);
+          acc2[ob] = fma(g, vr[ob], acc2[ob]);
+        }
+    }
+    const double er = erpt[s], pt = erpt[n + s];
+    T best = T(0);
+    int bo = 0;
+#pragma unroll
+    for (int ob = 0; ob < NBX; ++ob) {
+      if (ob < nb) {
+        const double u = fma(sfb, acc2[ob], acc1[ob]);
+        const double qd = fma(gamma, u, er - (cva_oa + dm.b_cvb * ob) * pt);
+        const T qv = static_cast<T>(qd);
+        if (ob == 0 || qv > best) {
+          best = qv;
+          bo = ob;
+        }
+        if (qout) qout[(s - lo) * dm.n_actions + static_cast<std::uint64_t>(oa) * nb + ob] = qv;
+      }
+    }
+    if (part_v) {
+      part_v[static_cast<std::uint64_t>(oa) * nr + (s - lo)] = best;
+      part_a[static_cast<std::uint64_t>(oa) * nr + (s - lo)] = static_cast<std::uint8_t>(bo);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K1-C: one thread per (state, order); the demand dimension unrolled into
 // DN register accumulators.  Blocks run heaviest order first.  Term order
 // and expression follow ScenarioC::q_row_impl (scenario_c.cpp:223-302):
@@ -846,6 +1055,101 @@ void profile_read(double* ms, std::uint64_t* main_launches, std::uint64_t* all_l
 // ---------------------------------------------------------------------------
 // Launchers
 
+// Factored Scenario B sweep; returns false when the geometry is not covered
+// (the caller then runs the exact kernel).
+namespace {
+std::vector<std::uint16_t> digit_sum_order(int radix, int digits) {
+  int n = 1;
+  for (int i = 0; i < digits; ++i) n *= radix;
+  std::vector<std::uint16_t> order(n);
+  std::vector<int> sum(n);
+  for (int v = 0; v < n; ++v) {
+    int s = 0, r = v;
+    for (int i = 0; i < digits; ++i) {
+      s += r % radix;
+      r /= radix;
+    }
+    sum[v] = s;
+    order[v] = static_cast<std::uint16_t>(v);
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return sum[x] < sum[y]; });
+  return order;
+}
+}  // namespace
+
+template <typename T>
+bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
+                       Scratch& scratch, cudaStream_t stream) {
+  const int M = dm.b_m, na = dm.b_na, nb = dm.b_nb;
+  if (M < 2 || M > 3 || nb > 32) return false;
+  long long n_xa = 1, n_xb = 1;
+  for (int i = 0; i < M; ++i) {
+    n_xa *= na;
+    n_xb *= nb;
+  }
+  const long long n_ap = n_xa / na, n_bp = n_xb / nb, n_r = n_xa;
+  if (n_xa > 65535 || n_xb > 65535) return false;
+  const int stride = nb | 1;
+  const std::size_t sm1 = sizeof(double) * n_bp * stride;
+  const std::size_t sm2 = sizeof(double) * 2 * n_ap * stride;
+  if (sm1 > 200 * 1024 || sm2 > 200 * 1024) return false;
+
+  int device = 0;
+  PVI_CUDA(cudaGetDevice(&device));
+  DeviceCopy& dc = model.device_copy(device);
+  {
+    std::lock_guard<std::mutex> lock(model.dev_mutex);
+    if (!dc.b_erpt) {
+      void* p = nullptr;
+      PVI_CUDA(cudaMalloc(&p, 2 * dm.n_states * sizeof(double)));
+      dc.allocations.push_back(p);
+      k_b_erpt<<<grid_for(dm.n_states, 256), 256, 0, stream>>>(dm, static_cast<double*>(p), dm.n_states);
+      PVI_CUDA(cudaGetLastError());
+      const auto oa_h = digit_sum_order(na, M), ob_h = digit_sum_order(nb, M);
+      void* q1 = nullptr;
+      void* q2 = nullptr;
+      PVI_CUDA(cudaMalloc(&q1, oa_h.size() * 2));
+      PVI_CUDA(cudaMalloc(&q2, ob_h.size() * 2));
+      PVI_CUDA(cudaMemcpy(q1, oa_h.data(), oa_h.size() * 2, cudaMemcpyHostToDevice));
+      PVI_CUDA(cudaMemcpy(q2, ob_h.data(), ob_h.size() * 2, cudaMemcpyHostToDevice));
+      dc.allocations.push_back(q1);
+      dc.allocations.push_back(q2);
+      dc.b_order_a = static_cast<std::uint16_t*>(q1);
+      dc.b_order_b = static_cast<std::uint16_t*>(q2);
+      dc.b_erpt = static_cast<double*>(p);
+    }
+  }
+  const std::uint64_t lo = a.lo, hi = a.hi, nr = hi - lo;
+  double* W = scratch.get<double>(3, static_cast<std::size_t>(n_xb) * n_r * nb, stream);
+  double* v0t = scratch.get<double>(4, static_cast<std::size_t>(n_r) * nb, stream);
+  T* pv = a.want_values ? scratch.get<T>(0, static_cast<std::size_t>(na) * nr, stream) : nullptr;
+  std::uint8_t* pa = a.want_values ? scratch.get<std::uint8_t>(1, static_cast<std::size_t>(na) * nr, stream) : nullptr;
+  count_launches(a.want_values ? 3 : 2);
+  {
+    MainKernelScope prof(stream);
+#define PVI_BF(MM, NBX)                                                                            \
+  if (M == MM && nb <= NBX) {                                                                      \
+    cudaFuncSetAttribute(k_b_fact_w<T, MM, NBX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+    cudaFuncSetAttribute(k_b_fact_q<T, MM, NBX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+    k_b_fact_w<T, MM, NBX><<<static_cast<unsigned>(n_r), 256, sm1, stream>>>(                       \
+        dm, a.v, W, v0t, dc.b_order_b, static_cast<int>(n_xb), static_cast<int>(n_bp), static_cast<int>(n_r)); \
+    k_b_fact_q<T, MM, NBX><<<dim3(static_cast<unsigned>(n_xb), static_cast<unsigned>(na)), 256, sm2, stream>>>( \
+        dm, W, v0t, dc.b_erpt, dc.b_order_a, pv, pa, a.qout, lo, hi, a.gamma, static_cast<int>(n_xa), \
+        static_cast<int>(n_xb), static_cast<int>(n_ap), static_cast<int>(n_r));                  \
+  } else
+    PVI_BF(2, 16) PVI_BF(2, 32) PVI_BF(3, 16) PVI_BF(3, 32) {
+      return false;
+    }
+#undef PVI_BF
+  }
+  PVI_CUDA(cudaGetLastError());
+  if (a.want_values)
+    k_finalize<T><<<grid_for(nr, 256), 256, 0, stream>>>(pv, pa, na, nb, a.v, a.vout, a.act, lo, hi,
+                                                        a.out_off, a.fa);
+  PVI_CUDA(cudaGetLastError());
+  return true;
+}
+
 template <typename T>
 void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
                   Scratch& scratch, cudaStream_t stream) {
@@ -881,6 +1185,7 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
       break;
     }
     case PVI_SCENARIO_B: {
+      if (a.algorithm == 1 && launch_b_factored<T>(model, dm, a, scratch, stream)) break;
       const int tile = dm.b_tile;
       const std::uint64_t t0 = lo / tile, t1 = (hi + tile - 1) / tile;
       const unsigned block = static_cast<unsigned>((tile + 31) / 32 * 32);

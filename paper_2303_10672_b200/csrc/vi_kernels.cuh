@@ -29,6 +29,7 @@ struct SweepArgs {
   std::uint64_t lo = 0, hi = 0, out_off = 0;
   double gamma = 0.0;
   bool want_values = true;       // false: Q rows only (B/C skip the partial buffers)
+  int algorithm = 0;             // 0 exact (reference order, bit-identical), 1 factored
   FinalizeArgs fa;
 };
 

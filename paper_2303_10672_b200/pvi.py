@@ -88,6 +88,7 @@ _BY_STATUS = {c.status: c for c in (Error, ParameterError, ConfigError, Indexing
 
 VALUE_SPAN, CHANGE_SPAN, PERIODIC_SPAN = 0, 1, 2
 _TEST_NAMES = {"value_span": 0, "change_span": 1, "periodic_span": 2}
+_ALGOS = {"exact": 0, "factored": 1}
 
 
 def _err_buf():
@@ -267,6 +268,13 @@ class Model:
         _raise(L.load().pvi_model_initial_values(self._h, _p(out), err, len(err)), err)
         return out
 
+    def set_algorithm(self, algorithm: str) -> "Model":
+        """'exact' (reference order, bit-identical) or 'factored' (Scenario B:
+        separable issued-pair contraction, agrees to rounding)."""
+        _raise(L.load().pvi_model_set_algorithm(self._h, _ALGOS[algorithm]), None)
+        self.algorithm = algorithm
+        return self
+
     def partition(self, parts: int) -> np.ndarray:
         b = np.zeros(parts + 1, np.uint64)
         _raise(L.load().pvi_partition(self._h, parts, _p(b)), None)
@@ -343,6 +351,7 @@ class ViConfig:
     max_states: int = 200_000_000
     device: int = -1
     sweeps_per_sync: int = 1
+    algorithm: Optional[str] = None  # None: the model's (Model.set_algorithm)
 
     def to_c(self) -> L.ViConfigC:
         c = L.ViConfigC()
@@ -361,6 +370,7 @@ class ViConfig:
         c.max_states = self.max_states
         c.device = self.device
         c.sweeps_per_sync = self.sweeps_per_sync
+        c.algorithm = -1 if self.algorithm is None else _ALGOS[self.algorithm]
         return c
 
 

@@ -17,8 +17,9 @@ ap.add_argument("--workload", default="b/m3/exp1")
 ap.add_argument("--frac", type=float, default=1 / 64)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--precision", default="f64")
+ap.add_argument("--algorithm", default="exact")
 a = ap.parse_args()
-m = P.make_preset(a.workload)
+m = P.make_preset(a.workload).set_algorithm(a.algorithm)
 n = m.state_count()
 cnt = max(1, int(n * a.frac))
 lo = (n // 2) // 4096 * 4096
