@@ -515,6 +515,18 @@ __global__ void __launch_bounds__(256) k_b_erpt(DevModel dm, double* __restrict_
   erpt[n + s] = pt;
 }
 
+// Shared-memory [row][o_b] slabs: odd row stride, and row r stored at
+// r + (r >> 4), so rows that differ only above the low 4 bits of the aged
+// profile index (the same low aged digit) fall into different banks.
+__host__ __device__ inline int slab_stride(int nb) { return nb | 1; }
+__host__ __device__ inline int slab_row(int r) { return r + (r >> 4); }
+__host__ __device__ inline int slab_rows(int n) { return n + (n >> 4) + 1; }
+
+// While the demand stays within the oldest bucket x_1, FIFO issuing only
+// consumes units that expire tonight, so the aged profile is unchanged:
+// every h <= x_1 maps to the same next-state digits.  Both stages merge that
+// block into one weighted term (prefix sums of the issued-law weights).
+
 // Stage 1: W[x_b][r][o_b].  grid.x = r (na^M values), threads stride over x_b.
 template <typename T, int M, int NBX>
 __global__ void __launch_bounds__(256) k_b_fact_w(DevModel dm, const T* __restrict__ V,
@@ -522,20 +534,22 @@ __global__ void __launch_bounds__(256) k_b_fact_w(DevModel dm, const T* __restri
                                                   double* __restrict__ v0t,
                                                   const std::uint16_t* __restrict__ order_b,
                                                   int n_xb, int n_bp, int n_r) {
-  extern __shared__ double slab[];  // [bp][ob], row stride nb|1
+  extern __shared__ double slab[];  // [bp][ob]
   const int nb = dm.b_nb;
-  const int stride = nb | 1;
+  const int stride = slab_stride(nb);
   const int r = blockIdx.x;
   const std::uint64_t base = static_cast<std::uint64_t>(r) * n_xb;  // r * nb^M
   for (int i = threadIdx.x; i < nb * n_bp; i += blockDim.x) {
     const int ob = i / n_bp, bp = i % n_bp;
-    slab[bp * stride + ob] = static_cast<double>(V[base + static_cast<std::uint64_t>(ob) * n_bp + bp]);
+    slab[slab_row(bp) * stride + ob] = static_cast<double>(V[base + static_cast<std::uint64_t>(ob) * n_bp + bp]);
+  }
+  __shared__ double s_pmf_b[128], s_cdf_b[128];
+  for (int i = threadIdx.x; i < 128 && i < dm.b_len_b; i += blockDim.x) {
+    s_pmf_b[i] = dm.b_pmf_b[i];
+    s_cdf_b[i] = dm.b_cdf_b[i];
   }
   __syncthreads();
   if (threadIdx.x < nb) v0t[static_cast<std::size_t>(r) * nb + threadIdx.x] = slab[threadIdx.x];
-  __shared__ double s_pmf_b[128];
-  for (int i = threadIdx.x; i < 128 && i < dm.b_len_b; i += blockDim.x) s_pmf_b[i] = dm.b_pmf_b[i];
-  __syncthreads();
   for (int t = threadIdx.x; t < n_xb; t += blockDim.x) {
     const int xbi = order_b[t];
     int xb[M + 1];
@@ -552,19 +566,34 @@ __global__ void __launch_bounds__(256) k_b_fact_w(DevModel dm, const T* __restri
     double acc[NBX];
 #pragma unroll
     for (int ob = 0; ob < NBX; ++ob) acc[ob] = 0.0;
-    for (int hb = 0; hb < ib; ++hb) {
-      int bp = 0, prefix = 0, w = 1;
+    if (ib > 0) {
+      // merged block h_b = 0..min(x_1, I_b - 1): aged profile (x_2..x_M)
+      const int h0 = min(xb[1], ib - 1);
+      int bp = 0, w = 1;
 #pragma unroll
       for (int j = 1; j <= M - 1; ++j) {
-        prefix += xb[j];
-        bp += ipos(xb[j + 1] - ipos(hb - prefix)) * w;
+        bp += xb[j + 1] * w;
         w *= nb;
       }
-      const double pw = hb < 128 ? s_pmf_b[hb] : dm.b_pmf_b[hb];
-      const double* row = slab + bp * stride;
+      const double pw = s_cdf_b[h0];
+      const double* row = slab + slab_row(bp) * stride;
 #pragma unroll
       for (int ob = 0; ob < NBX; ++ob)
-        if (ob < nb) acc[ob] = fma(pw, row[ob], acc[ob]);
+        if (ob < nb) acc[ob] = pw * row[ob];
+      for (int hb = h0 + 1; hb < ib; ++hb) {
+        int bq = 0, prefix = 0, wq = 1;
+#pragma unroll
+        for (int j = 1; j <= M - 1; ++j) {
+          prefix += xb[j];
+          bq += ipos(xb[j + 1] - ipos(hb - prefix)) * wq;
+          wq *= nb;
+        }
+        const double pw2 = hb < 128 ? s_pmf_b[hb] : dm.b_pmf_b[hb];
+        const double* row2 = slab + slab_row(bq) * stride;
+#pragma unroll
+        for (int ob = 0; ob < NBX; ++ob)
+          if (ob < nb) acc[ob] = fma(pw2, row2[ob], acc[ob]);
+      }
     }
     double* out = W + (static_cast<std::size_t>(xbi) * n_r + r) * nb;
 #pragma unroll
@@ -574,8 +603,10 @@ __global__ void __launch_bounds__(256) k_b_fact_w(DevModel dm, const T* __restri
 }
 
 // Stage 2: Q for states [lo, hi).  grid = (x_b, o_a), threads stride over x_a.
+// The two inner products (W with alpha, V[.,.,0] with g) share one
+// accumulator per order_b: U = sum_ha alpha W + (sf_b g) V0.
 template <typename T, int M, int NBX>
-__global__ void __launch_bounds__(256) k_b_fact_q(DevModel dm, const double* __restrict__ W,
+__global__ void __launch_bounds__(256, 2) k_b_fact_q(DevModel dm, const double* __restrict__ W,
                                                   const double* __restrict__ v0t,
                                                   const double* __restrict__ erpt,
                                                   const std::uint16_t* __restrict__ order_a,
@@ -586,18 +617,16 @@ __global__ void __launch_bounds__(256) k_b_fact_q(DevModel dm, const double* __r
                                                   int n_xb, int n_ap, int n_r) {
   extern __shared__ double sm[];
   const int nb = dm.b_nb, na = dm.b_na;
-  const int stride = nb | 1;
+  const int stride = slab_stride(nb);
+  const int rows = slab_rows(n_ap);
   double* w_sl = sm;                        // [ap][ob]
-  double* v0_sl = sm + n_ap * stride;       // [ap][ob]
+  double* v0_sl = sm + rows * stride;       // [ap][ob], pre-scaled by sf_b(I_b)
+  double* s_al = v0_sl + rows * stride;     // pmf_a[0..dn)
+  double* s_g = s_al + dm.b_dn;             // pz(I_b, 0..dn)
+  double* s_cal = s_g + dm.b_dn;            // cdf_a[0..dn)
+  double* s_cg = s_cal + dm.b_dn;           // pz_cum(I_b, 0..dn)
   const int xbi = blockIdx.x;
   const int oa = blockIdx.y;
-  const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
-  for (int i = threadIdx.x; i < n_ap * nb; i += blockDim.x) {
-    const int ap = i / nb, ob = i % nb;
-    w_sl[ap * stride + ob] = W[(static_cast<std::size_t>(xbi) * n_r + r0 + ap) * nb + ob];
-    v0_sl[ap * stride + ob] = v0t[(r0 + ap) * nb + ob];
-  }
-  __syncthreads();
   int xb[M + 1];
   int ib = 0;
   {
@@ -611,7 +640,19 @@ __global__ void __launch_bounds__(256) k_b_fact_q(DevModel dm, const double* __r
   }
   const double sfb = dm.b_sf_b[ib];
   const int dnp = dm.b_dn;
-  const double* pz_row = dm.b_pz + ib * dnp;
+  const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
+  for (int i = threadIdx.x; i < n_ap * nb; i += blockDim.x) {
+    const int ap = i / nb, ob = i % nb;
+    w_sl[slab_row(ap) * stride + ob] = W[(static_cast<std::size_t>(xbi) * n_r + r0 + ap) * nb + ob];
+    v0_sl[slab_row(ap) * stride + ob] = sfb * v0t[(r0 + ap) * nb + ob];
+  }
+  for (int i = threadIdx.x; i < dnp; i += blockDim.x) {
+    s_al[i] = dm.b_pmf_a[i];
+    s_g[i] = dm.b_pz[ib * dnp + i];
+    s_cal[i] = dm.b_cdf_a[i];
+    s_cg[i] = dm.b_pz_cum[ib * dnp + i];
+  }
+  __syncthreads();
   const std::uint64_t n = dm.n_states;
   const std::uint64_t nr = hi - lo;
   const double cva_oa = dm.b_cva * oa;
@@ -630,10 +671,30 @@ __global__ void __launch_bounds__(256) k_b_fact_q(DevModel dm, const double* __r
         ia += xa[j];
       }
     }
-    double acc1[NBX], acc2[NBX];
+    double acc[NBX];
+    {
+      // merged block h_a = 0..min(x_1, I_a): aged A digits (x_2..x_M)
+      int ap = 0, w = 1;
 #pragma unroll
-    for (int ob = 0; ob < NBX; ++ob) acc1[ob] = acc2[ob] = 0.0;
-    for (int ha = 0; ha <= ia; ++ha) {
+      for (int j = 1; j <= M - 1; ++j) {
+        ap += xa[j + 1] * w;
+        w *= na;
+      }
+      double al, g;
+      if (xa[1] < ia) {  // h_a = 0..x_1, all interior
+        al = s_cal[xa[1]];
+        g = s_cg[xa[1] + 1];
+      } else {           // the whole stock is in the oldest bucket: h_a = 0..I_a
+        al = (ia > 0 ? s_cal[ia - 1] : 0.0) + dm.b_sf_a[ia];
+        g = s_cg[ia] + (1.0 - s_cg[ia]);
+      }
+      const double* wr = w_sl + slab_row(ap) * stride;
+      const double* vr = v0_sl + slab_row(ap) * stride;
+#pragma unroll
+      for (int ob = 0; ob < NBX; ++ob)
+        if (ob < nb) acc[ob] = fma(al, wr[ob], g * vr[ob]);
+    }
+    for (int ha = xa[1] + 1; ha <= ia; ++ha) {
       int ap = 0, prefix = 0, w = 1;
 #pragma unroll
       for (int j = 1; j <= M - 1; ++j) {
@@ -642,16 +703,13 @@ __global__ void __launch_bounds__(256) k_b_fact_q(DevModel dm, const double* __r
         w *= na;
       }
       const bool interior = ha < ia;
-      const double al = interior ? __ldg(dm.b_pmf_a + ha) : __ldg(dm.b_sf_a + ia);
-      const double g = interior ? __ldg(pz_row + ha) : 1.0 - __ldg(dm.b_pz_cum + ib * dnp + ia);
-      const double* wr = w_sl + ap * stride;
-      const double* vr = v0_sl + ap * stride;
+      const double al = interior ? s_al[ha] : dm.b_sf_a[ia];
+      const double g = interior ? s_g[ha] : 1.0 - s_cg[ia];
+      const double* wr = w_sl + slab_row(ap) * stride;
+      const double* vr = v0_sl + slab_row(ap) * stride;
 #pragma unroll
       for (int ob = 0; ob < NBX; ++ob)
-        if (ob < nb) {
-          acc1[ob] = fma(al, wr[ob], acc1[ob]);
-          acc2[ob] = fma(g, vr[ob], acc2[ob]);
-        }
+        if (ob < nb) acc[ob] = fma(al, wr[ob], fma(g, vr[ob], acc[ob]));
     }
     const double er = erpt[s], pt = erpt[n + s];
     T best = T(0);
@@ -659,8 +717,7 @@ __global__ void __launch_bounds__(256) k_b_fact_q(DevModel dm, const double* __r
 #pragma unroll
     for (int ob = 0; ob < NBX; ++ob) {
       if (ob < nb) {
-        const double u = fma(sfb, acc2[ob], acc1[ob]);
-        const double qd = fma(gamma, u, er - (cva_oa + dm.b_cvb * ob) * pt);
+        const double qd = fma(gamma, acc[ob], er - (cva_oa + dm.b_cvb * ob) * pt);
         const T qv = static_cast<T>(qd);
         if (ob == 0 || qv > best) {
           best = qv;
@@ -1058,14 +1115,16 @@ void profile_read(double* ms, std::uint64_t* main_launches, std::uint64_t* all_l
 // Factored Scenario B sweep; returns false when the geometry is not covered
 // (the caller then runs the exact kernel).
 namespace {
+// Digit blocks ordered by the factored loops' trip count: the stock above
+// the oldest bucket (x_2 + ... + x_M; the h <= x_1 block is merged).
 std::vector<std::uint16_t> digit_sum_order(int radix, int digits) {
   int n = 1;
   for (int i = 0; i < digits; ++i) n *= radix;
   std::vector<std::uint16_t> order(n);
   std::vector<int> sum(n);
   for (int v = 0; v < n; ++v) {
-    int s = 0, r = v;
-    for (int i = 0; i < digits; ++i) {
+    int s = 0, r = v / radix;  // skip x_1, the least-significant digit
+    for (int i = 1; i < digits; ++i) {
       s += r % radix;
       r /= radix;
     }
@@ -1089,9 +1148,9 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
   }
   const long long n_ap = n_xa / na, n_bp = n_xb / nb, n_r = n_xa;
   if (n_xa > 65535 || n_xb > 65535) return false;
-  const int stride = nb | 1;
-  const std::size_t sm1 = sizeof(double) * n_bp * stride;
-  const std::size_t sm2 = sizeof(double) * 2 * n_ap * stride;
+  const int stride = slab_stride(nb);
+  const std::size_t sm1 = sizeof(double) * slab_rows(static_cast<int>(n_bp)) * stride;
+  const std::size_t sm2 = sizeof(double) * (2 * slab_rows(static_cast<int>(n_ap)) * stride + 4 * dm.b_dn);
   if (sm1 > 200 * 1024 || sm2 > 200 * 1024) return false;
 
   int device = 0;

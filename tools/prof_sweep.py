@@ -18,12 +18,13 @@ ap.add_argument("--frac", type=float, default=1 / 64)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--precision", default="f64")
 ap.add_argument("--algorithm", default="exact")
+ap.add_argument("--full", action="store_true", help="sweep all states")
 a = ap.parse_args()
 m = P.make_preset(a.workload).set_algorithm(a.algorithm)
 n = m.state_count()
 cnt = max(1, int(n * a.frac))
-lo = (n // 2) // 4096 * 4096
-hi = min(n, lo + cnt)
+lo = 0 if a.full else (n // 2) // 4096 * 4096
+hi = n if a.full else min(n, lo + cnt)
 V = m.initial_values().astype(np.float32 if a.precision == "f32" else np.float64)
 for r in range(a.reps):
     t = time.perf_counter()
