@@ -834,6 +834,126 @@ __global__ void __launch_bounds__(128) k_sweep_c(DevModel dm, const T* __restric
   if (qout) qout[(s - lo) * na + a] = qa;
 }
 
+// ---------------------------------------------------------------------------
+// K1-C factored ("algorithm = factored"; agrees with the reference to
+// rounding).  The demand sum only depends on the post-delivery profile
+// z = (min(x_1+y_1,cap), .., min(x_{m-1}+y_{m-1},cap), y_m):
+//
+//   Q(s,a) = fixed(a) PC(a) PD(tau) + sum_{c: |y_c| = a} p_c G[tau][z(x, y_c)]
+//   G[tau][z] = sum_d p_d(tau) (r0(z,d) + gamma V[next(tau, z, d)])
+//
+// (r0 = the reward without the fixed order cost, PC/PD the total composition
+// / demand mass).  Stage 1 builds G for all 7 x (A_max+1)^m profiles
+// (2.9e7 for c/m5, 21 demands each); stage 2 is one gather of G per
+// (state, order, composition): 7.2e10 instead of the reference's 1.5e12 terms.
+
+template <typename T, int M>
+__global__ void __launch_bounds__(256) k_c_fact_g(DevModel dm, const T* __restrict__ V,
+                                                  double* __restrict__ G, int n_prof,
+                                                  double gamma) {
+  const std::uint64_t gid = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int tau = blockIdx.y;
+  if (gid >= static_cast<std::uint64_t>(n_prof)) return;
+  const int cap = dm.c_max_order, r = cap + 1, dn = dm.c_dmax + 1;
+  // profile digits: zi = y_M r^(M-1) + sum_{j<M} z_j r^(j-1)
+  int z[M + 1];
+  {
+    int rem = static_cast<int>(gid);
+#pragma unroll
+    for (int j = 1; j <= M - 1; ++j) {
+      z[j] = rem % r;
+      rem /= r;
+    }
+    z[M] = rem;  // fresh units y_M
+  }
+  int sp[M + 1];
+  int prefix = 0;
+#pragma unroll
+  for (int j = 1; j <= M - 1; ++j) {
+    prefix += z[j];
+    sp[j] = prefix;
+  }
+  const int fresh = z[M];
+  const int total = prefix + fresh;
+  std::uint32_t w[M + 1];
+  {
+    std::uint32_t wk = 1;
+#pragma unroll
+    for (int j = 1; j <= M - 1; ++j) {
+      w[M - j] = wk;
+      wk *= static_cast<std::uint32_t>(r);
+    }
+    w[0] = wk;
+  }
+  const std::uint32_t tau_base = static_cast<std::uint32_t>((tau + 1) % 7) * w[0];
+  const double* pmf = dm.c_pmf + tau * dn;
+  double acc = 0.0;
+  for (int d = 0; d < dn; ++d) {
+    std::uint32_t idx = tau_base;
+#pragma unroll
+    for (int j = 1; j <= M - 2; ++j)
+      idx += static_cast<std::uint32_t>(max(min(sp[j + 1] - d, z[j + 1]), 0)) * w[M - j];
+    idx += static_cast<std::uint32_t>(max(min(total - d, fresh), 0)) * w[1];
+    const double r0 = -dm.c_ch * ipos(total - d) - dm.c_cs * ipos(d - total) - dm.c_cw * ipos(z[1] - d);
+    acc = fma(__ldg(pmf + d), fma(gamma, static_cast<double>(__ldg(V + idx)), r0), acc);
+  }
+  G[static_cast<std::size_t>(tau) * n_prof + gid] = acc;
+}
+
+// Stage 2: thread = (state, order); heaviest order first.
+template <typename T, int M>
+__global__ void __launch_bounds__(128) k_c_fact_q(DevModel dm, const double* __restrict__ G,
+                                                  T* __restrict__ part_v, T* __restrict__ qout,
+                                                  std::uint64_t lo, std::uint64_t hi, int n_prof) {
+  const int cap = dm.c_max_order, r = cap + 1, dn = dm.c_dmax + 1;
+  const int na = static_cast<int>(dm.n_actions);
+  const int a = na - 1 - static_cast<int>(blockIdx.y);
+  const std::uint64_t s = lo + static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= hi) return;
+  int x[M + 1];
+  int tau;
+  {
+    std::uint32_t rem = static_cast<std::uint32_t>(s);
+#pragma unroll
+    for (int j = 1; j <= M - 1; ++j) {
+      x[j] = static_cast<int>(rem % r);
+      rem /= r;
+    }
+    tau = static_cast<int>(rem);
+  }
+  const double* g = G + static_cast<std::size_t>(tau) * n_prof;
+  std::uint32_t wz[M + 1];  // profile digit weights: z_j -> r^(j-1), y_M -> r^(M-1)
+  {
+    std::uint32_t wk = 1;
+#pragma unroll
+    for (int j = 1; j <= M; ++j) {
+      wz[j] = wk;
+      wk *= static_cast<std::uint32_t>(r);
+    }
+  }
+  const std::uint32_t off = dm.c_offsets[a];
+  const std::uint32_t n_c = dm.c_offsets[a + 1] - off;
+  double acc = 0.0, pc_sum = 0.0;
+  for (std::uint32_t c = 0; c < n_c; ++c) {
+    const std::uint32_t id = __ldg(dm.c_ids + off + c);
+    const double prob = __ldg(dm.c_probs + off + c);
+    const std::int8_t* yt = dm.c_comp + static_cast<std::size_t>(id) * M;
+    std::uint32_t zi = static_cast<std::uint32_t>(yt[0]) * wz[M];
+#pragma unroll
+    for (int j = 1; j <= M - 1; ++j)
+      zi += static_cast<std::uint32_t>(min(x[j] + static_cast<int>(yt[M - j]), cap)) * wz[j];
+    acc = fma(prob, __ldg(g + zi), acc);
+    pc_sum += prob;
+  }
+  double pd_sum = 0.0;
+  for (int d = 0; d < dn; ++d) pd_sum += __ldg(dm.c_pmf + tau * dn + d);
+  const double fixed = a > 0 ? -dm.c_cf : 0.0;
+  const T qa = static_cast<T>(fma(fixed * pc_sum, pd_sum, acc));
+  const std::uint64_t nr = hi - lo;
+  if (part_v) part_v[static_cast<std::uint64_t>(a) * nr + (s - lo)] = qa;
+  if (qout) qout[(s - lo) * na + a] = qa;
+}
+
 // Generic Scenario C kernel for any (m, D_max): one thread per
 // (state, order, demand), so no demand-indexed register array is needed.
 // Writes inner_d into `inner_out` ((a, d, state) layout); k_reduce_c then
@@ -1210,6 +1330,40 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
 }
 
 template <typename T>
+bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
+                       Scratch& scratch, cudaStream_t stream) {
+  (void)model;
+  const int M = dm.c_m, r = dm.c_max_order + 1;
+  long long n_prof = 1;
+  for (int i = 0; i < M; ++i) n_prof *= r;
+  if (n_prof * 7 > (1ll << 31)) return false;
+  const std::uint64_t lo = a.lo, hi = a.hi, nr = hi - lo;
+  const int na = static_cast<int>(dm.n_actions);
+  double* G = scratch.get<double>(5, static_cast<std::size_t>(n_prof) * 7, stream);
+  T* pv = a.want_values ? scratch.get<T>(0, static_cast<std::size_t>(na) * nr, stream) : nullptr;
+  bool done = false;
+  {
+    MainKernelScope prof(stream);
+#define PVI_CF(MM)                                                                               \
+  if (!done && M == MM) {                                                                        \
+    k_c_fact_g<T, MM><<<dim3(grid_for(n_prof, 256), 7), 256, 0, stream>>>(dm, a.v, G, static_cast<int>(n_prof), a.gamma); \
+    k_c_fact_q<T, MM><<<dim3(grid_for(nr, 128), na), 128, 0, stream>>>(dm, G, pv, a.qout, lo, hi, static_cast<int>(n_prof)); \
+    done = true;                                                                                 \
+  }
+    PVI_CF(2) PVI_CF(3) PVI_CF(4) PVI_CF(5) PVI_CF(6)
+#undef PVI_CF
+  }
+  if (!done) return false;
+  count_launches(a.want_values ? 3 : 2);
+  PVI_CUDA(cudaGetLastError());
+  if (a.want_values)
+    k_finalize<T><<<grid_for(nr, 256), 256, 0, stream>>>(pv, nullptr, na, 1, a.v, a.vout, a.act, lo, hi,
+                                                        a.out_off, a.fa);
+  PVI_CUDA(cudaGetLastError());
+  return true;
+}
+
+template <typename T>
 void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
                   Scratch& scratch, cudaStream_t stream) {
   const std::uint64_t lo = a.lo, hi = a.hi, nr = hi - lo;
@@ -1301,6 +1455,7 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
       break;
     }
     case PVI_SCENARIO_C: {
+      if (a.algorithm == 1 && launch_c_factored<T>(model, dm, a, scratch, stream)) break;
       const int na = static_cast<int>(dm.n_actions);
       T* pv = a.want_values ? scratch.get<T>(0, static_cast<std::size_t>(na) * nr, stream) : nullptr;
       const int dn = dm.c_dmax + 1;

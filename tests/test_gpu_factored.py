@@ -74,3 +74,37 @@ def test_factored_q_rows_close_to_exact(pvi, preset, prec):
     qf = pvi.q_rows(fact, V, lo, hi, precision=prec).astype(np.float64)
     tol = 1e-12 if prec == "f64" else 2e-6
     np.testing.assert_allclose(qf, qe, rtol=tol, atol=tol)
+
+
+# --- Scenario C: demand summed per post-delivery profile first ------------
+
+@pytest.mark.parametrize("preset", ["c/m3/exp1", "c/m3/exp2"])
+def test_factored_c_solve_matches_reference(pvi, preset):
+    m = pvi.make_preset(preset).set_algorithm("factored")
+    res = pvi.run_value_iteration(m)
+    key = f"solve|{preset}|f64"
+    it, conv = GOLD[key + "|meta"]
+    assert res.iterations == it and res.converged == bool(conv)
+    np.testing.assert_allclose(res.values, GOLD[key + "|values"], rtol=1e-12, atol=0)
+    _near_tie_ok(pvi, preset, res.values, res.policy, GOLD[key + "|policy"])
+
+
+@pytest.mark.parametrize("preset", ["c/m5/exp1", "c/m5/exp2", "c/m3/exp2"])
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_factored_c_q_rows_close_to_exact(pvi, preset, prec):
+    exact = pvi.make_preset(preset)
+    fact = pvi.make_preset(preset).set_algorithm("factored")
+    n = exact.state_count()
+    V = np.random.default_rng(9).uniform(-50.0, 50.0, n)
+    lo = n // 2
+    hi = min(n, lo + 512)
+    qe = pvi.q_rows(exact, V, lo, hi, precision=prec).astype(np.float64)
+    qf = pvi.q_rows(fact, V, lo, hi, precision=prec).astype(np.float64)
+    tol = 1e-12 if prec == "f64" else 2e-6
+    np.testing.assert_allclose(qf, qe, rtol=tol, atol=tol * 100)
+    golden = GOLD.get(f"qrow|{preset}|q") if f"qrow|{preset}|q" in GOLD.files else None
+    if golden is not None and prec == "f64":
+        V7 = np.random.default_rng(7).uniform(-5.0, 5.0, n)
+        for i, s in enumerate(GOLD[f"qrow|{preset}|states"]):
+            q = pvi.q_rows(fact, V7, int(s), int(s) + 1)[0]
+            np.testing.assert_allclose(q, golden[i], rtol=1e-12, atol=1e-12)
