@@ -42,7 +42,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="b/m3/exp1")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
-    ap.add_argument("--algorithm", default="exact", choices=["exact", "factored"])
+    ap.add_argument("--algorithm", default="factored", choices=["exact", "factored"])
+    ap.add_argument("--no-alt", action="store_true", help="skip timing the other algorithm")
+    ap.add_argument("--no-simopt", action="store_true")
     ap.add_argument("--no-solve", action="store_true", help="skip the time-to-converge solve")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -243,6 +245,33 @@ def workload_config(model, args, world):
             "parallelism": f"state-shards x{world} (cost-weighted, NCCL all-gather)"}
 
 
+def factored_fmas(model) -> float:
+    """FP64 FMAs the factored kernels execute per sweep (both stages), from
+    their loop bounds: the work the algorithm actually does."""
+    sc = model.scenario()
+    if sc == "b":
+        m = model.state_arity() // 2
+        na, nb = model.info.max_order_a + 1, model.info.max_order_b + 1
+
+        def loops(radix, boundary):
+            v = np.arange(radix ** m)
+            digits = [(v // radix ** k) % radix for k in range(m)]  # digits[0] = x_1
+            tot = sum(digits)
+            above = tot - digits[0]
+            if boundary:  # stage 2: h_a = x_1+1..I_a plus the merged block
+                return float(np.sum(above + 1))
+            return float(np.sum(np.where(tot > 0, above + 1 - (digits[0] >= tot), 0)))
+        stage1 = na ** m * loops(nb, False) * nb
+        stage2 = nb ** m * na * loops(na, True) * nb * 2
+        return stage1 + stage2
+    if sc == "c":
+        r = model.info.max_order_a + 1
+        m = model.state_arity()
+        prof = 7 * r ** m * 21
+        return prof + model.state_count() * model.terms_per_sweep() / model.state_count() / 21
+    return model.terms_per_sweep()
+
+
 def ours_arm(args, world, rank, local):
     import torch
     import torch.distributed as dist
@@ -252,10 +281,9 @@ def ours_arm(args, world, rank, local):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    model = P.make_preset(args.workload).set_algorithm(args.algorithm)
+    model = P.make_preset(args.workload)
     n = model.state_count()
     cfg = P.ViConfig(precision=args.precision)
-    solver = ShardedValueIteration(model, cfg)
     dt = torch.float32 if args.precision == "f32" else torch.float64
     v0 = model.initial_values()
     vprev = torch.as_tensor(v0, device="cuda").to(dt)
@@ -272,30 +300,36 @@ def ours_arm(args, world, rank, local):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        solver.step(vprev, vnext, stats, test, hist)
-    barrier()
+    def timed(algorithm, steps, warmup, clocks=None):
+        model.set_algorithm(algorithm)
+        solver = ShardedValueIteration(model, cfg)
+        for _ in range(warmup):
+            solver.step(vprev, vnext, stats, test, hist)
+        barrier()
+        if clocks:
+            clocks.start()
+        P.profile_enable(True)
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        barrier()
+        for k in range(steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            starts[k].record()
+            solver.step(vprev, vnext, stats, test, hist)
+            ends[k].record()
+        barrier()
+        kernel_ms, k_launches, all_launches = P.profile_read()
+        P.profile_enable(False)
+        clk = clocks.stop() if clocks else None
+        step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+        total = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(total, op=dist.ReduceOp.MAX)
+        return solver, float(total.item()), step_ms, kernel_ms, k_launches, all_launches, clk
 
     clocks = Clocks(local)
-    clocks.start()
-    P.profile_enable(True)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    barrier()
-    for k in range(args.steps):
-        flush.zero_()
-        starts[k].record()
-        solver.step(vprev, vnext, stats, test, hist)
-        ends[k].record()
-    barrier()
-    kernel_ms, k_launches, all_launches = P.profile_read()
-    P.profile_enable(False)
-    clk = clocks.stop()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
-    total_ms = float(total_ms.item())
+    solver, total_ms, step_ms, kernel_ms, k_launches, all_launches, clk = timed(
+        args.algorithm, args.steps, args.warmup, clocks)
     terms = model.terms_per_sweep()
     value = terms * args.steps / (total_ms * 1e-3)
 
@@ -313,39 +347,67 @@ def ours_arm(args, world, rank, local):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
-            tj = json.load(f)
-            if tj.get("workload") == args.workload and tj.get("precision") == args.precision:
-                traffic = tj.get("dram_bytes_per_launch")
-    except OSError:
+            for tj in json.load(f):
+                if (tj.get("workload"), tj.get("precision"), tj.get("algorithm")) == \
+                        (args.workload, args.precision, args.algorithm):
+                    traffic = tj.get("dram_bytes_per_launch")
+    except (OSError, ValueError, AttributeError):
         pass
+    kernel_s = kernel_ms * 1e-3 / max(k_launches, 1)
     roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                 "frac": achieved_gbs / peak, "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)" if peaks else
                 "fallback 6650 GB/s (B200_PROFILING.md)",
-                "algorithmic_bytes": f"{bpt} B (one V[next] gather) per reference term; "
-                                     f"{shard_terms:.4e} terms per launch",
+                "algorithmic_bytes": f"{bpt} B (one V[next] gather) per reference term "
+                                     f"(SURVEY 8d); {shard_terms:.4e} terms per launch",
                 "kernel_ms_per_launch": kernel_ms / max(k_launches, 1),
                 "kernel_share_of_step": (kernel_ms / max(sum(step_ms), 1e-9)),
-                "fp64_pipe_note": "V (128 MiB) is L2/L1-resident across the 141k reuses per "
-                                  "element, so the gather roofline is an upper bound on bytes, "
-                                  "not the binding limit; see DESIGN.md"}
+                "note": "V is L1/L2-resident (re-read ~141k times per element per sweep); "
+                        "frac > 1 means the reference-term bytes never reach HBM. With the "
+                        "factored algorithm the kernel also does far fewer operations than "
+                        "reference terms; compute_roofline below is its real work. DESIGN.md 4-5."}
+    fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12  # 2:1 FP32:FP64 (ncu), nominal clock
+    if args.algorithm == "factored":
+        flops = 2.0 * factored_fmas(model) * (shard_terms / terms)
+    else:
+        flops = 5.0 * shard_terms  # the reference's 5 unfused f64 ops per term
+    compute = {"unit": "TFLOP/s (FP64)", "achieved": flops / kernel_s / 1e12 if kernel_ms else 0.0,
+               "peak": fp64_peak, "flops_per_launch": flops,
+               "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (nominal, not measured)"}
+    compute["frac"] = compute["achieved"] / fp64_peak
 
     line = {"metric": "bellman_evals_per_sec", "value": value, "unit": "evals/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": args.precision,
             "data": "synthetic (deterministic preset tables; V = initial value)",
-            "config": workload_config(model, args, world), "clocks": clk,
-            "gpu_launches": int(all_launches), "roofline": roofline}
+            "config": dict(workload_config(model, args, world), algorithm=args.algorithm),
+            "clocks": clk, "gpu_launches": int(all_launches), "roofline": roofline,
+            "compute_roofline": compute}
+
+    # the other algorithm on the same data (exact = bit-identical to the reference)
+    if not args.no_alt:
+        alt = "exact" if args.algorithm == "factored" else "factored"
+        if model.scenario() in ("b", "c") or alt == "exact":
+            _, t_alt, _, k_alt, kl_alt, _, _ = timed(alt, 2, 1)
+            line["alternate"] = {"algorithm": alt, "ms_per_step": t_alt / 2,
+                                 "value": terms * 2 / (t_alt * 1e-3), "unit": "evals/s",
+                                 "kernel_ms_per_launch": k_alt / max(kl_alt, 1)}
+        model.set_algorithm(args.algorithm)
 
     # e2e: the reference-facing call with HOST buffers, copies inside the timing
     if not args.no_e2e:
-        vh = np.ascontiguousarray(v0.astype(np.float32 if args.precision == "f32" else np.float64))
-        P.bellman_backup_batch(model, vh, solver.lo, solver.hi, precision=args.precision)
+        # pinned host buffers, as a serving caller would hold them
+        vh = torch.as_tensor(v0).to(dt).pin_memory().numpy()
+        ov = torch.empty(solver.hi - solver.lo, dtype=dt).pin_memory().numpy()
+        oa = torch.empty(solver.hi - solver.lo, dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+        P.bellman_backup_batch(model, vh, solver.lo, solver.hi, precision=args.precision,
+                               out_values=ov, out_actions=oa)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            P.bellman_backup_batch(model, vh, solver.lo, solver.hi, precision=args.precision)
+            P.bellman_backup_batch(model, vh, solver.lo, solver.hi, precision=args.precision,
+                                   out_values=ov, out_actions=oa)
         el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
@@ -358,11 +420,23 @@ def ours_arm(args, world, rank, local):
     # wall time to converge (the second half of the BASELINE metric)
     if not args.no_solve:
         barrier()
-        res = solver.solve()
+        res = ShardedValueIteration(model, cfg).solve()
         line["solve"] = {"preset": args.workload, "iterations": res.iterations,
                          "converged": res.converged, "wall_seconds": res.wall_seconds,
-                         "sweep_seconds": res.sweep_seconds,
+                         "sweep_seconds": res.sweep_seconds, "algorithm": args.algorithm,
                          "checkpoints": "off (the reference cmd_solve writes one per sweep)"}
+
+    # simulation optimisation (config 5): the reference GA on b/m2/exp1 with
+    # 4096 rollouts per candidate, every generation scored in one device batch
+    if rank == 0 and world == 1 and not args.no_simopt:
+        so = P.simopt(P.make_preset("b/m2/exp1"), rollouts_per_candidate=4096, base_seed=42,
+                      seed=1)
+        days = len(so.log) * 4096 * 465
+        line["simopt"] = {"preset": "b/m2/exp1", "sampler": "ga", "best": so.best,
+                          "best_mean": so.best_mean, "generations": so.generations,
+                          "candidates": len(so.log), "wall_seconds": so.wall_seconds,
+                          "device_seconds": so.device_seconds,
+                          "rollout_days_per_s": days / max(so.device_seconds, 1e-9)}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import refbind as R
@@ -376,6 +450,10 @@ def ours_arm(args, world, rank, local):
             if "solve" in line:
                 line["cpu_baseline"]["extrapolated_solve_seconds"] = (
                     line["solve"]["iterations"] + 1) * terms / rate
+            if "simopt" in line:
+                r = R.simopt("b/m2/exp1", rollouts=4096, eval_seed=42, ga_seed=1,
+                             threads=threads)
+                line["cpu_baseline"]["simopt_b_m2_exp1_seconds"] = r["wall"]
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

@@ -462,12 +462,15 @@ def profile_read():
 
 
 def bellman_backup_batch(model: Model, values, lo: int, hi: int, gamma: Optional[float] = None,
-                         precision: str = "f64"):
-    """(values[hi-lo], actions[hi-lo]) of one synchronous backup (vi.hpp:82-92)."""
+                         precision: str = "f64", out_values: Optional[np.ndarray] = None,
+                         out_actions: Optional[np.ndarray] = None):
+    """(values[hi-lo], actions[hi-lo]) of one synchronous backup (vi.hpp:82-92).
+    out_values / out_actions may be caller-owned (e.g. pinned) host arrays."""
     dt = _dtype(precision)
     v = np.ascontiguousarray(values, dt)
-    ov = np.zeros(hi - lo, dt)
-    oa = np.zeros(hi - lo, np.uint32)
+    ov = np.zeros(hi - lo, dt) if out_values is None else out_values
+    oa = np.zeros(hi - lo, np.uint32) if out_actions is None else out_actions
+    assert ov.dtype == dt and oa.dtype == np.uint32 and len(ov) == len(oa) == hi - lo
     err = _err_buf()
     g = model.discount() if gamma is None else gamma
     _raise(L.load().pvi_vi_backup(model.handle, int(dt == np.float32), g, _p(v), lo, hi,
