@@ -36,14 +36,35 @@ const U* upload(DeviceCopy& dc, const std::vector<U>& host) {
 
 }  // namespace
 
+// Device buffers reused across pvi_vi_backup / pvi_q_rows calls on one
+// model, so a serving caller pays for the copies and the sweep only.
+struct Workspace {
+  std::mutex mu;
+  Scratch scratch;  // sweep scratch (partials, factored tables)
+  Scratch io;       // 0: V, 1: V' slice, 2: argmax slice, 3: Q rows
+  cudaStream_t stream = nullptr;
+  Workspace() { PVI_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking)); }
+  ~Workspace() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
 Model::~Model() {
   int prev = -1;
   cudaGetDevice(&prev);
   for (auto& kv : dev) {
     cudaSetDevice(kv.first);
+    delete static_cast<Workspace*>(kv.second->workspace);
     for (void* p : kv.second->allocations) cudaFree(p);
   }
   if (prev >= 0) cudaSetDevice(prev);
+}
+
+Workspace& workspace(const Model& m, int device) {
+  DeviceCopy& dc = m.device_copy(device);
+  std::lock_guard<std::mutex> lock(m.dev_mutex);
+  if (!dc.workspace) dc.workspace = new Workspace();
+  return *static_cast<Workspace*>(dc.workspace);
 }
 
 const DevModel& Model::device_view(int device) const {
@@ -494,30 +515,31 @@ void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t
   if (lo > hi || hi > n) fail(PVI_ERR_PARAMETER, "state range out of bounds");
   const int device = select_device(-1);
   const DevModel& dm = m.device_view(device);
-  Stream stream;
-  Scratch scratch;
-  DevBuf v(n * sizeof(T));
-  PVI_CUDA(cudaMemcpyAsync(v.p, values, n * sizeof(T), cudaMemcpyHostToDevice, stream.s));
+  Workspace& ws = workspace(m, device);
+  std::lock_guard<std::mutex> lock(ws.mu);
+  cudaStream_t st = ws.stream;
+  T* v = ws.io.get<T>(0, n, st);
+  PVI_CUDA(cudaMemcpyAsync(v, values, n * sizeof(T), cudaMemcpyHostToDevice, st));
   const std::uint64_t nr = hi - lo;
-  DevBuf vo(out_values ? nr * sizeof(T) : 0);
-  DevBuf ao(out_actions ? nr * sizeof(std::uint32_t) : 0);
-  DevBuf qo(out_q ? nr * m.n_actions * sizeof(T) : 0);
+  T* vo = out_values ? ws.io.get<T>(1, nr, st) : nullptr;
+  std::uint32_t* ao = out_actions ? ws.io.get<std::uint32_t>(2, nr, st) : nullptr;
+  T* qo = out_q ? ws.io.get<T>(3, nr * m.n_actions, st) : nullptr;
   SweepArgs<T> a;
-  a.v = v.as<T>();
-  a.vout = vo.as<T>();
-  a.act = ao.as<std::uint32_t>();
-  a.qout = qo.as<T>();
+  a.v = v;
+  a.vout = vo;
+  a.act = ao;
+  a.qout = qo;
   a.lo = lo;
   a.hi = hi;
   a.out_off = lo;
   a.gamma = gamma;
   a.algorithm = m.algorithm;
   a.want_values = out_values || out_actions;
-  launch_sweep<T>(m, dm, a, scratch, stream.s);
-  if (out_values) PVI_CUDA(cudaMemcpyAsync(out_values, vo.p, nr * sizeof(T), cudaMemcpyDeviceToHost, stream.s));
-  if (out_actions) PVI_CUDA(cudaMemcpyAsync(out_actions, ao.p, nr * 4, cudaMemcpyDeviceToHost, stream.s));
-  if (out_q) PVI_CUDA(cudaMemcpyAsync(out_q, qo.p, nr * m.n_actions * sizeof(T), cudaMemcpyDeviceToHost, stream.s));
-  PVI_CUDA(cudaStreamSynchronize(stream.s));
+  launch_sweep<T>(m, dm, a, ws.scratch, st);
+  if (out_values) PVI_CUDA(cudaMemcpyAsync(out_values, vo, nr * sizeof(T), cudaMemcpyDeviceToHost, st));
+  if (out_actions) PVI_CUDA(cudaMemcpyAsync(out_actions, ao, nr * 4, cudaMemcpyDeviceToHost, st));
+  if (out_q) PVI_CUDA(cudaMemcpyAsync(out_q, qo, nr * m.n_actions * sizeof(T), cudaMemcpyDeviceToHost, st));
+  PVI_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace

@@ -98,6 +98,9 @@ struct DeviceCopy {
   double* b_erpt = nullptr;
   std::uint16_t* b_order_a = nullptr;
   std::uint16_t* b_order_b = nullptr;
+  // Per-device workspace reused by the host-buffer entry points
+  // (engine.cu Workspace: device copies of V / outputs, scratch, a stream).
+  void* workspace = nullptr;
 };
 
 struct Model {
