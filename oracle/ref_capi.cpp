@@ -457,6 +457,34 @@ int ref_tabular_brute_force(std::uint64_t ns, std::uint32_t na, std::uint64_t no
   return 0;
 }
 
+// The reference runner commands (runner.cpp:303-480), writing their files
+// into out_dir: 0 = solve, 1 = simopt, 2 = evaluate (with the VI policy CSV
+// and/or heuristic parameter file already in out_dir).  n_rollouts /
+// rollouts_per_candidate overrides are applied when > 0.
+int ref_cmd(const char* preset, int which, const char* out_dir, int threads, int n_rollouts,
+            const char* policy_csv, const char* heuristic_file, char* err, std::size_t errlen) {
+  return guarded(err, errlen, [&] {
+    ExperimentConfig cfg = make_preset(preset);
+    if (n_rollouts > 0) {
+      cfg.eval.n_rollouts = n_rollouts;
+      cfg.simopt.rollouts_per_candidate = n_rollouts;
+    }
+    RunnerOptions opt;
+    opt.output_dir = out_dir;
+    opt.threads = threads;
+    if (which == 0) {
+      (void)cmd_solve(cfg, opt);
+    } else if (which == 1) {
+      (void)cmd_simopt(cfg, opt);
+    } else {
+      std::optional<std::filesystem::path> vp, hp;
+      if (policy_csv && policy_csv[0]) vp = policy_csv;
+      if (heuristic_file && heuristic_file[0]) hp = heuristic_file;
+      (void)cmd_evaluate(cfg, opt, vp, hp);
+    }
+  });
+}
+
 // Raw Philox block (rng.hpp:15-33) and RolloutRng draws (rng.hpp:37-60).
 void ref_philox_block(const std::uint32_t* ctr, const std::uint32_t* key, std::uint32_t* out) {
   const auto o = Philox4x32::block({ctr[0], ctr[1], ctr[2], ctr[3]}, {key[0], key[1]});

@@ -7,11 +7,16 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
+#include <deque>
+#include <exception>
 #include <filesystem>
 #include <fstream>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "engine.hpp"
@@ -262,6 +267,114 @@ void load_checkpoint(const std::string& path, const std::uint8_t* expected, doub
   if (!in) fail(PVI_ERR_FORMAT, "checkpoint truncated: " + path);
 }
 
+// Asynchronous PVI1 writer: the sweep stream widens V into a
+// device slot and copies it into one of two pinned host slots; a worker
+// thread waits on the copy's event and writes the file (temp + rename)
+// while the next sweeps run.  Writes stay in iteration order; the first I/O
+// error is rethrown at the next submit or at finish().
+class AsyncCheckpointer {
+ public:
+  AsyncCheckpointer(std::string path, std::uint64_t n, const std::uint8_t fp[32])
+      : path_(std::move(path)), n_(n) {
+    std::memcpy(fp_, fp, 32);
+    PVI_CUDA(cudaGetDevice(&device_));
+    for (auto& s : slots_) {
+      PVI_CUDA(cudaMallocHost(&s.host, n * sizeof(double)));
+      PVI_CUDA(cudaMalloc(&s.dev, n * sizeof(double)));
+      PVI_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    }
+    worker_ = std::thread([this] { run(); });
+  }
+  ~AsyncCheckpointer() {
+    try {
+      finish();
+    } catch (...) {
+    }
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    if (worker_.joinable()) worker_.join();
+    for (auto& s : slots_) {
+      if (s.host) cudaFreeHost(s.host);
+      if (s.dev) cudaFree(s.dev);
+      if (s.done) cudaEventDestroy(s.done);
+    }
+  }
+  double* acquire() {
+    std::unique_lock<std::mutex> lock(mu_);
+    cur_ = (cur_ + 1) % 2;
+    cv_.wait(lock, [&] { return !slots_[cur_].busy || error_; });
+    if (error_) std::rethrow_exception(error_);
+    slots_[cur_].busy = true;
+    return slots_[cur_].host;
+  }
+  double* device_slot() { return slots_[cur_].dev; }
+  void submit(std::uint64_t iteration, cudaStream_t stream) {
+    PVI_CUDA(cudaEventRecord(slots_[cur_].done, stream));
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      queue_.push_back({cur_, iteration});
+    }
+    cv_.notify_all();
+  }
+  void finish() {
+    std::unique_lock<std::mutex> lock(mu_);
+    cv_.wait(lock, [&] { return (queue_.empty() && !slots_[0].busy && !slots_[1].busy) || error_; });
+    if (error_) {
+      auto e = error_;
+      error_ = nullptr;
+      std::rethrow_exception(e);
+    }
+  }
+
+ private:
+  struct Slot {
+    double* host = nullptr;
+    double* dev = nullptr;
+    cudaEvent_t done = nullptr;
+    bool busy = false;
+  };
+  void run() {
+    cudaSetDevice(device_);
+    for (;;) {
+      std::pair<int, std::uint64_t> job;
+      {
+        std::unique_lock<std::mutex> lock(mu_);
+        cv_.wait(lock, [&] { return stop_ || !queue_.empty(); });
+        if (queue_.empty()) return;
+        job = queue_.front();
+        queue_.pop_front();
+      }
+      try {
+        PVI_CUDA(cudaEventSynchronize(slots_[job.first].done));
+        save_checkpoint(path_, slots_[job.first].host, n_, job.second, fp_);
+      } catch (...) {
+        std::lock_guard<std::mutex> lock(mu_);
+        if (!error_) error_ = std::current_exception();
+      }
+      {
+        std::lock_guard<std::mutex> lock(mu_);
+        slots_[job.first].busy = false;
+      }
+      cv_.notify_all();
+    }
+  }
+  std::string path_;
+  std::uint64_t n_;
+  std::uint8_t fp_[32];
+  int device_ = 0;
+  Slot slots_[2];
+  int cur_ = 1;
+  std::thread worker_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<std::pair<int, std::uint64_t>> queue_;
+  bool stop_ = false;
+  std::exception_ptr error_;
+};
+
 std::string hex32(const std::uint8_t* fp) {
   static const char* digits = "0123456789abcdef";
   std::string s;
@@ -362,18 +475,14 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
   }
 
   const bool ckpt = cfg.checkpoint_every > 0 && cfg.checkpoint_path && cfg.checkpoint_path[0];
-  std::vector<double> host_wide;
-  std::unique_ptr<DevBuf> wide;
+  std::unique_ptr<AsyncCheckpointer> writer;
+  if (ckpt) writer = std::make_unique<AsyncCheckpointer>(cfg.checkpoint_path, n, fp);
   auto write_checkpoint = [&](const T* dv, std::uint64_t iter) {
     if (!ckpt) return;
-    if (!wide) {
-      wide = std::make_unique<DevBuf>(n * sizeof(double));
-      host_wide.resize(n);
-    }
-    launch_widen<T>(dv, wide->as<double>(), n, stream.s);
-    PVI_CUDA(cudaMemcpyAsync(host_wide.data(), wide->p, n * 8, cudaMemcpyDeviceToHost, stream.s));
-    PVI_CUDA(cudaStreamSynchronize(stream.s));
-    save_checkpoint(cfg.checkpoint_path, host_wide.data(), n, iter, fp);
+    double* wide = writer->acquire();  // waits only if both slots are still in flight
+    launch_widen<T>(dv, writer->device_slot(), n, stream.s);
+    PVI_CUDA(cudaMemcpyAsync(wide, writer->device_slot(), n * 8, cudaMemcpyDeviceToHost, stream.s));
+    writer->submit(iter, stream.s);  // the file write overlaps the next sweeps
   };
   if (ckpt && !resume_values) write_checkpoint(ring[order.back()]->as<T>(), iteration);
 
@@ -466,6 +575,7 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
     sweep_ms += ms;
     ++sweeps;
   }
+  if (writer) writer->finish();  // every checkpoint on disk before returning
   if (out_values) {
     DevBuf w(n * sizeof(double));
     launch_widen<T>(vfinal, w.as<double>(), n, stream.s);

@@ -566,10 +566,21 @@ double Model::state_cost(std::uint64_t s) const {
   int ia = 0, ib = 0;
   for (int i = 0; i < life; ++i) ia += st[i];
   for (int i = life; i < 2 * life; ++i) ib += st[i];
+  if (algorithm == PVI_ALGO_FACTORED) {
+    // factored stage 2: one merged block plus h_a = x_1+1..I_a, per order_a
+    const int x1 = st[life - 1];
+    return double(ia - x1 + 1) + 2.0;
+  }
   return double(ia + 1) * double(ib + 1);
 }
 
 std::uint64_t Model::tile_states() const {
+  if (scenario == PVI_SCENARIO_B && algorithm == PVI_ALGO_FACTORED) {
+    // shards own whole x_a blocks (all x_b) so stage 2's x_a loop splits cleanly
+    std::uint64_t t = 1;
+    for (int i = 0; i < pb.useful_life; ++i) t *= static_cast<std::uint64_t>(b_nb);
+    return t;
+  }
   if (scenario == PVI_SCENARIO_B) return b_lane_order.size();
   return 1;
 }

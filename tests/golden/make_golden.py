@@ -150,8 +150,51 @@ def simopt_golden():
     np.savez_compressed(os.path.join(HERE, "simopt_golden.npz"), **out)
 
 
+RUNNER_CASES = [("a/m2/exp1", 4096, 2000), ("b/m2/exp1", 4096, 1000), ("c/m3/exp1", 0, 500)]
+
+
+def runner_golden():
+    """Files written by the reference runner's cmd_solve / cmd_simopt /
+    cmd_evaluate (runner.cpp:303-480) for small presets."""
+    import ctypes as C
+    import tempfile
+    L = R.lib()
+    L.ref_cmd.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_int, C.c_int, C.c_char_p,
+                          C.c_char_p, C.c_char_p, C.c_size_t]
+    out = {}
+    err = C.create_string_buffer(1024)
+    for preset, simopt_rollouts, eval_rollouts in RUNNER_CASES:
+        d = tempfile.mkdtemp()
+        assert L.ref_cmd(preset.encode(), 0, d.encode(), 8, 0, b"", b"", err, 1024) == 0, err.value
+        heur = b""
+        if simopt_rollouts:
+            assert L.ref_cmd(preset.encode(), 1, d.encode(), 8, simopt_rollouts, b"", b"", err,
+                             1024) == 0, err.value
+            heur = (d + "/best_params.txt").encode()
+        else:  # c/m3: the published weekday (s, S) table (PAPER Table 13 exp1)
+            vals = [9, 7, 7, 6, 6, 3, 3, 13, 14, 14, 10, 11, 8, 8]
+            names = [f"s.{t}" for t in range(7)] + [f"S.{t}" for t in range(7)]
+            with open(d + "/heuristic.txt", "w") as f:
+                f.write("policy = weekday_sS\n" + "".join(f"{n} = {v}\n" for n, v in zip(names, vals)))
+            heur = (d + "/heuristic.txt").encode()
+        assert L.ref_cmd(preset.encode(), 2, d.encode(), 8, eval_rollouts,
+                         (d + "/policy.csv").encode(), heur, err, 1024) == 0, err.value
+        for fn in sorted(os.listdir(d)):
+            if fn.endswith(".tmp"):
+                continue
+            data = open(os.path.join(d, fn), "rb").read()
+            if fn == "report.txt":  # drop the machine-dependent lines
+                data = b"".join(l for l in data.splitlines(True)
+                                if not l.startswith((b"wall_seconds", b"threads")))
+            out[f"runner|{preset}|{fn}"] = np.frombuffer(data, np.uint8)
+        print(preset, sorted(os.listdir(d)))
+    np.savez_compressed(os.path.join(HERE, "runner_golden.npz"), **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "simopt":
         simopt_golden()
+    elif len(sys.argv) > 1 and sys.argv[1] == "runner":
+        runner_golden()
     else:
         main()
