@@ -14,6 +14,7 @@
 // state) scratch array so the cross-chunk argmax stays in action order.
 
 #include <algorithm>
+#include <cstdlib>
 #include <cfloat>
 #include <mutex>
 #include <utility>
@@ -511,8 +512,12 @@ __global__ void __launch_bounds__(256) k_b_erpt(DevModel dm, double* __restrict_
       er += p * (dm.b_cra * ha + dm.b_crb * hb);
       pt += p;
     }
-  erpt[s] = er;
-  erpt[n + s] = pt;
+  // layout [x_b][x_a][2]: a stage-2 CTA (fixed x_b) reads its states contiguously
+  std::uint64_t n_xb = 1;
+  for (int i = 0; i < m; ++i) n_xb *= static_cast<std::uint64_t>(dm.b_nb);
+  const std::uint64_t e = ((s % n_xb) * (n / n_xb) + s / n_xb) * 2;
+  erpt[e] = er;
+  erpt[e + 1] = pt;
 }
 
 // Shared-memory [row][o_b] slabs: odd row stride, and row r stored at
@@ -711,7 +716,8 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_q(DevModel dm, const double* 
       for (int ob = 0; ob < NBX; ++ob)
         if (ob < nb) acc[ob] = fma(al, wr[ob], fma(g, vr[ob], acc[ob]));
     }
-    const double er = erpt[s], pt = erpt[n + s];
+    const std::size_t e = (static_cast<std::size_t>(xbi) * n_xa + xai) * 2;
+    const double er = erpt[e], pt = erpt[e + 1];
     T best = T(0);
     int bo = 0;
 #pragma unroll
@@ -729,6 +735,216 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_q(DevModel dm, const double* 
     if (part_v) {
       part_v[static_cast<std::uint64_t>(oa) * nr + (s - lo)] = best;
       part_a[static_cast<std::uint64_t>(oa) * nr + (s - lo)] = static_cast<std::uint8_t>(bo);
+    }
+  }
+}
+
+// Stage 2, register-blocked (order_b radix 16, order_a radix <= 16).
+// The 16 states of an x_a "group" (same digits x_2..x_M, x_1 = 0..15) walk
+// the SAME sequence of aged profiles: after the merged h_a <= x_1 block,
+// step j consumes the j-th unit above x_1, so ap(j) does not depend on x_1,
+// and every state reaches its stock-out step j = S = x_2+..+x_M together.
+// Only the weights differ (pmf_a(x_1 + j), pz(I_b, x_1 + j)).  A thread
+// therefore owns 8 states x 4 order_b values of one group: each W / V0 row
+// element it reads from shared memory feeds 8 FMAs (vs 1 in k_b_fact_q),
+// which lifts the shared-memory delivery limit (16 doubles/clk/SM) above the
+// FP64 pipe.  Lanes: 32 groups x (2 state halves x 4 order_b quarters).
+template <typename T, int M>
+__global__ void __launch_bounds__(256, 2) k_b_fact_q16(DevModel dm, const double* __restrict__ W,
+                                                       const double* __restrict__ v0t,
+                                                       const double* __restrict__ erpt,
+                                                       const std::uint16_t* __restrict__ group_order,
+                                                       T* __restrict__ part_v,
+                                                       std::uint8_t* __restrict__ part_a,
+                                                       T* __restrict__ qout, std::uint64_t lo,
+                                                       std::uint64_t hi, double gamma,
+                                                       int n_groups, int n_xb, int n_ap, int n_r) {
+  constexpr int NB = 16, S8 = 8, OB4 = 4;
+  extern __shared__ double sm[];
+  const int na = dm.b_na;
+  const int stride = slab_stride(NB);
+  const int rows = slab_rows(n_ap);
+  double* w_sl = sm;
+  double* v0_sl = sm + rows * stride;
+  double* s_al = v0_sl + rows * stride;  // pmf_a
+  double* s_g = s_al + dm.b_dn;           // pz(I_b, .)
+  double* s_cal = s_g + dm.b_dn;          // cdf_a
+  double* s_cg = s_cal + dm.b_dn;         // pz_cum(I_b, .)
+  double* s_sfa = s_cg + dm.b_dn;         // sf_a
+  const int xbi = blockIdx.x;
+  const int oa = blockIdx.y;
+  int ib = 0;
+  {
+    int rem = xbi;
+#pragma unroll
+    for (int j = 1; j <= M; ++j) {
+      ib += rem % NB;
+      rem /= NB;
+    }
+  }
+  const double sfb = dm.b_sf_b[ib];
+  const int dnp = dm.b_dn;
+  const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
+  for (int i = threadIdx.x; i < n_ap * NB; i += blockDim.x) {
+    const int ap = i / NB, ob = i % NB;
+    w_sl[slab_row(ap) * stride + ob] = W[(static_cast<std::size_t>(xbi) * n_r + r0 + ap) * NB + ob];
+    v0_sl[slab_row(ap) * stride + ob] = sfb * v0t[(r0 + ap) * NB + ob];
+  }
+  for (int i = threadIdx.x; i < dnp; i += blockDim.x) {
+    s_al[i] = dm.b_pmf_a[i];
+    s_g[i] = dm.b_pz[ib * dnp + i];
+    s_cal[i] = dm.b_cdf_a[i];
+    s_cg[i] = dm.b_pz_cum[ib * dnp + i];
+    s_sfa[i] = dm.b_sf_a[i];
+  }
+  __syncthreads();
+  const std::uint64_t n = dm.n_states;
+  const std::uint64_t nr = hi - lo;
+  const int sub = threadIdx.x & 7;
+  const int x1b = (sub >> 2) * S8;  // first x_1 of this thread's 8 states
+  const int ob0 = (sub & 3) * OB4;   // first order_b of this thread's 4
+  const double cva_oa = dm.b_cva * oa;
+  for (int gbase = 0; gbase < n_groups; gbase += blockDim.x >> 3) {
+    // whole warps stay in the loop (the epilogue shuffles across lanes)
+    const int gi = gbase + (threadIdx.x >> 3);
+    const bool active = gi < n_groups;
+    const int grp = group_order[active ? gi : 0];
+    // group digits x_2..x_M (grp = sum_{j>=2} x_j na^(j-2))
+    int xg[M + 1];
+    int S = 0;
+    {
+      int rem = grp;
+#pragma unroll
+      for (int j = 2; j <= M; ++j) {
+        xg[j] = rem % na;
+        rem /= na;
+        S += xg[j];
+      }
+    }
+    const std::uint64_t xa0 = static_cast<std::uint64_t>(grp) * na;  // x_a of x_1 = 0
+    // skip (warp-uniformly) groups with no state of this shard
+    const bool in_shard = active && (xa0 * n_xb + xbi < hi) && ((xa0 + na - 1) * n_xb + xbi >= lo);
+    if (!__any_sync(0xffffffffu, in_shard)) continue;
+    double acc[S8][OB4];
+    // merged block: aged profile (x_2..x_M) for h_a <= x_1
+    {
+      int ap = 0, w = 1;
+#pragma unroll
+      for (int j = 1; j <= M - 1; ++j) {
+        ap += xg[j + 1] * w;
+        w *= na;
+      }
+      const double* wr = w_sl + slab_row(ap) * stride + ob0;
+      const double* vr = v0_sl + slab_row(ap) * stride + ob0;
+      double wv[OB4], vv[OB4];
+#pragma unroll
+      for (int k = 0; k < OB4; ++k) {
+        wv[k] = wr[k];
+        vv[k] = vr[k];
+      }
+#pragma unroll
+      for (int i = 0; i < S8; ++i) {
+        const int x1 = min(x1b + i, na - 1);
+        double al, g;
+        if (S > 0) {
+          al = s_cal[x1];
+          g = s_cg[x1 + 1];
+        } else {  // all stock in the oldest bucket: h_a = 0..I_a (= x_1)
+          al = (x1 > 0 ? s_cal[x1 - 1] : 0.0) + s_sfa[x1];
+          g = s_cg[x1] + (1.0 - s_cg[x1]);
+        }
+#pragma unroll
+        for (int k = 0; k < OB4; ++k) acc[i][k] = fma(al, wv[k], g * vv[k]);
+      }
+    }
+    // steps j = 1..S: h_a = x_1 + j; j = S is the stock-out boundary.  The
+    // interior weights pmf_a / pz(I_b, .) at x_1 + j slide by one state per
+    // step: keep an 8-wide register window and load one new entry per step.
+    // (x_1 + j <= 15 + S < dn, so no clamping is needed.)
+    double al[S8], gw[S8];
+#pragma unroll
+    for (int i = 0; i < S8; ++i) {
+      al[i] = s_al[x1b + i + 1];
+      gw[i] = s_g[x1b + i + 1];
+    }
+    for (int j = 1; j <= S; ++j) {
+      int ap = 0, w = 1, prefix = 0;
+#pragma unroll
+      for (int q = 1; q <= M - 1; ++q) {
+        ap += ipos(xg[q + 1] - ipos(j - prefix)) * w;
+        prefix += xg[q + 1];
+        w *= na;
+      }
+      const double* wr = w_sl + slab_row(ap) * stride + ob0;
+      const double* vr = v0_sl + slab_row(ap) * stride + ob0;
+      double wv[OB4], vv[OB4];
+#pragma unroll
+      for (int k = 0; k < OB4; ++k) {
+        wv[k] = wr[k];
+        vv[k] = vr[k];
+      }
+      if (j < S) {
+#pragma unroll
+        for (int i = 0; i < S8; ++i) {
+#pragma unroll
+          for (int k = 0; k < OB4; ++k) acc[i][k] = fma(al[i], wv[k], fma(gw[i], vv[k], acc[i][k]));
+        }
+#pragma unroll
+        for (int i = 0; i < S8 - 1; ++i) {
+          al[i] = al[i + 1];
+          gw[i] = gw[i + 1];
+        }
+        al[S8 - 1] = s_al[x1b + S8 + j];
+        gw[S8 - 1] = s_g[x1b + S8 + j];
+      } else {
+#pragma unroll
+        for (int i = 0; i < S8; ++i) {
+          const int ha = x1b + i + j;
+          const double a_b = s_sfa[ha];
+          const double g_b = 1.0 - s_cg[ha];
+#pragma unroll
+          for (int k = 0; k < OB4; ++k) acc[i][k] = fma(a_b, wv[k], fma(g_b, vv[k], acc[i][k]));
+        }
+      }
+    }
+    // Q, first-max over order_b across the 4 lanes that share the states
+#pragma unroll
+    for (int i = 0; i < S8; ++i) {
+      const int x1 = x1b + i;
+      const std::uint64_t s = (xa0 + x1) * n_xb + xbi;
+      const bool valid = active && x1 < na && s >= lo && s < hi;
+      double er = 0.0, pt = 0.0;
+      if (valid) {
+        const std::size_t e = (static_cast<std::size_t>(xbi) * (n / n_xb) + xa0 + x1) * 2;
+        er = erpt[e];
+        pt = erpt[e + 1];
+      }
+      T best = T(0);
+      int bo = 0;
+#pragma unroll
+      for (int k = 0; k < OB4; ++k) {
+        const int ob = ob0 + k;
+        const double qd = fma(gamma, acc[i][k], er - (cva_oa + dm.b_cvb * ob) * pt);
+        const T qv = static_cast<T>(qd);
+        if (k == 0 || qv > best) {
+          best = qv;
+          bo = ob;
+        }
+        if (qout && valid) qout[(s - lo) * dm.n_actions + static_cast<std::uint64_t>(oa) * NB + ob] = qv;
+      }
+#pragma unroll
+      for (int off = 1; off <= 2; off <<= 1) {
+        const T ob_v = __shfl_xor_sync(0xffffffffu, best, off);
+        const int ob_i = __shfl_xor_sync(0xffffffffu, bo, off);
+        if (ob_v > best || (ob_v == best && ob_i < bo)) {
+          best = ob_v;
+          bo = ob_i;
+        }
+      }
+      if ((sub & 3) == 0 && valid && part_v) {
+        part_v[static_cast<std::uint64_t>(oa) * nr + (s - lo)] = best;
+        part_a[static_cast<std::uint64_t>(oa) * nr + (s - lo)] = static_cast<std::uint8_t>(bo);
+      }
     }
   }
 }
@@ -1256,6 +1472,15 @@ std::vector<std::uint16_t> digit_sum_order(int radix, int digits) {
 }
 }  // namespace
 
+// PVI_B_Q16=0 selects the one-state-per-thread stage 2 (comparison runs).
+static bool q16_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PVI_B_Q16");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <typename T>
 bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
                        Scratch& scratch, cudaStream_t stream) {
@@ -1295,6 +1520,24 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
       dc.allocations.push_back(q2);
       dc.b_order_a = static_cast<std::uint16_t*>(q1);
       dc.b_order_b = static_cast<std::uint16_t*>(q2);
+      // x_2..x_M digit groups ordered by their stock (the q16 trip count)
+      std::vector<std::uint16_t> go(n_ap);
+      std::vector<int> gs(n_ap);
+      for (int v = 0; v < static_cast<int>(n_ap); ++v) {
+        int sum = 0, rem = v;
+        for (int i = 0; i < M - 1; ++i) {
+          sum += rem % na;
+          rem /= na;
+        }
+        gs[v] = sum;
+        go[v] = static_cast<std::uint16_t>(v);
+      }
+      std::stable_sort(go.begin(), go.end(), [&](int x, int y) { return gs[x] < gs[y]; });
+      void* q3 = nullptr;
+      PVI_CUDA(cudaMalloc(&q3, go.size() * 2));
+      PVI_CUDA(cudaMemcpy(q3, go.data(), go.size() * 2, cudaMemcpyHostToDevice));
+      dc.allocations.push_back(q3);
+      dc.b_group_order = static_cast<std::uint16_t*>(q3);
       dc.b_erpt = static_cast<double*>(p);
     }
   }
@@ -1312,9 +1555,17 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     cudaFuncSetAttribute(k_b_fact_q<T, MM, NBX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
     k_b_fact_w<T, MM, NBX><<<static_cast<unsigned>(n_r), 256, sm1, stream>>>(                       \
         dm, a.v, W, v0t, dc.b_order_b, static_cast<int>(n_xb), static_cast<int>(n_bp), static_cast<int>(n_r)); \
+    if (nb == 16 && na <= 16 && q16_enabled()) {                                                   \
+      const std::size_t sm3 = sizeof(double) * (2 * slab_rows(static_cast<int>(n_ap)) * slab_stride(16) + 5 * dm.b_dn); \
+      cudaFuncSetAttribute(k_b_fact_q16<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+      k_b_fact_q16<T, MM><<<dim3(static_cast<unsigned>(n_xb), static_cast<unsigned>(na)), 256, sm3, stream>>>( \
+          dm, W, v0t, dc.b_erpt, dc.b_group_order, pv, pa, a.qout, lo, hi, a.gamma,                  \
+          static_cast<int>(n_ap), static_cast<int>(n_xb), static_cast<int>(n_ap), static_cast<int>(n_r)); \
+    } else {                                                                                       \
     k_b_fact_q<T, MM, NBX><<<dim3(static_cast<unsigned>(n_xb), static_cast<unsigned>(na)), 256, sm2, stream>>>( \
         dm, W, v0t, dc.b_erpt, dc.b_order_a, pv, pa, a.qout, lo, hi, a.gamma, static_cast<int>(n_xa), \
         static_cast<int>(n_xb), static_cast<int>(n_ap), static_cast<int>(n_r));                  \
+    }                                                                                              \
   } else
     PVI_BF(2, 16) PVI_BF(2, 32) PVI_BF(3, 16) PVI_BF(3, 32) {
       return false;
