@@ -176,7 +176,6 @@ typedef struct {
   int convergence_test;      /* -1: model default, else pvi_convergence_test */
   uint64_t max_states;       /* capacity gate, 200'000'000 */
   int device;                /* CUDA ordinal, -1 = current */
-  int sweeps_per_sync;       /* >1: speculative multi-sweep launches between host syncs (0/1 = 1) */
   int algorithm;             /* -1: the model's (pvi_model_set_algorithm), else pvi_algorithm */
 } pvi_vi_config;
 

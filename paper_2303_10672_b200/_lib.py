@@ -60,7 +60,7 @@ class ViConfigC(C.Structure):
                 ("max_iterations", C.c_uint64), ("fixed_iterations", C.c_uint64),
                 ("checkpoint_every", C.c_uint64), ("checkpoint_path", C.c_char_p),
                 ("precision", C.c_int), ("convergence_test", C.c_int),
-                ("max_states", C.c_uint64), ("device", C.c_int), ("sweeps_per_sync", C.c_int),
+                ("max_states", C.c_uint64), ("device", C.c_int),
                 ("algorithm", C.c_int)]
 
 

@@ -264,7 +264,6 @@ void pvi_vi_config_defaults(pvi_vi_config* c) {
   c->convergence_test = -1;
   c->max_states = 200000000ull;
   c->device = -1;
-  c->sweeps_per_sync = 1;
   c->algorithm = -1;
 }
 

@@ -133,7 +133,10 @@ __device__ __forceinline__ void decode(const DevModel& dm, std::uint64_t s, int*
 // ScenarioA::q_row_impl (scenario_a.cpp:104-146): d outer, a inner,
 // term = T(p * (r_sd - C_v*a + gamma*V[base + a*W0])), accumulated in T.
 
-template <typename T, int NA>
+// ML = 10*m + L specialises the useful life and lead time at compile time
+// (ageing, decode and next-state weights unroll into registers); ML = 0 is
+// the runtime-generic build.
+template <typename T, int NA, int ML>
 __global__ void __launch_bounds__(256) k_sweep_a(DevModel dm, const T* __restrict__ V,
                                                  T* __restrict__ vout, std::uint32_t* __restrict__ act,
                                                  T* __restrict__ qout, std::uint64_t lo,
@@ -148,16 +151,32 @@ __global__ void __launch_bounds__(256) k_sweep_a(DevModel dm, const T* __restric
   double smax = -DBL_MAX, smin = DBL_MAX;
   unsigned long long bad = ~0ull;
   if (s < hi) {
-    const int m = dm.a_m, lead = dm.a_lead, na = static_cast<int>(dm.n_actions);
-    int st[kMaxDigits];
-    decode(dm, s, st);
-    int x[14], aged[14];
+    constexpr int MC = ML / 10, LC = ML % 10;
+    const int m = ML ? MC : dm.a_m, lead = ML ? LC : dm.a_lead;
+    const int na = static_cast<int>(dm.n_actions);
+    constexpr int ND = ML ? MC + LC - 1 : kMaxDigits;
+    int st[ND];
+    if (ML) {
+      // uniform radix A_max+1, digit 0 most significant
+      const std::uint32_t r = static_cast<std::uint32_t>(dm.a_max_order + 1);
+      std::uint64_t rem = s;
+#pragma unroll
+      for (int i = ND - 1; i >= 0; --i) {
+        st[i] = static_cast<int>(rem % r);
+        rem /= r;
+      }
+    } else {
+      decode(dm, s, st);
+    }
+    int x[ML ? MC + 1 : 14], aged[ML ? MC + 1 : 14];
     int xt = 0;
+#pragma unroll
     for (int j = 1; j <= m; ++j) {
       x[j] = st[lead - 1 + m - j];
       xt += x[j];
     }
     std::uint64_t base_static = 0;
+#pragma unroll
     for (int k = 1; k <= lead - 2; ++k) base_static += st[k - 1] * dm.weight[k];
     if (lead >= 2) base_static += st[lead - 2] * dm.weight[lead - 1];
     const std::uint64_t w0 = dm.weight[0];
@@ -1631,12 +1650,23 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
       const int na = static_cast<int>(dm.n_actions);
       MainKernelScope prof(stream);
       count_launches(1);
-      if (na <= 16)
-        k_sweep_a<T, 16><<<grid_for(nr, block), block, sm, stream>>>(dm, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
+      const int ml = 10 * dm.a_m + dm.a_lead;
+      bool done = false;
+#define PVI_A_ML(ML)                                                                                  \
+  if (!done && na <= 16 && ml == ML) {                                                                \
+    k_sweep_a<T, 16, ML><<<grid_for(nr, block), block, sm, stream>>>(dm, a.v, a.vout, a.act, a.qout, lo, \
+                                                                     hi, a.out_off, a.gamma, fa);    \
+    done = true;                                                                                      \
+  }
+      PVI_A_ML(21) PVI_A_ML(22) PVI_A_ML(31) PVI_A_ML(32) PVI_A_ML(41) PVI_A_ML(42) PVI_A_ML(51) PVI_A_ML(52)
+#undef PVI_A_ML
+      if (done) {
+      } else if (na <= 16)
+        k_sweep_a<T, 16, 0><<<grid_for(nr, block), block, sm, stream>>>(dm, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
       else if (na <= 32)
-        k_sweep_a<T, 32><<<grid_for(nr, block), block, sm, stream>>>(dm, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
+        k_sweep_a<T, 32, 0><<<grid_for(nr, block), block, sm, stream>>>(dm, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
       else if (na <= 64)
-        k_sweep_a<T, 64><<<grid_for(nr, block), block, sm, stream>>>(dm, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
+        k_sweep_a<T, 64, 0><<<grid_for(nr, block), block, sm, stream>>>(dm, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
       else
         fail(PVI_ERR_PARAMETER, "scenario a: max_order > 63 is not supported by the device kernel");
       break;

@@ -350,7 +350,6 @@ class ViConfig:
     convergence_test: Optional[str] = None
     max_states: int = 200_000_000
     device: int = -1
-    sweeps_per_sync: int = 1
     algorithm: Optional[str] = None  # None: the model's (Model.set_algorithm)
 
     def to_c(self) -> L.ViConfigC:
@@ -369,7 +368,6 @@ class ViConfig:
         c.convergence_test = -1 if self.convergence_test is None else _TEST_NAMES[self.convergence_test]
         c.max_states = self.max_states
         c.device = self.device
-        c.sweeps_per_sync = self.sweeps_per_sync
         c.algorithm = -1 if self.algorithm is None else _ALGOS[self.algorithm]
         return c
 
