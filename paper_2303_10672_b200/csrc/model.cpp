@@ -576,8 +576,9 @@ double Model::state_cost(std::uint64_t s) const {
 
 std::uint64_t Model::tile_states() const {
   if (scenario == PVI_SCENARIO_B && algorithm == PVI_ALGO_FACTORED) {
-    // shards own whole x_a blocks (all x_b) so stage 2's x_a loop splits cleanly
-    std::uint64_t t = 1;
+    // shards own whole x_a groups (x_1 = 0..A_a, all x_b): stage 2 works on
+    // groups of states that share x_2..x_m, so no group straddles two ranks
+    std::uint64_t t = static_cast<std::uint64_t>(b_na);
     for (int i = 0; i < pb.useful_life; ++i) t *= static_cast<std::uint64_t>(b_nb);
     return t;
   }

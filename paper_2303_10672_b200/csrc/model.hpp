@@ -98,7 +98,8 @@ struct DeviceCopy {
   double* b_erpt = nullptr;
   std::uint16_t* b_order_a = nullptr;
   std::uint16_t* b_order_b = nullptr;
-  std::uint16_t* b_group_order = nullptr;  // x_2..x_M digit groups by stock
+  std::uint16_t* b_group_order = nullptr;    // A-side x_2..x_M digit groups by stock
+  std::uint16_t* b_group_order_b = nullptr;  // B-side x_2..x_M digit groups by stock
   // Per-device workspace reused by the host-buffer entry points
   // (engine.cu Workspace: device copies of V / outputs, scratch, a stream).
   void* workspace = nullptr;

@@ -758,6 +758,108 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_q(DevModel dm, const double* 
   }
 }
 
+// Stage 1, register-blocked the same way as k_b_fact_q16 (order_b radix 16):
+// the 16 x_b states of a group (same x_2..x_M, x_1 = 0..15) walk the same
+// aged-B-profile path, so each slab element read feeds 8 states' FMAs.
+template <typename T, int M>
+__global__ void __launch_bounds__(256, 2) k_b_fact_w16(DevModel dm, const T* __restrict__ V,
+                                                       double* __restrict__ W,
+                                                       double* __restrict__ v0t,
+                                                       const std::uint16_t* __restrict__ group_order,
+                                                       int n_groups, int n_xb, int n_bp, int n_r) {
+  constexpr int NB = 16, S8 = 8, OB4 = 4;
+  extern __shared__ double slab[];  // [bp][ob]
+  const int stride = slab_stride(NB);
+  const int r = blockIdx.x;
+  const std::uint64_t base = static_cast<std::uint64_t>(r) * n_xb;
+  for (int i = threadIdx.x; i < NB * n_bp; i += blockDim.x) {
+    const int ob = i / n_bp, bp = i % n_bp;
+    slab[slab_row(bp) * stride + ob] = static_cast<double>(V[base + static_cast<std::uint64_t>(ob) * n_bp + bp]);
+  }
+  __shared__ double s_pmf_b[64], s_cdf_b[64];
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+    s_pmf_b[i] = i < dm.b_len_b ? dm.b_pmf_b[i] : 0.0;
+    s_cdf_b[i] = i < dm.b_len_b ? dm.b_cdf_b[i] : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < NB) v0t[static_cast<std::size_t>(r) * NB + threadIdx.x] = slab[threadIdx.x];
+  const int sub = threadIdx.x & 7;
+  const int x1b = (sub >> 2) * S8;
+  const int ob0 = (sub & 3) * OB4;
+  for (int gbase = 0; gbase < n_groups; gbase += blockDim.x >> 3) {
+    const int gi = gbase + (threadIdx.x >> 3);
+    const bool active = gi < n_groups;
+    const int grp = group_order[active ? gi : 0];
+    int xg[M + 1];
+    int S = 0;
+    {
+      int rem = grp;
+#pragma unroll
+      for (int j = 2; j <= M; ++j) {
+        xg[j] = rem % NB;
+        rem /= NB;
+        S += xg[j];
+      }
+    }
+    double acc[S8][OB4];
+    // merged block h_b = 0..min(x_1, I_b - 1): aged profile (x_2..x_M)
+    {
+      int bp = 0, w = 1;
+#pragma unroll
+      for (int j = 1; j <= M - 1; ++j) {
+        bp += xg[j + 1] * w;
+        w *= NB;
+      }
+      const double* row = slab + slab_row(bp) * stride + ob0;
+      double rv[OB4];
+#pragma unroll
+      for (int k = 0; k < OB4; ++k) rv[k] = row[k];
+#pragma unroll
+      for (int i = 0; i < S8; ++i) {
+        const int x1 = x1b + i;
+        // S > 0: h_b = 0..x_1; S == 0 (I_b = x_1): h_b = 0..x_1-1 (none when x_1 = 0)
+        const double pw = S > 0 ? s_cdf_b[x1] : (x1 > 0 ? s_cdf_b[x1 - 1] : 0.0);
+#pragma unroll
+        for (int k = 0; k < OB4; ++k) acc[i][k] = pw * rv[k];
+      }
+    }
+    // interior steps j = 1..S-1: h_b = x_1 + j < I_b
+    double pw[S8];
+#pragma unroll
+    for (int i = 0; i < S8; ++i) pw[i] = s_pmf_b[x1b + i + 1];
+    for (int j = 1; j < S; ++j) {
+      int bp = 0, w = 1, prefix = 0;
+#pragma unroll
+      for (int q = 1; q <= M - 1; ++q) {
+        bp += ipos(xg[q + 1] - ipos(j - prefix)) * w;
+        prefix += xg[q + 1];
+        w *= NB;
+      }
+      const double* row = slab + slab_row(bp) * stride + ob0;
+      double rv[OB4];
+#pragma unroll
+      for (int k = 0; k < OB4; ++k) rv[k] = row[k];
+#pragma unroll
+      for (int i = 0; i < S8; ++i) {
+#pragma unroll
+        for (int k = 0; k < OB4; ++k) acc[i][k] = fma(pw[i], rv[k], acc[i][k]);
+      }
+#pragma unroll
+      for (int i = 0; i < S8 - 1; ++i) pw[i] = pw[i + 1];
+      pw[S8 - 1] = s_pmf_b[x1b + S8 + j];
+    }
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < S8; ++i) {
+        const int xbi = grp * NB + x1b + i;
+        double* out = W + (static_cast<std::size_t>(xbi) * n_r + r) * NB + ob0;
+#pragma unroll
+        for (int k = 0; k < OB4; ++k) out[k] = acc[i][k];
+      }
+    }
+  }
+}
+
 // Stage 2, register-blocked (order_b radix 16, order_a radix <= 16).
 // The 16 states of an x_a "group" (same digits x_2..x_M, x_1 = 0..15) walk
 // the SAME sequence of aged profiles: after the merged h_a <= x_1 block,
@@ -1539,24 +1641,30 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
       dc.allocations.push_back(q2);
       dc.b_order_a = static_cast<std::uint16_t*>(q1);
       dc.b_order_b = static_cast<std::uint16_t*>(q2);
-      // x_2..x_M digit groups ordered by their stock (the q16 trip count)
-      std::vector<std::uint16_t> go(n_ap);
-      std::vector<int> gs(n_ap);
-      for (int v = 0; v < static_cast<int>(n_ap); ++v) {
-        int sum = 0, rem = v;
-        for (int i = 0; i < M - 1; ++i) {
-          sum += rem % na;
-          rem /= na;
+      // x_2..x_M digit groups ordered by their stock (the *16 kernels' trip count)
+      auto group_order = [&](int radix) {
+        int count = 1;
+        for (int i = 0; i < M - 1; ++i) count *= radix;
+        std::vector<std::uint16_t> go(count);
+        std::vector<int> gs(count);
+        for (int v = 0; v < count; ++v) {
+          int sum = 0, rem = v;
+          for (int i = 0; i < M - 1; ++i) {
+            sum += rem % radix;
+            rem /= radix;
+          }
+          gs[v] = sum;
+          go[v] = static_cast<std::uint16_t>(v);
         }
-        gs[v] = sum;
-        go[v] = static_cast<std::uint16_t>(v);
-      }
-      std::stable_sort(go.begin(), go.end(), [&](int x, int y) { return gs[x] < gs[y]; });
-      void* q3 = nullptr;
-      PVI_CUDA(cudaMalloc(&q3, go.size() * 2));
-      PVI_CUDA(cudaMemcpy(q3, go.data(), go.size() * 2, cudaMemcpyHostToDevice));
-      dc.allocations.push_back(q3);
-      dc.b_group_order = static_cast<std::uint16_t*>(q3);
+        std::stable_sort(go.begin(), go.end(), [&](int x, int y) { return gs[x] < gs[y]; });
+        void* q = nullptr;
+        PVI_CUDA(cudaMalloc(&q, go.size() * 2));
+        PVI_CUDA(cudaMemcpy(q, go.data(), go.size() * 2, cudaMemcpyHostToDevice));
+        dc.allocations.push_back(q);
+        return static_cast<std::uint16_t*>(q);
+      };
+      dc.b_group_order = group_order(na);
+      dc.b_group_order_b = group_order(nb);
       dc.b_erpt = static_cast<double*>(p);
     }
   }
@@ -1572,8 +1680,16 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
   if (M == MM && nb <= NBX) {                                                                      \
     cudaFuncSetAttribute(k_b_fact_w<T, MM, NBX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
     cudaFuncSetAttribute(k_b_fact_q<T, MM, NBX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+    if (nb == 16 && q16_enabled()) {                                                               \
+      const std::size_t sm0 = sizeof(double) * slab_rows(static_cast<int>(n_bp)) * slab_stride(16); \
+      cudaFuncSetAttribute(k_b_fact_w16<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+      k_b_fact_w16<T, MM><<<static_cast<unsigned>(n_r), 256, sm0, stream>>>(                       \
+          dm, a.v, W, v0t, dc.b_group_order_b, static_cast<int>(n_bp), static_cast<int>(n_xb),      \
+          static_cast<int>(n_bp), static_cast<int>(n_r));                                          \
+    } else {                                                                                       \
     k_b_fact_w<T, MM, NBX><<<static_cast<unsigned>(n_r), 256, sm1, stream>>>(                       \
         dm, a.v, W, v0t, dc.b_order_b, static_cast<int>(n_xb), static_cast<int>(n_bp), static_cast<int>(n_r)); \
+    }                                                                                              \
     if (nb == 16 && na <= 16 && q16_enabled()) {                                                   \
       const std::size_t sm3 = sizeof(double) * (2 * slab_rows(static_cast<int>(n_ap)) * slab_stride(16) + 5 * dm.b_dn); \
       cudaFuncSetAttribute(k_b_fact_q16<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
