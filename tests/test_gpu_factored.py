@@ -108,3 +108,25 @@ def test_factored_c_q_rows_close_to_exact(pvi, preset, prec):
         for i, s in enumerate(GOLD[f"qrow|{preset}|states"]):
             q = pvi.q_rows(fact, V7, int(s), int(s) + 1)[0]
             np.testing.assert_allclose(q, golden[i], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("preset,parts", [("b/m3/exp1", 8), ("b/m3/exp4", 3), ("c/m5/exp1", 4),
+                                          ("b/m2/p4", 5)])
+def test_factored_shards_equal_full_sweep(pvi, preset, parts):
+    """What each rank of the sharded driver computes (its cost-weighted,
+    group-aligned [lo, hi) slice) is bit-identical to that slice of a
+    single full sweep."""
+    m = pvi.make_preset(preset).set_algorithm("factored")
+    n = m.state_count()
+    V = np.random.default_rng(5).uniform(-20.0, 20.0, n)
+    full_v, full_a = pvi.bellman_backup_batch(m, V, 0, n)
+    bounds = [int(b) for b in m.partition(parts)]
+    assert bounds[0] == 0 and bounds[-1] == n
+    for lo, hi in zip(bounds, bounds[1:]):
+        v, a = pvi.bellman_backup_batch(m, V, lo, hi)
+        np.testing.assert_array_equal(v, full_v[lo:hi])
+        np.testing.assert_array_equal(a, full_a[lo:hi])
+    # an arbitrary unaligned range as well
+    lo, hi = n // 3 + 17, n // 3 + 17 + 5000
+    v, a = pvi.bellman_backup_batch(m, V, lo, hi)
+    np.testing.assert_array_equal(v, full_v[lo:hi])
