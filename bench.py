@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--algorithm", default="factored", choices=["exact", "factored"])
     ap.add_argument("--no-alt", action="store_true", help="skip timing the other algorithm")
     ap.add_argument("--no-simopt", action="store_true")
+    ap.add_argument("--no-ckpt-solve", action="store_true",
+                    help="skip the second solve with the preset's checkpoint cadence")
     ap.add_argument("--no-solve", action="store_true", help="skip the time-to-converge solve")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -420,11 +422,32 @@ def ours_arm(args, world, rank, local):
     # wall time to converge (the second half of the BASELINE metric)
     if not args.no_solve:
         barrier()
-        res = ShardedValueIteration(model, cfg).solve()
+        runs = []
+        for _ in range(2):  # first call in the process pays allocations; report both
+            if world == 1:  # the product API: pvi_vi_solve, V resident on the device throughout
+                res = P.run_value_iteration(model, cfg)
+                api = "pvi_vi_solve (run_value_iteration)"
+            else:           # one process per GPU, NCCL exchange per sweep
+                res = ShardedValueIteration(model, cfg).solve()
+                api = "sharded.ShardedValueIteration"
+            runs.append(res)
+        res = min(runs, key=lambda r: r.wall_seconds)
         line["solve"] = {"preset": args.workload, "iterations": res.iterations,
                          "converged": res.converged, "wall_seconds": res.wall_seconds,
+                         "first_call_wall_seconds": runs[0].wall_seconds,
                          "sweep_seconds": res.sweep_seconds, "algorithm": args.algorithm,
+                         "api": api,
                          "checkpoints": "off (the reference cmd_solve writes one per sweep)"}
+        if world == 1 and not args.no_ckpt_solve:
+            import tempfile
+            with tempfile.TemporaryDirectory() as tmp:
+                every = model.preset_checkpoint_every or 1
+                ck = P.ViConfig(precision=args.precision, checkpoint_every=every,
+                                checkpoint_path=os.path.join(tmp, "checkpoint.ckpt"))
+                rc = P.run_value_iteration(model, ck)
+                line["solve"]["with_checkpoints"] = {
+                    "checkpoint_every": every, "wall_seconds": rc.wall_seconds,
+                    "writer": "async PVI1 (pinned double buffer + writer thread)"}
 
     # simulation optimisation (config 5): the reference GA on b/m2/exp1 with
     # 4096 rollouts per candidate, every generation scored in one device batch

@@ -450,7 +450,10 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
   const int device = select_device(cfg.device);
   const DevModel& dm = m.device_view(device);
   Stream stream;
-  Scratch scratch;
+  // sweep scratch (GB-scale for B: partials, factored W) reused across calls
+  Workspace& ws = workspace(m, device);
+  std::lock_guard<std::mutex> ws_lock(ws.mu);
+  Scratch& scratch = ws.scratch;
   PinnedStats pstats;
   DevBuf dstats(sizeof(SweepStats));
 

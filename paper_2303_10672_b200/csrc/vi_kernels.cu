@@ -892,8 +892,8 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_q16(DevModel dm, const double
   double* s_cal = s_g + dm.b_dn;          // cdf_a
   double* s_cg = s_cal + dm.b_dn;         // pz_cum(I_b, .)
   double* s_sfa = s_cg + dm.b_dn;         // sf_a
-  const int xbi = blockIdx.x;
-  const int oa = blockIdx.y;
+  const int xbi = blockIdx.y;  // order_a fastest: the 16 CTAs of one x_b share its L2-resident rows
+  const int oa = blockIdx.x;
   int ib = 0;
   {
     int rem = xbi;
@@ -1693,7 +1693,7 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     if (nb == 16 && na <= 16 && q16_enabled()) {                                                   \
       const std::size_t sm3 = sizeof(double) * (2 * slab_rows(static_cast<int>(n_ap)) * slab_stride(16) + 5 * dm.b_dn); \
       cudaFuncSetAttribute(k_b_fact_q16<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-      k_b_fact_q16<T, MM><<<dim3(static_cast<unsigned>(n_xb), static_cast<unsigned>(na)), 256, sm3, stream>>>( \
+      k_b_fact_q16<T, MM><<<dim3(static_cast<unsigned>(na), static_cast<unsigned>(n_xb)), 256, sm3, stream>>>( \
           dm, W, v0t, dc.b_erpt, dc.b_group_order, pv, pa, a.qout, lo, hi, a.gamma,                  \
           static_cast<int>(n_ap), static_cast<int>(n_xb), static_cast<int>(n_ap), static_cast<int>(n_r)); \
     } else {                                                                                       \

@@ -3,7 +3,6 @@
 # sweeps) and the launch list of the default bench command.
 set -u
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
 B="python bench.py --steps 2 --warmup 1 --no-solve --no-e2e --no-cpu-baseline --no-alt --no-simopt"
 $B > gpurun_out/plain_launch_f.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv \
