@@ -143,6 +143,8 @@ const DevModel& Model::device_view(int device) const {
       d.c_probs = upload(*dc, c_probs);
       d.c_offsets = upload(*dc, c_offsets);
       d.c_receipt = upload(*dc, c_receipt);
+      d.c_exogenous = c_exogenous ? 1 : 0;
+      d.c_binom = c_binom.empty() ? nullptr : upload(*dc, c_binom);
       break;
     default:
       d.t_outcomes = n_outcomes;

@@ -404,6 +404,40 @@ std::unique_ptr<Model> build_scenario_c(const pvi_scenario_c_params& p) {
   }
   m.c_offsets[cap + 1] = static_cast<std::uint32_t>(m.c_ids.size());
 
+  // Factored-sweep helper (not used by the exact path): the multinomial
+  // split of a units over the age categories 1..m equals sequential
+  // binomials -- y_1 ~ Bin(a, q_1), y_2 ~ Bin(a - y_1, q_2), ... with
+  // q_k = p_k / (p_k + .. + p_m) and p = receipt_category_probs(a).
+  // c_binom[a][k-1][b][y] = Bin(y; b, q_k(a)).  With an exogenous law (all
+  // receipt rows equal) the tables are shared by every order size.
+  m.c_exogenous = true;
+  for (int a = 1; a <= cap && m.c_exogenous; ++a)
+    for (int j = 0; j < life; ++j)
+      if (m.c_receipt[static_cast<std::size_t>(a) * life + j] != m.c_receipt[j]) m.c_exogenous = false;
+  if (life >= 2) {
+    const int r = cap + 1;
+    const std::size_t per_k = static_cast<std::size_t>(r) * r;
+    m.c_binom.assign(static_cast<std::size_t>(r) * (life - 1) * per_k, 0.0);
+    for (int a = 0; a <= cap; ++a) {
+      const double* p_a = &m.c_receipt[static_cast<std::size_t>(a) * life];
+      for (int k = 1; k <= life - 1; ++k) {
+        double tail = 0.0;
+        for (int j = k; j <= life; ++j) tail += p_a[j - 1];
+        const double q = tail > 0.0 ? p_a[k - 1] / tail : 0.0;
+        double* tab = &m.c_binom[(static_cast<std::size_t>(a) * (life - 1) + (k - 1)) * per_k];
+        for (int b = 0; b <= cap; ++b)
+          for (int y = 0; y <= b; ++y) {
+            double w;
+            if (q <= 0.0) w = y == 0 ? 1.0 : 0.0;
+            else if (q >= 1.0) w = y == b ? 1.0 : 0.0;
+            else w = std::exp(log_fact[b] - log_fact[y] - log_fact[b - y] + y * std::log(q) +
+                              (b - y) * std::log1p(-q));
+            tab[b * r + y] = w;
+          }
+      }
+    }
+  }
+
   std::ostringstream os;
   os << "scenario=c;m=" << life << ";A_max=" << p.max_order << ";D_max=" << p.max_demand
      << ";C_f=" << p.fixed_order_cost << ";C_h=" << p.holding_cost << ";C_s=" << p.shortage_cost

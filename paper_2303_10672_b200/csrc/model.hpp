@@ -81,6 +81,12 @@ struct DevModel {
   const double* c_probs;          // aligned with c_ids
   const std::uint32_t* c_offsets; // A_max+2
   const double* c_receipt;        // (A_max+1) x m
+  // The multinomial over age categories factors into m-1 sequential
+  // binomials: c_binom[a][k-1][b][y] = Bin(y; b, q_k(a)), shape
+  // (A_max+1) x (m-1) x (A_max+1) x (A_max+1).  c_exogenous: the receipt law
+  // does not depend on a (all c_receipt rows equal).
+  int c_exogenous;
+  const double* c_binom;
 
   // tabular
   std::uint64_t t_outcomes;
@@ -129,6 +135,8 @@ struct Model {
   std::vector<std::int8_t> c_comp, c_comp_sum;
   std::vector<std::uint32_t> c_ids, c_offsets;
   std::vector<double> c_probs, c_receipt;
+  bool c_exogenous = false;
+  std::vector<double> c_binom;
   // tabular
   std::vector<std::uint64_t> t_next;
   std::vector<double> t_reward, t_prob, t_initial;

@@ -1291,6 +1291,90 @@ __global__ void __launch_bounds__(128) k_c_fact_q(DevModel dm, const double* __r
   if (qout) qout[(s - lo) * na + a] = qa;
 }
 
+// Binomial factoring of the composition sum.  Stage 2 is a multinomial
+// expectation of G over the split of the a ordered units into the age
+// categories 1..m (scenario_c.cpp:72-99 enumerates it composition by
+// composition).  The multinomial is a chain of binomials, so the sum factors
+// into m-1 passes over tables shaped like G:
+//
+//   H_m(b, z_1..z_{m-1}) = G(z_1..z_{m-1}, y_m = b)
+//   H_k(b, ..z_{k-1}, x_k, ..) = sum_y Bin(y; b, q_k) H_{k+1}(b-y, ..z_{k-1}, min(x_k+y,cap), ..)
+//   Q(s, a) = fixed(a) PD(tau) + H_1(a, x_1..x_{m-1})
+//
+// Each pass changes only the top digit b (units not yet placed) and digit
+// k.  Exogenous law: one table per pass shared by all orders, ~1.5e9 FMAs
+// for c/m5 against the 7.2e10 gathers of k_c_fact_q.  Endogenous law
+// (q_k depends on a): one triangular table per order, b <= a, ~9e9 FMAs.
+// The last pass (k = 1, only b = a needed) is fused with the Q output.
+
+__host__ __device__ inline std::size_t c_tri_base(int a, std::uint32_t wb) {
+  return static_cast<std::size_t>(a) * (a + 1) / 2 * 7 * wb;
+}
+
+// One pass k >= 2.  grid (blocks over b*wb + rest, tau, a); exo: a = 0 and
+// the tables are [tau][b][rest] (tau stride n_prof); endo: table a is
+// [tau][b <= a][rest] at c_tri_base(a).  `in_is_g`: the input is G itself.
+__global__ void __launch_bounds__(256) k_c_bin_level(const double* __restrict__ Hin,
+                                                     double* __restrict__ Hout,
+                                                     const double* __restrict__ binom_k,
+                                                     std::size_t binom_a_stride, int r,
+                                                     std::uint32_t wk, std::uint32_t wb,
+                                                     int endo, int in_is_g, int n_prof) {
+  extern __shared__ double s_bin[];
+  const int a = static_cast<int>(blockIdx.z);
+  const int nb = endo ? a + 1 : r;
+  const double* bt = binom_k + a * binom_a_stride;
+  for (int i = threadIdx.x; i < nb * r; i += blockDim.x) s_bin[i] = bt[i];
+  __syncthreads();
+  const int gid = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= nb * static_cast<int>(wb)) return;
+  const int tau = static_cast<int>(blockIdx.y);
+  const int b = gid / static_cast<int>(wb);
+  const int dk = (gid / static_cast<int>(wk)) % r;
+  const std::size_t out_base =
+      endo ? c_tri_base(a, wb) + static_cast<std::size_t>(tau) * nb * wb
+           : static_cast<std::size_t>(tau) * n_prof;
+  const std::size_t in_base = (endo && !in_is_g) ? out_base : static_cast<std::size_t>(tau) * n_prof;
+  const double* h = Hin + in_base + (gid - b * static_cast<int>(wb) - dk * static_cast<int>(wk));
+  const double* w = s_bin + b * r;
+  const int cap = r - 1;
+  double acc = 0.0;
+  for (int y = 0; y <= b; ++y)
+    acc = fma(w[y], __ldg(h + min(dk + y, cap) * wk + (b - y) * wb), acc);
+  Hout[out_base + gid] = acc;
+}
+
+// Pass k = 1 fused with the Q output: thread = (state, order).
+template <typename T>
+__global__ void __launch_bounds__(256) k_c_bin_q(DevModel dm, const double* __restrict__ H2,
+                                                 T* __restrict__ part_v, T* __restrict__ qout,
+                                                 std::uint64_t lo, std::uint64_t hi, int n_prof,
+                                                 std::uint32_t wb, int endo, int in_is_g) {
+  const int na = static_cast<int>(dm.n_actions), dn = dm.c_dmax + 1;
+  const int r = dm.c_max_order + 1, cap = r - 1, m = dm.c_m;
+  const int a = na - 1 - static_cast<int>(blockIdx.y);  // heaviest first
+  const std::uint64_t s = lo + static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= hi) return;
+  const int tau = static_cast<int>(s / wb);
+  const int rest = static_cast<int>(s - static_cast<std::uint64_t>(tau) * wb);
+  const int x1 = rest % r;
+  const std::size_t base =
+      (endo && !in_is_g) ? c_tri_base(a, wb) + static_cast<std::size_t>(tau) * (a + 1) * wb
+                         : static_cast<std::size_t>(tau) * n_prof;
+  const double* h = H2 + base + (rest - x1);
+  const double* w = dm.c_binom + (static_cast<std::size_t>(a) * (m - 1) * r + a) * r;  // Bin(.; a, q_1(a))
+  double acc = 0.0;
+  for (int y = 0; y <= a; ++y)
+    acc = fma(__ldg(w + y), __ldg(h + min(x1 + y, cap) + static_cast<std::size_t>(a - y) * wb), acc);
+  double pd_sum = 0.0;
+  for (int d = 0; d < dn; ++d) pd_sum += __ldg(dm.c_pmf + tau * dn + d);
+  const double fixed = a > 0 ? -dm.c_cf : 0.0;
+  const T qa = static_cast<T>(fma(fixed, pd_sum, acc));
+  const std::uint64_t nr = hi - lo;
+  if (part_v) part_v[static_cast<std::uint64_t>(a) * nr + (s - lo)] = qa;
+  if (qout) qout[(s - lo) * na + a] = qa;
+}
+
 // Generic Scenario C kernel for any (m, D_max): one thread per
 // (state, order, demand), so no demand-indexed register array is needed.
 // Writes inner_d into `inner_out` ((a, d, state) layout); k_reduce_c then
@@ -1594,6 +1678,14 @@ std::vector<std::uint16_t> digit_sum_order(int radix, int digits) {
 }  // namespace
 
 // PVI_B_Q16=0 selects the one-state-per-thread stage 2 (comparison runs).
+static bool c_bin_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PVI_C_BINOM");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static bool q16_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PVI_B_Q16");
@@ -1727,20 +1819,53 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
   const int na = static_cast<int>(dm.n_actions);
   double* G = scratch.get<double>(5, static_cast<std::size_t>(n_prof) * 7, stream);
   T* pv = a.want_values ? scratch.get<T>(0, static_cast<std::size_t>(na) * nr, stream) : nullptr;
+  const bool bin = dm.c_binom != nullptr && c_bin_enabled();
+  const bool endo = bin && !dm.c_exogenous;
+  const std::uint32_t wb = static_cast<std::uint32_t>(n_prof / r);  // r^(M-1)
+  // pass tables: exo 7*n_prof each; endo sum_a 7 (a+1) wb each
+  const std::size_t tab = endo ? c_tri_base(r, wb) : static_cast<std::size_t>(n_prof) * 7;
+  double* Hb[2] = {nullptr, nullptr};
+  if (bin && M > 2) {
+    Hb[0] = scratch.get<double>(6, tab, stream);
+    if (M > 3) Hb[1] = scratch.get<double>(7, tab, stream);
+  }
   bool done = false;
+  int launches = 0;
   {
     MainKernelScope prof(stream);
 #define PVI_CF(MM)                                                                               \
   if (!done && M == MM) {                                                                        \
     k_c_fact_g<T, MM><<<dim3(grid_for(n_prof, 256), 7), 256, 0, stream>>>(dm, a.v, G, static_cast<int>(n_prof), a.gamma); \
-    k_c_fact_q<T, MM><<<dim3(grid_for(nr, 128), na), 128, 0, stream>>>(dm, G, pv, a.qout, lo, hi, static_cast<int>(n_prof)); \
+    if (!bin)                                                                                    \
+      k_c_fact_q<T, MM><<<dim3(grid_for(nr, 128), na), 128, 0, stream>>>(dm, G, pv, a.qout, lo, hi, static_cast<int>(n_prof)); \
     done = true;                                                                                 \
   }
     PVI_CF(2) PVI_CF(3) PVI_CF(4) PVI_CF(5) PVI_CF(6)
 #undef PVI_CF
+    launches = 2;
+    if (done && bin) {
+      // passes k = m-1 .. 2 (G -> Hb[0] -> Hb[1] -> ..), then k = 1 fused with Q
+      const double* src = G;
+      std::uint32_t wk = wb;
+      const std::size_t per_k = static_cast<std::size_t>(r) * r;
+      const std::size_t a_stride = static_cast<std::size_t>(M - 1) * per_k;
+      const std::size_t smem = per_k * sizeof(double);
+      for (int k = M - 1, i = 0; k >= 2; --k, ++i) {
+        wk /= static_cast<std::uint32_t>(r);
+        double* dst = Hb[i & 1];
+        const unsigned blocks = grid_for(static_cast<std::uint64_t>(r) * wb, 256);
+        k_c_bin_level<<<dim3(blocks, 7, endo ? r : 1), 256, smem, stream>>>(
+            src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, endo ? a_stride : 0, r, wk,
+            wb, endo ? 1 : 0, src == G ? 1 : 0, static_cast<int>(n_prof));
+        src = dst;
+      }
+      k_c_bin_q<T><<<dim3(grid_for(nr, 256), na), 256, 0, stream>>>(
+          dm, src, pv, a.qout, lo, hi, static_cast<int>(n_prof), wb, endo ? 1 : 0, src == G ? 1 : 0);
+      launches = M;  // G, m-2 passes, fused pass + Q
+    }
   }
   if (!done) return false;
-  count_launches(a.want_values ? 3 : 2);
+  count_launches(a.want_values ? launches + 1 : launches);
   PVI_CUDA(cudaGetLastError());
   if (a.want_values)
     k_finalize<T><<<grid_for(nr, 256), 256, 0, stream>>>(pv, nullptr, na, 1, a.v, a.vout, a.act, lo, hi,

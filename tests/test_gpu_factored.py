@@ -130,3 +130,23 @@ def test_factored_shards_equal_full_sweep(pvi, preset, parts):
     lo, hi = n // 3 + 17, n // 3 + 17 + 5000
     v, a = pvi.bellman_backup_batch(m, V, lo, hi)
     np.testing.assert_array_equal(v, full_v[lo:hi])
+
+
+@pytest.mark.parametrize("preset", ["c/m5/exp1", "c/m5/exp2"])
+def test_factored_c_full_sweep_close_to_exact(pvi, preset):
+    """Whole-space backup: c/m5/exp1 has an exogenous receipt law and runs
+    the sequential-binomial passes (k_c_exo_level); exp2 is endogenous and
+    runs the composition gather (k_c_fact_q).  Both agree with the exact
+    (reference-order) sweep to rounding."""
+    exact = pvi.make_preset(preset)
+    fact = pvi.make_preset(preset).set_algorithm("factored")
+    n = exact.state_count()
+    V = np.random.default_rng(11).uniform(-30.0, 30.0, n)
+    ve, ae = pvi.bellman_backup_batch(exact, V, 0, n)
+    vf, af = pvi.bellman_backup_batch(fact, V, 0, n)
+    np.testing.assert_allclose(vf, ve, rtol=1e-12, atol=1e-10)
+    bad = np.nonzero(af != ae)[0]
+    assert len(bad) <= n // 10000
+    for s in bad[:50]:
+        q = pvi.q_rows(exact, V, int(s), int(s) + 1)[0]
+        assert abs(q[af[s]] - q[ae[s]]) <= 1e-9 * max(1.0, abs(q[ae[s]]))
