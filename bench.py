@@ -247,33 +247,6 @@ def workload_config(model, args, world):
             "parallelism": f"state-shards x{world} (cost-weighted, NCCL all-gather)"}
 
 
-def factored_fmas(model) -> float:
-    """FP64 FMAs the factored kernels execute per sweep (both stages), from
-    their loop bounds: the work the algorithm actually does."""
-    sc = model.scenario()
-    if sc == "b":
-        m = model.state_arity() // 2
-        na, nb = model.info.max_order_a + 1, model.info.max_order_b + 1
-
-        def loops(radix, boundary):
-            v = np.arange(radix ** m)
-            digits = [(v // radix ** k) % radix for k in range(m)]  # digits[0] = x_1
-            tot = sum(digits)
-            above = tot - digits[0]
-            if boundary:  # stage 2: h_a = x_1+1..I_a plus the merged block
-                return float(np.sum(above + 1))
-            return float(np.sum(np.where(tot > 0, above + 1 - (digits[0] >= tot), 0)))
-        stage1 = na ** m * loops(nb, False) * nb
-        stage2 = nb ** m * na * loops(na, True) * nb * 2
-        return stage1 + stage2
-    if sc == "c":
-        r = model.info.max_order_a + 1
-        m = model.state_arity()
-        prof = 7 * r ** m * 21
-        return prof + model.state_count() * model.terms_per_sweep() / model.state_count() / 21
-    return model.terms_per_sweep()
-
-
 def ours_arm(args, world, rank, local):
     import torch
     import torch.distributed as dist
@@ -370,7 +343,7 @@ def ours_arm(args, world, rank, local):
                         "reference terms; compute_roofline below is its real work. DESIGN.md 4-5."}
     fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12  # 2:1 FP32:FP64 (ncu), nominal clock
     if args.algorithm == "factored":
-        flops = 2.0 * factored_fmas(model) * (shard_terms / terms)
+        flops = 2.0 * model.info.factored_fmas * (shard_terms / terms)
     else:
         flops = 5.0 * shard_terms  # the reference's 5 unfused f64 ops per term
     compute = {"unit": "TFLOP/s (FP64)", "achieved": flops / kernel_s / 1e12 if kernel_ms else 0.0,

@@ -138,6 +138,9 @@ typedef struct {
   int products;                 /* Simulator::products */
   double terms_per_sweep;       /* reference backup terms (s,a,w) per sweep */
   int max_order_a, max_order_b; /* B: resolved caps; A/C: max_order, 0 */
+  double factored_fmas;         /* FP64 FMAs per full sweep of the factored kernels (B, C;
+                                   A: = terms_per_sweep) -- the work the algorithm does */
+  int receipt_exogenous;        /* C: receipt law independent of the order size */
 } pvi_model_info;
 
 int pvi_model_get_info(const pvi_model* m, pvi_model_info* out);

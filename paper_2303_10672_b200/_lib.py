@@ -52,7 +52,8 @@ class ModelInfo(C.Structure):
                 ("periodicity", C.c_int), ("state_arity", C.c_uint32),
                 ("action_arity", C.c_uint32), ("products", C.c_int),
                 ("terms_per_sweep", C.c_double), ("max_order_a", C.c_int),
-                ("max_order_b", C.c_int)]
+                ("max_order_b", C.c_int), ("factored_fmas", C.c_double),
+                ("receipt_exogenous", C.c_int)]
 
 
 class ViConfigC(C.Structure):

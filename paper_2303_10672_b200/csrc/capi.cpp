@@ -179,6 +179,8 @@ int pvi_model_get_info(const pvi_model* m, pvi_model_info* out) {
     i.action_arity = md.scenario == PVI_SCENARIO_B ? 2 : 1;
     i.products = md.scenario == PVI_SCENARIO_B ? 2 : 1;
     i.terms_per_sweep = md.terms_per_sweep();
+    i.factored_fmas = md.factored_fmas();
+    i.receipt_exogenous = md.scenario == PVI_SCENARIO_C && md.c_exogenous ? 1 : 0;
     if (md.scenario == PVI_SCENARIO_B) {
       i.max_order_a = md.b_na - 1;
       i.max_order_b = md.b_nb - 1;

@@ -592,6 +592,51 @@ double Model::terms_per_sweep() const {
   }
 }
 
+// Loop bounds of the factored kernels (vi_kernels.cu, K1-B / K1-C factored),
+// summed over one full sweep.
+double Model::factored_fmas() const {
+  if (scenario == PVI_SCENARIO_B) {
+    const int life = pb.useful_life;
+    // sum over the `life` digits (x_1 = digits[0]) of one product's block
+    auto loops = [&](int radix, bool boundary) {
+      double acc = 0.0;
+      const long long count = static_cast<long long>(std::pow(double(radix), life));
+      for (long long v = 0; v < count; ++v) {
+        long long rem = v;
+        int x1 = 0, tot = 0;
+        for (int k = 0; k < life; ++k) {
+          const int d = static_cast<int>(rem % radix);
+          rem /= radix;
+          if (k == 0) x1 = d;
+          tot += d;
+        }
+        const int above = tot - x1;
+        if (boundary) acc += above + 1;  // stage 2: h_a = x_1+1..I_a plus the merged block
+        else if (tot > 0) acc += above + 1 - (x1 >= tot ? 1 : 0);
+      }
+      return acc;
+    };
+    const double na = b_na, nb = b_nb;
+    const double stage1 = std::pow(na, life) * loops(b_nb, false) * nb;
+    const double stage2 = std::pow(nb, life) * na * loops(b_na, true) * nb * 2.0;
+    return stage1 + stage2;
+  }
+  if (scenario == PVI_SCENARIO_C) {
+    const int life = pc.useful_life;
+    const double r = pc.max_order + 1;
+    const double wb = std::pow(r, life - 1);
+    const double g = 7.0 * wb * r * (pc.max_demand + 1);  // profile table
+    double pass = 0.0, fin = 0.0;
+    for (int a = 0; a <= pc.max_order; ++a) {
+      fin += a + 1;                                       // fused k = 1 pass, per state
+      if (c_exogenous) pass += a + 1;                     // shared table: b = a, all b
+      else pass += (a + 1.0) * (a + 2.0) / 2.0;           // table a: b <= a
+    }
+    return g + (life - 2) * 7.0 * wb * pass + static_cast<double>(space.count) * fin;
+  }
+  return terms_per_sweep();
+}
+
 double Model::state_cost(std::uint64_t s) const {
   if (scenario != PVI_SCENARIO_B) return 1.0;
   int st[kMaxDigits];

@@ -151,6 +151,7 @@ struct Model {
   const DevModel& device_view(int device) const;  // uploads on first use
   DeviceCopy& device_copy(int device) const;      // device_view's backing record
   double terms_per_sweep() const;
+  double factored_fmas() const;  // FP64 FMAs per sweep of the factored kernels
   double state_cost(std::uint64_t s) const;  // relative backup cost of one state
   std::uint64_t tile_states() const;         // partition alignment
 };

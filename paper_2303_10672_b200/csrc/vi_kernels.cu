@@ -1070,6 +1070,155 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_q16(DevModel dm, const double
   }
 }
 
+// Stage 2 for m = 3 by diagonals (order_b radix 16, order_a radix <= 16).
+// Splitting the issued-A law as pmf_a(h) for every h <= I_a plus a boundary
+// correction at h = I_a (whose aged profile is always (0, 0)), the sum over
+// h_a of a state x_a = (x_1, x_2, x_3) becomes
+//
+//   U = cdf(x_1) R(x_2, x_3)                                  h <= x_1
+//     + sum_{j < x_2} pmf(x_1 + x_2 - j) R(j, x_3)            x_1 < h <= x_1 + x_2
+//     + sum_{j < x_3} pmf(I_a - j) R(0, j)                    x_1 + x_2 < h <= I_a
+//     + (sf(I_a) - pmf(I_a)) R(0, 0)
+//
+// for both inner products (R = W with pmf_a / cdf_a, and R = sf_b V0 with
+// pz(I_b, .) / pz_cum(I_b, .)).  The second line only depends on
+// S2 = x_1 + x_2 and the prefix j < x_2, so walking a diagonal S2 = const
+// with u = x_2 = 0, 1, .. carries it as a running sum, and the last two
+// lines are constant along the diagonal (I_a = S2 + x_3): one accumulator per
+// order_b holds all of it.  ~6 FP64 ops per (state, order) instead of
+// ~2 (I_a - x_1 + 1) FMAs in k_b_fact_q16.  Warp = one x_3, lane = one
+// diagonal S2 with all 16 orders_b in registers (no cross-lane max): at
+// every step the lanes read the same R row (shared-memory broadcast), the
+// weights are consecutive table entries and the lanes' ER/PT are contiguous.
+// Not the reference's summation order (factored contract).
+template <typename T, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_b_fact_qd3(DevModel dm, const double* __restrict__ W,
+                                                          const double* __restrict__ v0t,
+                                                          const double* __restrict__ erpt,
+                                                          T* __restrict__ part_v,
+                                                          std::uint8_t* __restrict__ part_a,
+                                                          T* __restrict__ qout, std::uint64_t lo,
+                                                          std::uint64_t hi, double gamma, int n_xb,
+                                                          int n_ap, int n_r) {
+  constexpr int NB = 16;
+  extern __shared__ double sm[];
+  const int na = dm.b_na, dn = dm.b_dn;
+  double* w_sl = sm;                   // [ap][ob] gamma W
+  double* v_sl = w_sl + n_ap * NB;     // [ap][ob] gamma sf_b(I_b) V0
+  double* s_pa = v_sl + n_ap * NB;     // pmf_a
+  double* s_ca = s_pa + dn;            // cdf_a (inclusive)
+  double* s_pz = s_ca + dn;            // pz(I_b, .)
+  double* s_cg = s_pz + dn;            // pz_cum(I_b, .) (exclusive)
+  double* s_sa = s_cg + dn;            // sf_a
+  const int xbi = blockIdx.y;
+  const int oa = blockIdx.x;
+  int ib = 0;
+  {
+    int rem = xbi;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      ib += rem % NB;
+      rem /= NB;
+    }
+  }
+  const double gsf = gamma * dm.b_sf_b[ib];
+  const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
+  {
+    const double2* wsrc = reinterpret_cast<const double2*>(W + (static_cast<std::size_t>(xbi) * n_r + r0) * NB);
+    const double2* vsrc = reinterpret_cast<const double2*>(v0t + r0 * NB);
+    double2* wd = reinterpret_cast<double2*>(w_sl);
+    double2* vd = reinterpret_cast<double2*>(v_sl);
+    for (int i = threadIdx.x; i < n_ap * NB / 2; i += blockDim.x) {
+      const double2 w = wsrc[i], v = __ldg(vsrc + i);
+      wd[i] = make_double2(gamma * w.x, gamma * w.y);
+      vd[i] = make_double2(gsf * v.x, gsf * v.y);
+    }
+  }
+  for (int i = threadIdx.x; i < dn; i += blockDim.x) {
+    s_pa[i] = dm.b_pmf_a[i];
+    s_ca[i] = dm.b_cdf_a[i];
+    s_pz[i] = dm.b_pz[ib * dn + i];
+    s_cg[i] = dm.b_pz_cum[ib * dn + i];
+    s_sa[i] = dm.b_sf_a[i];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S2 = lane;                        // this lane's diagonal x_1 + x_2
+  const int smax = 2 * (na - 1);
+  const bool lane_ok = S2 <= smax;
+  // 32-bit state arithmetic (the launcher requires |S| < 2^31)
+  const int n_xa = na * na * na;
+  const int ilo = static_cast<int>(lo), ihi = static_cast<int>(hi);
+  const double c0 = dm.b_cva * oa, cvb = dm.b_cvb;
+  const double2* er_base = reinterpret_cast<const double2*>(erpt) + static_cast<std::size_t>(xbi) * n_xa;
+  T* pv_base = part_v ? part_v + static_cast<std::size_t>(oa) * (hi - lo) : nullptr;
+  std::uint8_t* pa_base = part_a ? part_a + static_cast<std::size_t>(oa) * (hi - lo) : nullptr;
+  for (int x3 = warp; x3 < na; x3 += blockDim.x >> 5) {
+    const int xa_lo = x3 * na * na;
+    if ((xa_lo + na * na - 1) * n_xb + xbi < ilo || xa_lo * n_xb + xbi >= ihi)
+      continue;  // warp-uniform: no state of this x_3 in the shard
+    const int I = min(S2 + x3, dn - 1);
+    // the diagonal constant: third block + both boundary corrections
+    double acc[NB];
+    {
+      const double cw = s_sa[I] - s_pa[I];
+      const double cg = (1.0 - s_cg[I]) - s_pz[I];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) acc[k] = fma(cw, w_sl[k], cg * v_sl[k]);
+      for (int j = 0; j < x3; ++j) {
+        const double* wr = w_sl + (j * na) * NB;
+        const double* vr = v_sl + (j * na) * NB;
+        const double pa = s_pa[max(I - j, 0)], pg = s_pz[max(I - j, 0)];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) acc[k] = fma(pa, wr[k], fma(pg, vr[k], acc[k]));
+      }
+    }
+    // state of step u: x_1 = S2 - u, x_2 = u; each step moves x_a by na - 1
+    int xa = S2 + xa_lo;
+    double2 e_next = __ldg(er_base + min(xa, n_xa - 1));
+    const double* wrow = w_sl + (x3 * na) * NB;
+    const double* vrow = v_sl + (x3 * na) * NB;
+    for (int u = 0; u < na; ++u, xa += na - 1, wrow += NB, vrow += NB) {
+      const double2 e = e_next;
+      if (u + 1 < na) e_next = __ldg(er_base + min(max(xa + na - 1, 0), n_xa - 1));
+      const int x1 = S2 - u;
+      const int xc = max(min(x1, dn - 2), 0);
+      const bool out = lane_ok && x1 >= 0 && x1 <= na - 1;
+      const int st = xa * n_xb + xbi;
+      const bool valid = out && st >= ilo && st < ihi;
+      const double pa = s_pa[xc], pg = s_pz[xc];
+      if (__any_sync(0xffffffffu, out)) {
+        const double ca = s_ca[xc], cgx = s_cg[xc + 1];
+        const double d = cvb * e.y;
+        double base = fma(-c0, e.y, e.x);  // ER - C_v^a o_a PT, then - C_v^b o_b PT
+        T best = T(0);
+        int bo = 0;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          const double wk = wrow[k], vk = vrow[k];
+          const double qd = base + fma(ca, wk, fma(cgx, vk, acc[k]));
+          const T qv = static_cast<T>(qd);
+          if (k == 0 || qv > best) {
+            best = qv;
+            bo = k;
+          }
+          if (qout != nullptr && valid)
+            qout[static_cast<std::uint64_t>(st - ilo) * dm.n_actions + static_cast<std::uint64_t>(oa) * NB + k] = qv;
+          acc[k] = fma(pa, wk, fma(pg, vk, acc[k]));
+          base -= d;
+        }
+        if (valid && pv_base) {
+          pv_base[st - ilo] = best;
+          pa_base[st - ilo] = static_cast<std::uint8_t>(bo);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NB; ++k) acc[k] = fma(pa, wrow[k], fma(pg, vrow[k], acc[k]));
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K1-C: one thread per (state, order); the demand dimension unrolled into
 // DN register accumulators.  Blocks run heaviest order first.  Term order
@@ -1686,6 +1835,22 @@ static bool c_bin_enabled() {
   return on;
 }
 
+static bool qd_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PVI_B_QD");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static int qd_occ() {
+  static const int v = [] {
+    const char* e = std::getenv("PVI_QD_OCC");
+    return e ? std::atoi(e) : 2;
+  }();
+  return v;
+}
+
 static bool q16_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PVI_B_Q16");
@@ -1782,7 +1947,14 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     k_b_fact_w<T, MM, NBX><<<static_cast<unsigned>(n_r), 256, sm1, stream>>>(                       \
         dm, a.v, W, v0t, dc.b_order_b, static_cast<int>(n_xb), static_cast<int>(n_bp), static_cast<int>(n_r)); \
     }                                                                                              \
-    if (nb == 16 && na <= 16 && q16_enabled()) {                                                   \
+    if (MM == 3 && nb == 16 && na <= 16 && dm.n_states < (1ull << 31) && qd_enabled()) {       \
+      const std::size_t sm4 = sizeof(double) * (2 * static_cast<std::size_t>(n_ap) * 16 + 5 * dm.b_dn); \
+      auto kq = qd_occ() == 3 ? k_b_fact_qd3<T, 3> : k_b_fact_qd3<T, 2>;                           \
+      cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);           \
+      kq<<<dim3(static_cast<unsigned>(na), static_cast<unsigned>(n_xb)), 256, sm4, stream>>>(      \
+          dm, W, v0t, dc.b_erpt, pv, pa, a.qout, lo, hi, a.gamma, static_cast<int>(n_xb),           \
+          static_cast<int>(n_ap), static_cast<int>(n_r));                                          \
+    } else if (nb == 16 && na <= 16 && q16_enabled()) {                                            \
       const std::size_t sm3 = sizeof(double) * (2 * slab_rows(static_cast<int>(n_ap)) * slab_stride(16) + 5 * dm.b_dn); \
       cudaFuncSetAttribute(k_b_fact_q16<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
       k_b_fact_q16<T, MM><<<dim3(static_cast<unsigned>(na), static_cast<unsigned>(n_xb)), 256, sm3, stream>>>( \

@@ -150,3 +150,26 @@ def test_factored_c_full_sweep_close_to_exact(pvi, preset):
     for s in bad[:50]:
         q = pvi.q_rows(exact, V, int(s), int(s) + 1)[0]
         assert abs(q[af[s]] - q[ae[s]]) <= 1e-9 * max(1.0, abs(q[ae[s]]))
+
+
+@pytest.mark.parametrize("preset", ["b/m3/exp1", "b/m3/exp4"])
+def test_factored_b_full_sweep_close_to_exact(pvi, preset):
+    """Whole-space backup against the exact (reference-order) sweep: every
+    x_a digit pattern goes through the diagonal stage-2 kernel
+    (k_b_fact_qd3 on b/m3/exp1)."""
+    exact = pvi.make_preset(preset)
+    fact = pvi.make_preset(preset).set_algorithm("factored")
+    n = exact.state_count()
+    V = np.random.default_rng(13).uniform(-8.0, 8.0, n)
+    ve, ae = pvi.bellman_backup_batch(exact, V, 0, n)
+    vf, af = pvi.bellman_backup_batch(fact, V, 0, n)
+    np.testing.assert_allclose(vf, ve, rtol=1e-12, atol=1e-11)
+    bad = np.nonzero(af != ae)[0]
+    assert len(bad) <= n // 10000
+    for s in bad[:50]:
+        q = pvi.q_rows(exact, V, int(s), int(s) + 1)[0]
+        assert abs(q[af[s]] - q[ae[s]]) <= 1e-9 * max(1.0, abs(q[ae[s]]))
+    # scattered single-state Q rows (every order pair)
+    for s in np.random.default_rng(14).integers(0, n, 16):
+        np.testing.assert_allclose(pvi.q_rows(fact, V, int(s), int(s) + 1),
+                                   pvi.q_rows(exact, V, int(s), int(s) + 1), rtol=1e-12, atol=1e-11)
