@@ -1091,8 +1091,8 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_q16(DevModel dm, const double
 // every step the lanes read the same R row (shared-memory broadcast), the
 // weights are consecutive table entries and the lanes' ER/PT are contiguous.
 // Not the reference's summation order (factored contract).
-template <typename T, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_b_fact_qd3(DevModel dm, const double* __restrict__ W,
+template <typename T, bool WA, bool WQ>  // WA: argmax wanted, WQ: write every Q
+__global__ void __launch_bounds__(256, 2) k_b_fact_qd3(DevModel dm, const double* __restrict__ W,
                                                           const double* __restrict__ v0t,
                                                           const double* __restrict__ erpt,
                                                           T* __restrict__ part_v,
@@ -1103,13 +1103,15 @@ __global__ void __launch_bounds__(256, MINB) k_b_fact_qd3(DevModel dm, const dou
   constexpr int NB = 16;
   extern __shared__ double sm[];
   const int na = dm.b_na, dn = dm.b_dn;
-  double* w_sl = sm;                   // [ap][ob] gamma W
-  double* v_sl = w_sl + n_ap * NB;     // [ap][ob] gamma sf_b(I_b) V0
-  double* s_pa = v_sl + n_ap * NB;     // pmf_a
-  double* s_ca = s_pa + dn;            // cdf_a (inclusive)
-  double* s_pz = s_ca + dn;            // pz(I_b, .)
-  double* s_cg = s_pz + dn;            // pz_cum(I_b, .) (exclusive)
-  double* s_sa = s_cg + dn;            // sf_a
+  double* w_sl = sm;                   // [ap][ob] W rows of this (x_b, o_a)
+  double* v_sl = w_sl + n_ap * NB;     // [ap][ob] V0 rows of this o_a
+  // gamma and sf_b(I_b) are folded into the weights, so the rows are copied
+  // verbatim (cp.async, 16 B per request, no register round trip)
+  double* s_pa = v_sl + n_ap * NB;     // gamma pmf_a
+  double* s_ca = s_pa + dn;            // gamma cdf_a (inclusive)
+  double* s_pz = s_ca + dn;            // gamma sf_b pz(I_b, .)
+  double* s_cg = s_pz + dn;            // gamma sf_b pz_cum(I_b, .) (exclusive)
+  double* s_sa = s_cg + dn;            // gamma sf_a
   const int xbi = blockIdx.y;
   const int oa = blockIdx.x;
   int ib = 0;
@@ -1126,21 +1128,22 @@ __global__ void __launch_bounds__(256, MINB) k_b_fact_qd3(DevModel dm, const dou
   {
     const double2* wsrc = reinterpret_cast<const double2*>(W + (static_cast<std::size_t>(xbi) * n_r + r0) * NB);
     const double2* vsrc = reinterpret_cast<const double2*>(v0t + r0 * NB);
-    double2* wd = reinterpret_cast<double2*>(w_sl);
-    double2* vd = reinterpret_cast<double2*>(v_sl);
+    const unsigned wd = static_cast<unsigned>(__cvta_generic_to_shared(w_sl));
+    const unsigned vd = static_cast<unsigned>(__cvta_generic_to_shared(v_sl));
     for (int i = threadIdx.x; i < n_ap * NB / 2; i += blockDim.x) {
-      const double2 w = wsrc[i], v = __ldg(vsrc + i);
-      wd[i] = make_double2(gamma * w.x, gamma * w.y);
-      vd[i] = make_double2(gsf * v.x, gsf * v.y);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wd + 16u * i), "l"(wsrc + i));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(vd + 16u * i), "l"(vsrc + i));
     }
+    asm volatile("cp.async.commit_group;\n" ::);
   }
   for (int i = threadIdx.x; i < dn; i += blockDim.x) {
-    s_pa[i] = dm.b_pmf_a[i];
-    s_ca[i] = dm.b_cdf_a[i];
-    s_pz[i] = dm.b_pz[ib * dn + i];
-    s_cg[i] = dm.b_pz_cum[ib * dn + i];
-    s_sa[i] = dm.b_sf_a[i];
+    s_pa[i] = gamma * dm.b_pmf_a[i];
+    s_ca[i] = gamma * dm.b_cdf_a[i];
+    s_pz[i] = gsf * dm.b_pz[ib * dn + i];
+    s_cg[i] = gsf * dm.b_pz_cum[ib * dn + i];
+    s_sa[i] = gamma * dm.b_sf_a[i];
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S2 = lane;                        // this lane's diagonal x_1 + x_2
@@ -1162,7 +1165,7 @@ __global__ void __launch_bounds__(256, MINB) k_b_fact_qd3(DevModel dm, const dou
     double acc[NB];
     {
       const double cw = s_sa[I] - s_pa[I];
-      const double cg = (1.0 - s_cg[I]) - s_pz[I];
+      const double cg = (gsf - s_cg[I]) - s_pz[I];
 #pragma unroll
       for (int k = 0; k < NB; ++k) acc[k] = fma(cw, w_sl[k], cg * v_sl[k]);
       for (int j = 0; j < x3; ++j) {
@@ -1173,14 +1176,17 @@ __global__ void __launch_bounds__(256, MINB) k_b_fact_qd3(DevModel dm, const dou
         for (int k = 0; k < NB; ++k) acc[k] = fma(pa, wr[k], fma(pg, vr[k], acc[k]));
       }
     }
-    // state of step u: x_1 = S2 - u, x_2 = u; each step moves x_a by na - 1
+    // state of step u: x_1 = S2 - u, x_2 = u; each step moves x_a by na - 1.
+    // ER/PT are prefetched two steps ahead.
     int xa = S2 + xa_lo;
-    double2 e_next = __ldg(er_base + min(xa, n_xa - 1));
+    double2 e_n1 = __ldg(er_base + min(xa, n_xa - 1));
+    double2 e_n2 = __ldg(er_base + min(max(xa + na - 1, 0), n_xa - 1));
     const double* wrow = w_sl + (x3 * na) * NB;
     const double* vrow = v_sl + (x3 * na) * NB;
     for (int u = 0; u < na; ++u, xa += na - 1, wrow += NB, vrow += NB) {
-      const double2 e = e_next;
-      if (u + 1 < na) e_next = __ldg(er_base + min(max(xa + na - 1, 0), n_xa - 1));
+      const double2 e = e_n1;
+      e_n1 = e_n2;
+      if (u + 2 < na) e_n2 = __ldg(er_base + min(max(xa + 2 * (na - 1), 0), n_xa - 1));
       const int x1 = S2 - u;
       const int xc = max(min(x1, dn - 2), 0);
       const bool out = lane_ok && x1 >= 0 && x1 <= na - 1;
@@ -1188,28 +1194,31 @@ __global__ void __launch_bounds__(256, MINB) k_b_fact_qd3(DevModel dm, const dou
       const bool valid = out && st >= ilo && st < ihi;
       const double pa = s_pa[xc], pg = s_pz[xc];
       if (__any_sync(0xffffffffu, out)) {
+        // Q(o_b) = base + t(o_b), base = ER - C_v^a o_a PT common to the
+        // row: the first max is taken over t = U(o_b) - o_b C_v^b PT
         const double ca = s_ca[xc], cgx = s_cg[xc + 1];
         const double d = cvb * e.y;
-        double base = fma(-c0, e.y, e.x);  // ER - C_v^a o_a PT, then - C_v^b o_b PT
-        T best = T(0);
+        const double base = fma(-c0, e.y, e.x);
+        double best = 0.0;
         int bo = 0;
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
           const double wk = wrow[k], vk = vrow[k];
-          const double qd = base + fma(ca, wk, fma(cgx, vk, acc[k]));
-          const T qv = static_cast<T>(qd);
-          if (k == 0 || qv > best) {
-            best = qv;
-            bo = k;
+          const double t = fma(-static_cast<double>(k), d, fma(ca, wk, fma(cgx, vk, acc[k])));
+          if (WQ) {
+            if (valid)
+              qout[static_cast<std::uint64_t>(st - ilo) * dm.n_actions + static_cast<std::uint64_t>(oa) * NB + k] =
+                  static_cast<T>(base + t);
           }
-          if (qout != nullptr && valid)
-            qout[static_cast<std::uint64_t>(st - ilo) * dm.n_actions + static_cast<std::uint64_t>(oa) * NB + k] = qv;
+          if (k == 0 || t > best) {
+            best = t;
+            if (WA) bo = k;
+          }
           acc[k] = fma(pa, wk, fma(pg, vk, acc[k]));
-          base -= d;
         }
         if (valid && pv_base) {
-          pv_base[st - ilo] = best;
-          pa_base[st - ilo] = static_cast<std::uint8_t>(bo);
+          pv_base[st - ilo] = static_cast<T>(base + best);
+          if (WA) pa_base[st - ilo] = static_cast<std::uint8_t>(bo);
         }
       } else {
 #pragma unroll
@@ -1843,14 +1852,6 @@ static bool qd_enabled() {
   return on;
 }
 
-static int qd_occ() {
-  static const int v = [] {
-    const char* e = std::getenv("PVI_QD_OCC");
-    return e ? std::atoi(e) : 2;
-  }();
-  return v;
-}
-
 static bool q16_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PVI_B_Q16");
@@ -1949,7 +1950,9 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     }                                                                                              \
     if (MM == 3 && nb == 16 && na <= 16 && dm.n_states < (1ull << 31) && qd_enabled()) {       \
       const std::size_t sm4 = sizeof(double) * (2 * static_cast<std::size_t>(n_ap) * 16 + 5 * dm.b_dn); \
-      auto kq = qd_occ() == 3 ? k_b_fact_qd3<T, 3> : k_b_fact_qd3<T, 2>;                           \
+      auto kq = a.qout ? k_b_fact_qd3<T, true, true>                                               \
+                       : (a.act ? k_b_fact_qd3<T, true, false> : k_b_fact_qd3<T, false, false>);    \
+      if (!a.act) pa = nullptr;                                                                    \
       cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);           \
       kq<<<dim3(static_cast<unsigned>(na), static_cast<unsigned>(n_xb)), 256, sm4, stream>>>(      \
           dm, W, v0t, dc.b_erpt, pv, pa, a.qout, lo, hi, a.gamma, static_cast<int>(n_xb),           \
