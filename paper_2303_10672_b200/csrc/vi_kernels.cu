@@ -1091,7 +1091,12 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_q16(DevModel dm, const double
 // every step the lanes read the same R row (shared-memory broadcast), the
 // weights are consecutive table entries and the lanes' ER/PT are contiguous.
 // Not the reference's summation order (factored contract).
-template <typename T, bool WA, bool WQ>  // WA: argmax wanted, WQ: write every Q
+//
+// FUSED (the sweep path): one CTA per x_b loops over the orders_a, keeps the
+// running first-max per x_a in shared memory and ends with the finalize work
+// (V', argmax, convergence statistics) -- no (o_a, state) partial buffers.
+// Otherwise one CTA per (o_a, x_b) writes per-o_a partials (q_rows path).
+template <typename T, bool WA, bool WQ, bool FUSED>  // WA: argmax, WQ: every Q
 __global__ void __launch_bounds__(256, 2) k_b_fact_qd3(DevModel dm, const double* __restrict__ W,
                                                           const double* __restrict__ v0t,
                                                           const double* __restrict__ erpt,
@@ -1099,10 +1104,14 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qd3(DevModel dm, const double
                                                           std::uint8_t* __restrict__ part_a,
                                                           T* __restrict__ qout, std::uint64_t lo,
                                                           std::uint64_t hi, double gamma, int n_xb,
-                                                          int n_ap, int n_r) {
+                                                          int n_ap, int n_r, const T* __restrict__ V,
+                                                          T* __restrict__ vout,
+                                                          std::uint32_t* __restrict__ act,
+                                                          std::uint64_t out_off, FinalizeArgs fa) {
   constexpr int NB = 16;
   extern __shared__ double sm[];
   const int na = dm.b_na, dn = dm.b_dn;
+  const int n_xa = na * na * na;
   double* w_sl = sm;                   // [ap][ob] W rows of this (x_b, o_a)
   double* v_sl = w_sl + n_ap * NB;     // [ap][ob] V0 rows of this o_a
   // gamma and sf_b(I_b) are folded into the weights, so the rows are copied
@@ -1112,8 +1121,9 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qd3(DevModel dm, const double
   double* s_pz = s_ca + dn;            // gamma sf_b pz(I_b, .)
   double* s_cg = s_pz + dn;            // gamma sf_b pz_cum(I_b, .) (exclusive)
   double* s_sa = s_cg + dn;            // gamma sf_a
-  const int xbi = blockIdx.y;
-  const int oa = blockIdx.x;
+  T* s_best = reinterpret_cast<T*>(s_sa + dn);                             // FUSED: [x_a]
+  std::uint8_t* s_arg = reinterpret_cast<std::uint8_t*>(s_best + n_xa);   // FUSED: [x_a]
+  const int xbi = FUSED ? blockIdx.x : blockIdx.y;
   int ib = 0;
   {
     int rem = xbi;
@@ -1124,18 +1134,6 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qd3(DevModel dm, const double
     }
   }
   const double gsf = gamma * dm.b_sf_b[ib];
-  const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
-  {
-    const double2* wsrc = reinterpret_cast<const double2*>(W + (static_cast<std::size_t>(xbi) * n_r + r0) * NB);
-    const double2* vsrc = reinterpret_cast<const double2*>(v0t + r0 * NB);
-    const unsigned wd = static_cast<unsigned>(__cvta_generic_to_shared(w_sl));
-    const unsigned vd = static_cast<unsigned>(__cvta_generic_to_shared(v_sl));
-    for (int i = threadIdx.x; i < n_ap * NB / 2; i += blockDim.x) {
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wd + 16u * i), "l"(wsrc + i));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(vd + 16u * i), "l"(vsrc + i));
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-  }
   for (int i = threadIdx.x; i < dn; i += blockDim.x) {
     s_pa[i] = gamma * dm.b_pmf_a[i];
     s_ca[i] = gamma * dm.b_cdf_a[i];
@@ -1143,88 +1141,129 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qd3(DevModel dm, const double
     s_cg[i] = gsf * dm.b_pz_cum[ib * dn + i];
     s_sa[i] = gamma * dm.b_sf_a[i];
   }
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S2 = lane;                        // this lane's diagonal x_1 + x_2
   const int smax = 2 * (na - 1);
   const bool lane_ok = S2 <= smax;
   // 32-bit state arithmetic (the launcher requires |S| < 2^31)
-  const int n_xa = na * na * na;
   const int ilo = static_cast<int>(lo), ihi = static_cast<int>(hi);
-  const double c0 = dm.b_cva * oa, cvb = dm.b_cvb;
+  const double cvb = dm.b_cvb;
   const double2* er_base = reinterpret_cast<const double2*>(erpt) + static_cast<std::size_t>(xbi) * n_xa;
-  T* pv_base = part_v ? part_v + static_cast<std::size_t>(oa) * (hi - lo) : nullptr;
-  std::uint8_t* pa_base = part_a ? part_a + static_cast<std::size_t>(oa) * (hi - lo) : nullptr;
-  for (int x3 = warp; x3 < na; x3 += blockDim.x >> 5) {
-    const int xa_lo = x3 * na * na;
-    if ((xa_lo + na * na - 1) * n_xb + xbi < ilo || xa_lo * n_xb + xbi >= ihi)
-      continue;  // warp-uniform: no state of this x_3 in the shard
-    const int I = min(S2 + x3, dn - 1);
-    // the diagonal constant: third block + both boundary corrections
-    double acc[NB];
+  const int oa_first = FUSED ? 0 : static_cast<int>(blockIdx.x);
+  const int oa_end = FUSED ? na : oa_first + 1;
+  for (int oa = oa_first; oa < oa_end; ++oa) {
+    const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
+    if (FUSED && oa > 0) __syncthreads();  // every warp is done with the previous rows
     {
-      const double cw = s_sa[I] - s_pa[I];
-      const double cg = (gsf - s_cg[I]) - s_pz[I];
+      const double2* wsrc = reinterpret_cast<const double2*>(W + (static_cast<std::size_t>(xbi) * n_r + r0) * NB);
+      const double2* vsrc = reinterpret_cast<const double2*>(v0t + r0 * NB);
+      const unsigned wd = static_cast<unsigned>(__cvta_generic_to_shared(w_sl));
+      const unsigned vd = static_cast<unsigned>(__cvta_generic_to_shared(v_sl));
+      for (int i = threadIdx.x; i < n_ap * NB / 2; i += blockDim.x) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wd + 16u * i), "l"(wsrc + i));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(vd + 16u * i), "l"(vsrc + i));
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double c0 = dm.b_cva * oa;
+    T* pv_base = part_v ? part_v + static_cast<std::size_t>(oa) * (hi - lo) : nullptr;
+    std::uint8_t* pa_base = part_a ? part_a + static_cast<std::size_t>(oa) * (hi - lo) : nullptr;
+    for (int x3 = warp; x3 < na; x3 += blockDim.x >> 5) {
+      const int xa_lo = x3 * na * na;
+      if ((xa_lo + na * na - 1) * n_xb + xbi < ilo || xa_lo * n_xb + xbi >= ihi)
+        continue;  // warp-uniform: no state of this x_3 in the shard
+      const int I = min(S2 + x3, dn - 1);
+      // the diagonal constant: third block + both boundary corrections
+      double acc[NB];
+      {
+        const double cw = s_sa[I] - s_pa[I];
+        const double cg = (gsf - s_cg[I]) - s_pz[I];
 #pragma unroll
-      for (int k = 0; k < NB; ++k) acc[k] = fma(cw, w_sl[k], cg * v_sl[k]);
-      for (int j = 0; j < x3; ++j) {
-        const double* wr = w_sl + (j * na) * NB;
-        const double* vr = v_sl + (j * na) * NB;
-        const double pa = s_pa[max(I - j, 0)], pg = s_pz[max(I - j, 0)];
+        for (int k = 0; k < NB; ++k) acc[k] = fma(cw, w_sl[k], cg * v_sl[k]);
+        for (int j = 0; j < x3; ++j) {
+          const double* wr = w_sl + (j * na) * NB;
+          const double* vr = v_sl + (j * na) * NB;
+          const double pa = s_pa[max(I - j, 0)], pg = s_pz[max(I - j, 0)];
 #pragma unroll
-        for (int k = 0; k < NB; ++k) acc[k] = fma(pa, wr[k], fma(pg, vr[k], acc[k]));
+          for (int k = 0; k < NB; ++k) acc[k] = fma(pa, wr[k], fma(pg, vr[k], acc[k]));
+        }
+      }
+      // state of step u: x_1 = S2 - u, x_2 = u; each step moves x_a by na - 1.
+      // ER/PT are prefetched two steps ahead.
+      int xa = S2 + xa_lo;
+      double2 e_n1 = __ldg(er_base + min(xa, n_xa - 1));
+      double2 e_n2 = __ldg(er_base + min(max(xa + na - 1, 0), n_xa - 1));
+      const double* wrow = w_sl + (x3 * na) * NB;
+      const double* vrow = v_sl + (x3 * na) * NB;
+      for (int u = 0; u < na; ++u, xa += na - 1, wrow += NB, vrow += NB) {
+        const double2 e = e_n1;
+        e_n1 = e_n2;
+        if (u + 2 < na) e_n2 = __ldg(er_base + min(max(xa + 2 * (na - 1), 0), n_xa - 1));
+        const int x1 = S2 - u;
+        const int xc = max(min(x1, dn - 2), 0);
+        const bool out = lane_ok && x1 >= 0 && x1 <= na - 1;
+        const int st = xa * n_xb + xbi;
+        const bool valid = out && st >= ilo && st < ihi;
+        const double pa = s_pa[xc], pg = s_pz[xc];
+        if (__any_sync(0xffffffffu, out)) {
+          // Q(o_b) = base + t(o_b), base = ER - C_v^a o_a PT common to the
+          // row: the first max is taken over t = U(o_b) - o_b C_v^b PT
+          const double ca = s_ca[xc], cgx = s_cg[xc + 1];
+          const double d = cvb * e.y;
+          const double base = fma(-c0, e.y, e.x);
+          double best = 0.0;
+          int bo = 0;
+#pragma unroll
+          for (int k = 0; k < NB; ++k) {
+            const double wk = wrow[k], vk = vrow[k];
+            const double t = fma(-static_cast<double>(k), d, fma(ca, wk, fma(cgx, vk, acc[k])));
+            if (WQ) {
+              if (valid)
+                qout[static_cast<std::uint64_t>(st - ilo) * dm.n_actions + static_cast<std::uint64_t>(oa) * NB + k] =
+                    static_cast<T>(base + t);
+            }
+            if (k == 0 || t > best) {
+              best = t;
+              if (WA) bo = k;
+            }
+            acc[k] = fma(pa, wk, fma(pg, vk, acc[k]));
+          }
+          if (valid) {
+            const T bv = static_cast<T>(base + best);
+            if (FUSED) {
+              // first max over o_a ascending (k_finalize's rule)
+              if (oa == 0 || bv > s_best[xa]) {
+                s_best[xa] = bv;
+                if (WA) s_arg[xa] = static_cast<std::uint8_t>(oa * NB + bo);
+              }
+            } else if (pv_base) {
+              pv_base[st - ilo] = bv;
+              if (WA) pa_base[st - ilo] = static_cast<std::uint8_t>(bo);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < NB; ++k) acc[k] = fma(pa, wrow[k], fma(pg, vrow[k], acc[k]));
+        }
       }
     }
-    // state of step u: x_1 = S2 - u, x_2 = u; each step moves x_a by na - 1.
-    // ER/PT are prefetched two steps ahead.
-    int xa = S2 + xa_lo;
-    double2 e_n1 = __ldg(er_base + min(xa, n_xa - 1));
-    double2 e_n2 = __ldg(er_base + min(max(xa + na - 1, 0), n_xa - 1));
-    const double* wrow = w_sl + (x3 * na) * NB;
-    const double* vrow = v_sl + (x3 * na) * NB;
-    for (int u = 0; u < na; ++u, xa += na - 1, wrow += NB, vrow += NB) {
-      const double2 e = e_n1;
-      e_n1 = e_n2;
-      if (u + 2 < na) e_n2 = __ldg(er_base + min(max(xa + 2 * (na - 1), 0), n_xa - 1));
-      const int x1 = S2 - u;
-      const int xc = max(min(x1, dn - 2), 0);
-      const bool out = lane_ok && x1 >= 0 && x1 <= na - 1;
+  }
+  if (FUSED) {
+    // finalize: V', argmax and the convergence statistics of this x_b's states
+    __syncthreads();
+    double smx = -DBL_MAX, smn = DBL_MAX;
+    unsigned long long bad = ~0ull;
+    for (int xa = threadIdx.x; xa < n_xa; xa += blockDim.x) {
       const int st = xa * n_xb + xbi;
-      const bool valid = out && st >= ilo && st < ihi;
-      const double pa = s_pa[xc], pg = s_pz[xc];
-      if (__any_sync(0xffffffffu, out)) {
-        // Q(o_b) = base + t(o_b), base = ER - C_v^a o_a PT common to the
-        // row: the first max is taken over t = U(o_b) - o_b C_v^b PT
-        const double ca = s_ca[xc], cgx = s_cg[xc + 1];
-        const double d = cvb * e.y;
-        const double base = fma(-c0, e.y, e.x);
-        double best = 0.0;
-        int bo = 0;
-#pragma unroll
-        for (int k = 0; k < NB; ++k) {
-          const double wk = wrow[k], vk = vrow[k];
-          const double t = fma(-static_cast<double>(k), d, fma(ca, wk, fma(cgx, vk, acc[k])));
-          if (WQ) {
-            if (valid)
-              qout[static_cast<std::uint64_t>(st - ilo) * dm.n_actions + static_cast<std::uint64_t>(oa) * NB + k] =
-                  static_cast<T>(base + t);
-          }
-          if (k == 0 || t > best) {
-            best = t;
-            if (WA) bo = k;
-          }
-          acc[k] = fma(pa, wk, fma(pg, vk, acc[k]));
-        }
-        if (valid && pv_base) {
-          pv_base[st - ilo] = static_cast<T>(base + best);
-          if (WA) pa_base[st - ilo] = static_cast<std::uint8_t>(bo);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < NB; ++k) acc[k] = fma(pa, wrow[k], fma(pg, vrow[k], acc[k]));
-      }
+      if (st < ilo || st >= ihi) continue;
+      const T best = s_best[xa];
+      if (vout) vout[st - out_off] = best;
+      if (WA && act) act[st - out_off] = s_arg[xa];
+      state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
     }
+    reduce_stats(smx, smn, bad, fa.stats);
   }
 }
 
@@ -1929,9 +1968,14 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
   const std::uint64_t lo = a.lo, hi = a.hi, nr = hi - lo;
   double* W = scratch.get<double>(3, static_cast<std::size_t>(n_xb) * n_r * nb, stream);
   double* v0t = scratch.get<double>(4, static_cast<std::size_t>(n_r) * nb, stream);
-  T* pv = a.want_values ? scratch.get<T>(0, static_cast<std::size_t>(na) * nr, stream) : nullptr;
-  std::uint8_t* pa = a.want_values ? scratch.get<std::uint8_t>(1, static_cast<std::size_t>(na) * nr, stream) : nullptr;
-  count_launches(a.want_values ? 3 : 2);
+  // m = 3, radix-16 order_b: the diagonal stage 2; on the sweep path fused
+  // over the orders_a with the finalize (no partial buffers, no k_finalize)
+  const bool use_qd = M == 3 && nb == 16 && na <= 16 && dm.n_states < (1ull << 31) && qd_enabled();
+  const bool fused = use_qd && a.want_values && a.qout == nullptr;
+  const bool partials = a.want_values && !fused;
+  T* pv = partials ? scratch.get<T>(0, static_cast<std::size_t>(na) * nr, stream) : nullptr;
+  std::uint8_t* pa = partials ? scratch.get<std::uint8_t>(1, static_cast<std::size_t>(na) * nr, stream) : nullptr;
+  count_launches(partials ? 3 : 2);
   {
     MainKernelScope prof(stream);
 #define PVI_BF(MM, NBX)                                                                            \
@@ -1948,15 +1992,24 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     k_b_fact_w<T, MM, NBX><<<static_cast<unsigned>(n_r), 256, sm1, stream>>>(                       \
         dm, a.v, W, v0t, dc.b_order_b, static_cast<int>(n_xb), static_cast<int>(n_bp), static_cast<int>(n_r)); \
     }                                                                                              \
-    if (MM == 3 && nb == 16 && na <= 16 && dm.n_states < (1ull << 31) && qd_enabled()) {       \
+    if (MM == 3 && use_qd) {                                                                       \
       const std::size_t sm4 = sizeof(double) * (2 * static_cast<std::size_t>(n_ap) * 16 + 5 * dm.b_dn); \
-      auto kq = a.qout ? k_b_fact_qd3<T, true, true>                                               \
-                       : (a.act ? k_b_fact_qd3<T, true, false> : k_b_fact_qd3<T, false, false>);    \
-      if (!a.act) pa = nullptr;                                                                    \
-      cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);           \
-      kq<<<dim3(static_cast<unsigned>(na), static_cast<unsigned>(n_xb)), 256, sm4, stream>>>(      \
-          dm, W, v0t, dc.b_erpt, pv, pa, a.qout, lo, hi, a.gamma, static_cast<int>(n_xb),           \
-          static_cast<int>(n_ap), static_cast<int>(n_r));                                          \
+      if (fused) {                                                                                 \
+        auto kq = a.act ? k_b_fact_qd3<T, true, false, true> : k_b_fact_qd3<T, false, false, true>; \
+        const std::size_t smf = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(T) + 1);            \
+        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);         \
+        kq<<<static_cast<unsigned>(n_xb), 256, smf, stream>>>(                                     \
+            dm, W, v0t, dc.b_erpt, nullptr, nullptr, nullptr, lo, hi, a.gamma, static_cast<int>(n_xb), \
+            static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa);   \
+      } else {                                                                                     \
+        auto kq = a.qout ? k_b_fact_qd3<T, true, true, false>                                      \
+                         : (a.act ? k_b_fact_qd3<T, true, false, false> : k_b_fact_qd3<T, false, false, false>); \
+        if (!a.act) pa = nullptr;                                                                  \
+        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);         \
+        kq<<<dim3(static_cast<unsigned>(na), static_cast<unsigned>(n_xb)), 256, sm4, stream>>>(    \
+            dm, W, v0t, dc.b_erpt, pv, pa, a.qout, lo, hi, a.gamma, static_cast<int>(n_xb),         \
+            static_cast<int>(n_ap), static_cast<int>(n_r), nullptr, nullptr, nullptr, 0, FinalizeArgs{}); \
+      }                                                                                            \
     } else if (nb == 16 && na <= 16 && q16_enabled()) {                                            \
       const std::size_t sm3 = sizeof(double) * (2 * slab_rows(static_cast<int>(n_ap)) * slab_stride(16) + 5 * dm.b_dn); \
       cudaFuncSetAttribute(k_b_fact_q16<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
@@ -1975,7 +2028,7 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
 #undef PVI_BF
   }
   PVI_CUDA(cudaGetLastError());
-  if (a.want_values)
+  if (partials)
     k_finalize<T><<<grid_for(nr, 256), 256, 0, stream>>>(pv, pa, na, nb, a.v, a.vout, a.act, lo, hi,
                                                         a.out_off, a.fa);
   PVI_CUDA(cudaGetLastError());
