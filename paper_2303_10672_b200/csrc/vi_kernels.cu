@@ -1267,6 +1267,169 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qd3(DevModel dm, const double
   }
 }
 
+// Paired diagonals (sweep path, fused over the orders_a like k_b_fact_qd3).
+// In k_b_fact_qd3 a lane owns one diagonal S2 and only 16 of the 31 lanes
+// have a state at any step u.  Here lane L owns the two diagonals S2 = L
+// (states at u = 0..L) and S2 = L + na (a prefix at u <= L, states at
+// u = L+1..na-1), so every lane emits one state per step; the two running
+// sums advance together and the output takes the one whose diagonal is
+// live.  Half-warp = one x_3 (rows broadcast within the half).
+template <typename T, bool WA>
+__global__ void __launch_bounds__(256, 2) k_b_fact_qp3(DevModel dm, const double* __restrict__ W,
+                                                          const double* __restrict__ v0t,
+                                                          const double* __restrict__ erpt,
+                                                          std::uint64_t lo, std::uint64_t hi,
+                                                          double gamma, int n_xb, int n_ap, int n_r,
+                                                          const T* __restrict__ V,
+                                                          T* __restrict__ vout,
+                                                          std::uint32_t* __restrict__ act,
+                                                          std::uint64_t out_off, FinalizeArgs fa) {
+  constexpr int NB = 16;
+  extern __shared__ double sm[];
+  const int na = dm.b_na, dn = dm.b_dn;
+  const int n_xa = na * na * na;
+  double* w_sl = sm;
+  double* v_sl = w_sl + n_ap * NB;
+  double* s_pa = v_sl + n_ap * NB;     // gamma pmf_a
+  double* s_ca = s_pa + dn;            // gamma cdf_a (inclusive)
+  double* s_pz = s_ca + dn;            // gamma sf_b pz(I_b, .)
+  double* s_cg = s_pz + dn;            // gamma sf_b pz_cum(I_b, .) (exclusive)
+  double* s_sa = s_cg + dn;            // gamma sf_a
+  T* s_best = reinterpret_cast<T*>(s_sa + dn);
+  std::uint8_t* s_arg = reinterpret_cast<std::uint8_t*>(s_best + n_xa);
+  const int xbi = blockIdx.x;
+  int ib = 0;
+  {
+    int rem = xbi;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      ib += rem % NB;
+      rem /= NB;
+    }
+  }
+  const double gsf = gamma * dm.b_sf_b[ib];
+  for (int i = threadIdx.x; i < dn; i += blockDim.x) {
+    s_pa[i] = gamma * dm.b_pmf_a[i];
+    s_ca[i] = gamma * dm.b_cdf_a[i];
+    s_pz[i] = gsf * dm.b_pz[ib * dn + i];
+    s_cg[i] = gsf * dm.b_pz_cum[ib * dn + i];
+    s_sa[i] = gamma * dm.b_sf_a[i];
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int L = lane & 15, half = lane >> 4;
+  const int ilo = static_cast<int>(lo), ihi = static_cast<int>(hi);
+  const double cvb = dm.b_cvb;
+  const double2* er_base = reinterpret_cast<const double2*>(erpt) + static_cast<std::size_t>(xbi) * n_xa;
+  const int n_pairs = (na + 1) / 2;
+  for (int oa = 0; oa < na; ++oa) {
+    const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
+    if (oa > 0) __syncthreads();
+    {
+      const double2* wsrc = reinterpret_cast<const double2*>(W + (static_cast<std::size_t>(xbi) * n_r + r0) * NB);
+      const double2* vsrc = reinterpret_cast<const double2*>(v0t + r0 * NB);
+      const unsigned wd = static_cast<unsigned>(__cvta_generic_to_shared(w_sl));
+      const unsigned vd = static_cast<unsigned>(__cvta_generic_to_shared(v_sl));
+      for (int i = threadIdx.x; i < n_ap * NB / 2; i += blockDim.x) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wd + 16u * i), "l"(wsrc + i));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(vd + 16u * i), "l"(vsrc + i));
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double c0 = dm.b_cva * oa;
+    for (int pr = warp; pr < n_pairs; pr += blockDim.x >> 5) {
+      const int x3 = 2 * pr + half;
+      const int xlo0 = 2 * pr * na * na;
+      const int xhi0 = min(2 * pr + 2, na) * na * na - 1;
+      if (xhi0 * n_xb + xbi < ilo || xlo0 * n_xb + xbi >= ihi) continue;  // warp-uniform
+      const bool lane_ok = L < na && x3 < na;
+      const int x3c = min(x3, na - 1);
+      const int xa_lo = x3c * na * na;
+      // diagonal constants of S2 = L (a) and S2 = L + na (b)
+      const int Ia = min(L + x3c, dn - 1), Ib = min(L + na + x3c, dn - 1);
+      double acc_a[NB], acc_b[NB];
+      {
+        const double cwa = s_sa[Ia] - s_pa[Ia], cga = (gsf - s_cg[Ia]) - s_pz[Ia];
+        const double cwb = s_sa[Ib] - s_pa[Ib], cgb = (gsf - s_cg[Ib]) - s_pz[Ib];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          const double w0 = w_sl[k], v0 = v_sl[k];
+          acc_a[k] = fma(cwa, w0, cga * v0);
+          acc_b[k] = fma(cwb, w0, cgb * v0);
+        }
+        for (int j = 0; j < x3c; ++j) {
+          const double* wr = w_sl + (j * na) * NB;
+          const double* vr = v_sl + (j * na) * NB;
+          const double pa = s_pa[max(Ia - j, 0)], pg = s_pz[max(Ia - j, 0)];
+          const double pb = s_pa[max(Ib - j, 0)], qb = s_pz[max(Ib - j, 0)];
+#pragma unroll
+          for (int k = 0; k < NB; ++k) {
+            const double wk = wr[k], vk = vr[k];
+            acc_a[k] = fma(pa, wk, fma(pg, vk, acc_a[k]));
+            acc_b[k] = fma(pb, wk, fma(qb, vk, acc_b[k]));
+          }
+        }
+      }
+      // step u emits x_1 = L - u (u <= L, diagonal a) or L + na - u (b)
+      auto xa_of = [&](int u) { return (u <= L ? L - u : L + na - u) + u * na + xa_lo; };
+      double2 e_n1 = __ldg(er_base + min(xa_of(0), n_xa - 1));
+      double2 e_n2 = __ldg(er_base + min(xa_of(1), n_xa - 1));
+      const double* wrow = w_sl + (x3c * na) * NB;
+      const double* vrow = v_sl + (x3c * na) * NB;
+      for (int u = 0; u < na; ++u, wrow += NB, vrow += NB) {
+        const double2 e = e_n1;
+        e_n1 = e_n2;
+        if (u + 2 < na) e_n2 = __ldg(er_base + min(xa_of(u + 2), n_xa - 1));
+        const bool sw = u > L;
+        const int x1 = sw ? L + na - u : L - u;
+        const int xa = x1 + u * na + xa_lo;
+        const int st = xa * n_xb + xbi;
+        const bool valid = lane_ok && st >= ilo && st < ihi;
+        const int ia = max(L - u, 0), ibb = min(L + na - u, dn - 1);
+        const double pa = s_pa[ia], pg = s_pz[ia], pb = s_pa[ibb], qb = s_pz[ibb];
+        const int xc = min(max(x1, 0), dn - 2);
+        const double ca = s_ca[xc], cgx = s_cg[xc + 1];
+        const double d = cvb * e.y;
+        const double base = fma(-c0, e.y, e.x);
+        double best = 0.0;
+        int bo = 0;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          const double wk = wrow[k], vk = vrow[k];
+          const double r = sw ? acc_b[k] : acc_a[k];
+          const double t = fma(-static_cast<double>(k), d, fma(ca, wk, fma(cgx, vk, r)));
+          if (k == 0 || t > best) {
+            best = t;
+            if (WA) bo = k;
+          }
+          acc_a[k] = fma(pa, wk, fma(pg, vk, acc_a[k]));
+          acc_b[k] = fma(pb, wk, fma(qb, vk, acc_b[k]));
+        }
+        if (valid) {
+          const T bv = static_cast<T>(base + best);
+          if (oa == 0 || bv > s_best[xa]) {
+            s_best[xa] = bv;
+            if (WA) s_arg[xa] = static_cast<std::uint8_t>(oa * NB + bo);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  double smx = -DBL_MAX, smn = DBL_MAX;
+  unsigned long long bad = ~0ull;
+  for (int xa = threadIdx.x; xa < n_xa; xa += blockDim.x) {
+    const int st = xa * n_xb + xbi;
+    if (st < ilo || st >= ihi) continue;
+    const T best = s_best[xa];
+    if (vout) vout[st - out_off] = best;
+    if (WA && act) act[st - out_off] = s_arg[xa];
+    state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
+  }
+  reduce_stats(smx, smn, bad, fa.stats);
+}
+
 // ---------------------------------------------------------------------------
 // K1-C: one thread per (state, order); the demand dimension unrolled into
 // DN register accumulators.  Blocks run heaviest order first.  Term order
@@ -1891,6 +2054,14 @@ static bool qd_enabled() {
   return on;
 }
 
+static bool qp_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PVI_B_QP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static bool q16_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PVI_B_Q16");
@@ -1994,9 +2165,15 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     }                                                                                              \
     if (MM == 3 && use_qd) {                                                                       \
       const std::size_t sm4 = sizeof(double) * (2 * static_cast<std::size_t>(n_ap) * 16 + 5 * dm.b_dn); \
-      if (fused) {                                                                                 \
+      const std::size_t smf = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(T) + 1);              \
+      if (fused && qp_enabled()) {                                                                 \
+        auto kq = a.act ? k_b_fact_qp3<T, true> : k_b_fact_qp3<T, false>;                          \
+        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);         \
+        kq<<<static_cast<unsigned>(n_xb), 256, smf, stream>>>(                                     \
+            dm, W, v0t, dc.b_erpt, lo, hi, a.gamma, static_cast<int>(n_xb),                        \
+            static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa);   \
+      } else if (fused) {                                                                          \
         auto kq = a.act ? k_b_fact_qd3<T, true, false, true> : k_b_fact_qd3<T, false, false, true>; \
-        const std::size_t smf = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(T) + 1);            \
         cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);         \
         kq<<<static_cast<unsigned>(n_xb), 256, smf, stream>>>(                                     \
             dm, W, v0t, dc.b_erpt, nullptr, nullptr, nullptr, lo, hi, a.gamma, static_cast<int>(n_xb), \
