@@ -104,6 +104,9 @@ struct DeviceCopy {
   double* b_erpt = nullptr;
   std::uint16_t* b_order_a = nullptr;
   std::uint16_t* b_order_b = nullptr;
+  // every state's issued-pair law sums to 1 (|PT - 1| <= 1e-12), so the
+  // paired-diagonal kernel may fold the order costs into its running sums
+  bool b_pt_unit = false;
   std::uint16_t* b_group_order = nullptr;    // A-side x_2..x_M digit groups by stock
   std::uint16_t* b_group_order_b = nullptr;  // B-side x_2..x_M digit groups by stock
   // Per-device workspace reused by the host-buffer entry points

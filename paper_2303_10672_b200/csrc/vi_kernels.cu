@@ -1295,7 +1295,9 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qp3(DevModel dm, const double
   double* s_pz = s_ca + dn;            // gamma sf_b pz(I_b, .)
   double* s_cg = s_pz + dn;            // gamma sf_b pz_cum(I_b, .) (exclusive)
   double* s_sa = s_cg + dn;            // gamma sf_a
-  T* s_best = reinterpret_cast<T*>(s_sa + dn);
+  // running max over (o_a, o_b) of Q - ER(s): ER is common to the row and is
+  // added once in the finalize, so the sweep never reads it per order
+  double* s_best = s_sa + dn;
   std::uint8_t* s_arg = reinterpret_cast<std::uint8_t*>(s_best + n_xa);
   const int xbi = blockIdx.x;
   int ib = 0;
@@ -1319,7 +1321,7 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qp3(DevModel dm, const double
   const int L = lane & 15, half = lane >> 4;
   const int ilo = static_cast<int>(lo), ihi = static_cast<int>(hi);
   const double cvb = dm.b_cvb;
-  const double2* er_base = reinterpret_cast<const double2*>(erpt) + static_cast<std::size_t>(xbi) * n_xa;
+  const double* er_base = erpt + static_cast<std::size_t>(xbi) * n_xa * 2;  // [x_a][ER, PT]
   const int n_pairs = (na + 1) / 2;
   for (int oa = 0; oa < na; ++oa) {
     const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
@@ -1352,11 +1354,15 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qp3(DevModel dm, const double
       {
         const double cwa = s_sa[Ia] - s_pa[Ia], cga = (gsf - s_cg[Ia]) - s_pz[Ia];
         const double cwb = s_sa[Ib] - s_pa[Ib], cgb = (gsf - s_cg[Ib]) - s_pz[Ib];
+        // PT(s) = 1 (checked by the launcher), so the order cost
+        // C_v^a o_a + C_v^b o_b is a per-o_b constant of every row: it starts
+        // in the running sums
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
           const double w0 = w_sl[k], v0 = v_sl[k];
-          acc_a[k] = fma(cwa, w0, cga * v0);
-          acc_b[k] = fma(cwb, w0, cgb * v0);
+          const double cost = -fma(static_cast<double>(k), cvb, c0);
+          acc_a[k] = fma(cwa, w0, fma(cga, v0, cost));
+          acc_b[k] = fma(cwb, w0, fma(cgb, v0, cost));
         }
         for (int j = 0; j < x3c; ++j) {
           const double* wr = w_sl + (j * na) * NB;
@@ -1372,15 +1378,9 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qp3(DevModel dm, const double
         }
       }
       // step u emits x_1 = L - u (u <= L, diagonal a) or L + na - u (b)
-      auto xa_of = [&](int u) { return (u <= L ? L - u : L + na - u) + u * na + xa_lo; };
-      double2 e_n1 = __ldg(er_base + min(xa_of(0), n_xa - 1));
-      double2 e_n2 = __ldg(er_base + min(xa_of(1), n_xa - 1));
       const double* wrow = w_sl + (x3c * na) * NB;
       const double* vrow = v_sl + (x3c * na) * NB;
       for (int u = 0; u < na; ++u, wrow += NB, vrow += NB) {
-        const double2 e = e_n1;
-        e_n1 = e_n2;
-        if (u + 2 < na) e_n2 = __ldg(er_base + min(xa_of(u + 2), n_xa - 1));
         const bool sw = u > L;
         const int x1 = sw ? L + na - u : L - u;
         const int xa = x1 + u * na + xa_lo;
@@ -1390,15 +1390,13 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qp3(DevModel dm, const double
         const double pa = s_pa[ia], pg = s_pz[ia], pb = s_pa[ibb], qb = s_pz[ibb];
         const int xc = min(max(x1, 0), dn - 2);
         const double ca = s_ca[xc], cgx = s_cg[xc + 1];
-        const double d = cvb * e.y;
-        const double base = fma(-c0, e.y, e.x);
         double best = 0.0;
         int bo = 0;
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
           const double wk = wrow[k], vk = vrow[k];
           const double r = sw ? acc_b[k] : acc_a[k];
-          const double t = fma(-static_cast<double>(k), d, fma(ca, wk, fma(cgx, vk, r)));
+          const double t = fma(ca, wk, fma(cgx, vk, r));
           if (k == 0 || t > best) {
             best = t;
             if (WA) bo = k;
@@ -1406,12 +1404,9 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qp3(DevModel dm, const double
           acc_a[k] = fma(pa, wk, fma(pg, vk, acc_a[k]));
           acc_b[k] = fma(pb, wk, fma(qb, vk, acc_b[k]));
         }
-        if (valid) {
-          const T bv = static_cast<T>(base + best);
-          if (oa == 0 || bv > s_best[xa]) {
-            s_best[xa] = bv;
-            if (WA) s_arg[xa] = static_cast<std::uint8_t>(oa * NB + bo);
-          }
+        if (valid && (oa == 0 || best > s_best[xa])) {
+          s_best[xa] = best;
+          if (WA) s_arg[xa] = static_cast<std::uint8_t>(oa * NB + bo);
         }
       }
     }
@@ -1422,7 +1417,7 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qp3(DevModel dm, const double
   for (int xa = threadIdx.x; xa < n_xa; xa += blockDim.x) {
     const int st = xa * n_xb + xbi;
     if (st < ilo || st >= ihi) continue;
-    const T best = s_best[xa];
+    const T best = static_cast<T>(__ldg(er_base + 2 * xa) + s_best[xa]);
     if (vout) vout[st - out_off] = best;
     if (WA && act) act[st - out_off] = s_arg[xa];
     state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
@@ -2133,6 +2128,28 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
       };
       dc.b_group_order = group_order(na);
       dc.b_group_order_b = group_order(nb);
+      // PT depends on (I_a, I_b) only: check the law's mass on the host
+      {
+        const int dnh = model.b_dmax + 1, ima = M * (na - 1), imb = M * (nb - 1);
+        double worst = 0.0;
+        for (int ia = 0; ia <= ima; ++ia)
+          for (int ibh = 0; ibh <= imb; ++ibh) {
+            double pt = 0.0;
+            for (int ha = 0; ha <= ia; ++ha)
+              for (int hb = 0; hb <= ibh; ++hb) {
+                double pr;
+                if (ha < ia)
+                  pr = hb < ibh ? model.b_pmf_a[ha] * model.b_pmf_b[hb]
+                                : model.b_pz[ibh * dnh + ha] * model.b_sf_b[ibh];
+                else
+                  pr = hb < ibh ? model.b_sf_a[ia] * model.b_pmf_b[hb]
+                                : (1.0 - model.b_pz_cum[ibh * dnh + ia]) * model.b_sf_b[ibh];
+                pt += pr;
+              }
+            worst = std::max(worst, std::fabs(pt - 1.0));
+          }
+        dc.b_pt_unit = worst <= 1e-12;
+      }
       dc.b_erpt = static_cast<double*>(p);
     }
   }
@@ -2166,10 +2183,11 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     if (MM == 3 && use_qd) {                                                                       \
       const std::size_t sm4 = sizeof(double) * (2 * static_cast<std::size_t>(n_ap) * 16 + 5 * dm.b_dn); \
       const std::size_t smf = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(T) + 1);              \
-      if (fused && qp_enabled()) {                                                                 \
+      if (fused && dc.b_pt_unit && qp_enabled()) {                                                 \
         auto kq = a.act ? k_b_fact_qp3<T, true> : k_b_fact_qp3<T, false>;                          \
+        const std::size_t smp = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(double) + 1);       \
         cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);         \
-        kq<<<static_cast<unsigned>(n_xb), 256, smf, stream>>>(                                     \
+        kq<<<static_cast<unsigned>(n_xb), 256, smp, stream>>>(                                     \
             dm, W, v0t, dc.b_erpt, lo, hi, a.gamma, static_cast<int>(n_xb),                        \
             static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa);   \
       } else if (fused) {                                                                          \
