@@ -618,6 +618,13 @@ double Model::factored_fmas() const {
     };
     const double na = b_na, nb = b_nb;
     const double stage1 = std::pow(na, life) * loops(b_nb, false) * nb;
+    if (life == 3 && b_nb == 16 && b_na <= 16) {
+      // k_b_fact_qp3 per (x_b, o_a): 2 FMAs per Q, both running sums of
+      // every lane at every step, and the x_3-long diagonal constants
+      const double n_xa = na * na * na;
+      const double per = 2.0 * n_xa * nb + 4.0 * na * na * na * nb + 2.0 * na * na * (na - 1) * nb;
+      return stage1 + std::pow(nb, life) * na * per;
+    }
     const double stage2 = std::pow(nb, life) * na * loops(b_na, true) * nb * 2.0;
     return stage1 + stage2;
   }

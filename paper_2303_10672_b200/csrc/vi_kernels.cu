@@ -1425,6 +1425,162 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qp3(DevModel dm, const double
   reduce_stats(smx, smn, bad, fa.stats);
 }
 
+// k_b_fact_qp3 with one warp per CTA: CTA = (x_3 pair, x_b).  The CTA stages
+// only the rows its two x_3 use -- R(u, x_3) for its own x_3 and R(0, j) for
+// the diagonal constants -- so there is no block-wide barrier per order_a and
+// no warp waits for the slowest x_3 pair; the SM interleaves the CTAs.
+template <typename T, bool WA>
+__global__ void __launch_bounds__(32, 16) k_b_fact_qw3(DevModel dm, const double* __restrict__ W,
+                                                       const double* __restrict__ v0t,
+                                                       const double* __restrict__ erpt,
+                                                       std::uint64_t lo, std::uint64_t hi,
+                                                       double gamma, int n_xb, int n_ap, int n_r,
+                                                       const T* __restrict__ V,
+                                                       T* __restrict__ vout,
+                                                       std::uint32_t* __restrict__ act,
+                                                       std::uint64_t out_off, FinalizeArgs fa) {
+  constexpr int NB = 16;
+  extern __shared__ double sm[];
+  const int na = dm.b_na, dn = dm.b_dn;
+  const int n_xa = na * na * na;
+  const int pr = blockIdx.x, xbi = blockIdx.y;
+  const int x3_0 = 2 * pr, n_x3 = min(2, na - x3_0);   // this CTA's x_3 values
+  const int n_f = min(x3_0 + n_x3 - 1, na - 1) + 1;    // R(0, j) rows, j = 0..n_f-1
+  const int n_rows = n_x3 * na + n_f;
+  double* w_sl = sm;                   // rows [n_x3*na main | n_f F rows][ob]
+  double* v_sl = w_sl + n_rows * NB;
+  double* s_pa = v_sl + n_rows * NB;
+  double* s_ca = s_pa + dn;
+  double* s_pz = s_ca + dn;
+  double* s_cg = s_pz + dn;
+  double* s_sa = s_cg + dn;
+  double* s_best = s_sa + dn;          // [n_x3 * na * na]
+  std::uint8_t* s_arg = reinterpret_cast<std::uint8_t*>(s_best + 2 * na * na);
+  const int ilo = static_cast<int>(lo), ihi = static_cast<int>(hi);
+  {
+    const int s_first = (x3_0 * na * na) * n_xb + xbi;
+    const int s_last = ((x3_0 + n_x3) * na * na - 1) * n_xb + xbi;
+    if (s_last < ilo || s_first >= ihi) return;  // no state of this CTA in the shard
+  }
+  int ib = 0;
+  {
+    int rem = xbi;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      ib += rem % NB;
+      rem /= NB;
+    }
+  }
+  const double gsf = gamma * dm.b_sf_b[ib];
+  for (int i = threadIdx.x; i < dn; i += 32) {
+    s_pa[i] = gamma * dm.b_pmf_a[i];
+    s_ca[i] = gamma * dm.b_cdf_a[i];
+    s_pz[i] = gsf * dm.b_pz[ib * dn + i];
+    s_cg[i] = gsf * dm.b_pz_cum[ib * dn + i];
+    s_sa[i] = gamma * dm.b_sf_a[i];
+  }
+  const int lane = threadIdx.x & 31;
+  const int L = lane & 15, half = lane >> 4;
+  const int x3 = x3_0 + half;
+  const bool lane_ok = L < na && half < n_x3;
+  const int x3c = min(x3, na - 1);
+  const int Ia = min(L + x3c, dn - 1), Ib = min(L + na + x3c, dn - 1);
+  const double cvb = dm.b_cvb;
+  const double* er_base = erpt + static_cast<std::size_t>(xbi) * n_xa * 2;
+  const unsigned wd = static_cast<unsigned>(__cvta_generic_to_shared(w_sl));
+  const unsigned vd = static_cast<unsigned>(__cvta_generic_to_shared(v_sl));
+  for (int oa = 0; oa < na; ++oa) {
+    const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
+    __syncwarp();
+    {
+      // main rows: ap = x3_0*na .. (x3_0+n_x3)*na - 1 (contiguous); F rows ap = j*na
+      const double2* wsrc = reinterpret_cast<const double2*>(W + (static_cast<std::size_t>(xbi) * n_r + r0) * NB);
+      const double2* vsrc = reinterpret_cast<const double2*>(v0t + r0 * NB);
+      for (int i = lane; i < n_rows * (NB / 2); i += 32) {
+        const int row = i >> 3, c = i & 7;
+        const int ap = row < n_x3 * na ? x3_0 * na + row : (row - n_x3 * na) * na;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wd + 16u * i), "l"(wsrc + ap * 8 + c));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(vd + 16u * i), "l"(vsrc + ap * 8 + c));
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
+    __syncwarp();
+    const double c0 = dm.b_cva * oa;
+    const double* f_w = w_sl + n_x3 * na * NB;  // R(0, j) rows
+    const double* f_v = v_sl + n_x3 * na * NB;
+    double acc_a[NB], acc_b[NB];
+    {
+      const double cwa = s_sa[Ia] - s_pa[Ia], cga = (gsf - s_cg[Ia]) - s_pz[Ia];
+      const double cwb = s_sa[Ib] - s_pa[Ib], cgb = (gsf - s_cg[Ib]) - s_pz[Ib];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        const double w0 = f_w[k], v0 = f_v[k];
+        const double cost = -fma(static_cast<double>(k), cvb, c0);
+        acc_a[k] = fma(cwa, w0, fma(cga, v0, cost));
+        acc_b[k] = fma(cwb, w0, fma(cgb, v0, cost));
+      }
+      for (int j = 0; j < x3c; ++j) {
+        const double* wr = f_w + j * NB;
+        const double* vr = f_v + j * NB;
+        const double pa = s_pa[max(Ia - j, 0)], pg = s_pz[max(Ia - j, 0)];
+        const double pb = s_pa[max(Ib - j, 0)], qb = s_pz[max(Ib - j, 0)];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          const double wk = wr[k], vk = vr[k];
+          acc_a[k] = fma(pa, wk, fma(pg, vk, acc_a[k]));
+          acc_b[k] = fma(pb, wk, fma(qb, vk, acc_b[k]));
+        }
+      }
+    }
+    const int xa_lo = x3c * na * na;
+    const double* wrow = w_sl + (min(half, n_x3 - 1) * na) * NB;
+    const double* vrow = v_sl + (min(half, n_x3 - 1) * na) * NB;
+    for (int u = 0; u < na; ++u, wrow += NB, vrow += NB) {
+      const bool sw = u > L;
+      const int x1 = sw ? L + na - u : L - u;
+      const int xl = x1 + u * na + half * na * na;  // local state index
+      const int st = (x1 + u * na + xa_lo) * n_xb + xbi;
+      const bool valid = lane_ok && st >= ilo && st < ihi;
+      const int ia = max(L - u, 0), ibb = min(L + na - u, dn - 1);
+      const double pa = s_pa[ia], pg = s_pz[ia], pb = s_pa[ibb], qb = s_pz[ibb];
+      const int xc = min(max(x1, 0), dn - 2);
+      const double ca = s_ca[xc], cgx = s_cg[xc + 1];
+      double best = 0.0;
+      int bo = 0;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        const double wk = wrow[k], vk = vrow[k];
+        const double r = sw ? acc_b[k] : acc_a[k];
+        const double t = fma(ca, wk, fma(cgx, vk, r));
+        if (k == 0 || t > best) {
+          best = t;
+          if (WA) bo = k;
+        }
+        acc_a[k] = fma(pa, wk, fma(pg, vk, acc_a[k]));
+        acc_b[k] = fma(pb, wk, fma(qb, vk, acc_b[k]));
+      }
+      if (valid && (oa == 0 || best > s_best[xl])) {
+        s_best[xl] = best;
+        if (WA) s_arg[xl] = static_cast<std::uint8_t>(oa * NB + bo);
+      }
+    }
+  }
+  __syncwarp();
+  double smx = -DBL_MAX, smn = DBL_MAX;
+  unsigned long long bad = ~0ull;
+  for (int xl = lane; xl < n_x3 * na * na; xl += 32) {
+    const int xa = x3_0 * na * na + xl;
+    const int st = xa * n_xb + xbi;
+    if (st < ilo || st >= ihi) continue;
+    const T best = static_cast<T>(__ldg(er_base + 2 * xa) + s_best[xl]);
+    if (vout) vout[st - out_off] = best;
+    if (WA && act) act[st - out_off] = s_arg[xl];
+    state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
+  }
+  reduce_stats(smx, smn, bad, fa.stats);
+}
+
 // ---------------------------------------------------------------------------
 // K1-C: one thread per (state, order); the demand dimension unrolled into
 // DN register accumulators.  Blocks run heaviest order first.  Term order
@@ -2057,6 +2213,14 @@ static bool qp_enabled() {
   return on;
 }
 
+static bool qw_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PVI_B_QW");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static bool q16_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PVI_B_Q16");
@@ -2183,7 +2347,15 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     if (MM == 3 && use_qd) {                                                                       \
       const std::size_t sm4 = sizeof(double) * (2 * static_cast<std::size_t>(n_ap) * 16 + 5 * dm.b_dn); \
       const std::size_t smf = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(T) + 1);              \
-      if (fused && dc.b_pt_unit && qp_enabled()) {                                                 \
+      if (fused && dc.b_pt_unit && qw_enabled()) {                                                 \
+        auto kq = a.act ? k_b_fact_qw3<T, true> : k_b_fact_qw3<T, false>;                          \
+        const int n_f = na;                                                                        \
+        const std::size_t smq = sizeof(double) * ((2 * na + n_f) * 16 * 2 + 5 * dm.b_dn + 2 * na * na) + 2 * na * na; \
+        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);         \
+        kq<<<dim3(static_cast<unsigned>((na + 1) / 2), static_cast<unsigned>(n_xb)), 32, smq, stream>>>( \
+            dm, W, v0t, dc.b_erpt, lo, hi, a.gamma, static_cast<int>(n_xb),                        \
+            static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa);   \
+      } else if (fused && dc.b_pt_unit && qp_enabled()) {                                          \
         auto kq = a.act ? k_b_fact_qp3<T, true> : k_b_fact_qp3<T, false>;                          \
         const std::size_t smp = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(double) + 1);       \
         cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);         \
