@@ -766,11 +766,18 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16(DevModel dm, const T* __r
                                                        double* __restrict__ W,
                                                        double* __restrict__ v0t,
                                                        const std::uint16_t* __restrict__ group_order,
-                                                       int n_groups, int n_xb, int n_bp, int n_r) {
+                                                       int n_groups, int n_xb, int n_bp, int n_r,
+                                                       int x3_lo, int x3_hi) {
   constexpr int NB = 16, S8 = 8, OB4 = 4;
   extern __shared__ double slab[];  // [bp][ob]
   const int stride = slab_stride(NB);
   const int r = blockIdx.x;
+  if (M == 3) {
+    // a state shard only reads the W rows of its own x_3 digits and the
+    // R(0, j) rows of the diagonal constants (k_b_fact_qw3)
+    const int na = dm.b_na, ap = r % (na * na), x2r = ap % na, x3r = ap / na;
+    if ((x3r < x3_lo || x3r > x3_hi) && !(x2r == 0 && x3r <= x3_hi)) return;
+  }
   const std::uint64_t base = static_cast<std::uint64_t>(r) * n_xb;
   for (int i = threadIdx.x; i < NB * n_bp; i += blockDim.x) {
     const int ob = i / n_bp, bp = i % n_bp;
@@ -2328,6 +2335,14 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
   T* pv = partials ? scratch.get<T>(0, static_cast<std::size_t>(na) * nr, stream) : nullptr;
   std::uint8_t* pa = partials ? scratch.get<std::uint8_t>(1, static_cast<std::size_t>(na) * nr, stream) : nullptr;
   count_launches(partials ? 3 : 2);
+  // stage-1 rows the (fused, one-warp) stage 2 of this shard reads
+  const bool qw = fused && dc.b_pt_unit && qw_enabled();
+  int x3_lo = 0, x3_hi = na - 1;
+  if (qw && M == 3) {
+    const std::uint64_t per = static_cast<std::uint64_t>(na) * na * n_xb;  // states per x_3 digit
+    x3_lo = static_cast<int>(lo / per) / 2 * 2;
+    x3_hi = std::min(na - 1, static_cast<int>((hi - 1) / per) / 2 * 2 + 1);
+  }
   {
     MainKernelScope prof(stream);
 #define PVI_BF(MM, NBX)                                                                            \
@@ -2339,7 +2354,7 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
       cudaFuncSetAttribute(k_b_fact_w16<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
       k_b_fact_w16<T, MM><<<static_cast<unsigned>(n_r), 256, sm0, stream>>>(                       \
           dm, a.v, W, v0t, dc.b_group_order_b, static_cast<int>(n_bp), static_cast<int>(n_xb),      \
-          static_cast<int>(n_bp), static_cast<int>(n_r));                                          \
+          static_cast<int>(n_bp), static_cast<int>(n_r), x3_lo, x3_hi);                            \
     } else {                                                                                       \
     k_b_fact_w<T, MM, NBX><<<static_cast<unsigned>(n_r), 256, sm1, stream>>>(                       \
         dm, a.v, W, v0t, dc.b_order_b, static_cast<int>(n_xb), static_cast<int>(n_bp), static_cast<int>(n_r)); \
@@ -2347,7 +2362,7 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     if (MM == 3 && use_qd) {                                                                       \
       const std::size_t sm4 = sizeof(double) * (2 * static_cast<std::size_t>(n_ap) * 16 + 5 * dm.b_dn); \
       const std::size_t smf = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(T) + 1);              \
-      if (fused && dc.b_pt_unit && qw_enabled()) {                                                 \
+      if (qw) {                                                                                    \
         auto kq = a.act ? k_b_fact_qw3<T, true> : k_b_fact_qw3<T, false>;                          \
         const int n_f = na;                                                                        \
         const std::size_t smq = sizeof(double) * ((2 * na + n_f) * 16 * 2 + 5 * dm.b_dn + 2 * na * na) + 2 * na * na; \
