@@ -341,6 +341,17 @@ def ours_arm(args, world, rank, local):
                         "frac > 1 means the reference-term bytes never reach HBM. With the "
                         "factored algorithm the kernel also does far fewer operations than "
                         "reference terms; compute_roofline below is its real work. DESIGN.md 4-5."}
+    # also against the measured L2 random-gather bandwidth
+    # (tools/gather_peak.cu, 8-byte gathers from a 64 MiB buffer)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_gather_peak.json")) as f:
+            gp = {r["buffer_mib"]: r for r in json.load(f)["results"]}
+        l2g = float(gp[64]["random_gather_gbs"])
+        roofline["l2_gather_peak"] = l2g
+        roofline["frac_vs_l2_gather"] = achieved_gbs / l2g
+        roofline["l2_gather_source"] = "profiles/r1_gather_peak.json (64 MiB, measured on a B200)"
+    except (OSError, ValueError, KeyError):
+        pass
     fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12  # 2:1 FP32:FP64 (ncu), nominal clock
     if args.algorithm == "factored":
         flops = 2.0 * model.info.factored_fmas * (shard_terms / terms)
