@@ -767,7 +767,7 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16(DevModel dm, const T* __r
                                                        double* __restrict__ v0t,
                                                        const std::uint16_t* __restrict__ group_order,
                                                        int n_groups, int n_xb, int n_bp, int n_r,
-                                                       int x3_lo, int x3_hi) {
+                                                       int x3_lo, int x3_hi, int tiled) {
   constexpr int NB = 16, S8 = 8, OB4 = 4;
   extern __shared__ double slab[];  // [bp][ob]
   const int stride = slab_stride(NB);
@@ -859,7 +859,10 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16(DevModel dm, const T* __r
 #pragma unroll
       for (int i = 0; i < S8; ++i) {
         const int xbi = grp * NB + x1b + i;
-        double* out = W + (static_cast<std::size_t>(xbi) * n_r + r) * NB + ob0;
+        // tiled layout [x_b / 16][r][x_b % 16][o_b]: the 16 x_1 of a group form
+        // one 2 KB run per r (k_b_fact_qw3 reads it); else [x_b][r][o_b]
+        double* out = tiled ? W + ((static_cast<std::size_t>(grp) * n_r + r) * NB + x1b + i) * NB + ob0
+                            : W + (static_cast<std::size_t>(xbi) * n_r + r) * NB + ob0;
 #pragma unroll
         for (int k = 0; k < OB4; ++k) out[k] = acc[i][k];
       }
@@ -1501,12 +1504,15 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw3(DevModel dm, const double
     __syncwarp();
     {
       // main rows: ap = x3_0*na .. (x3_0+n_x3)*na - 1 (contiguous); F rows ap = j*na
-      const double2* wsrc = reinterpret_cast<const double2*>(W + (static_cast<std::size_t>(xbi) * n_r + r0) * NB);
+      // W tiled [x_b / 16][r][x_b % 16][o_b] (k_b_fact_w16, tiled = 1): row r
+      // of this x_b at ((x_b/16) n_r + r) 256 + (x_b%16) 16
+      const double2* wsrc = reinterpret_cast<const double2*>(
+          W + ((static_cast<std::size_t>(xbi >> 4) * n_r + r0) * NB + (xbi & 15)) * NB);
       const double2* vsrc = reinterpret_cast<const double2*>(v0t + r0 * NB);
       for (int i = lane; i < n_rows * (NB / 2); i += 32) {
         const int row = i >> 3, c = i & 7;
         const int ap = row < n_x3 * na ? x3_0 * na + row : (row - n_x3 * na) * na;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wd + 16u * i), "l"(wsrc + ap * 8 + c));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wd + 16u * i), "l"(wsrc + ap * 128 + c));
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(vd + 16u * i), "l"(vsrc + ap * 8 + c));
       }
       asm volatile("cp.async.commit_group;\n" ::);
@@ -2354,7 +2360,7 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
       cudaFuncSetAttribute(k_b_fact_w16<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
       k_b_fact_w16<T, MM><<<static_cast<unsigned>(n_r), 256, sm0, stream>>>(                       \
           dm, a.v, W, v0t, dc.b_group_order_b, static_cast<int>(n_bp), static_cast<int>(n_xb),      \
-          static_cast<int>(n_bp), static_cast<int>(n_r), x3_lo, x3_hi);                            \
+          static_cast<int>(n_bp), static_cast<int>(n_r), x3_lo, x3_hi, qw && MM == 3 ? 1 : 0);       \
     } else {                                                                                       \
     k_b_fact_w<T, MM, NBX><<<static_cast<unsigned>(n_r), 256, sm1, stream>>>(                       \
         dm, a.v, W, v0t, dc.b_order_b, static_cast<int>(n_xb), static_cast<int>(n_bp), static_cast<int>(n_r)); \

@@ -399,8 +399,13 @@ def run_value_iteration(model: Model, config: Optional[ViConfig] = None,
     config = config or ViConfig()
     n = model.state_count()
     fits = n <= config.max_states  # else the C side raises CapacityError first
-    values = np.zeros(n, np.float64) if fits else None
-    policy = np.zeros(n, np.uint32) if fits else None
+    # value-initialised like the reference's std::vector results (pages
+    # touched here, so the device-to-host copy does not page-fault)
+    values = np.empty(n, np.float64) if fits else None
+    policy = np.empty(n, np.uint32) if fits else None
+    if fits:
+        values.fill(0.0)
+        policy.fill(0)
     st = L.ViStats()
     ev = C.c_uint64()
     err = _err_buf()
