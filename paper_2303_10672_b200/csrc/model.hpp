@@ -102,6 +102,11 @@ struct DeviceCopy {
   // probability (V-independent, built once), and the A / B digit-block
   // orders sorted by stock so warps share loop trip counts.
   double* b_erpt = nullptr;
+  // Scenario A factored sweep: per-state expected one-step reward (without
+  // the order cost) and the demand law's cdf / survival tables
+  double* a_reward = nullptr;
+  double* a_cdf_sf = nullptr;  // [cdf(0..D) | sf(0..D+1)]
+  double a_pd = 0.0;           // sum of the demand pmf
   std::uint16_t* b_order_a = nullptr;
   std::uint16_t* b_order_b = nullptr;
   // every state's issued-pair law sums to 1 (|PT - 1| <= 1e-12), so the

@@ -489,6 +489,230 @@ __global__ void __launch_bounds__(256, NCH == 1 ? 2 : 3) k_sweep_b_geo(DevModel 
 }
 
 // ---------------------------------------------------------------------------
+// K1-A factored ("algorithm = factored"; agrees with the reference to
+// rounding).  Q(s,a) = sum_d p_d (r_sd - C_v a + gamma V[b_sd + a W0]):
+// the reward does not depend on the order and the next-state base b_sd only
+// through the aged stock, so
+//   Q(s,a) = R(s) - C_v a PD + gamma sum_{distinct b} w_b V[b + a W0]
+// with R(s) = sum_d p_d r_sd built once per model (k_a_reward) and the
+// demand values that leave the same aged stock merged into one weight:
+// LIFO uses the freshest units first, so every d >= x_2 + .. + x_m empties the
+// carried stock (one sf-weighted term) and d < x_2 + .. + x_m are distinct;
+// FIFO uses the oldest first, so all d <= x_1 leave (x_2, .., x_m) (one
+// cdf-weighted term), then x_1 < d < I are distinct and d >= I empties it.
+// ~x_2 + .. + x_m + 2 profiles per state instead of D_max + 1 = 101.
+
+template <int ML>
+__global__ void __launch_bounds__(256) k_a_reward(DevModel dm, double* __restrict__ out,
+                                                  std::uint64_t n) {
+  const std::uint64_t s = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  constexpr int MC = ML / 10, LC = ML % 10;
+  const int m = ML ? MC : dm.a_m, lead = ML ? LC : dm.a_lead;
+  int st[kMaxDigits];
+  decode(dm, s, st);
+  int x[14], aged[14];
+  int xt = 0;
+  for (int j = 1; j <= m; ++j) {
+    x[j] = st[lead - 1 + m - j];
+    xt += x[j];
+  }
+  double acc = 0.0;
+  for (int d = 0; d <= dm.a_dmax; ++d) {
+    const int expired = dm.a_lifo ? age_lifo(x, m, d, aged) : age_fifo(x, m, d, aged);
+    const double r = -dm.a_ch * ipos(xt - d - expired) - dm.a_cs * ipos(d - xt) - dm.a_cw * expired;
+    acc = fma(dm.a_pmf[d], r, acc);
+  }
+  out[s] = acc;
+}
+
+template <typename T, int NA, int ML>
+__global__ void __launch_bounds__(256) k_a_fact(DevModel dm, const T* __restrict__ V,
+                                                const double* __restrict__ reward,
+                                                const double* __restrict__ cdf_sf, double pd,
+                                                T* __restrict__ vout, std::uint32_t* __restrict__ act,
+                                                T* __restrict__ qout, std::uint64_t lo,
+                                                std::uint64_t hi, std::uint64_t out_off,
+                                                double gamma, FinalizeArgs fa) {
+  extern __shared__ double s_tab[];  // pmf | cdf | sf
+  const int dn = dm.a_dmax + 1;
+  double* s_pmf = s_tab;
+  double* s_cdf = s_pmf + dn;
+  double* s_sf = s_cdf + dn;
+  for (int i = threadIdx.x; i < dn; i += blockDim.x) {
+    s_pmf[i] = dm.a_pmf[i];
+    s_cdf[i] = cdf_sf[i];
+  }
+  for (int i = threadIdx.x; i <= dn; i += blockDim.x) s_sf[i] = cdf_sf[dn + i];
+  __syncthreads();
+  const std::uint64_t s = lo + static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double smax = -DBL_MAX, smin = DBL_MAX;
+  unsigned long long bad = ~0ull;
+  if (s < hi) {
+    constexpr int MC = ML / 10, LC = ML % 10;
+    const int m = ML ? MC : dm.a_m, lead = ML ? LC : dm.a_lead;
+    const int na = static_cast<int>(dm.n_actions);
+    constexpr int ND = ML ? MC + LC - 1 : kMaxDigits;
+    int st[ND];
+    if (ML) {
+      const std::uint32_t r = static_cast<std::uint32_t>(dm.a_max_order + 1);
+      std::uint64_t rem = s;
+#pragma unroll
+      for (int i = ND - 1; i >= 0; --i) {
+        st[i] = static_cast<int>(rem % r);
+        rem /= r;
+      }
+    } else {
+      decode(dm, s, st);
+    }
+    int x[ML ? MC + 1 : 14], aged[ML ? MC + 1 : 14];
+    int xt = 0;
+#pragma unroll
+    for (int j = 1; j <= m; ++j) {
+      x[j] = st[lead - 1 + m - j];
+      xt += x[j];
+    }
+    std::uint64_t base_static = 0;
+#pragma unroll
+    for (int k = 1; k <= lead - 2; ++k) base_static += st[k - 1] * dm.weight[k];
+    if (lead >= 2) base_static += st[lead - 2] * dm.weight[lead - 1];
+    const std::uint64_t w0 = dm.weight[0];
+    double u[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) u[a] = 0.0;
+    const int carried = xt - x[1];  // x_2 + .. + x_m
+    auto add_profile = [&](int d, double w) {
+      if (dm.a_lifo) age_lifo(x, m, d, aged);
+      else age_fifo(x, m, d, aged);
+      std::uint64_t base = base_static;
+      for (int j = 1; j <= m - 1; ++j) base += aged[j] * dm.weight[lead + m - 1 - j];
+      const T* vb = V + base;
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+        if (a < na) u[a] = fma(w, static_cast<double>(__ldg(vb + a * w0)), u[a]);
+    };
+    if (dm.a_lifo) {
+      for (int d = 0; d < carried; ++d) add_profile(d, s_pmf[d]);
+      add_profile(carried, s_sf[carried]);  // every d >= x_2 + .. + x_m empties the carried stock
+    } else {
+      add_profile(x[1], s_cdf[x[1]]);  // d <= x_1: (x_2, .., x_m) unchanged
+      for (int d = x[1] + 1; d < xt; ++d) add_profile(d, s_pmf[d]);
+      add_profile(xt, s_sf[max(xt, x[1] + 1)]);  // the rest empties the stock
+    }
+    const double rs = reward[s];
+    T best = T(0);
+    std::uint32_t besta = 0;
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      if (a < na) {
+        const T qa = static_cast<T>(fma(gamma, u[a], fma(-dm.a_cv * a, pd, rs)));
+        if (a == 0 || qa > best) {
+          best = qa;
+          besta = a;
+        }
+        if (qout) qout[(s - lo) * na + a] = qa;
+      }
+    }
+    if (vout) vout[s - out_off] = best;
+    if (act) act[s - out_off] = besta;
+    state_stat<T>(fa, s, best, V, smax, smin, bad);
+  }
+  reduce_stats(smax, smin, bad, fa.stats);
+}
+
+// LIFO: the carried stock's fate does not depend on the oldest bucket x_1
+// (it is used last and expires anyway), so U(s, .) is shared by the
+// A_max + 1 states that differ only in x_1 -- consecutive indices, since x_1
+// is the least significant digit.  One thread per such group.
+template <typename T, int NA, int ML>
+__global__ void __launch_bounds__(128) k_a_fact_lifo(DevModel dm, const T* __restrict__ V,
+                                                     const double* __restrict__ reward,
+                                                     const double* __restrict__ cdf_sf, double pd,
+                                                     T* __restrict__ vout,
+                                                     std::uint32_t* __restrict__ act,
+                                                     T* __restrict__ qout, std::uint64_t lo,
+                                                     std::uint64_t hi, std::uint64_t out_off,
+                                                     double gamma, FinalizeArgs fa) {
+  extern __shared__ double s_tab[];  // pmf | cdf | sf
+  const int dn = dm.a_dmax + 1;
+  double* s_pmf = s_tab;
+  double* s_sf = s_pmf + 2 * dn;
+  for (int i = threadIdx.x; i < dn; i += blockDim.x) s_pmf[i] = dm.a_pmf[i];
+  for (int i = threadIdx.x; i <= dn; i += blockDim.x) s_sf[i] = cdf_sf[dn + i];
+  __syncthreads();
+  const int rx = dm.a_max_order + 1;  // radix of x_1
+  const std::uint64_t g = lo / rx + static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double smax = -DBL_MAX, smin = DBL_MAX;
+  unsigned long long bad = ~0ull;
+  const std::uint64_t s0 = g * rx;
+  if (s0 < hi) {
+    constexpr int MC = ML / 10, LC = ML % 10;
+    const int m = ML ? MC : dm.a_m, lead = ML ? LC : dm.a_lead;
+    const int na = static_cast<int>(dm.n_actions);
+    constexpr int ND = ML ? MC + LC - 1 : kMaxDigits;
+    int st[ND];
+    if (ML) {
+      const std::uint32_t r = static_cast<std::uint32_t>(rx);
+      std::uint64_t rem = s0;
+#pragma unroll
+      for (int i = ND - 1; i >= 0; --i) {
+        st[i] = static_cast<int>(rem % r);
+        rem /= r;
+      }
+    } else {
+      decode(dm, s0, st);
+    }
+    int x[ML ? MC + 1 : 14], aged[ML ? MC + 1 : 14];
+    int carried = 0;
+#pragma unroll
+    for (int j = 1; j <= m; ++j) {
+      x[j] = st[lead - 1 + m - j];  // x_1 = 0 here
+      if (j > 1) carried += x[j];
+    }
+    std::uint64_t base_static = 0;
+#pragma unroll
+    for (int k = 1; k <= lead - 2; ++k) base_static += st[k - 1] * dm.weight[k];
+    if (lead >= 2) base_static += st[lead - 2] * dm.weight[lead - 1];
+    const std::uint64_t w0 = dm.weight[0];
+    double u[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) u[a] = 0.0;
+    for (int d = 0; d <= carried; ++d) {
+      age_lifo(x, m, d, aged);
+      std::uint64_t base = base_static;
+      for (int j = 1; j <= m - 1; ++j) base += aged[j] * dm.weight[lead + m - 1 - j];
+      const double w = d < carried ? s_pmf[d] : s_sf[carried];
+      const T* vb = V + base;
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+        if (a < na) u[a] = fma(w, static_cast<double>(__ldg(vb + a * w0)), u[a]);
+    }
+    for (int x1 = 0; x1 < rx; ++x1) {
+      const std::uint64_t s = s0 + x1;
+      if (s < lo || s >= hi) continue;
+      const double rs = reward[s];
+      T best = T(0);
+      std::uint32_t besta = 0;
+#pragma unroll
+      for (int a = 0; a < NA; ++a) {
+        if (a < na) {
+          const T qa = static_cast<T>(fma(gamma, u[a], fma(-dm.a_cv * a, pd, rs)));
+          if (a == 0 || qa > best) {
+            best = qa;
+            besta = a;
+          }
+          if (qout) qout[(s - lo) * na + a] = qa;
+        }
+      }
+      if (vout) vout[s - out_off] = best;
+      if (act) act[s - out_off] = besta;
+      state_stat<T>(fa, s, best, V, smax, smin, bad);
+    }
+  }
+  reduce_stats(smax, smin, bad, fa.stats);
+}
+
+// ---------------------------------------------------------------------------
 // K1-B factored ("algorithm = factored"; not the reference's summation order,
 // parity contract 1e-9 relative instead of bits).
 //
@@ -2234,6 +2458,14 @@ static bool qw_enabled() {
   return on;
 }
 
+static bool a_group_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PVI_A_GROUP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static bool q16_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PVI_B_Q16");
@@ -2505,9 +2737,88 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
       const unsigned block = 256;
       const std::size_t sm = (dm.a_dmax + 1) * sizeof(double);
       const int na = static_cast<int>(dm.n_actions);
+      const int ml = 10 * dm.a_m + dm.a_lead;
+      if (a.algorithm == 1 && na <= 16) {
+        int device = 0;
+        PVI_CUDA(cudaGetDevice(&device));
+        DeviceCopy& dc = model.device_copy(device);
+        {
+          std::lock_guard<std::mutex> lock(model.dev_mutex);
+          if (!dc.a_reward) {
+            void* p = nullptr;
+            PVI_CUDA(cudaMalloc(&p, dm.n_states * sizeof(double)));
+            dc.allocations.push_back(p);
+            bool spec = false;
+#define PVI_AR(ML)                                                                                   \
+  if (!spec && ml == ML) {                                                                           \
+    k_a_reward<ML><<<grid_for(dm.n_states, 256), 256, 0, stream>>>(dm, static_cast<double*>(p), dm.n_states); \
+    spec = true;                                                                                     \
+  }
+            PVI_AR(21) PVI_AR(22) PVI_AR(31) PVI_AR(32) PVI_AR(41) PVI_AR(42) PVI_AR(51) PVI_AR(52)
+#undef PVI_AR
+            if (!spec)
+              k_a_reward<0><<<grid_for(dm.n_states, 256), 256, 0, stream>>>(dm, static_cast<double*>(p), dm.n_states);
+            PVI_CUDA(cudaGetLastError());
+            // cdf (inclusive) and survival sf(i) = sum_{d >= i} p_d, host-built
+            const int dnh = dm.a_dmax + 1;
+            std::vector<double> tab(2 * static_cast<std::size_t>(dnh) + 1, 0.0);
+            double c = 0.0, pdh = 0.0;
+            for (int d = 0; d < dnh; ++d) {
+              c += model.a_pmf[d];
+              tab[d] = c;
+              pdh += model.a_pmf[d];
+            }
+            double tail = 0.0;
+            for (int d = dnh; d >= 0; --d) {
+              if (d < dnh) tail += model.a_pmf[d];
+              tab[dnh + d] = tail;
+            }
+            void* q = nullptr;
+            PVI_CUDA(cudaMalloc(&q, tab.size() * sizeof(double)));
+            PVI_CUDA(cudaMemcpy(q, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+            dc.allocations.push_back(q);
+            dc.a_cdf_sf = static_cast<double*>(q);
+            dc.a_pd = pdh;
+            dc.a_reward = static_cast<double*>(p);
+          }
+        }
+        const std::size_t smf = (3 * static_cast<std::size_t>(dm.a_dmax + 1) + 1) * sizeof(double);
+        MainKernelScope prof(stream);
+        count_launches(1);
+        bool spec = false;
+        if (dm.a_lifo && a_group_enabled()) {
+          const int rx = dm.a_max_order + 1;
+          const std::uint64_t g0 = lo / rx, g1 = (hi + rx - 1) / rx;
+#define PVI_AL(ML)                                                                                   \
+  if (!spec && ml == ML) {                                                                           \
+    k_a_fact_lifo<T, 16, ML><<<grid_for(g1 - g0, 128), 128, smf, stream>>>(dm, a.v, dc.a_reward, dc.a_cdf_sf, \
+        dc.a_pd, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);                             \
+    spec = true;                                                                                     \
+  }
+          PVI_AL(21) PVI_AL(22) PVI_AL(31) PVI_AL(32) PVI_AL(41) PVI_AL(42) PVI_AL(51) PVI_AL(52)
+#undef PVI_AL
+          if (!spec) {
+            k_a_fact_lifo<T, 16, 0><<<grid_for(g1 - g0, 128), 128, smf, stream>>>(dm, a.v, dc.a_reward, dc.a_cdf_sf,
+                dc.a_pd, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
+            spec = true;
+          }
+          break;
+        }
+#define PVI_AF(ML)                                                                                   \
+  if (!spec && ml == ML) {                                                                           \
+    k_a_fact<T, 16, ML><<<grid_for(nr, block), block, smf, stream>>>(dm, a.v, dc.a_reward, dc.a_cdf_sf, \
+        dc.a_pd, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);                             \
+    spec = true;                                                                                     \
+  }
+        PVI_AF(21) PVI_AF(22) PVI_AF(31) PVI_AF(32) PVI_AF(41) PVI_AF(42) PVI_AF(51) PVI_AF(52)
+#undef PVI_AF
+        if (!spec)
+          k_a_fact<T, 16, 0><<<grid_for(nr, block), block, smf, stream>>>(dm, a.v, dc.a_reward, dc.a_cdf_sf,
+              dc.a_pd, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
+        break;
+      }
       MainKernelScope prof(stream);
       count_launches(1);
-      const int ml = 10 * dm.a_m + dm.a_lead;
       bool done = false;
 #define PVI_A_ML(ML)                                                                                  \
   if (!done && na <= 16 && ml == ML) {                                                                \
