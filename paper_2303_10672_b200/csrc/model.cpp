@@ -641,6 +641,33 @@ double Model::factored_fmas() const {
     }
     return g + (life - 2) * 7.0 * wb * pass + static_cast<double>(space.count) * fin;
   }
+  if (scenario == PVI_SCENARIO_A && n_actions <= 16) {
+    // k_a_fact_lifo: one (carried + 1)-profile sum per x_1 group;
+    // k_a_fact_fifo: per diagonal the x_3.. block plus one running-sum step
+    // per x_2; both then 2 FMAs per (state, order) for Q.
+    const int m = pa.useful_life, rx = pa.max_order + 1;
+    const double na = n_actions, pipe = std::pow(double(rx), pa.lead_time - 1);
+    long long count = 1;
+    for (int j = 0; j < m; ++j) count *= rx;
+    double per_pipe = 0.0;
+    for (long long v = 0; v < count; ++v) {
+      long long rem = v;
+      int xs[14], above = 0, carried = 0;
+      for (int j = 1; j <= m; ++j) {  // x_1 = least significant
+        xs[j] = static_cast<int>(rem % rx);
+        rem /= rx;
+        if (j >= 2) carried += xs[j];
+        if (j >= 3) above += xs[j];
+      }
+      if (pa.issuing != 0) {
+        if (xs[1] == 0) per_pipe += (carried + 1) * na;
+      } else if (xs[1] == 0 && xs[2] == 0) {
+        for (int s2 = 0; s2 <= 2 * (rx - 1); ++s2)
+          per_pipe += (std::max(above, 1) + std::min(s2, rx - 1) + 1) * na;
+      }
+    }
+    return pipe * per_pipe + 2.0 * na * static_cast<double>(space.count);
+  }
   return terms_per_sweep();
 }
 

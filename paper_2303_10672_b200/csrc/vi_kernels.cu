@@ -712,6 +712,124 @@ __global__ void __launch_bounds__(128) k_a_fact_lifo(DevModel dm, const T* __res
   reduce_stats(smax, smin, bad, fa.stats);
 }
 
+// FIFO by diagonals (the K1-B stage-2 construction on the A side): with
+// S2 = x_1 + x_2 and R(j) = V[next stock (j, x_3, .., x_m) + a W0],
+//   U(x_1, x_2) = cdf(x_1) R(x_2) + sum_{j < x_2} pmf(S2 - j) R(j) + K(S2)
+// where K(S2) collects the demands that reach x_3.. (d > S2) and does not
+// depend on how S2 splits.  Thread = one diagonal (S2, x_3.., pipeline),
+// walking x_2 = u with the middle sum as a running sum.  Warp = 32 digit
+// groups with the same S2 (uniform trip counts).
+template <typename T, int NA, int ML>
+__global__ void __launch_bounds__(128) k_a_fact_fifo(DevModel dm, const T* __restrict__ V,
+                                                     const double* __restrict__ reward,
+                                                     const double* __restrict__ cdf_sf, double pd,
+                                                     T* __restrict__ vout,
+                                                     std::uint32_t* __restrict__ act,
+                                                     T* __restrict__ qout, std::uint64_t lo,
+                                                     std::uint64_t hi, std::uint64_t out_off,
+                                                     double gamma, std::uint64_t n_groups,
+                                                     FinalizeArgs fa) {
+  extern __shared__ double s_tab[];  // pmf | cdf | sf
+  const int dn = dm.a_dmax + 1;
+  double* s_pmf = s_tab;
+  double* s_cdf = s_pmf + dn;
+  double* s_sf = s_cdf + dn;
+  for (int i = threadIdx.x; i < dn; i += blockDim.x) {
+    s_pmf[i] = dm.a_pmf[i];
+    s_cdf[i] = cdf_sf[i];
+  }
+  for (int i = threadIdx.x; i <= dn; i += blockDim.x) s_sf[i] = cdf_sf[dn + i];
+  __syncthreads();
+  const int rx = dm.a_max_order + 1;
+  const std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int S2 = static_cast<int>(t / n_groups);
+  const std::uint64_t g = t % n_groups;   // digits above x_2
+  double smax = -DBL_MAX, smin = DBL_MAX;
+  unsigned long long bad = ~0ull;
+  const std::uint64_t s0 = g * rx * rx;
+  if (S2 <= 2 * (rx - 1) && s0 < hi && s0 + rx * rx > lo) {
+    constexpr int MC = ML / 10, LC = ML % 10;
+    const int m = ML ? MC : dm.a_m, lead = ML ? LC : dm.a_lead;
+    const int na = static_cast<int>(dm.n_actions);
+    constexpr int ND = ML ? MC + LC - 1 : kMaxDigits;
+    int st[ND];
+    if (ML) {
+      const std::uint32_t r = static_cast<std::uint32_t>(rx);
+      std::uint64_t rem = s0;
+#pragma unroll
+      for (int i = ND - 1; i >= 0; --i) {
+        st[i] = static_cast<int>(rem % r);
+        rem /= r;
+      }
+    } else {
+      decode(dm, s0, st);
+    }
+    int x[ML ? MC + 1 : 14], aged[ML ? MC + 1 : 14];
+    int above = 0;  // x_3 + .. + x_m
+#pragma unroll
+    for (int j = 1; j <= m; ++j) {
+      x[j] = j <= 2 ? 0 : st[lead - 1 + m - j];
+      if (j > 2) above += x[j];
+    }
+    std::uint64_t base_static = 0;
+#pragma unroll
+    for (int k = 1; k <= lead - 2; ++k) base_static += st[k - 1] * dm.weight[k];
+    if (lead >= 2) base_static += st[lead - 2] * dm.weight[lead - 1];
+    const std::uint64_t w0 = dm.weight[0];
+    auto base_of = [&]() {
+      std::uint64_t b = base_static;
+      for (int j = 1; j <= m - 1; ++j) b += aged[j] * dm.weight[lead + m - 1 - j];
+      return b;
+    };
+    // K(S2): demands S2 + k, k >= 1, consume x_3.. (x_1 = x_2 = 0 in x here)
+    double acc[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) acc[a] = 0.0;
+    for (int k = 1; k <= max(above, 1); ++k) {
+      age_fifo(x, m, k, aged);
+      const double w = k < above ? s_pmf[min(S2 + k, dn - 1)] : s_sf[min(S2 + k, dn)];
+      const T* vb = V + base_of();
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+        if (a < na) acc[a] = fma(w, static_cast<double>(__ldg(vb + a * w0)), acc[a]);
+    }
+    const int ulast = min(S2, rx - 1);
+    for (int u = 0; u <= ulast; ++u) {
+      x[2] = u;  // R(u): next stock (u, x_3, .., x_m)
+      age_fifo(x, m, 0, aged);
+      const T* vb = V + base_of();
+      double rv[NA];
+#pragma unroll
+      for (int a = 0; a < NA; ++a) rv[a] = a < na ? static_cast<double>(__ldg(vb + a * w0)) : 0.0;
+      const int x1 = S2 - u;
+      const std::uint64_t s = s0 + static_cast<std::uint64_t>(u) * rx + x1;
+      if (x1 < rx && s >= lo && s < hi) {
+        const double c = s_cdf[x1], rs = reward[s];
+        T best = T(0);
+        std::uint32_t besta = 0;
+#pragma unroll
+        for (int a = 0; a < NA; ++a) {
+          if (a < na) {
+            const T qa = static_cast<T>(fma(gamma, fma(c, rv[a], acc[a]), fma(-dm.a_cv * a, pd, rs)));
+            if (a == 0 || qa > best) {
+              best = qa;
+              besta = a;
+            }
+            if (qout) qout[(s - lo) * na + a] = qa;
+          }
+        }
+        if (vout) vout[s - out_off] = best;
+        if (act) act[s - out_off] = besta;
+        state_stat<T>(fa, s, best, V, smax, smin, bad);
+      }
+      const double p = s_pmf[x1];
+#pragma unroll
+      for (int a = 0; a < NA; ++a) acc[a] = fma(p, rv[a], acc[a]);
+    }
+  }
+  reduce_stats(smax, smin, bad, fa.stats);
+}
+
 // ---------------------------------------------------------------------------
 // K1-B factored ("algorithm = factored"; not the reference's summation order,
 // parity contract 1e-9 relative instead of bits).
@@ -2802,6 +2920,23 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
                 dc.a_pd, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
             spec = true;
           }
+          break;
+        }
+        if (!dm.a_lifo && a_group_enabled()) {
+          const int rx = dm.a_max_order + 1;
+          const std::uint64_t n_groups = dm.n_states / (static_cast<std::uint64_t>(rx) * rx);
+          const std::uint64_t n_thr = n_groups * (2 * rx - 1);
+#define PVI_AD(ML)                                                                                   \
+  if (!spec && ml == ML) {                                                                           \
+    k_a_fact_fifo<T, 16, ML><<<grid_for(n_thr, 128), 128, smf, stream>>>(dm, a.v, dc.a_reward, dc.a_cdf_sf, \
+        dc.a_pd, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, n_groups, fa);                   \
+    spec = true;                                                                                     \
+  }
+          PVI_AD(21) PVI_AD(22) PVI_AD(31) PVI_AD(32) PVI_AD(41) PVI_AD(42) PVI_AD(51) PVI_AD(52)
+#undef PVI_AD
+          if (!spec)
+            k_a_fact_fifo<T, 16, 0><<<grid_for(n_thr, 128), 128, smf, stream>>>(dm, a.v, dc.a_reward, dc.a_cdf_sf,
+                dc.a_pd, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, n_groups, fa);
           break;
         }
 #define PVI_AF(ML)                                                                                   \
