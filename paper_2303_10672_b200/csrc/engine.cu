@@ -5,6 +5,7 @@
 // statistics record (max/min of the convergence statistic and the first
 // non-finite state), so the only host round trip is that flag.
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
@@ -44,12 +45,22 @@ const U* upload(DeviceCopy& dc, const std::vector<U>& host) {
 // Device buffers reused across pvi_vi_backup / pvi_q_rows calls on one
 // model, so a serving caller pays for the copies and the sweep only.
 struct Workspace {
+  static constexpr int kChunkEvents = 16;
   std::mutex mu;
   Scratch scratch;  // sweep scratch (partials, factored tables)
   Scratch io;       // 0: V, 1: V' slice, 2: argmax slice, 3: Q rows
   cudaStream_t stream = nullptr;
-  Workspace() { PVI_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking)); }
+  cudaStream_t copy = nullptr;  // device-to-host results of finished chunks
+  cudaEvent_t done[kChunkEvents] = {};
+  Workspace() {
+    PVI_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    PVI_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    for (auto& e : done) PVI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   ~Workspace() {
+    for (auto& e : done)
+      if (e) cudaEventDestroy(e);
+    if (copy) cudaStreamDestroy(copy);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -623,6 +634,15 @@ void vi_solve(const Model& m, const pvi_vi_config& cfg, const double* resume_val
 
 namespace {
 
+int backup_chunks() {
+  static const int v = [] {
+    const char* e = std::getenv("PVI_BACKUP_CHUNKS");
+    const int c = e ? std::atoi(e) : 4;
+    return std::max(1, std::min(c, Workspace::kChunkEvents));
+  }();
+  return v;
+}
+
 template <typename T>
 void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t lo,
                  std::uint64_t hi, void* out_values, std::uint32_t* out_actions, void* out_q) {
@@ -634,8 +654,15 @@ void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t
   std::lock_guard<std::mutex> lock(ws.mu);
   cudaStream_t st = ws.stream;
   T* v = ws.io.get<T>(0, n, st);
-  PVI_CUDA(cudaMemcpyAsync(v, values, n * sizeof(T), cudaMemcpyHostToDevice, st));
   const std::uint64_t nr = hi - lo;
+  // Factored B (m = 3, radix-16 orders): stage 1 CTA r reads only
+  // V[r |x_b| .. (r+1) |x_b|), so the upload of V is split into pieces and
+  // each piece's stage-1 CTAs start as soon as it lands.
+  const bool b_pipe = m.scenario == PVI_SCENARIO_B && m.algorithm == PVI_ALGO_FACTORED &&
+                      m.pb.useful_life == 3 && m.b_nb == 16 && m.b_na <= 16 && !out_q &&
+                      (out_values || out_actions) && n >= (std::uint64_t(1) << 22) && backup_chunks() > 1;
+  const int n_pieces = b_pipe ? 4 : 1;
+  if (!b_pipe) PVI_CUDA(cudaMemcpyAsync(v, values, n * sizeof(T), cudaMemcpyHostToDevice, st));
   T* vo = out_values ? ws.io.get<T>(1, nr, st) : nullptr;
   std::uint32_t* ao = out_actions ? ws.io.get<std::uint32_t>(2, nr, st) : nullptr;
   T* qo = out_q ? ws.io.get<T>(3, nr * m.n_actions, st) : nullptr;
@@ -644,17 +671,98 @@ void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t
   a.vout = vo;
   a.act = ao;
   a.qout = qo;
-  a.lo = lo;
-  a.hi = hi;
   a.out_off = lo;
   a.gamma = gamma;
   a.algorithm = m.algorithm;
   a.want_values = out_values || out_actions;
-  launch_sweep<T>(m, dm, a, ws.scratch, st);
-  if (out_values) PVI_CUDA(cudaMemcpyAsync(out_values, vo, nr * sizeof(T), cudaMemcpyDeviceToHost, st));
-  if (out_actions) PVI_CUDA(cudaMemcpyAsync(out_actions, ao, nr * 4, cudaMemcpyDeviceToHost, st));
-  if (out_q) PVI_CUDA(cudaMemcpyAsync(out_q, qo, nr * m.n_actions * sizeof(T), cudaMemcpyDeviceToHost, st));
+  if (b_pipe) {
+    const std::uint64_t n_xb = static_cast<std::uint64_t>(m.b_nb) * m.b_nb * m.b_nb;
+    const std::uint64_t n_r = n / n_xb;
+    a.lo = lo;
+    a.hi = hi;
+    a.stages = 1;
+    for (int k = 0; k < n_pieces; ++k) {
+      const std::uint64_t r_lo = n_r * k / n_pieces, r_hi = n_r * (k + 1) / n_pieces;
+      const std::uint64_t s_lo = r_lo * n_xb, s_hi = r_hi * n_xb;
+      PVI_CUDA(cudaMemcpyAsync(v + s_lo, static_cast<const T*>(values) + s_lo, (s_hi - s_lo) * sizeof(T),
+                               cudaMemcpyHostToDevice, ws.copy));
+      PVI_CUDA(cudaEventRecord(ws.done[Workspace::kChunkEvents / 2 + k], ws.copy));
+      PVI_CUDA(cudaStreamWaitEvent(st, ws.done[Workspace::kChunkEvents / 2 + k], 0));
+      a.r_lo = r_lo;
+      a.r_hi = r_hi;
+      launch_sweep<T>(m, dm, a, ws.scratch, st);
+    }
+    a.stages = 2;
+    a.r_lo = 0;
+    a.r_hi = ~0ull;
+    if (lo == 0 && hi == n && b_sweep_honours_xb_range(m, device)) {
+      // stage 2 by x_b column blocks: every block carries the same mix of
+      // light and heavy x_3 pairs (a state-range split would not), and a
+      // finished block's V' / argmax is a strided column set -- copied back
+      // with one 2-D copy while the next block runs
+      const std::uint64_t n_xb = static_cast<std::uint64_t>(m.b_nb) * m.b_nb * m.b_nb;
+      const std::uint64_t n_xa = n / n_xb;
+      const int cols = std::min(backup_chunks(), Workspace::kChunkEvents / 2);
+      for (int c = 0; c < cols; ++c) {
+        const std::uint64_t x0 = n_xb * c / cols, x1 = n_xb * (c + 1) / cols;
+        a.lo = lo;
+        a.hi = hi;
+        a.xb_lo = x0;
+        a.xb_hi = x1;
+        launch_sweep<T>(m, dm, a, ws.scratch, st);
+        PVI_CUDA(cudaEventRecord(ws.done[c], st));
+        PVI_CUDA(cudaStreamWaitEvent(ws.copy, ws.done[c], 0));
+        if (out_values)
+          PVI_CUDA(cudaMemcpy2DAsync(static_cast<T*>(out_values) + x0, n_xb * sizeof(T), vo + x0,
+                                     n_xb * sizeof(T), (x1 - x0) * sizeof(T), n_xa,
+                                     cudaMemcpyDeviceToHost, ws.copy));
+        if (out_actions)
+          PVI_CUDA(cudaMemcpy2DAsync(out_actions + x0, n_xb * 4, ao + x0, n_xb * 4, (x1 - x0) * 4, n_xa,
+                                     cudaMemcpyDeviceToHost, ws.copy));
+      }
+      PVI_CUDA(cudaStreamSynchronize(st));
+      PVI_CUDA(cudaStreamSynchronize(ws.copy));
+      return;
+    }
+  }
+  // Large sweeps run as a few state-range chunks so the device-to-host copy
+  // of a finished chunk's V' / argmax overlaps the next chunk's sweep (the
+  // upload of V cannot overlap: every state may read any V entry).  Only for
+  // kernels whose cost scales with the range (not the factored C sweep,
+  // which builds whole-space tables per launch).
+  const std::uint64_t align = m.chunk_align();
+  int chunks = 1;
+  if (!out_q && (out_values || out_actions) && align > 0 && nr >= 4 * align &&
+      nr >= (std::uint64_t(1) << 22))
+    chunks = static_cast<int>(std::min<std::uint64_t>(std::min(backup_chunks(), Workspace::kChunkEvents / 2),
+                                                      nr / align));
+  std::uint64_t c_lo = lo;
+  for (int c = 0; c < chunks; ++c) {
+    std::uint64_t c_hi = c + 1 == chunks ? hi : lo + nr * (c + 1) / chunks;
+    if (c + 1 < chunks) c_hi = std::max(c_lo, c_hi / align * align);
+    if (c_hi <= c_lo) continue;
+    a.lo = c_lo;
+    a.hi = c_hi;
+    launch_sweep<T>(m, dm, a, ws.scratch, st);
+    if (chunks > 1) {
+      PVI_CUDA(cudaEventRecord(ws.done[c], st));
+      PVI_CUDA(cudaStreamWaitEvent(ws.copy, ws.done[c], 0));
+      const std::uint64_t off = c_lo - lo, len = c_hi - c_lo;
+      if (out_values)
+        PVI_CUDA(cudaMemcpyAsync(static_cast<T*>(out_values) + off, vo + off, len * sizeof(T),
+                                 cudaMemcpyDeviceToHost, ws.copy));
+      if (out_actions)
+        PVI_CUDA(cudaMemcpyAsync(out_actions + off, ao + off, len * 4, cudaMemcpyDeviceToHost, ws.copy));
+    }
+    c_lo = c_hi;
+  }
+  if (chunks == 1) {
+    if (out_values) PVI_CUDA(cudaMemcpyAsync(out_values, vo, nr * sizeof(T), cudaMemcpyDeviceToHost, st));
+    if (out_actions) PVI_CUDA(cudaMemcpyAsync(out_actions, ao, nr * 4, cudaMemcpyDeviceToHost, st));
+    if (out_q) PVI_CUDA(cudaMemcpyAsync(out_q, qo, nr * m.n_actions * sizeof(T), cudaMemcpyDeviceToHost, st));
+  }
   PVI_CUDA(cudaStreamSynchronize(st));
+  PVI_CUDA(cudaStreamSynchronize(ws.copy));
 }
 
 }  // namespace

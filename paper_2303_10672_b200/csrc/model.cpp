@@ -687,6 +687,15 @@ double Model::state_cost(std::uint64_t s) const {
   return double(ia + 1) * double(ib + 1);
 }
 
+std::uint64_t Model::chunk_align() const {
+  if (scenario == PVI_SCENARIO_C && algorithm == PVI_ALGO_FACTORED) return 0;
+  if (scenario == PVI_SCENARIO_B && algorithm == PVI_ALGO_FACTORED && pb.useful_life == 3) {
+    // k_b_fact_qw3 works on pairs of x_3 digits: 2 * na^2 * nb^3 states
+    return 2ull * b_na * b_na * b_nb * b_nb * b_nb;
+  }
+  return std::max<std::uint64_t>(tile_states(), 1);
+}
+
 std::uint64_t Model::tile_states() const {
   if (scenario == PVI_SCENARIO_B && algorithm == PVI_ALGO_FACTORED) {
     // shards own whole x_a groups (x_1 = 0..A_a, all x_b): stage 2 works on

@@ -162,6 +162,7 @@ struct Model {
   double factored_fmas() const;  // FP64 FMAs per sweep of the factored kernels
   double state_cost(std::uint64_t s) const;  // relative backup cost of one state
   std::uint64_t tile_states() const;         // partition alignment
+  std::uint64_t chunk_align() const;         // 0: sweeps do not chunk (whole-space tables)
 };
 
 std::unique_ptr<Model> build_scenario_a(const pvi_scenario_a_params& p);

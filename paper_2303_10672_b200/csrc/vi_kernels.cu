@@ -1109,11 +1109,11 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16(DevModel dm, const T* __r
                                                        double* __restrict__ v0t,
                                                        const std::uint16_t* __restrict__ group_order,
                                                        int n_groups, int n_xb, int n_bp, int n_r,
-                                                       int x3_lo, int x3_hi, int tiled) {
+                                                       int x3_lo, int x3_hi, int tiled, int r_base) {
   constexpr int NB = 16, S8 = 8, OB4 = 4;
   extern __shared__ double slab[];  // [bp][ob]
   const int stride = slab_stride(NB);
-  const int r = blockIdx.x;
+  const int r = r_base + static_cast<int>(blockIdx.x);
   if (M == 3) {
     // a state shard only reads the W rows of its own x_3 digits and the
     // R(0, j) rows of the diagonal constants (k_b_fact_qw3)
@@ -1790,12 +1790,13 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw3(DevModel dm, const double
                                                        const T* __restrict__ V,
                                                        T* __restrict__ vout,
                                                        std::uint32_t* __restrict__ act,
-                                                       std::uint64_t out_off, FinalizeArgs fa) {
+                                                       std::uint64_t out_off, FinalizeArgs fa,
+                                                       int xb_base) {
   constexpr int NB = 16;
   extern __shared__ double sm[];
   const int na = dm.b_na, dn = dm.b_dn;
   const int n_xa = na * na * na;
-  const int pr = blockIdx.x, xbi = blockIdx.y;
+  const int pr = blockIdx.x, xbi = xb_base + static_cast<int>(blockIdx.y);
   const int x3_0 = 2 * pr, n_x3 = min(2, na - x3_0);   // this CTA's x_3 values
   const int n_f = min(x3_0 + n_x3 - 1, na - 1) + 1;    // R(0, j) rows, j = 0..n_f-1
   const int n_rows = n_x3 * na + n_f;
@@ -2687,10 +2688,11 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
   // over the orders_a with the finalize (no partial buffers, no k_finalize)
   const bool use_qd = M == 3 && nb == 16 && na <= 16 && dm.n_states < (1ull << 31) && qd_enabled();
   const bool fused = use_qd && a.want_values && a.qout == nullptr;
-  const bool partials = a.want_values && !fused;
+  const bool partials = a.want_values && !fused && (a.stages & 2);
+  const std::uint64_t r0 = std::min<std::uint64_t>(a.r_lo, n_r), r1 = std::min<std::uint64_t>(a.r_hi, n_r);
   T* pv = partials ? scratch.get<T>(0, static_cast<std::size_t>(na) * nr, stream) : nullptr;
   std::uint8_t* pa = partials ? scratch.get<std::uint8_t>(1, static_cast<std::size_t>(na) * nr, stream) : nullptr;
-  count_launches(partials ? 3 : 2);
+  count_launches((partials ? 1 : 0) + ((a.stages & 1) && r1 > r0 ? 1 : 0) + ((a.stages & 2) ? 1 : 0));
   // stage-1 rows the (fused, one-warp) stage 2 of this shard reads
   const bool qw = fused && dc.b_pt_unit && qw_enabled();
   int x3_lo = 0, x3_hi = na - 1;
@@ -2708,14 +2710,19 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     if (nb == 16 && q16_enabled()) {                                                               \
       const std::size_t sm0 = sizeof(double) * slab_rows(static_cast<int>(n_bp)) * slab_stride(16); \
       cudaFuncSetAttribute(k_b_fact_w16<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-      k_b_fact_w16<T, MM><<<static_cast<unsigned>(n_r), 256, sm0, stream>>>(                       \
-          dm, a.v, W, v0t, dc.b_group_order_b, static_cast<int>(n_bp), static_cast<int>(n_xb),      \
-          static_cast<int>(n_bp), static_cast<int>(n_r), x3_lo, x3_hi, qw && MM == 3 ? 1 : 0);       \
-    } else {                                                                                       \
+      if ((a.stages & 1) && r1 > r0)                                                              \
+        k_b_fact_w16<T, MM><<<static_cast<unsigned>(r1 - r0), 256, sm0, stream>>>(                 \
+            dm, a.v, W, v0t, dc.b_group_order_b, static_cast<int>(n_bp), static_cast<int>(n_xb),    \
+            static_cast<int>(n_bp), static_cast<int>(n_r), x3_lo, x3_hi, qw && MM == 3 ? 1 : 0,     \
+            static_cast<int>(r0));                                                                 \
+    } else if (a.stages & 1) {                                                                     \
+      if (r0 != 0 || r1 != static_cast<std::uint64_t>(n_r))                                        \
+        fail(PVI_ERR_PARAMETER, "factored b: partial stage-1 ranges need the radix-16 kernel");    \
     k_b_fact_w<T, MM, NBX><<<static_cast<unsigned>(n_r), 256, sm1, stream>>>(                       \
         dm, a.v, W, v0t, dc.b_order_b, static_cast<int>(n_xb), static_cast<int>(n_bp), static_cast<int>(n_r)); \
     }                                                                                              \
-    if (MM == 3 && use_qd) {                                                                       \
+    if (!(a.stages & 2)) {                                                                         \
+    } else if (MM == 3 && use_qd) {                                                                \
       const std::size_t sm4 = sizeof(double) * (2 * static_cast<std::size_t>(n_ap) * 16 + 5 * dm.b_dn); \
       const std::size_t smf = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(T) + 1);              \
       if (qw) {                                                                                    \
@@ -2723,9 +2730,13 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
         const int n_f = na;                                                                        \
         const std::size_t smq = sizeof(double) * ((2 * na + n_f) * 16 * 2 + 5 * dm.b_dn + 2 * na * na) + 2 * na * na; \
         cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);         \
-        kq<<<dim3(static_cast<unsigned>((na + 1) / 2), static_cast<unsigned>(n_xb)), 32, smq, stream>>>( \
-            dm, W, v0t, dc.b_erpt, lo, hi, a.gamma, static_cast<int>(n_xb),                        \
-            static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa);   \
+        const std::uint64_t xb0 = std::min<std::uint64_t>(a.xb_lo, n_xb);                          \
+        const std::uint64_t xb1 = std::min<std::uint64_t>(a.xb_hi, n_xb);                          \
+        if (xb1 > xb0)                                                                             \
+          kq<<<dim3(static_cast<unsigned>((na + 1) / 2), static_cast<unsigned>(xb1 - xb0)), 32, smq, stream>>>( \
+              dm, W, v0t, dc.b_erpt, lo, hi, a.gamma, static_cast<int>(n_xb),                      \
+              static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa,  \
+              static_cast<int>(xb0));                                                              \
       } else if (fused && dc.b_pt_unit && qp_enabled()) {                                          \
         auto kq = a.act ? k_b_fact_qp3<T, true> : k_b_fact_qp3<T, false>;                          \
         const std::size_t smp = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(double) + 1);       \
@@ -2771,6 +2782,18 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
                                                         a.out_off, a.fa);
   PVI_CUDA(cudaGetLastError());
   return true;
+}
+
+// True when the factored B sweep of this model runs k_b_fact_qw3 (which
+// honours SweepArgs::xb_lo/xb_hi).  Valid after the first factored launch
+// (the law-mass check runs there).
+bool b_sweep_honours_xb_range(const Model& model, int device) {
+  if (model.scenario != PVI_SCENARIO_B || model.algorithm != PVI_ALGO_FACTORED) return false;
+  if (model.pb.useful_life != 3 || model.b_nb != 16 || model.b_na > 16) return false;
+  if (model.space.count >= (1ull << 31) || !qd_enabled() || !qw_enabled()) return false;
+  DeviceCopy& dc = model.device_copy(device);
+  std::lock_guard<std::mutex> lock(model.dev_mutex);
+  return dc.b_erpt != nullptr && dc.b_pt_unit;
 }
 
 template <typename T>

@@ -31,6 +31,14 @@ struct SweepArgs {
   bool want_values = true;       // false: Q rows only (B/C skip the partial buffers)
   int algorithm = 0;             // 0 exact (reference order, bit-identical), 1 factored
   FinalizeArgs fa;
+  // factored B only: which stages to run (1: W from V, 2: Q / argmax / finalize)
+  // and the stage-1 CTA range r in [r_lo, r_hi) (CTA r reads V[r |x_b| .. (r+1) |x_b|)),
+  // so a caller can start stage 1 on the part of V already uploaded
+  int stages = 3;
+  std::uint64_t r_lo = 0, r_hi = ~0ull;
+  // factored B stage 2 (k_b_fact_qw3 only): the x_b columns [xb_lo, xb_hi)
+  // to process; V' / argmax then land in a strided column block
+  std::uint64_t xb_lo = 0, xb_hi = ~0ull;
 };
 
 // Grow-only device scratch buffers, keyed by slot.
@@ -67,6 +75,7 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
 template <typename T>
 void launch_stats(const T* vnew, const T* vprev, std::uint64_t n, const FinalizeArgs& fa,
                   cudaStream_t stream);
+bool b_sweep_honours_xb_range(const Model& model, int device);
 void profile_enable(bool on);
 void profile_read(double* ms, std::uint64_t* main_launches, std::uint64_t* all_launches);
 void launch_initial_b(const DevModel& dm, double* out, std::uint64_t n, cudaStream_t stream);
