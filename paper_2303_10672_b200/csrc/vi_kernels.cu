@@ -2206,9 +2206,91 @@ __global__ void __launch_bounds__(256) k_c_bin_level(const double* __restrict__ 
   const double* w = s_bin + b * r;
   const int cap = r - 1;
   double acc = 0.0;
+#pragma unroll 4
   for (int y = 0; y <= b; ++y)
     acc = fma(w[y], __ldg(h + min(dk + y, cap) * wk + (b - y) * wb), acc);
   Hout[out_base + gid] = acc;
+}
+
+// Last pass (k = 1) fused with the Q rows, the first max over the orders and
+// the finalize.  CTA = CQ_GROUPS groups of the A_max+1 states that differ
+// only in x_1; a group's H_2 entries (b, z_1) for b, z_1 in [0, A_max] are one
+// 21 x 21 tile, staged in shared memory once (per order for the endogenous
+// per-order tables) instead of being re-read per (state, order) from L2/DRAM.
+constexpr int CQ_GROUPS = 12;
+template <typename T>
+__global__ void __launch_bounds__(256) k_c_bin_qf(DevModel dm, const double* __restrict__ H2,
+                                                  const T* __restrict__ V, T* __restrict__ vout,
+                                                  std::uint32_t* __restrict__ act,
+                                                  T* __restrict__ qout, std::uint64_t lo,
+                                                  std::uint64_t hi, std::uint64_t out_off,
+                                                  int n_prof, std::uint32_t wb, int endo,
+                                                  int in_is_g, std::uint64_t n_groups,
+                                                  FinalizeArgs fa) {
+  extern __shared__ double sm[];
+  const int na = static_cast<int>(dm.n_actions), dn = dm.c_dmax + 1;
+  const int r = dm.c_max_order + 1, cap = r - 1, m = dm.c_m;
+  double* s_bin = sm;                       // [a][y] = Bin(y; a, q_1(a))
+  double* s_pd = s_bin + r * r;             // PD(tau), 7 values
+  double* s_tile = s_pd + 8;                // [group][b][z_1]
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
+    const int a = i / r, y = i % r;
+    s_bin[i] = dm.c_binom[(static_cast<std::size_t>(a) * (m - 1) * r + a) * r + y];
+  }
+  if (threadIdx.x < 7) {
+    double pd = 0.0;
+    for (int d = 0; d < dn; ++d) pd += dm.c_pmf[threadIdx.x * dn + d];
+    s_pd[threadIdx.x] = pd;
+  }
+  const int g = threadIdx.x / r, x1 = threadIdx.x % r;
+  const std::uint64_t grp = static_cast<std::uint64_t>(blockIdx.x) * CQ_GROUPS + g;
+  const bool live = g < CQ_GROUPS && grp < n_groups;
+  const std::uint64_t s = grp * r + x1;
+  const int tau = live ? static_cast<int>(s / wb) : 0;
+  const bool valid = live && s >= lo && s < hi;
+  T best = T(0);
+  std::uint32_t besta = 0;
+  double* tile = s_tile + (g < CQ_GROUPS ? g : 0) * r * r;
+  const std::uint64_t grp_lo = static_cast<std::uint64_t>(blockIdx.x) * CQ_GROUPS;
+  for (int a = 0; a < na; ++a) {
+    // stage the tiles: exogenous once (a == 0, all b); endogenous per order
+    if (a == 0 || (endo && !in_is_g)) {
+      __syncthreads();
+      const int nbr = (endo && !in_is_g) ? a + 1 : r;
+      for (int i = threadIdx.x; i < CQ_GROUPS * nbr * r; i += blockDim.x) {
+        const int gg = i / (nbr * r), e = i % (nbr * r), b = e / r, z = e % r;
+        const std::uint64_t gq = grp_lo + gg;
+        if (gq >= n_groups) continue;
+        const std::uint64_t s0 = gq * r;
+        const int tq = static_cast<int>(s0 / wb);
+        const std::size_t rest0 = static_cast<std::size_t>(s0 - static_cast<std::uint64_t>(tq) * wb);
+        const std::size_t base = (endo && !in_is_g)
+                                     ? c_tri_base(a, wb) + static_cast<std::size_t>(tq) * (a + 1) * wb
+                                     : static_cast<std::size_t>(tq) * n_prof;
+        s_tile[(gg * r + b) * r + z] = __ldg(H2 + base + static_cast<std::size_t>(b) * wb + rest0 + z);
+      }
+      __syncthreads();
+    }
+    if (!live) continue;
+    const double* w = s_bin + a * r;
+    double acc = 0.0;
+    for (int y = 0; y <= a; ++y) acc = fma(w[y], tile[(a - y) * r + min(x1 + y, cap)], acc);
+    const double fixed = a > 0 ? -dm.c_cf : 0.0;
+    const T qa = static_cast<T>(fma(fixed, s_pd[tau], acc));
+    if (a == 0 || qa > best) {
+      best = qa;
+      besta = static_cast<std::uint32_t>(a);
+    }
+    if (qout && valid) qout[(s - lo) * na + a] = qa;
+  }
+  double smx = -DBL_MAX, smn = DBL_MAX;
+  unsigned long long bad = ~0ull;
+  if (valid) {
+    if (vout) vout[s - out_off] = best;
+    if (act) act[s - out_off] = besta;
+    state_stat<T>(fa, s, best, V, smx, smn, bad);
+  }
+  reduce_stats(smx, smn, bad, fa.stats);
 }
 
 // Pass k = 1 fused with the Q output: thread = (state, order).
@@ -2585,6 +2667,14 @@ static bool a_group_enabled() {
   return on;
 }
 
+static bool qf_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PVI_C_QF");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static bool q16_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PVI_B_Q16");
@@ -2818,7 +2908,7 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     Hb[0] = scratch.get<double>(6, tab, stream);
     if (M > 3) Hb[1] = scratch.get<double>(7, tab, stream);
   }
-  bool done = false;
+  bool done = false, qf_done = false;
   int launches = 0;
   {
     MainKernelScope prof(stream);
@@ -2848,15 +2938,26 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
             wb, endo ? 1 : 0, src == G ? 1 : 0, static_cast<int>(n_prof));
         src = dst;
       }
-      k_c_bin_q<T><<<dim3(grid_for(nr, 256), na), 256, 0, stream>>>(
-          dm, src, pv, a.qout, lo, hi, static_cast<int>(n_prof), wb, endo ? 1 : 0, src == G ? 1 : 0);
+      if (qf_enabled() && !endo) {  // endogenous: per-order restaging loses to k_c_bin_q
+        const std::uint64_t n_groups = dm.n_states / static_cast<std::uint64_t>(r);
+        const std::size_t smq = sizeof(double) * (static_cast<std::size_t>(r) * r + 8 +
+                                                  static_cast<std::size_t>(CQ_GROUPS) * r * r);
+        cudaFuncSetAttribute(k_c_bin_qf<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        k_c_bin_qf<T><<<static_cast<unsigned>((n_groups + CQ_GROUPS - 1) / CQ_GROUPS), 256, smq, stream>>>(
+            dm, src, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, static_cast<int>(n_prof), wb,
+            endo ? 1 : 0, src == G ? 1 : 0, n_groups, a.fa);
+        qf_done = true;
+      } else {
+        k_c_bin_q<T><<<dim3(grid_for(nr, 256), na), 256, 0, stream>>>(
+            dm, src, pv, a.qout, lo, hi, static_cast<int>(n_prof), wb, endo ? 1 : 0, src == G ? 1 : 0);
+      }
       launches = M;  // G, m-2 passes, fused pass + Q
     }
   }
   if (!done) return false;
-  count_launches(a.want_values ? launches + 1 : launches);
+  count_launches(a.want_values && !qf_done ? launches + 1 : launches);
   PVI_CUDA(cudaGetLastError());
-  if (a.want_values)
+  if (a.want_values && !qf_done)
     k_finalize<T><<<grid_for(nr, 256), 256, 0, stream>>>(pv, nullptr, na, 1, a.v, a.vout, a.act, lo, hi,
                                                         a.out_off, a.fa);
   PVI_CUDA(cudaGetLastError());
