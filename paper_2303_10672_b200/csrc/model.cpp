@@ -680,6 +680,12 @@ double Model::state_cost(std::uint64_t s) const {
   for (int i = 0; i < life; ++i) ia += st[i];
   for (int i = life; i < 2 * life; ++i) ib += st[i];
   if (algorithm == PVI_ALGO_FACTORED) {
+    if (life == 3 && b_nb == 16 && b_na <= 16) {
+      // k_b_fact_qw3: per x_3 pair p, 16 diagonal steps (~245 instructions)
+      // plus 2p + 2 diagonal-constant steps (~114), per order_a
+      const int p = st[0] / 2;
+      return 34.4 + 2.0 * (p + 1);
+    }
     // factored stage 2: one merged block plus h_a = x_1+1..I_a, per order_a
     const int x1 = st[life - 1];
     return double(ia - x1 + 1) + 2.0;
@@ -697,6 +703,11 @@ std::uint64_t Model::chunk_align() const {
 }
 
 std::uint64_t Model::tile_states() const {
+  if (scenario == PVI_SCENARIO_B && algorithm == PVI_ALGO_FACTORED && pb.useful_life == 3 &&
+      b_nb == 16 && b_na <= 16) {
+    // k_b_fact_qw3 works on pairs of x_3 digits: a shard owns whole pairs
+    return 2ull * b_na * b_na * b_nb * b_nb * b_nb;
+  }
   if (scenario == PVI_SCENARIO_B && algorithm == PVI_ALGO_FACTORED) {
     // shards own whole x_a groups (x_1 = 0..A_a, all x_b): stage 2 works on
     // groups of states that share x_2..x_m, so no group straddles two ranks
