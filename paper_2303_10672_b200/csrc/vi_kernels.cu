@@ -1937,6 +1937,268 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw3(DevModel dm, const double
   reduce_stats(smx, smn, bad, fa.stats);
 }
 
+// k_b_fact_qw3 with three changes:
+//  * the diagonal constants C(I, x_3) are computed once per distinct
+//    I = x_3 + S2 (lane l: I = x3_0 + l, x_3 = x3_0) and handed to the lanes
+//    that need them by shuffles; the upper half-warp (x_3 = x3_0 + 1) adds
+//    its one extra R(0, x3_0) term.  33 constants per x_3 pair instead of
+//    64, with the same operations in the same order as k_b_fact_qw3.
+//  * the R(0, j) rows of the constants are not staged with the main rows:
+//    PF (the default) stages them one order_a ahead into their own buffer
+//    (cp.async group issued once the constants of this order_a are done),
+//    and the next order_a's main rows are issued right after this order_a's
+//    u loop, so both copies land behind computation; without PF they are
+//    read through L1/L2.  DB (double-buffered main rows) costs more in
+//    occupancy than it hides (measured 5.36 vs 4.88 ms per sweep).
+//  * the order_b maximum runs as two independent compare chains (even /
+//    odd o_b) merged with the first-maximum rule.
+// b/m3/exp1 sweep (stage 1 + 2): qw3 5.15 ms, qw4 4.88 ms, qw4+PF 4.62 ms.
+template <typename T, bool WA, bool DB, bool PF>
+__global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double* __restrict__ W,
+                                                       const double* __restrict__ v0t,
+                                                       const double* __restrict__ erpt,
+                                                       std::uint64_t lo, std::uint64_t hi,
+                                                       double gamma, int n_xb, int n_ap, int n_r,
+                                                       const T* __restrict__ V,
+                                                       T* __restrict__ vout,
+                                                       std::uint32_t* __restrict__ act,
+                                                       std::uint64_t out_off, FinalizeArgs fa,
+                                                       int xb_base) {
+  constexpr int NB = 16;
+  extern __shared__ double sm[];
+  const int na = dm.b_na, dn = dm.b_dn;
+  const int n_xa = na * na * na;
+  const int pr = blockIdx.x, xbi = xb_base + static_cast<int>(blockIdx.y);
+  const int x3_0 = 2 * pr, n_x3 = min(2, na - x3_0);  // this CTA's x_3 values
+  const int n_rows = n_x3 * na;
+  // main rows R(u, x_3) [n_x3*na][ob] of W and V0; DB: two buffers (the
+  // next order_a's rows land while this one is computed)
+  constexpr int NBUF = DB ? 2 : 1;
+  const int rb = 2 * na * NB;          // doubles per row array
+  double* w_sl0 = sm;
+  double* v_sl0 = w_sl0 + rb;
+  // PF: the R(0, j) rows of the constants (j < max(x3_0, 1)) staged in
+  // shared memory one order_a ahead
+  const int n_fr = PF ? max(na - 2, 1) : 0;
+  double* f_w = sm + NBUF * 2 * rb;
+  double* f_v = f_w + n_fr * NB;
+  double* s_pa = f_v + n_fr * NB;
+  double* s_ca = s_pa + dn;
+  double* s_pz = s_ca + dn;
+  double* s_cg = s_pz + dn;
+  double* s_sa = s_cg + dn;
+  double* s_best = s_sa + dn;          // [n_x3 * na * na]
+  std::uint8_t* s_arg = reinterpret_cast<std::uint8_t*>(s_best + 2 * na * na);
+  const int ilo = static_cast<int>(lo), ihi = static_cast<int>(hi);
+  {
+    const int s_first = (x3_0 * na * na) * n_xb + xbi;
+    const int s_last = ((x3_0 + n_x3) * na * na - 1) * n_xb + xbi;
+    if (s_last < ilo || s_first >= ihi) return;  // no state of this CTA in the shard
+  }
+  int ib = 0;
+  {
+    int rem = xbi;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      ib += rem % NB;
+      rem /= NB;
+    }
+  }
+  const double gsf = gamma * dm.b_sf_b[ib];
+  for (int i = threadIdx.x; i < dn; i += 32) {
+    s_pa[i] = gamma * dm.b_pmf_a[i];
+    s_ca[i] = gamma * dm.b_cdf_a[i];
+    s_pz[i] = gsf * dm.b_pz[ib * dn + i];
+    s_cg[i] = gsf * dm.b_pz_cum[ib * dn + i];
+    s_sa[i] = gamma * dm.b_sf_a[i];
+  }
+  const int lane = threadIdx.x & 31;
+  const int L = lane & 15, half = lane >> 4;
+  const int x3 = x3_0 + half;
+  const bool lane_ok = L < na && half < n_x3;
+  const int x3c = min(x3, na - 1);
+  const int Ia = min(L + x3c, dn - 1), Ib = min(L + na + x3c, dn - 1);
+  // constant producer: lane l owns I = x3_0 + l at x_3 = x3_0
+  const int Il = min(x3_0 + lane, dn - 1);
+  const int srcA = L + half, srcB = min(L + na + half, 31);
+  const double cvb = dm.b_cvb;
+  const double* er_base = erpt + static_cast<std::size_t>(xbi) * n_xa * 2;
+  const unsigned wd = static_cast<unsigned>(__cvta_generic_to_shared(w_sl0));
+  const unsigned vd = static_cast<unsigned>(__cvta_generic_to_shared(v_sl0));
+  const std::size_t wtile = (static_cast<std::size_t>(xbi >> 4) * n_r) * NB * NB + (xbi & 15) * NB;
+  // main rows ap = x3_0*na .. (x3_0+n_x3)*na - 1 (contiguous); W tiled
+  // [x_b / 16][r][x_b % 16][o_b] (k_b_fact_w16, tiled = 1)
+  auto stage = [&](int o, int buf) {
+    const std::size_t rs = static_cast<std::size_t>(o) * n_ap;
+    const double2* wsrc = reinterpret_cast<const double2*>(W + wtile + rs * NB * NB);
+    const double2* vsrc = reinterpret_cast<const double2*>(v0t + rs * NB);
+    const unsigned off = static_cast<unsigned>(buf) * 2u * rb * 8u;
+    for (int i = lane; i < n_rows * (NB / 2); i += 32) {
+      const int row = i >> 3, c = i & 7;
+      const int ap = x3_0 * na + row;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wd + off + 16u * i), "l"(wsrc + ap * 128 + c));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(vd + off + 16u * i), "l"(vsrc + ap * 8 + c));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  const unsigned fwd = static_cast<unsigned>(__cvta_generic_to_shared(f_w));
+  const unsigned fvd = static_cast<unsigned>(__cvta_generic_to_shared(f_v));
+  const int n_fj = max(x3_0, 1);
+  auto stage_f = [&](int o) {
+    const std::size_t rs = static_cast<std::size_t>(o) * n_ap;
+    const double2* wsrc = reinterpret_cast<const double2*>(W + wtile + rs * NB * NB);
+    const double2* vsrc = reinterpret_cast<const double2*>(v0t + rs * NB);
+    for (int i = lane; i < n_fj * (NB / 2); i += 32) {
+      const int j = i >> 3, c = i & 7;
+      const int ap = j * na;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(fwd + 16u * i), "l"(wsrc + ap * 128 + c));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(fvd + 16u * i), "l"(vsrc + ap * 8 + c));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  __syncwarp();
+  // the extra R(0, x3_0) term of the upper half (zero weights in the lower)
+  const int ea_i = max(Ia - x3_0, 0), eb_i = max(Ib - x3_0, 0);
+  const double ea = half ? s_pa[ea_i] : 0.0, eg = half ? s_pz[ea_i] : 0.0;
+  const double eb = half ? s_pa[eb_i] : 0.0, eq = half ? s_pz[eb_i] : 0.0;
+  if (PF) {
+    stage_f(0);
+    stage(0, 0);
+  } else if (DB) {
+    stage(0, 0);
+  }
+  for (int oa = 0; oa < na; ++oa) {
+    const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
+    __syncwarp();
+    if (PF) {
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // F rows of oa landed
+      __syncwarp();
+    } else if (!DB) {
+      stage(oa, 0);
+    } else if (oa + 1 < na) {
+      stage(oa + 1, (oa + 1) & 1);
+    }
+    const double* w_sl = w_sl0 + (DB ? (oa & 1) * 2 * rb : 0);
+    const double* v_sl = w_sl + rb;
+    const double c0 = dm.b_cva * oa;
+    double acc_a[NB], acc_b[NB];
+    {
+      // C(I_l, x3_0) from the R(0, j) rows (j < x3_0), read through L1/L2
+      const double* fw = PF ? f_w : W + wtile + r0 * NB * NB;  // row j at fw + j * fstride
+      const double* fv = PF ? f_v : v0t + r0 * NB;
+      const std::size_t fws = PF ? NB : static_cast<std::size_t>(na) * NB * NB;
+      const int fvs = PF ? NB : na * NB;
+      double c[NB];
+      {
+        const double cw = s_sa[Il] - s_pa[Il], cg = (gsf - s_cg[Il]) - s_pz[Il];
+#pragma unroll
+        for (int k = 0; k < NB; k += 2) {
+          const double2 w0 = PF ? *reinterpret_cast<const double2*>(fw + k) : __ldg(reinterpret_cast<const double2*>(fw + k));
+          const double2 v0 = PF ? *reinterpret_cast<const double2*>(fv + k) : __ldg(reinterpret_cast<const double2*>(fv + k));
+          c[k] = fma(cw, w0.x, fma(cg, v0.x, -fma(static_cast<double>(k), cvb, c0)));
+          c[k + 1] = fma(cw, w0.y, fma(cg, v0.y, -fma(static_cast<double>(k + 1), cvb, c0)));
+        }
+      }
+      for (int j = 0; j < x3_0; ++j) {
+        const double* wr = fw + j * fws;
+        const double* vr = fv + j * fvs;
+        const double p = s_pa[max(Il - j, 0)], q = s_pz[max(Il - j, 0)];
+#pragma unroll
+        for (int k = 0; k < NB; k += 2) {
+          const double2 wk = PF ? *reinterpret_cast<const double2*>(wr + k) : __ldg(reinterpret_cast<const double2*>(wr + k));
+          const double2 vk = PF ? *reinterpret_cast<const double2*>(vr + k) : __ldg(reinterpret_cast<const double2*>(vr + k));
+          c[k] = fma(p, wk.x, fma(q, vk.x, c[k]));
+          c[k + 1] = fma(p, wk.y, fma(q, vk.y, c[k + 1]));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        acc_a[k] = __shfl_sync(0xffffffffu, c[k], srcA);
+        acc_b[k] = __shfl_sync(0xffffffffu, c[k], srcB);
+      }
+    }
+    if (PF) {
+      __syncwarp();  // every lane is done with the F rows of oa
+      if (oa + 1 < na) stage_f(oa + 1);
+      if (oa + 1 < na)
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // main rows of oa landed
+      else
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+    } else if (DB && oa + 1 < na)
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    else
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const double wk = w_sl[k], vk = v_sl[k];  // R(0, x3_0)
+      acc_a[k] = fma(ea, wk, fma(eg, vk, acc_a[k]));
+      acc_b[k] = fma(eb, wk, fma(eq, vk, acc_b[k]));
+    }
+    const int xa_lo = x3c * na * na;
+    const double* wrow = w_sl + (min(half, n_x3 - 1) * na) * NB;
+    const double* vrow = v_sl + (min(half, n_x3 - 1) * na) * NB;
+    for (int u = 0; u < na; ++u, wrow += NB, vrow += NB) {
+      const bool sw = u > L;
+      const int x1 = sw ? L + na - u : L - u;
+      const int xl = x1 + u * na + half * na * na;  // local state index
+      const int st = (x1 + u * na + xa_lo) * n_xb + xbi;
+      const bool valid = lane_ok && st >= ilo && st < ihi;
+      const int ia = max(L - u, 0), ibb = min(L + na - u, dn - 1);
+      const double pa = s_pa[ia], pg = s_pz[ia], pb = s_pa[ibb], qb = s_pz[ibb];
+      const int xc = min(max(x1, 0), dn - 2);
+      const double ca = s_ca[xc], cgx = s_cg[xc + 1];
+      double b0 = 0.0, b1 = 0.0;
+      int o0 = 0, o1 = 1;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        const double wk = wrow[k], vk = vrow[k];
+        const double r = sw ? acc_b[k] : acc_a[k];
+        const double t = fma(ca, wk, fma(cgx, vk, r));
+        if (k == 0) {
+          b0 = t;
+        } else if (k == 1) {
+          b1 = t;
+        } else if (k & 1) {
+          if (t > b1) {
+            b1 = t;
+            if (WA) o1 = k;
+          }
+        } else if (t > b0) {
+          b0 = t;
+          if (WA) o0 = k;
+        }
+        acc_a[k] = fma(pa, wk, fma(pg, vk, acc_a[k]));
+        acc_b[k] = fma(pb, wk, fma(qb, vk, acc_b[k]));
+      }
+      // first maximum over o_b: the odd chain wins if larger, or equal at a smaller index
+      const bool odd = b1 > b0 || (WA && b1 == b0 && o1 < o0);
+      const double best = odd ? b1 : b0;
+      if (valid && (oa == 0 || best > s_best[xl])) {
+        s_best[xl] = best;
+        if (WA) s_arg[xl] = static_cast<std::uint8_t>(oa * NB + (odd ? o1 : o0));
+      }
+    }
+    if (PF && oa + 1 < na) {
+      __syncwarp();  // every lane is done with the main rows of oa
+      stage(oa + 1, 0);
+    }
+  }
+  __syncwarp();
+  double smx = -DBL_MAX, smn = DBL_MAX;
+  unsigned long long bad = ~0ull;
+  for (int xl = lane; xl < n_x3 * na * na; xl += 32) {
+    const int xa = x3_0 * na * na + xl;
+    const int st = xa * n_xb + xbi;
+    if (st < ilo || st >= ihi) continue;
+    const T best = static_cast<T>(__ldg(er_base + 2 * xa) + s_best[xl]);
+    if (vout) vout[st - out_off] = best;
+    if (WA && act) act[st - out_off] = s_arg[xl];
+    state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
+  }
+  reduce_stats(smx, smn, bad, fa.stats);
+}
+
 // ---------------------------------------------------------------------------
 // K1-C: one thread per (state, order); the demand dimension unrolled into
 // DN register accumulators.  Blocks run heaviest order first.  Term order
@@ -2659,6 +2921,17 @@ static bool qw_enabled() {
   return on;
 }
 
+// PVI_B_QW4: 0 = k_b_fact_qw3, 1 = k_b_fact_qw4, 2 = k_b_fact_qw4 with
+// double-buffered row staging, 3 = k_b_fact_qw4 with the constants' rows
+// prefetched into shared memory
+static int qw4_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("PVI_B_QW4");
+    return e && e[0] >= '0' && e[0] <= '3' ? e[0] - '0' : 3;
+  }();
+  return mode;
+}
+
 static bool a_group_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PVI_A_GROUP");
@@ -2816,8 +3089,12 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
       const std::size_t sm4 = sizeof(double) * (2 * static_cast<std::size_t>(n_ap) * 16 + 5 * dm.b_dn); \
       const std::size_t smf = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(T) + 1);              \
       if (qw) {                                                                                    \
-        auto kq = a.act ? k_b_fact_qw3<T, true> : k_b_fact_qw3<T, false>;                          \
-        const int n_f = na;                                                                        \
+        const int q4 = qw4_mode();                                                                 \
+        auto kq = q4 == 3 ? (a.act ? k_b_fact_qw4<T, true, false, true> : k_b_fact_qw4<T, false, false, true>)  \
+                : q4 == 2 ? (a.act ? k_b_fact_qw4<T, true, true, false> : k_b_fact_qw4<T, false, true, false>)  \
+                : q4 == 1 ? (a.act ? k_b_fact_qw4<T, true, false, false> : k_b_fact_qw4<T, false, false, false>) \
+                          : (a.act ? k_b_fact_qw3<T, true> : k_b_fact_qw3<T, false>);              \
+        const int n_f = q4 >= 3 ? std::max(na - 2, 1) : q4 == 2 ? 2 * na : q4 == 1 ? 0 : na;         \
         const std::size_t smq = sizeof(double) * ((2 * na + n_f) * 16 * 2 + 5 * dm.b_dn + 2 * na * na) + 2 * na * na; \
         cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);         \
         const std::uint64_t xb0 = std::min<std::uint64_t>(a.xb_lo, n_xb);                          \
