@@ -180,6 +180,13 @@ typedef struct {
   uint64_t max_states;       /* capacity gate, 200'000'000 */
   int device;                /* CUDA ordinal, -1 = current */
   int algorithm;             /* -1: the model's (pvi_model_set_algorithm), else pvi_algorithm */
+  int loop;                  /* sweep loop control: -1 auto (graph-resident when no checkpoint
+                                falls inside the loop and the test keeps <= 2 vectors), 0 host
+                                loop (one 32-byte read-back per sweep), 1 graph-resident loop
+                                (CUDA graph with a device-evaluated WHILE condition: no host
+                                round trip per sweep; PVI_ERR_PARAMETER where unsupported) */
+  int l2_persist;            /* -1 auto / 1 on: an L2 access-policy window (persisting) over the
+                                value-vector ring; 0 off */
 } pvi_vi_config;
 
 /* Backup algorithm.  EXACT reproduces the reference's per-term expression
@@ -202,6 +209,9 @@ typedef struct {
   uint64_t sweeps;       /* sweeps launched, incl. the policy-extraction sweep */
   double span_lo, span_hi; /* last convergence statistic (min/max, or 0/max|dV|) */
   double terms_per_sweep;
+  uint64_t graph_sweeps; /* sweeps run inside the graph-resident loop */
+  uint64_t l2_window_bytes; /* bytes covered by the persisting L2 window (0: none) */
+  double l2_hit_ratio;   /* the window's hitRatio */
 } pvi_vi_stats;
 
 /* run_value_iteration(model, config, resume) (vi.hpp:295-302).

@@ -62,14 +62,15 @@ class ViConfigC(C.Structure):
                 ("checkpoint_every", C.c_uint64), ("checkpoint_path", C.c_char_p),
                 ("precision", C.c_int), ("convergence_test", C.c_int),
                 ("max_states", C.c_uint64), ("device", C.c_int),
-                ("algorithm", C.c_int)]
+                ("algorithm", C.c_int), ("loop", C.c_int), ("l2_persist", C.c_int)]
 
 
 class ViStats(C.Structure):
     _fields_ = [("iterations", C.c_uint64), ("converged", C.c_int),
                 ("wall_seconds", C.c_double), ("sweep_seconds", C.c_double),
                 ("sweeps", C.c_uint64), ("span_lo", C.c_double), ("span_hi", C.c_double),
-                ("terms_per_sweep", C.c_double)]
+                ("terms_per_sweep", C.c_double), ("graph_sweeps", C.c_uint64),
+                ("l2_window_bytes", C.c_uint64), ("l2_hit_ratio", C.c_double)]
 
 
 class RolloutConfigC(C.Structure):

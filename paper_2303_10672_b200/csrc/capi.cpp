@@ -267,6 +267,8 @@ void pvi_vi_config_defaults(pvi_vi_config* c) {
   c->max_states = 200000000ull;
   c->device = -1;
   c->algorithm = -1;
+  c->loop = -1;
+  c->l2_persist = -1;
 }
 
 int pvi_model_set_algorithm(pvi_model* m, int algorithm) {

@@ -208,6 +208,38 @@ struct DevBuf {
   }
 };
 
+// Stream-ordered allocation from the device's default memory pool, which
+// keeps freed memory (release threshold = max), so repeated solves on the
+// same device do not pay cudaMalloc / cudaFree of the GB-scale buffers.
+struct PoolBuf {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  PoolBuf(std::size_t bytes, cudaStream_t stream) : s(stream) {
+    static bool configured[64] = {};
+    int dev = 0;
+    PVI_CUDA(cudaGetDevice(&dev));
+    if (dev < 64 && !configured[dev]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        std::uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      cudaGetLastError();
+      configured[dev] = true;
+    }
+    if (bytes) PVI_CUDA(cudaMallocAsync(&p, bytes, stream));
+  }
+  PoolBuf(const PoolBuf&) = delete;
+  PoolBuf& operator=(const PoolBuf&) = delete;
+  ~PoolBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  template <typename U>
+  U* as() const {
+    return static_cast<U*>(p);
+  }
+};
+
 struct Stream {
   cudaStream_t s = nullptr;
   Stream() { PVI_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
@@ -216,11 +248,14 @@ struct Stream {
   }
 };
 
+// Pinned 32-byte statistics record, one per host thread (cudaMallocHost is
+// a driver call of ~ms; a solve should not pay it each time).
 struct PinnedStats {
   SweepStats* h = nullptr;
-  PinnedStats() { PVI_CUDA(cudaMallocHost(&h, sizeof(SweepStats))); }
-  ~PinnedStats() {
-    if (h) cudaFreeHost(h);
+  PinnedStats() {
+    static thread_local SweepStats* cached = nullptr;
+    if (!cached) PVI_CUDA(cudaMallocHost(&cached, sizeof(SweepStats)));
+    h = cached;
   }
 };
 
@@ -443,6 +478,112 @@ bool evaluate_test(int test, double hi, double lo, double epsilon, std::uint64_t
   }
 }
 
+// Graph-resident sweep loop.  The loop control of run_value_iteration
+// (vi.hpp:220-265: divergence check, convergence test, iteration limit) is
+// evaluated by a one-thread kernel after every sweep, which sets the
+// condition of the CUDA graph's WHILE node, so a solve runs as ONE graph
+// launch with no host round trip per sweep.  The value ring has two slots
+// (value / change span), so the WHILE body holds two sweeps (b -> a, then
+// a -> b inside an IF node the first decision also sets).
+bool loop_trace() {
+  static const bool on = [] {
+    const char* e = std::getenv("PVI_LOOP_TRACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+// one slot of the device value ring (a view into one allocation)
+struct RingSlot {
+  void* p;
+  template <typename U>
+  U* as() const {
+    return static_cast<U*>(p);
+  }
+};
+
+struct LoopState {
+  unsigned long long iteration;  // absolute sweep count
+  unsigned long long limit;      // stop once iteration reaches it
+  unsigned long long first_bad;  // first non-finite state, ~0 when none
+  unsigned long long bad_iteration;
+  double last_hi, last_lo;
+  double epsilon;
+  int test;                      // -1: no test (fixed iterations)
+  int fixed;                     // fixed_iterations mode: reaching the limit converges
+  int converged;
+  int pad;
+};
+
+__global__ void k_loop_decide(LoopState* ls, const SweepStats* st, cudaGraphConditionalHandle h_while,
+                              cudaGraphConditionalHandle h_if, int set_if) {
+  LoopState s = *ls;
+  s.iteration += 1;
+  bool stop = false;
+  if (st->first_bad != ~0ull) {
+    s.first_bad = st->first_bad;
+    s.bad_iteration = s.iteration;
+    stop = true;
+  } else {
+    if (s.test >= 0) {
+      const double hi = dkey_inv(st->max_key);
+      const double lo = s.test == PVI_TEST_VALUE_SPAN ? 0.0 : dkey_inv(st->min_key);
+      s.last_hi = hi;
+      s.last_lo = lo;
+      bool c;
+      if (s.test == PVI_TEST_VALUE_SPAN) c = (0.0 < hi ? hi : 0.0) < s.epsilon;  // std::max(0.0, hi)
+      else c = hi - lo < s.epsilon;  // change span (periodic span needs 8 vectors: host loop)
+      s.converged = c ? 1 : 0;
+      stop = c;
+    }
+    if (!stop && s.iteration >= s.limit) {
+      if (s.fixed) s.converged = 1;
+      stop = true;
+    }
+  }
+  *ls = s;
+  cudaGraphSetConditional(h_while, stop ? 0u : 1u);
+  if (set_if) cudaGraphSetConditional(h_if, stop ? 0u : 1u);
+}
+
+// Persisting L2 window over [base, base + bytes) for kernels launched on
+// `stream` (and captured from it): the value ring stays resident in L2
+// while the sweeps gather from it.  Returns the window size (0: none).
+std::size_t set_l2_window(cudaStream_t stream, const void* base, std::size_t bytes, int device,
+                          double* hit_ratio) {
+  int max_persist = 0, max_window = 0;
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+  cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
+  if (max_persist <= 0 || max_window <= 0 || bytes == 0) return 0;
+  const std::size_t win = std::min<std::size_t>(bytes, static_cast<std::size_t>(max_window));
+  const std::size_t persist = std::min<std::size_t>(win, static_cast<std::size_t>(max_persist));
+  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaStreamAttrValue attr = {};
+  attr.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  attr.accessPolicyWindow.num_bytes = win;
+  attr.accessPolicyWindow.hitRatio = static_cast<float>(std::min(1.0, static_cast<double>(persist) / win));
+  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  if (cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &attr) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  *hit_ratio = attr.accessPolicyWindow.hitRatio;
+  return win;
+}
+
+void clear_l2_window(cudaStream_t stream) {
+  cudaStreamAttrValue attr = {};
+  attr.accessPolicyWindow.num_bytes = 0;
+  cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+  cudaCtxResetPersistingL2Cache();
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  cudaGetLastError();
+}
+
 template <typename T>
 void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_values,
                 std::uint64_t resume_iteration, const std::uint8_t* resume_fp, double* out_values,
@@ -468,15 +609,30 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
   std::lock_guard<std::mutex> ws_lock(ws.mu);
   Scratch& scratch = ws.scratch;
   PinnedStats pstats;
-  DevBuf dstats(sizeof(SweepStats));
+  PoolBuf dstats(sizeof(SweepStats), stream.s);
 
   const int hist_cap = test == PVI_TEST_PERIODIC_SPAN ? 8 : 2;
-  std::vector<std::unique_ptr<DevBuf>> ring;
-  for (int i = 0; i < hist_cap; ++i) ring.push_back(std::make_unique<DevBuf>(n * sizeof(T)));
+  // the value ring is one allocation, so one L2 window covers every slot
+  PoolBuf ring_mem(static_cast<std::size_t>(hist_cap) * n * sizeof(T), stream.s);
+  std::vector<std::unique_ptr<RingSlot>> ring;
+  for (int i = 0; i < hist_cap; ++i)
+    ring.push_back(std::make_unique<RingSlot>(RingSlot{ring_mem.as<T>() + static_cast<std::size_t>(i) * n}));
+  double l2_ratio = 0.0;
+  const std::size_t l2_bytes =
+      cfg.l2_persist == 0 ? 0
+                          : set_l2_window(stream.s, ring_mem.p, static_cast<std::size_t>(hist_cap) * n * sizeof(T),
+                                          device, &l2_ratio);
+  struct L2Reset {
+    cudaStream_t s;
+    bool on;
+    ~L2Reset() {
+      if (on) clear_l2_window(s);
+    }
+  } l2_reset{stream.s, l2_bytes > 0};
   std::vector<int> order;  // slots oldest..newest
   std::uint64_t iteration = 0;
   {
-    DevBuf v0(n * sizeof(double));
+    PoolBuf v0(n * sizeof(double), stream.s);
     if (resume_values) {
       if (resume_fp && std::memcmp(resume_fp, fp, 32) != 0)
         fail(PVI_ERR_FINGERPRINT, "resume checkpoint fingerprint " + hex32(resume_fp) +
@@ -511,6 +667,14 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
 
   bool converged = false;
   const std::uint64_t start_iteration = iteration;
+  // graph-resident loop: two-vector tests, no checkpoint inside the loop,
+  // not while the bench's per-launch profiler records events
+  const bool graph_possible = hist_cap == 2 && !ckpt && !profiling_enabled();
+  if (cfg.loop == 1 && !graph_possible)
+    fail(PVI_ERR_PARAMETER, "graph-resident loop needs a value- or change-span test and no checkpoints");
+  const bool use_graph = graph_possible && cfg.loop != 0;
+  std::uint64_t graph_sweeps = 0;
+  const auto t_loop_start = std::chrono::steady_clock::now();
   while (true) {
     if (cfg.fixed_iterations > 0) {
       if (iteration >= cfg.fixed_iterations) {
@@ -518,6 +682,114 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
         break;
       }
     } else if (iteration >= start_iteration + cfg.max_iterations) {
+      break;
+    }
+    if (use_graph && sweeps > 0) {
+      // every remaining sweep in one graph launch (the first sweep ran eagerly:
+      // it builds the per-model tables and scratch the captured sweeps reuse)
+      const int a_slot = order.front(), b_slot = order.back();
+      PoolBuf dls(sizeof(LoopState), stream.s);
+      LoopState h{};
+      h.iteration = iteration;
+      h.limit = cfg.fixed_iterations > 0 ? cfg.fixed_iterations : start_iteration + cfg.max_iterations;
+      h.first_bad = ~0ull;
+      h.epsilon = cfg.epsilon;
+      h.test = cfg.fixed_iterations == 0 ? test : -1;
+      h.fixed = cfg.fixed_iterations > 0 ? 1 : 0;
+      PVI_CUDA(cudaMemcpyAsync(dls.p, &h, sizeof(h), cudaMemcpyHostToDevice, stream.s));
+      cudaGraph_t graph = nullptr;
+      const auto tr0 = std::chrono::steady_clock::now();
+      PVI_CUDA(cudaGraphCreate(&graph, 0));
+      cudaGraphConditionalHandle h_while, h_if;
+      PVI_CUDA(cudaGraphConditionalHandleCreate(&h_while, graph, 1, cudaGraphCondAssignDefault));
+      PVI_CUDA(cudaGraphConditionalHandleCreate(&h_if, graph, 0, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams wp = {};
+      wp.type = cudaGraphNodeTypeConditional;
+      wp.conditional.handle = h_while;
+      wp.conditional.type = cudaGraphCondTypeWhile;
+      wp.conditional.size = 1;
+      cudaGraphNode_t wnode;
+      PVI_CUDA(cudaGraphAddNode(&wnode, graph, nullptr, 0, &wp));
+      cudaGraph_t body = wp.conditional.phGraph_out[0];
+      auto sweep_args = [&](int from, int to) {
+        SweepArgs<T> a;
+        a.v = ring[from]->as<T>();
+        a.vout = ring[to]->as<T>();
+        a.lo = 0;
+        a.hi = n;
+        a.gamma = gamma;
+        a.algorithm = algo;
+        a.fa.test = h.test;
+        a.fa.gamma = gamma;
+        a.fa.stats = dstats.as<SweepStats>();
+        return a;
+      };
+      cudaStream_t cs = stream.s;
+      // body: sweep b -> a, decide (sets WHILE and IF), IF { sweep a -> b, decide }
+      PVI_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+      launch_sweep<T>(m, dm, sweep_args(b_slot, a_slot), scratch, cs);
+      k_loop_decide<<<1, 1, 0, cs>>>(dls.as<LoopState>(), dstats.as<SweepStats>(), h_while, h_if, 1);
+      PVI_CUDA(cudaGetLastError());
+      {
+        cudaStreamCaptureStatus cst;
+        const cudaGraphNode_t* deps = nullptr;
+        std::size_t ndeps = 0;
+        cudaGraph_t cap = nullptr;
+        PVI_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cap, &deps, &ndeps));
+        cudaGraphNodeParams ip = {};
+        ip.type = cudaGraphNodeTypeConditional;
+        ip.conditional.handle = h_if;
+        ip.conditional.type = cudaGraphCondTypeIf;
+        ip.conditional.size = 1;
+        cudaGraphNode_t inode;
+        PVI_CUDA(cudaGraphAddNode(&inode, cap, deps, ndeps, &ip));
+        PVI_CUDA(cudaStreamUpdateCaptureDependencies(cs, &inode, 1, cudaStreamSetCaptureDependencies));
+        cudaGraph_t tmp = nullptr;
+        PVI_CUDA(cudaStreamEndCapture(cs, &tmp));
+        cudaGraph_t ibody = ip.conditional.phGraph_out[0];
+        PVI_CUDA(cudaStreamBeginCaptureToGraph(cs, ibody, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        launch_sweep<T>(m, dm, sweep_args(a_slot, b_slot), scratch, cs);
+        k_loop_decide<<<1, 1, 0, cs>>>(dls.as<LoopState>(), dstats.as<SweepStats>(), h_while, h_if, 0);
+        PVI_CUDA(cudaGetLastError());
+        PVI_CUDA(cudaStreamEndCapture(cs, &tmp));
+      }
+      cudaGraphExec_t exec = nullptr;
+      const auto tr1 = std::chrono::steady_clock::now();
+      PVI_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      const auto tr2 = std::chrono::steady_clock::now();
+      PVI_CUDA(cudaEventRecord(ev0, cs));
+      PVI_CUDA(cudaGraphLaunch(exec, cs));
+      PVI_CUDA(cudaEventRecord(ev1, cs));
+      PVI_CUDA(cudaMemcpyAsync(&h, dls.p, sizeof(h), cudaMemcpyDeviceToHost, cs));
+      PVI_CUDA(cudaStreamSynchronize(cs));
+      const auto tr3 = std::chrono::steady_clock::now();
+      cudaGraphExecDestroy(exec);
+      cudaGraphDestroy(graph);
+      if (loop_trace())
+        std::fprintf(stderr, "[pvi loop] capture %.3f ms, instantiate %.3f ms, launch+sync %.3f ms, destroy %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(tr1 - tr0).count(),
+                     std::chrono::duration<double, std::milli>(tr2 - tr1).count(),
+                     std::chrono::duration<double, std::milli>(tr3 - tr2).count(),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr3).count());
+      float ms = 0.f;
+      PVI_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+      sweep_ms += ms;
+      graph_sweeps = h.iteration - iteration;
+      sweeps += graph_sweeps;
+      iteration = h.iteration;
+      if (graph_sweeps % 2 == 1) {  // newest is slot a
+        order.clear();
+        order.push_back(b_slot);
+        order.push_back(a_slot);
+      }
+      if (h.first_bad != ~0ull)
+        fail(PVI_ERR_DIVERGENCE, "non-finite value for state " + std::to_string(h.first_bad) +
+                                     " at iteration " + std::to_string(h.bad_iteration), h.bad_iteration);
+      if (h.test >= 0) {
+        last_hi = h.last_hi;
+        last_lo = h.last_lo;
+      }
+      converged = h.converged != 0;
       break;
     }
     ++iteration;
@@ -571,9 +843,10 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
     if (converged) break;
   }
 
+  const auto t_loop_end = std::chrono::steady_clock::now();
   // Policy extraction (vi.hpp:267-280): one more argmax sweep.
   const T* vfinal = ring[order.back()]->as<T>();
-  DevBuf policy(n * sizeof(std::uint32_t));
+  PoolBuf policy(n * sizeof(std::uint32_t), stream.s);
   {
     SweepArgs<T> a;
     a.v = vfinal;
@@ -593,7 +866,7 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
   }
   if (writer) writer->finish();  // every checkpoint on disk before returning
   if (out_values) {
-    DevBuf w(n * sizeof(double));
+    PoolBuf w(n * sizeof(double), stream.s);
     launch_widen<T>(vfinal, w.as<double>(), n, stream.s);
     PVI_CUDA(cudaMemcpyAsync(out_values, w.p, n * 8, cudaMemcpyDeviceToHost, stream.s));
     PVI_CUDA(cudaStreamSynchronize(stream.s));
@@ -604,6 +877,11 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
   }
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
+  if (loop_trace())
+    std::fprintf(stderr, "[pvi loop] setup %.3f ms, loop %.3f ms, extraction+copies %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(t_loop_start - t_start).count(),
+                 std::chrono::duration<double, std::milli>(t_loop_end - t_loop_start).count(),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_loop_end).count());
   if (stats) {
     stats->iterations = iteration;
     stats->converged = converged ? 1 : 0;
@@ -614,6 +892,9 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
     stats->span_lo = last_lo;
     stats->span_hi = last_hi;
     stats->terms_per_sweep = m.terms_per_sweep();
+    stats->graph_sweeps = graph_sweeps;
+    stats->l2_window_bytes = l2_bytes;
+    stats->l2_hit_ratio = l2_ratio;
   }
 }
 

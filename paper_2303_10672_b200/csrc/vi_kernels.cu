@@ -2831,6 +2831,11 @@ void count_launches(int n) {
 }
 }  // namespace
 
+bool profiling_enabled() {
+  std::lock_guard<std::mutex> lock(g_prof.mu);
+  return g_prof.on;
+}
+
 void profile_enable(bool on) {
   std::lock_guard<std::mutex> lock(g_prof.mu);
   for (auto& e : g_prof.events) {

@@ -77,6 +77,7 @@ void launch_stats(const T* vnew, const T* vprev, std::uint64_t n, const Finalize
                   cudaStream_t stream);
 bool b_sweep_honours_xb_range(const Model& model, int device);
 void profile_enable(bool on);
+bool profiling_enabled();
 void profile_read(double* ms, std::uint64_t* main_launches, std::uint64_t* all_launches);
 void launch_initial_b(const DevModel& dm, double* out, std::uint64_t n, cudaStream_t stream);
 template <typename T>

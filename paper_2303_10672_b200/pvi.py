@@ -351,6 +351,8 @@ class ViConfig:
     max_states: int = 200_000_000
     device: int = -1
     algorithm: Optional[str] = None  # None: the model's (Model.set_algorithm)
+    loop: str = "auto"               # "auto" | "host" | "graph" (pvi_vi_config::loop)
+    l2_persist: Optional[bool] = None  # None: auto (on)
 
     def to_c(self) -> L.ViConfigC:
         c = L.ViConfigC()
@@ -369,6 +371,8 @@ class ViConfig:
         c.max_states = self.max_states
         c.device = self.device
         c.algorithm = -1 if self.algorithm is None else _ALGOS[self.algorithm]
+        c.loop = {"auto": -1, "host": 0, "graph": 1}[self.loop]
+        c.l2_persist = -1 if self.l2_persist is None else int(bool(self.l2_persist))
         return c
 
 
@@ -392,6 +396,9 @@ class ViResult:
     span_hi: float = 0.0
     terms_per_sweep: float = 0.0
     fingerprint: bytes = b""
+    graph_sweeps: int = 0        # sweeps inside the graph-resident loop
+    l2_window_bytes: int = 0     # persisting L2 access-policy window
+    l2_hit_ratio: float = 0.0
 
 
 def run_value_iteration(model: Model, config: Optional[ViConfig] = None,
@@ -424,7 +431,8 @@ def run_value_iteration(model: Model, config: Optional[ViConfig] = None,
     _raise(rc, err, ev.value)
     return ViResult(values, policy, int(st.iterations), bool(st.converged), st.wall_seconds,
                     st.sweep_seconds, int(st.sweeps), st.span_lo, st.span_hi,
-                    st.terms_per_sweep, model.fingerprint())
+                    st.terms_per_sweep, model.fingerprint(), int(st.graph_sweeps),
+                    int(st.l2_window_bytes), float(st.l2_hit_ratio))
 
 
 def _dtype(precision: str):
