@@ -19,6 +19,7 @@
 #include <mutex>
 #include <utility>
 #include <vector>
+#include <type_traits>
 
 #include "common.cuh"
 #include "vi_kernels.cuh"
@@ -1103,34 +1104,16 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_q(DevModel dm, const double* 
 // Stage 1, register-blocked the same way as k_b_fact_q16 (order_b radix 16):
 // the 16 x_b states of a group (same x_2..x_M, x_1 = 0..15) walk the same
 // aged-B-profile path, so each slab element read feeds 8 states' FMAs.
-template <typename T, int M>
-__global__ void __launch_bounds__(256, 2) k_b_fact_w16(DevModel dm, const T* __restrict__ V,
-                                                       double* __restrict__ W,
-                                                       double* __restrict__ v0t,
-                                                       const std::uint16_t* __restrict__ group_order,
-                                                       int n_groups, int n_xb, int n_bp, int n_r,
-                                                       int x3_lo, int x3_hi, int tiled, int r_base) {
+// Stage-1 work of one r (the r-slab of V staged in shared memory as
+// [bp][ob]), shared by k_b_fact_w16 and the persistent k_b_fact_w16p.
+template <int M>
+__device__ __forceinline__ void w16_row(const double* __restrict__ slab, double* __restrict__ W,
+                                        double* __restrict__ v0t,
+                                        const std::uint16_t* __restrict__ group_order,
+                                        int n_groups, int n_r, int r, int tiled,
+                                        const double* s_pmf_b, const double* s_cdf_b) {
   constexpr int NB = 16, S8 = 8, OB4 = 4;
-  extern __shared__ double slab[];  // [bp][ob]
   const int stride = slab_stride(NB);
-  const int r = r_base + static_cast<int>(blockIdx.x);
-  if (M == 3) {
-    // a state shard only reads the W rows of its own x_3 digits and the
-    // R(0, j) rows of the diagonal constants (k_b_fact_qw3)
-    const int na = dm.b_na, ap = r % (na * na), x2r = ap % na, x3r = ap / na;
-    if ((x3r < x3_lo || x3r > x3_hi) && !(x2r == 0 && x3r <= x3_hi)) return;
-  }
-  const std::uint64_t base = static_cast<std::uint64_t>(r) * n_xb;
-  for (int i = threadIdx.x; i < NB * n_bp; i += blockDim.x) {
-    const int ob = i / n_bp, bp = i % n_bp;
-    slab[slab_row(bp) * stride + ob] = static_cast<double>(V[base + static_cast<std::uint64_t>(ob) * n_bp + bp]);
-  }
-  __shared__ double s_pmf_b[64], s_cdf_b[64];
-  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
-    s_pmf_b[i] = i < dm.b_len_b ? dm.b_pmf_b[i] : 0.0;
-    s_cdf_b[i] = i < dm.b_len_b ? dm.b_cdf_b[i] : 0.0;
-  }
-  __syncthreads();
   if (threadIdx.x < NB) v0t[static_cast<std::size_t>(r) * NB + threadIdx.x] = slab[threadIdx.x];
   const int sub = threadIdx.x & 7;
   const int x1b = (sub >> 2) * S8;
@@ -1205,10 +1188,105 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16(DevModel dm, const T* __r
         // one 2 KB run per r (k_b_fact_qw3 reads it); else [x_b][r][o_b]
         double* out = tiled ? W + ((static_cast<std::size_t>(grp) * n_r + r) * NB + x1b + i) * NB + ob0
                             : W + (static_cast<std::size_t>(xbi) * n_r + r) * NB + ob0;
-#pragma unroll
-        for (int k = 0; k < OB4; ++k) out[k] = acc[i][k];
+        // one 32-byte store per lane (4 lanes write a 128-byte row)
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(out), "d"(acc[i][0]), "d"(acc[i][1]),
+                     "d"(acc[i][2]), "d"(acc[i][3])
+                     : "memory");
       }
     }
+  }
+}
+
+template <typename T, int M>
+__global__ void __launch_bounds__(256, 2) k_b_fact_w16(DevModel dm, const T* __restrict__ V,
+                                                       double* __restrict__ W,
+                                                       double* __restrict__ v0t,
+                                                       const std::uint16_t* __restrict__ group_order,
+                                                       int n_groups, int n_xb, int n_bp, int n_r,
+                                                       int x3_lo, int x3_hi, int tiled, int r_base) {
+  constexpr int NB = 16, S8 = 8, OB4 = 4;
+  extern __shared__ double slab[];  // [bp][ob]
+  const int stride = slab_stride(NB);
+  const int r = r_base + static_cast<int>(blockIdx.x);
+  if (M == 3) {
+    // a state shard only reads the W rows of its own x_3 digits and the
+    // R(0, j) rows of the diagonal constants (k_b_fact_qw3)
+    const int na = dm.b_na, ap = r % (na * na), x2r = ap % na, x3r = ap / na;
+    if ((x3r < x3_lo || x3r > x3_hi) && !(x2r == 0 && x3r <= x3_hi)) return;
+  }
+  const std::uint64_t base = static_cast<std::uint64_t>(r) * n_xb;
+  for (int i = threadIdx.x; i < NB * n_bp; i += blockDim.x) {
+    const int ob = i / n_bp, bp = i % n_bp;
+    slab[slab_row(bp) * stride + ob] = static_cast<double>(V[base + static_cast<std::uint64_t>(ob) * n_bp + bp]);
+  }
+  __shared__ double s_pmf_b[64], s_cdf_b[64];
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+    s_pmf_b[i] = i < dm.b_len_b ? dm.b_pmf_b[i] : 0.0;
+    s_cdf_b[i] = i < dm.b_len_b ? dm.b_cdf_b[i] : 0.0;
+  }
+  __syncthreads();
+  w16_row<M>(slab, W, v0t, group_order, n_groups, n_r, r, tiled, s_pmf_b, s_cdf_b);
+}
+
+// Persistent stage 1 (f64 V): one CTA per SM pair slot walks the r rows
+// with a stride of gridDim.x, the next row's V slab landing by cp.async
+// (8-byte copies into the transposed [bp][ob] layout) while this row is
+// computed, so the slab load latency and the W write stream overlap the
+// FMAs instead of alternating with them.
+template <int M>
+__global__ void __launch_bounds__(256, 2) k_b_fact_w16p(DevModel dm, const double* __restrict__ V,
+                                                        double* __restrict__ W,
+                                                        double* __restrict__ v0t,
+                                                        const std::uint16_t* __restrict__ group_order,
+                                                        int n_groups, int n_xb, int n_bp, int n_r,
+                                                        int x3_lo, int x3_hi, int tiled, int r_base,
+                                                        int r_count) {
+  constexpr int NB = 16;
+  extern __shared__ double slabs[];  // 2 x [bp][ob]
+  const int stride = slab_stride(NB);
+  const int slab_sz = slab_rows(n_bp) * stride;
+  __shared__ double s_pmf_b[64], s_cdf_b[64];
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+    s_pmf_b[i] = i < dm.b_len_b ? dm.b_pmf_b[i] : 0.0;
+    s_cdf_b[i] = i < dm.b_len_b ? dm.b_cdf_b[i] : 0.0;
+  }
+  const int na = dm.b_na;
+  // rows a state shard never reads are skipped (see k_b_fact_w16)
+  auto wanted = [&](int r) {
+    if (M != 3) return true;
+    const int ap = r % (na * na), x2r = ap % na, x3r = ap / na;
+    return !((x3r < x3_lo || x3r > x3_hi) && !(x2r == 0 && x3r <= x3_hi));
+  };
+  auto next_row = [&](int t) {
+    while (t < r_count && !wanted(r_base + t)) t += gridDim.x;
+    return t;
+  };
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(slabs));
+  auto stage = [&](int t, int buf) {
+    const std::uint64_t base = static_cast<std::uint64_t>(r_base + t) * n_xb;
+    const unsigned dst = sbase + static_cast<unsigned>(buf * slab_sz) * 8u;
+    for (int i = threadIdx.x; i < NB * n_bp; i += blockDim.x) {
+      const int ob = i / n_bp, bp = i % n_bp;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * (slab_row(bp) * stride + ob)),
+                   "l"(V + base + static_cast<std::uint64_t>(ob) * n_bp + bp));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  int t = next_row(static_cast<int>(blockIdx.x));
+  if (t < r_count) stage(t, 0);
+  for (int buf = 0; t < r_count; buf ^= 1) {
+    const int tn = next_row(t + gridDim.x);
+    if (tn < r_count) {
+      stage(tn, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
+    __syncthreads();
+    w16_row<M>(slabs + buf * slab_sz, W, v0t, group_order, n_groups, n_r, r_base + t, tiled, s_pmf_b,
+               s_cdf_b);
+    __syncthreads();  // the slab is refilled two rows later
+    t = tn;
   }
 }
 
@@ -2937,6 +3015,24 @@ static int qw4_mode() {
   return mode;
 }
 
+static bool w16p_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PVI_B_W16P");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static int num_sms() {
+  static const int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
 static bool a_group_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PVI_A_GROUP");
@@ -3078,11 +3174,23 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     if (nb == 16 && q16_enabled()) {                                                               \
       const std::size_t sm0 = sizeof(double) * slab_rows(static_cast<int>(n_bp)) * slab_stride(16); \
       cudaFuncSetAttribute(k_b_fact_w16<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-      if ((a.stages & 1) && r1 > r0)                                                              \
-        k_b_fact_w16<T, MM><<<static_cast<unsigned>(r1 - r0), 256, sm0, stream>>>(                 \
-            dm, a.v, W, v0t, dc.b_group_order_b, static_cast<int>(n_bp), static_cast<int>(n_xb),    \
-            static_cast<int>(n_bp), static_cast<int>(n_r), x3_lo, x3_hi, qw && MM == 3 ? 1 : 0,     \
-            static_cast<int>(r0));                                                                 \
+      if ((a.stages & 1) && r1 > r0) {                                                            \
+        if (std::is_same<T, double>::value && w16p_enabled()) {                                    \
+          auto kp = k_b_fact_w16p<MM>;                                                             \
+          cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sm0);          \
+          const unsigned g = static_cast<unsigned>(std::min<std::uint64_t>(r1 - r0, 2 * num_sms())); \
+          kp<<<g, 256, 2 * sm0, stream>>>(                                                         \
+              dm, reinterpret_cast<const double*>(a.v), W, v0t, dc.b_group_order_b,                \
+              static_cast<int>(n_bp), static_cast<int>(n_xb), static_cast<int>(n_bp),               \
+              static_cast<int>(n_r), x3_lo, x3_hi, qw && MM == 3 ? 1 : 0, static_cast<int>(r0),     \
+              static_cast<int>(r1 - r0));                                                          \
+        } else {                                                                                   \
+          k_b_fact_w16<T, MM><<<static_cast<unsigned>(r1 - r0), 256, sm0, stream>>>(               \
+              dm, a.v, W, v0t, dc.b_group_order_b, static_cast<int>(n_bp), static_cast<int>(n_xb),  \
+              static_cast<int>(n_bp), static_cast<int>(n_r), x3_lo, x3_hi, qw && MM == 3 ? 1 : 0,   \
+              static_cast<int>(r0));                                                               \
+        }                                                                                          \
+      }                                                                                            \
     } else if (a.stages & 1) {                                                                     \
       if (r0 != 0 || r1 != static_cast<std::uint64_t>(n_r))                                        \
         fail(PVI_ERR_PARAMETER, "factored b: partial stage-1 ranges need the radix-16 kernel");    \
