@@ -852,16 +852,16 @@ __global__ void __launch_bounds__(128) k_a_fact_fifo(DevModel dm, const T* __res
 // and V[o_a, ., ., 0] in shared memory.  A sweep is ~1.5e11 FMAs instead of the
 // reference's 2.4e12 terms x 5 operations.
 
-__global__ void __launch_bounds__(256) k_b_erpt(DevModel dm, double* __restrict__ erpt,
-                                                std::uint64_t n) {
-  const std::uint64_t s = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  const int m = dm.b_m;
-  int st[kMaxDigits];
-  decode(dm, s, st);
-  int ia = 0, ib = 0;
-  for (int i = 0; i < m; ++i) ia += st[i];
-  for (int i = m; i < 2 * m; ++i) ib += st[i];
+// The issued-pair law depends on the state only through the two stock
+// totals (issued_probability, scenario_b.cpp:168-176), so the expected
+// one-step revenue (initial_value, scenario_b.cpp:178-192) and the law's
+// mass are tables over (I_a, I_b): (M(A_a)+1) x (M(A_b)+1) entries, each
+// summed in the reference's (h_a, h_b) order, then expanded per state.
+__global__ void __launch_bounds__(128) k_b_pair_table(DevModel dm, double* __restrict__ tab, int ima,
+                                                      int imb) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (ima + 1) * (imb + 1)) return;
+  const int ia = idx / (imb + 1), ib = idx % (imb + 1);
   const int dn = dm.b_dn;
   double er = 0.0, pt = 0.0;
   for (int ha = 0; ha <= ia; ++ha)
@@ -874,12 +874,31 @@ __global__ void __launch_bounds__(256) k_b_erpt(DevModel dm, double* __restrict_
       er += p * (dm.b_cra * ha + dm.b_crb * hb);
       pt += p;
     }
+  tab[2 * idx] = er;
+  tab[2 * idx + 1] = pt;
+}
+
+__device__ __forceinline__ int b_pair_index(const DevModel& dm, std::uint64_t s, int imb) {
+  const int m = dm.b_m;
+  int st[kMaxDigits];
+  decode(dm, s, st);
+  int ia = 0, ib = 0;
+  for (int i = 0; i < m; ++i) ia += st[i];
+  for (int i = m; i < 2 * m; ++i) ib += st[i];
+  return ia * (imb + 1) + ib;
+}
+
+__global__ void __launch_bounds__(256) k_b_erpt(DevModel dm, const double* __restrict__ tab,
+                                                double* __restrict__ erpt, std::uint64_t n, int imb) {
+  const std::uint64_t s = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int k = b_pair_index(dm, s, imb);
   // layout [x_b][x_a][2]: a stage-2 CTA (fixed x_b) reads its states contiguously
   std::uint64_t n_xb = 1;
-  for (int i = 0; i < m; ++i) n_xb *= static_cast<std::uint64_t>(dm.b_nb);
+  for (int i = 0; i < dm.b_m; ++i) n_xb *= static_cast<std::uint64_t>(dm.b_nb);
   const std::uint64_t e = ((s % n_xb) * (n / n_xb) + s / n_xb) * 2;
-  erpt[e] = er;
-  erpt[e + 1] = pt;
+  erpt[e] = tab[2 * k];
+  erpt[e + 1] = tab[2 * k + 1];
 }
 
 // Shared-memory [row][o_b] slabs: odd row stride, and row r stored at
@@ -2824,28 +2843,11 @@ __global__ void __launch_bounds__(256) k_stats(const T* __restrict__ vnew, const
 
 // ---------------------------------------------------------------------------
 // K4: ScenarioB::initial_value (scenario_b.cpp:178-192), one thread per state.
-__global__ void __launch_bounds__(256) k_initial_b(DevModel dm, double* __restrict__ out,
-                                                   std::uint64_t n) {
+__global__ void __launch_bounds__(256) k_initial_b(DevModel dm, const double* __restrict__ tab,
+                                                   double* __restrict__ out, std::uint64_t n, int imb) {
   const std::uint64_t s = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= n) return;
-  const int m = dm.b_m;
-  int st[kMaxDigits];
-  decode(dm, s, st);
-  int ia = 0, ib = 0;
-  for (int i = 0; i < m; ++i) ia += st[i];
-  for (int i = m; i < 2 * m; ++i) ib += st[i];
-  const int dn = dm.b_dn;
-  double expected = 0.0;
-  for (int ha = 0; ha <= ia; ++ha)
-    for (int hb = 0; hb <= ib; ++hb) {
-      double p;
-      if (ha < ia)
-        p = hb < ib ? dm.b_pmf_a[ha] * dm.b_pmf_b[hb] : dm.b_pz[ib * dn + ha] * dm.b_sf_b[ib];
-      else
-        p = hb < ib ? dm.b_sf_a[ia] * dm.b_pmf_b[hb] : (1.0 - dm.b_pz_cum[ib * dn + ia]) * dm.b_sf_b[ib];
-      expected += p * (dm.b_cra * ha + dm.b_crb * hb);
-    }
-  out[s] = expected;
+  out[s] = tab[2 * b_pair_index(dm, s, imb)];
 }
 
 template <typename T>
@@ -3083,7 +3085,15 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
       void* p = nullptr;
       PVI_CUDA(cudaMalloc(&p, 2 * dm.n_states * sizeof(double)));
       dc.allocations.push_back(p);
-      k_b_erpt<<<grid_for(dm.n_states, 256), 256, 0, stream>>>(dm, static_cast<double*>(p), dm.n_states);
+      {
+        const int ima = M * (na - 1), imb = M * (nb - 1);
+        const int np = (ima + 1) * (imb + 1);
+        double* tab = nullptr;
+        PVI_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tab), 2 * np * sizeof(double), stream));
+        k_b_pair_table<<<(np + 127) / 128, 128, 0, stream>>>(dm, tab, ima, imb);
+        k_b_erpt<<<grid_for(dm.n_states, 256), 256, 0, stream>>>(dm, tab, static_cast<double*>(p), dm.n_states, imb);
+        PVI_CUDA(cudaFreeAsync(tab, stream));
+      }
       PVI_CUDA(cudaGetLastError());
       const auto oa_h = digit_sum_order(na, M), ob_h = digit_sum_order(nb, M);
       void* q1 = nullptr;
@@ -3607,7 +3617,13 @@ void launch_stats(const T* vnew, const T* vprev, std::uint64_t n, const Finalize
 }
 
 void launch_initial_b(const DevModel& dm, double* out, std::uint64_t n, cudaStream_t stream) {
-  k_initial_b<<<grid_for(n, 256), 256, 0, stream>>>(dm, out, n);
+  const int ima = dm.b_m * (dm.b_na - 1), imb = dm.b_m * (dm.b_nb - 1);
+  const int np = (ima + 1) * (imb + 1);
+  double* tab = nullptr;
+  PVI_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tab), 2 * np * sizeof(double), stream));
+  k_b_pair_table<<<(np + 127) / 128, 128, 0, stream>>>(dm, tab, ima, imb);
+  k_initial_b<<<grid_for(n, 256), 256, 0, stream>>>(dm, tab, out, n, imb);
+  PVI_CUDA(cudaFreeAsync(tab, stream));
   PVI_CUDA(cudaGetLastError());
 }
 
