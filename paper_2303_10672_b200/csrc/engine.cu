@@ -18,6 +18,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "engine.hpp"
@@ -51,16 +52,27 @@ struct Workspace {
   Scratch io;       // 0: V, 1: V' slice, 2: argmax slice, 3: Q rows
   cudaStream_t stream = nullptr;
   cudaStream_t copy = nullptr;  // device-to-host results of finished chunks
+  cudaStream_t up = nullptr;    // host-to-device pieces (the other PCIe direction)
+  cudaStream_t s2[2] = {};      // stage 2 of consecutive x_3 pairs, overlapping
   cudaEvent_t done[kChunkEvents] = {};
+  cudaEvent_t ev[3 * kChunkEvents] = {};
   Workspace() {
     PVI_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     PVI_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    PVI_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    for (auto& x : s2) PVI_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
     for (auto& e : done) PVI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : ev) PVI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   ~Workspace() {
     for (auto& e : done)
       if (e) cudaEventDestroy(e);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& x : s2)
+      if (x) cudaStreamDestroy(x);
     if (copy) cudaStreamDestroy(copy);
+    if (up) cudaStreamDestroy(up);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -915,6 +927,16 @@ void vi_solve(const Model& m, const pvi_vi_config& cfg, const double* resume_val
 
 namespace {
 
+// PVI_E2E_PAIRS=0: the host-buffer factored B backup uploads V in
+// contiguous quarters instead of x_3-pair blocks
+bool e2e_pairs() {
+  static const bool on = [] {
+    const char* e = std::getenv("PVI_E2E_PAIRS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int backup_chunks() {
   static const int v = [] {
     const char* e = std::getenv("PVI_BACKUP_CHUNKS");
@@ -956,6 +978,90 @@ void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t
   a.gamma = gamma;
   a.algorithm = m.algorithm;
   a.want_values = out_values || out_actions;
+  if (b_pipe && lo == 0 && hi == n && std::is_same<T, double>::value && e2e_pairs() &&
+      b_sweep_honours_xb_range(m, device) && m.b_na % 2 == 0 && m.b_na / 2 <= Workspace::kChunkEvents / 2) {
+    // Pipelined by x_3 pairs.  Stage 2 of the states with top A digit
+    // x_3 in {2p, 2p+1} reads the W rows r = (o_a, x_3, x_2) of that pair
+    // (and the constants' rows of lower x_3, done by earlier pairs); stage 1
+    // builds row r from the V slab r, i.e. the states whose two LOW A digits
+    // are (x_3, x_2).  So piece p of V is the 2-D block {top digit t,
+    // low digits in pair p}: 16 runs of 32 slabs.  Upload piece p (up
+    // stream) -> stage 1 rows of pair p -> stage 2 of pair p -> its V' and
+    // argmax (one contiguous range) back on the copy stream, while the next
+    // piece uploads and the next pair computes: both PCIe directions and the
+    // SMs stay busy.
+    const int na = m.b_na, pairs = na / 2;
+    const std::uint64_t n_xb = static_cast<std::uint64_t>(m.b_nb) * m.b_nb * m.b_nb;
+    const std::uint64_t slab_run = 2ull * na * n_xb;                 // states per (t, pair) run
+    const std::uint64_t pitch = static_cast<std::uint64_t>(na) * na * n_xb;  // states per top digit
+    const std::uint64_t per_pair = 2 * pitch;                         // output states per pair
+    // PVI_LOOP_TRACE=1: timestamps of every piece (timing events, trace only)
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t sm) {
+      if (!loop_trace()) return;
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, sm);
+      tev.push_back(e);
+    };
+    mark(st);
+    for (int p = 0; p < pairs; ++p) {
+      const std::uint64_t off = static_cast<std::uint64_t>(p) * slab_run;
+      PVI_CUDA(cudaMemcpy2DAsync(v + off, pitch * sizeof(T), static_cast<const T*>(values) + off,
+                                 pitch * sizeof(T), slab_run * sizeof(T), na, cudaMemcpyHostToDevice, ws.up));
+      PVI_CUDA(cudaEventRecord(ws.done[Workspace::kChunkEvents / 2 + p], ws.up));
+      mark(ws.up);
+    }
+    // stage 1 pieces in order on `st`; stage 2 of pair p on s2[p % 2] once
+    // stage 1 of pieces <= p is done (it also reads the constants' rows of
+    // lower pairs), so consecutive pairs' stage-2 grids fill each other's tail
+    for (int p = 0; p < pairs; ++p) {
+      PVI_CUDA(cudaStreamWaitEvent(st, ws.done[Workspace::kChunkEvents / 2 + p], 0));
+      a.stages = 1;
+      a.lo = 0;
+      a.hi = n;
+      a.x3_rows_lo = 2 * p;
+      a.x3_rows_hi = 2 * p + 1;
+      launch_sweep<T>(m, dm, a, ws.scratch, st);
+      PVI_CUDA(cudaEventRecord(ws.ev[p], st));
+      mark(st);
+    }
+    for (int p = 0; p < pairs; ++p) {
+      cudaStream_t cs = ws.s2[p % 2];
+      PVI_CUDA(cudaStreamWaitEvent(cs, ws.ev[p], 0));
+      a.stages = 2;
+      a.x3_rows_lo = a.x3_rows_hi = -1;
+      a.lo = p * per_pair;
+      a.hi = (p + 1) * per_pair;
+      launch_sweep<T>(m, dm, a, ws.scratch, cs);
+      mark(cs);
+      PVI_CUDA(cudaEventRecord(ws.done[p], cs));
+      PVI_CUDA(cudaStreamWaitEvent(ws.copy, ws.done[p], 0));
+      if (out_values)
+        PVI_CUDA(cudaMemcpyAsync(static_cast<T*>(out_values) + a.lo, vo + a.lo, per_pair * sizeof(T),
+                                 cudaMemcpyDeviceToHost, ws.copy));
+      if (out_actions)
+        PVI_CUDA(cudaMemcpyAsync(out_actions + a.lo, ao + a.lo, per_pair * 4, cudaMemcpyDeviceToHost, ws.copy));
+      mark(ws.copy);
+    }
+    PVI_CUDA(cudaStreamSynchronize(st));
+    for (auto x : ws.s2) PVI_CUDA(cudaStreamSynchronize(x));
+    PVI_CUDA(cudaStreamSynchronize(ws.copy));
+    PVI_CUDA(cudaStreamSynchronize(ws.up));
+    if (!tev.empty()) {
+      // order: t0, up[0..P), s1[0..P), then per pair: s2 done, d2h done
+      std::string line = "[pvi e2e] ms:";
+      for (std::size_t i = 1; i < tev.size(); ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, tev[0], tev[i]);
+        line += " " + std::to_string(ms).substr(0, 6);
+        cudaEventDestroy(tev[i]);
+      }
+      cudaEventDestroy(tev[0]);
+      std::fprintf(stderr, "%s\n", line.c_str());
+    }
+    return;
+  }
   if (b_pipe) {
     const std::uint64_t n_xb = static_cast<std::uint64_t>(m.b_nb) * m.b_nb * m.b_nb;
     const std::uint64_t n_r = n / n_xb;

@@ -1259,7 +1259,7 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16p(DevModel dm, const doubl
                                                         const std::uint16_t* __restrict__ group_order,
                                                         int n_groups, int n_xb, int n_bp, int n_r,
                                                         int x3_lo, int x3_hi, int tiled, int r_base,
-                                                        int r_count) {
+                                                        int r_count, int strict) {
   constexpr int NB = 16;
   extern __shared__ double slabs[];  // 2 x [bp][ob]
   const int stride = slab_stride(NB);
@@ -1274,6 +1274,7 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16p(DevModel dm, const doubl
   auto wanted = [&](int r) {
     if (M != 3) return true;
     const int ap = r % (na * na), x2r = ap % na, x3r = ap / na;
+    if (strict) return x3r >= x3_lo && x3r <= x3_hi;
     return !((x3r < x3_lo || x3r > x3_hi) && !(x2r == 0 && x3r <= x3_hi));
   };
   auto next_row = [&](int t) {
@@ -1888,12 +1889,12 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw3(DevModel dm, const double
                                                        T* __restrict__ vout,
                                                        std::uint32_t* __restrict__ act,
                                                        std::uint64_t out_off, FinalizeArgs fa,
-                                                       int xb_base) {
+                                                       int xb_base, int pr_base) {
   constexpr int NB = 16;
   extern __shared__ double sm[];
   const int na = dm.b_na, dn = dm.b_dn;
   const int n_xa = na * na * na;
-  const int pr = blockIdx.x, xbi = xb_base + static_cast<int>(blockIdx.y);
+  const int pr = pr_base + static_cast<int>(blockIdx.x), xbi = xb_base + static_cast<int>(blockIdx.y);
   const int x3_0 = 2 * pr, n_x3 = min(2, na - x3_0);   // this CTA's x_3 values
   const int n_f = min(x3_0 + n_x3 - 1, na - 1) + 1;    // R(0, j) rows, j = 0..n_f-1
   const int n_rows = n_x3 * na + n_f;
@@ -2060,12 +2061,12 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
                                                        T* __restrict__ vout,
                                                        std::uint32_t* __restrict__ act,
                                                        std::uint64_t out_off, FinalizeArgs fa,
-                                                       int xb_base) {
+                                                       int xb_base, int pr_base) {
   constexpr int NB = 16;
   extern __shared__ double sm[];
   const int na = dm.b_na, dn = dm.b_dn;
   const int n_xa = na * na * na;
-  const int pr = blockIdx.x, xbi = xb_base + static_cast<int>(blockIdx.y);
+  const int pr = pr_base + static_cast<int>(blockIdx.x), xbi = xb_base + static_cast<int>(blockIdx.y);
   const int x3_0 = 2 * pr, n_x3 = min(2, na - x3_0);  // this CTA's x_3 values
   const int n_rows = n_x3 * na;
   // main rows R(u, x_3) [n_x3*na][ob] of W and V0; DB: two buffers (the
@@ -3175,6 +3176,10 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     x3_lo = static_cast<int>(lo / per) / 2 * 2;
     x3_hi = std::min(na - 1, static_cast<int>((hi - 1) / per) / 2 * 2 + 1);
   }
+  // stage-1 row filter: the shard's rows (+ constants' rows), or exactly the
+  // caller's x_3 rows (pipelined host-buffer backup)
+  const bool s1_strict = a.x3_rows_lo >= 0 && qw && M == 3 && std::is_same<T, double>::value && w16p_enabled();
+  const int s1_x3_lo = s1_strict ? a.x3_rows_lo : x3_lo, s1_x3_hi = s1_strict ? a.x3_rows_hi : x3_hi;
   {
     MainKernelScope prof(stream);
 #define PVI_BF(MM, NBX)                                                                            \
@@ -3192,8 +3197,8 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
           kp<<<g, 256, 2 * sm0, stream>>>(                                                         \
               dm, reinterpret_cast<const double*>(a.v), W, v0t, dc.b_group_order_b,                \
               static_cast<int>(n_bp), static_cast<int>(n_xb), static_cast<int>(n_bp),               \
-              static_cast<int>(n_r), x3_lo, x3_hi, qw && MM == 3 ? 1 : 0, static_cast<int>(r0),     \
-              static_cast<int>(r1 - r0));                                                          \
+              static_cast<int>(n_r), s1_x3_lo, s1_x3_hi, qw && MM == 3 ? 1 : 0, static_cast<int>(r0), \
+              static_cast<int>(r1 - r0), s1_strict);                                               \
         } else {                                                                                   \
           k_b_fact_w16<T, MM><<<static_cast<unsigned>(r1 - r0), 256, sm0, stream>>>(               \
               dm, a.v, W, v0t, dc.b_group_order_b, static_cast<int>(n_bp), static_cast<int>(n_xb),  \
@@ -3222,11 +3227,15 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
         cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);         \
         const std::uint64_t xb0 = std::min<std::uint64_t>(a.xb_lo, n_xb);                          \
         const std::uint64_t xb1 = std::min<std::uint64_t>(a.xb_hi, n_xb);                          \
-        if (xb1 > xb0)                                                                             \
-          kq<<<dim3(static_cast<unsigned>((na + 1) / 2), static_cast<unsigned>(xb1 - xb0)), 32, smq, stream>>>( \
+        /* only the x_3 pairs holding states of [lo, hi) */                                       \
+        const std::uint64_t per_pr = 2ull * na * na * n_xb;                                       \
+        const std::uint64_t pr0 = lo / per_pr;                                                    \
+        const std::uint64_t pr1 = std::min<std::uint64_t>((hi + per_pr - 1) / per_pr, (na + 1) / 2); \
+        if (xb1 > xb0 && pr1 > pr0)                                                                \
+          kq<<<dim3(static_cast<unsigned>(pr1 - pr0), static_cast<unsigned>(xb1 - xb0)), 32, smq, stream>>>( \
               dm, W, v0t, dc.b_erpt, lo, hi, a.gamma, static_cast<int>(n_xb),                      \
               static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa,  \
-              static_cast<int>(xb0));                                                              \
+              static_cast<int>(xb0), static_cast<int>(pr0));                                       \
       } else if (fused && dc.b_pt_unit && qp_enabled()) {                                          \
         auto kq = a.act ? k_b_fact_qp3<T, true> : k_b_fact_qp3<T, false>;                          \
         const std::size_t smp = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(double) + 1);       \

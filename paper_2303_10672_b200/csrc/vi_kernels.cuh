@@ -39,6 +39,9 @@ struct SweepArgs {
   // factored B stage 2 (k_b_fact_qw3 only): the x_b columns [xb_lo, xb_hi)
   // to process; V' / argmax then land in a strided column block
   std::uint64_t xb_lo = 0, xb_hi = ~0ull;
+  // factored B stage 1 (m = 3, f64): when >= 0, only the W rows whose x_3
+  // digit lies in [x3_rows_lo, x3_rows_hi] (no constants' rows of lower x_3)
+  int x3_rows_lo = -1, x3_rows_hi = -1;
 };
 
 // Grow-only device scratch buffers, keyed by slot.

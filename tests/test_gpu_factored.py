@@ -213,3 +213,22 @@ def test_factored_a_full_sweep_close_to_exact(pvi, preset, prec):
         np.testing.assert_allclose(pvi.q_rows(fact, V, int(s), int(s) + 1, precision=prec),
                                    pvi.q_rows(exact, V, int(s), int(s) + 1, precision=prec),
                                    rtol=tol, atol=tol * 10)
+
+
+def test_factored_b_host_buffer_pipelines_agree(pvi):
+    """pvi_vi_backup with host buffers (the e2e leg): the first full-range
+    call runs the quarter-piece pipeline, later ones the x_3-pair pipeline
+    (V uploaded in 2-D blocks, stage 1 / stage 2 / copy-back per pair).
+    Both must equal the device-resident sweep bit for bit."""
+    m = pvi.make_preset("b/m3/exp1").set_algorithm("factored")
+    n = m.state_count()
+    V = np.random.default_rng(21).uniform(-8.0, 8.0, n)
+    v1, a1 = pvi.bellman_backup_batch(m, V, 0, n)
+    v2, a2 = pvi.bellman_backup_batch(m, V, 0, n)
+    np.testing.assert_array_equal(v1, v2)
+    np.testing.assert_array_equal(a1, a2)
+    # a sub-range call (no pipeline) agrees on its states
+    lo, hi = 5 * 4096 * 256 + 77, 9 * 4096 * 256 + 5
+    v3, a3 = pvi.bellman_backup_batch(m, V, lo, hi)
+    np.testing.assert_array_equal(v3, v2[lo:hi])
+    np.testing.assert_array_equal(a3, a2[lo:hi])
