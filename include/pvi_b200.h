@@ -262,6 +262,15 @@ int pvi_vi_sweep_device(const pvi_model* m, int precision, double gamma,
  * shards (bounds has parts+1 entries), aligned to the kernel's state tiles. */
 int pvi_partition(const pvi_model* m, int parts, uint64_t* bounds);
 
+/* The parts of V a sweep of shard [lo, hi) reads (with the model's current
+ * algorithm), as sorted disjoint state runs: runs[2i] .. runs[2i+1].  A
+ * multi-GPU driver only has to refresh these between sweeps: for the
+ * factored Scenario B sweep of an x_3-pair shard that is ~1/8 of V per pair
+ * plus the shard's own states; every other sweep reads all of V (one run).
+ * *count receives the number of runs; pass runs = NULL to query it. */
+int pvi_sweep_read_runs(const pvi_model* m, uint64_t lo, uint64_t hi, uint64_t* runs, size_t capacity,
+                        size_t* count);
+
 /* ---- simulation (sim.hpp:40-170, rng.hpp, policies.hpp) ----------------- */
 
 typedef struct {

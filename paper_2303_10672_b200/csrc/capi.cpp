@@ -7,6 +7,7 @@
 #include <string>
 
 #include "engine.hpp"
+#include "vi_kernels.cuh"
 #include "model.hpp"
 
 using namespace pvi_b200;
@@ -330,6 +331,23 @@ int pvi_vi_sweep_device(const pvi_model* m, int precision, double gamma, const v
 
 int pvi_partition(const pvi_model* m, int parts, uint64_t* bounds) {
   return guarded(nullptr, 0, nullptr, [&] { partition(M(m), parts, bounds); });
+}
+
+int pvi_sweep_read_runs(const pvi_model* m, uint64_t lo, uint64_t hi, uint64_t* runs, size_t capacity,
+                        size_t* count) {
+  return guarded(nullptr, 0, nullptr, [&] {
+    if (!m || !m->impl) fail(PVI_ERR_PARAMETER, "null model");
+    if (lo > hi || hi > M(m).space.count) fail(PVI_ERR_PARAMETER, "state range out of bounds");
+    const auto r = sweep_read_runs(M(m), lo, hi);
+    if (count) *count = r.size();
+    if (runs) {
+      if (capacity < r.size()) fail(PVI_ERR_PARAMETER, "sweep_read_runs: capacity too small");
+      for (std::size_t i = 0; i < r.size(); ++i) {
+        runs[2 * i] = r[i].first;
+        runs[2 * i + 1] = r[i].second;
+      }
+    }
+  });
 }
 
 void pvi_rollout_config_defaults(pvi_rollout_config* c) {

@@ -671,6 +671,30 @@ double Model::factored_fmas() const {
   return terms_per_sweep();
 }
 
+bool Model::b_law_unit() const {
+  std::call_once(b_law_once, [&] {
+    if (scenario != PVI_SCENARIO_B) return;
+    const int m = pb.useful_life, dnh = b_dmax + 1, ima = m * (b_na - 1), imb = m * (b_nb - 1);
+    double worst = 0.0;
+    for (int ia = 0; ia <= ima; ++ia)
+      for (int ibh = 0; ibh <= imb; ++ibh) {
+        double pt = 0.0;
+        for (int ha = 0; ha <= ia; ++ha)
+          for (int hb = 0; hb <= ibh; ++hb) {
+            double pr;
+            if (ha < ia)
+              pr = hb < ibh ? b_pmf_a[ha] * b_pmf_b[hb] : b_pz[ibh * dnh + ha] * b_sf_b[ibh];
+            else
+              pr = hb < ibh ? b_sf_a[ia] * b_pmf_b[hb] : (1.0 - b_pz_cum[ibh * dnh + ia]) * b_sf_b[ibh];
+            pt += pr;
+          }
+        worst = std::max(worst, std::fabs(pt - 1.0));
+      }
+    b_law_unit_v = worst <= 1e-12;
+  });
+  return b_law_unit_v;
+}
+
 double Model::state_cost(std::uint64_t s) const {
   if (scenario != PVI_SCENARIO_B) return 1.0;
   int st[kMaxDigits];

@@ -154,6 +154,8 @@ struct Model {
 
   mutable std::mutex dev_mutex;
   mutable std::map<int, std::unique_ptr<DeviceCopy>> dev;
+  mutable std::once_flag b_law_once;
+  mutable bool b_law_unit_v = false;
 
   ~Model();
   const DevModel& device_view(int device) const;  // uploads on first use
@@ -163,6 +165,8 @@ struct Model {
   double state_cost(std::uint64_t s) const;  // relative backup cost of one state
   std::uint64_t tile_states() const;         // partition alignment
   std::uint64_t chunk_align() const;         // 0: sweeps do not chunk (whole-space tables)
+  // B: every (I_a, I_b)'s issued-pair law sums to 1 within 1e-12 (host check, cached)
+  bool b_law_unit() const;
 };
 
 std::unique_ptr<Model> build_scenario_a(const pvi_scenario_a_params& p);

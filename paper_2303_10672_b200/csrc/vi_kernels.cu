@@ -3131,28 +3131,8 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
       };
       dc.b_group_order = group_order(na);
       dc.b_group_order_b = group_order(nb);
-      // PT depends on (I_a, I_b) only: check the law's mass on the host
-      {
-        const int dnh = model.b_dmax + 1, ima = M * (na - 1), imb = M * (nb - 1);
-        double worst = 0.0;
-        for (int ia = 0; ia <= ima; ++ia)
-          for (int ibh = 0; ibh <= imb; ++ibh) {
-            double pt = 0.0;
-            for (int ha = 0; ha <= ia; ++ha)
-              for (int hb = 0; hb <= ibh; ++hb) {
-                double pr;
-                if (ha < ia)
-                  pr = hb < ibh ? model.b_pmf_a[ha] * model.b_pmf_b[hb]
-                                : model.b_pz[ibh * dnh + ha] * model.b_sf_b[ibh];
-                else
-                  pr = hb < ibh ? model.b_sf_a[ia] * model.b_pmf_b[hb]
-                                : (1.0 - model.b_pz_cum[ibh * dnh + ia]) * model.b_sf_b[ibh];
-                pt += pr;
-              }
-            worst = std::max(worst, std::fabs(pt - 1.0));
-          }
-        dc.b_pt_unit = worst <= 1e-12;
-      }
+      // PT depends on (I_a, I_b) only: the law's mass is checked on the host
+      dc.b_pt_unit = model.b_law_unit();
       dc.b_erpt = static_cast<double*>(p);
     }
   }
@@ -3290,9 +3270,47 @@ bool b_sweep_honours_xb_range(const Model& model, int device) {
   if (model.scenario != PVI_SCENARIO_B || model.algorithm != PVI_ALGO_FACTORED) return false;
   if (model.pb.useful_life != 3 || model.b_nb != 16 || model.b_na > 16) return false;
   if (model.space.count >= (1ull << 31) || !qd_enabled() || !qw_enabled()) return false;
-  DeviceCopy& dc = model.device_copy(device);
-  std::lock_guard<std::mutex> lock(model.dev_mutex);
-  return dc.b_erpt != nullptr && dc.b_pt_unit;
+  (void)device;
+  return model.b_law_unit();
+}
+
+// State runs [a, b) of V that the sweep of shard [lo, hi) reads.  The
+// one-warp factored B stage 2 of x_3 pairs P reads only the W rows
+// r = (o_a, x_3, x_2) with x_3 in P, plus the constants' rows (x_2 = 0,
+// lower x_3), and stage-1 row r reads exactly the V slab r (|x_b| states);
+// the finalize reads the shard's own states.  Every other sweep gathers
+// from anywhere in V.
+std::vector<std::pair<std::uint64_t, std::uint64_t>> sweep_read_runs(const Model& model,
+                                                                     std::uint64_t lo,
+                                                                     std::uint64_t hi) {
+  const std::uint64_t n = model.space.count;
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> runs;
+  if (lo >= hi) return runs;
+  if (!b_sweep_honours_xb_range(model, 0)) {
+    runs.emplace_back(0, n);
+    return runs;
+  }
+  const int na = model.b_na;
+  const std::uint64_t n_xb = static_cast<std::uint64_t>(model.b_nb) * model.b_nb * model.b_nb;
+  const std::uint64_t per = static_cast<std::uint64_t>(na) * na * n_xb;  // states per x_3 digit
+  const int x3_lo = static_cast<int>(lo / per) / 2 * 2;
+  const int x3_hi = std::min(na - 1, static_cast<int>((hi - 1) / per) / 2 * 2 + 1);
+  const int n_r = na * na * na;
+  for (int r = 0; r < n_r; ++r) {
+    const int ap = r % (na * na), x2r = ap % na, x3r = ap / na;
+    if ((x3r >= x3_lo && x3r <= x3_hi) || (x2r == 0 && x3r <= x3_hi))
+      runs.emplace_back(static_cast<std::uint64_t>(r) * n_xb, static_cast<std::uint64_t>(r + 1) * n_xb);
+  }
+  runs.emplace_back(lo, hi);  // the shard's own states (convergence statistic)
+  std::sort(runs.begin(), runs.end());
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> out;
+  for (const auto& r : runs) {
+    if (!out.empty() && out.back().second >= r.first)
+      out.back().second = std::max(out.back().second, r.second);
+    else
+      out.push_back(r);
+  }
+  return out;
 }
 
 template <typename T>

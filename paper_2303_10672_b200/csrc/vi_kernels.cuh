@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -79,6 +80,8 @@ template <typename T>
 void launch_stats(const T* vnew, const T* vprev, std::uint64_t n, const FinalizeArgs& fa,
                   cudaStream_t stream);
 bool b_sweep_honours_xb_range(const Model& model, int device);
+std::vector<std::pair<std::uint64_t, std::uint64_t>> sweep_read_runs(const Model& model, std::uint64_t lo,
+                                                                     std::uint64_t hi);
 void profile_enable(bool on);
 bool profiling_enabled();
 void profile_read(double* ms, std::uint64_t* main_launches, std::uint64_t* all_launches);

@@ -280,6 +280,16 @@ class Model:
         _raise(L.load().pvi_partition(self._h, parts, _p(b)), None)
         return b
 
+    def sweep_read_runs(self, lo: int, hi: int) -> list:
+        """State runs [(a, b), ...] of V that a sweep of shard [lo, hi) reads
+        (pvi_sweep_read_runs): what a multi-GPU driver must refresh."""
+        cnt = C.c_size_t()
+        _raise(L.load().pvi_sweep_read_runs(self._h, lo, hi, None, 0, C.byref(cnt)), None)
+        buf = np.zeros(2 * cnt.value, np.uint64)
+        _raise(L.load().pvi_sweep_read_runs(self._h, lo, hi, buf.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                            cnt.value, C.byref(cnt)), None)
+        return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(cnt.value)]
+
 
 def _create(fn, params) -> C.c_void_p:
     h = C.c_void_p()

@@ -10,6 +10,17 @@ one 4-double MAX all-reduce.  Max and min are exact, so the convergence
 decision, the iteration count and the value vector are identical to the
 single-GPU run (and to the reference).
 
+Read-set exchange.  A sweep of shard [lo, hi) does not always read all of
+V: the factored Scenario B sweep of an x_3-pair shard reads ~1/8 of the
+value slabs plus its own states (pvi_sweep_read_runs).  Then the per-sweep
+refresh is not an all-gather of every slice but ONE uneven all-to-all
+(NCCL all_to_all_single over NVLink): rank q sends rank r exactly
+runs(r) ∩ [lo_q, hi_q), gathered by one index_select and scattered by one
+index_copy_ on each side (index tensors built once).  For b/m3/exp1 at 8
+ranks that is ~16 MiB received per rank per sweep instead of 112 MiB.
+The full replica is re-assembled (one all-gather) only where a caller needs
+all of V: checkpoints and the returned value vector.
+
 The per-slice sweep is injectable so the host logic (partition, exchange,
 reduction, history window, convergence) runs under `gloo` on CPU in tests;
 the default sweep is the device kernel through pvi_vi_sweep_device.
@@ -91,6 +102,48 @@ class ShardedValueIteration:
         self.hist_cap = 8 if self.test == P.PERIODIC_SPAN else 2
         self._send = torch.empty(self.maxlen, dtype=self.dtype, device=self.device)
         self._recv = torch.empty(self.maxlen * self.world, dtype=self.dtype, device=self.device)
+        self._setup_read_sets()
+
+    # -- read sets -----------------------------------------------------------
+    def _setup_read_sets(self):
+        """Index plan of the read-set all-to-all (or None: every rank reads
+        all of V, so the refresh is the all-gather)."""
+        self.plan = None
+        if self.world == 1:
+            return
+        runs = [self.model.sweep_read_runs(self.bounds[r], self.bounds[r + 1])
+                for r in range(self.world)]
+        if all(rr == [(0, self.n)] for rr in runs):
+            return
+
+        def clip(rr, a, b):
+            parts = [np.arange(max(x, a), min(y, b), dtype=np.int64) for x, y in rr
+                     if max(x, a) < min(y, b)]
+            return np.concatenate(parts) if parts else np.zeros(0, np.int64)
+
+        me = self.rank
+        send = [clip(runs[q], self.lo, self.hi) if q != me else np.zeros(0, np.int64)
+                for q in range(self.world)]
+        recv = [clip(runs[me], self.bounds[q], self.bounds[q + 1]) if q != me
+                else np.zeros(0, np.int64) for q in range(self.world)]
+        dev = self.device
+        self.plan = {
+            "send_idx": torch.from_numpy(np.concatenate(send)).to(dev),
+            "recv_idx": torch.from_numpy(np.concatenate(recv)).to(dev),
+            "send_splits": [len(x) for x in send],
+            "recv_splits": [len(x) for x in recv],
+            "runs": runs,
+        }
+        self.plan["recv_buf"] = torch.empty(len(self.plan["recv_idx"]), dtype=self.dtype, device=dev)
+
+    def read_set_bytes(self) -> int:
+        """Bytes this rank receives per sweep refresh."""
+        if self.world == 1:
+            return 0
+        item = torch.empty(0, dtype=self.dtype).element_size()
+        if self.plan is None:
+            return (self.n - (self.hi - self.lo)) * item
+        return sum(self.plan["recv_splits"]) * item
 
     # -- collectives ---------------------------------------------------------
     def exchange(self, v: torch.Tensor, send=None, recv=None):
@@ -107,6 +160,21 @@ class ShardedValueIteration:
             if r != self.rank and b > a:
                 v[a:b].copy_(recv[r * self.maxlen:r * self.maxlen + (b - a)])
 
+    def refresh(self, v: torch.Tensor):
+        """Make every entry the next sweep of this rank reads current: the
+        read-set all-to-all where the sweep reads part of V, else the
+        all-gather of the slices."""
+        if self.world == 1:
+            return
+        if self.plan is None:
+            self.exchange(v)
+            return
+        pl = self.plan
+        sendbuf = v.index_select(0, pl["send_idx"])
+        dist.all_to_all_single(pl["recv_buf"], sendbuf, pl["recv_splits"], pl["send_splits"],
+                               group=self.group)
+        v.index_copy_(0, pl["recv_idx"], pl["recv_buf"])
+
     def reduce_stats(self, stats: torch.Tensor):
         if self.world > 1:
             dist.all_reduce(stats, op=dist.ReduceOp.MAX, group=self.group)
@@ -119,7 +187,7 @@ class ShardedValueIteration:
         self.sweep(vprev, vnext, None, self.lo, self.hi, test, list(hist), stats)
         if stats is not None:
             self.reduce_stats(stats)
-        self.exchange(vnext)
+        self.refresh(vnext)
 
     # -- full solve ----------------------------------------------------------
     def solve(self, resume: Optional[P.Checkpoint] = None) -> ShardedResult:
@@ -168,7 +236,7 @@ class ShardedValueIteration:
             self.sweep(ring[prev], ring[nxt], None, self.lo, self.hi,
                        self.test if want else None, hist, stats)
             self.reduce_stats(stats)
-            self.exchange(ring[nxt])
+            self.refresh(ring[nxt])
             st = stats.cpu().numpy()  # the one host round trip per sweep
             sweep_s += time.perf_counter() - ts
             order.append(nxt)
@@ -180,9 +248,12 @@ class ShardedValueIteration:
                 hi = st[0]
                 lo = 0.0 if self.test == P.VALUE_SPAN else -st[1]
                 converged = bool(evaluate_test(self.test, float(hi), float(lo), cfg.epsilon, iteration))
-            if ckpt and iteration % cfg.checkpoint_every == 0 and self.rank == 0:
-                P.save_checkpoint(cfg.checkpoint_path, ring[order[-1]].double().cpu().numpy(),
-                                  iteration, fp)
+            if ckpt and iteration % cfg.checkpoint_every == 0:
+                if self.plan is not None:
+                    self.exchange(ring[order[-1]])  # a checkpoint holds all of V
+                if self.rank == 0:
+                    P.save_checkpoint(cfg.checkpoint_path, ring[order[-1]].double().cpu().numpy(),
+                                      iteration, fp)
             if converged:
                 break
         vfinal = ring[order[-1]]
@@ -192,6 +263,8 @@ class ShardedValueIteration:
         self.exchange(actions, send=torch.empty(self.maxlen, dtype=torch.int32, device=self.device),
                       recv=torch.empty(self.maxlen * self.world, dtype=torch.int32,
                                        device=self.device))
+        if self.plan is not None:
+            self.exchange(vfinal)  # the result is the full value vector
         values = vfinal.double().cpu().numpy()
         policy = actions.cpu().numpy().astype(np.uint32)
         return ShardedResult(values, policy, iteration, converged, time.perf_counter() - t0,

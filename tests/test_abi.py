@@ -240,3 +240,22 @@ def test_partition_is_cost_weighted_and_tile_aligned():
     import bench
     costs = [bench.state_terms(m, b[i], b[i + 1]) for i in range(8)]
     assert max(costs) / (sum(costs) / 8) < 1.01  # equal-count sharding gives 1.30
+
+
+def test_sweep_read_runs_host_logic(pvi):
+    """pvi_sweep_read_runs needs no device: factored B x_3-pair shards read
+    their own rows' slabs, the lower pairs' constants rows and their own
+    states; everything else reads all of V."""
+    m = pvi.make_preset("b/m3/exp1").set_algorithm("factored")
+    n = m.state_count()
+    b = [int(x) for x in m.partition(8)]
+    assert b == [i * n // 8 for i in range(9)]  # one x_3 pair per shard
+    slab = 16 ** 3
+    for r in range(8):
+        runs = m.sweep_read_runs(b[r], b[r + 1])
+        cover = sum(y - x for x, y in runs)
+        # own pair rows (32 slabs per top digit) + constants rows of lower
+        # pairs (2r per top digit) + own states, minus their overlap
+        want = (16 * (32 + 2 * r) + 256 * 2 - 2 * (32 + 2 * r)) * slab
+        assert cover == want, (r, cover, want)
+    assert pvi.make_preset("b/m3/exp1").sweep_read_runs(0, 5) == [(0, n)]

@@ -232,3 +232,35 @@ def test_factored_b_host_buffer_pipelines_agree(pvi):
     v3, a3 = pvi.bellman_backup_batch(m, V, lo, hi)
     np.testing.assert_array_equal(v3, v2[lo:hi])
     np.testing.assert_array_equal(a3, a2[lo:hi])
+
+
+@pytest.mark.parametrize("preset,parts", [("b/m3/exp1", 8), ("b/m3/exp1", 3), ("b/m3/exp1", 5)])
+def test_shard_reads_only_its_runs(pvi, preset, parts):
+    """pvi_sweep_read_runs is what the sharded driver refreshes between
+    sweeps: with every V entry OUTSIDE a shard's runs set to NaN, the
+    shard's backup must be unchanged (and finite)."""
+    m = pvi.make_preset(preset).set_algorithm("factored")
+    n = m.state_count()
+    V = np.random.default_rng(8).uniform(-20.0, 20.0, n)
+    bounds = [int(b) for b in m.partition(parts)]
+    for r in sorted({0, parts // 2, parts - 1}):
+        lo, hi = bounds[r], bounds[r + 1]
+        runs = m.sweep_read_runs(lo, hi)
+        covered = sum(b - a for a, b in runs)
+        assert covered < n  # the factored B sweep of a shard reads part of V
+        assert all(a < b for a, b in runs) and all(runs[i][1] < runs[i + 1][0] for i in range(len(runs) - 1))
+        Vp = np.full(n, np.nan)
+        for a, b in runs:
+            Vp[a:b] = V[a:b]
+        v0, a0 = pvi.bellman_backup_batch(m, V, lo, hi)
+        v1, a1 = pvi.bellman_backup_batch(m, Vp, lo, hi)
+        assert np.isfinite(v1).all()
+        np.testing.assert_array_equal(v1, v0)
+        np.testing.assert_array_equal(a1, a0)
+
+
+def test_read_runs_whole_space_for_gather_sweeps(pvi):
+    for preset, algo in [("b/m3/exp4", "exact"), ("c/m5/exp1", "factored"), ("a/m5/exp5", "factored")]:
+        m = pvi.make_preset(preset).set_algorithm(algo)
+        n = m.state_count()
+        assert m.sweep_read_runs(n // 3, n // 2) == [(0, n)]

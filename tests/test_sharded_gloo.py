@@ -101,3 +101,85 @@ def test_sharded_solve_matches_single_process(preset, world):
     np.testing.assert_array_equal(values, want.values)
     np.testing.assert_array_equal(policy, want.policy)
     assert len(bounds) == world + 1 and bounds[-1] == len(values)
+
+
+# --- read-set exchange (factored Scenario B x_3-pair shards) ---------------
+
+MOD = 1009.0
+
+
+def _runs_checksum(v, runs):
+    return float(sum(float(v[a:b].sum()) for a, b in runs))
+
+
+def _fake_sweep(rank_runs):
+    """A sweep that reads EVERY entry of its shard's read set: V'[s] =
+    (3 V[s] + checksum(V over the read set) + s) mod 1009 (integer-valued
+    doubles, so every sum is exact in any order)."""
+    def sweep(vprev, vnext, actions, lo, hi, test, hist, stats):
+        c = _runs_checksum(vprev, rank_runs(lo, hi))
+        s = torch.arange(lo, hi, dtype=torch.float64)
+        vnext[lo:hi] = torch.remainder(3.0 * vprev[lo:hi] + c + s, MOD)
+        if stats is not None:
+            stats[:] = torch.tensor([0.0, 0.0, NEG, 0.0], dtype=torch.float64)
+    return sweep
+
+
+def _rs_worker(rank, world, port, preset, steps, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2303_10672_b200 as P
+        from paper_2303_10672_b200.sharded import ShardedValueIteration
+        m = P.make_preset(preset).set_algorithm("factored")
+        n = m.state_count()
+        solver = ShardedValueIteration(m, P.ViConfig(), device=torch.device("cpu"),
+                                       sweep=_fake_sweep(m.sweep_read_runs))
+        assert solver.plan is not None
+        v = torch.remainder(torch.arange(n, dtype=torch.float64) * 7.0, MOD)
+        w = torch.empty_like(v)
+        for _ in range(steps):
+            solver.step(v, w)
+            v, w = w, v
+        runs = m.sweep_read_runs(solver.lo, solver.hi)
+        mine = {(a, b): v[a:b].clone().numpy() for a, b in runs}
+        received = solver.read_set_bytes()
+        solver.exchange(v)  # full replica (what solve() returns)
+        out_q.put((rank, runs, mine, v.numpy().copy(), received))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [3, 4])
+def test_read_set_exchange_delivers_every_read(world):
+    import paper_2303_10672_b200 as P
+    preset, steps = "b/m3/exp1", 3
+    m = P.make_preset(preset).set_algorithm("factored")
+    n = m.state_count()
+    bounds = [int(b) for b in m.partition(world)]
+    # single-process reference: every shard applies the rule on the global V
+    v = torch.remainder(torch.arange(n, dtype=torch.float64) * 7.0, MOD)
+    for _ in range(steps):
+        w = v.clone()
+        for r in range(world):
+            lo, hi = bounds[r], bounds[r + 1]
+            c = _runs_checksum(v, m.sweep_read_runs(lo, hi))
+            w[lo:hi] = torch.remainder(3.0 * v[lo:hi] + c + torch.arange(lo, hi, dtype=torch.float64), MOD)
+        v = w
+    want = v.numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rs_worker, args=(r, world, port, preset, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, runs, mine, full, received in got:
+        for (a, b), vals in mine.items():
+            np.testing.assert_array_equal(vals, want[a:b])
+        np.testing.assert_array_equal(full, want)
+        # the read set is a fraction of the all-gather's volume
+        assert received < 0.5 * (n - (bounds[rank + 1] - bounds[rank])) * 8
