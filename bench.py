@@ -244,7 +244,8 @@ def workload_config(model, args, world):
             "preset": args.workload, "states": model.state_count(),
             "actions": model.action_count(), "terms_per_sweep": model.terms_per_sweep(),
             "l2_flush": "256 MiB write between timed steps (V is 128 MiB, partials 2.4 GB)",
-            "parallelism": f"state-shards x{world} (cost-weighted, NCCL all-gather)"}
+            "parallelism": f"state-shards x{world} (cost-weighted; per sweep the V runs each shard "
+                           f"reads: NCCL all-to-all for factored B, all-gather otherwise)"}
 
 
 def ours_arm(args, world, rank, local):
@@ -362,6 +363,8 @@ def ours_arm(args, world, rank, local):
                "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (nominal, not measured)"}
     compute["frac"] = compute["achieved"] / fp64_peak
 
+    if world > 1:
+        roofline["exchange_bytes_per_rank"] = solver.read_set_bytes()
     line = {"metric": "bellman_evals_per_sec", "value": value, "unit": "evals/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
