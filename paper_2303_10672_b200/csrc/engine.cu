@@ -220,38 +220,6 @@ struct DevBuf {
   }
 };
 
-// Stream-ordered allocation from the device's default memory pool, which
-// keeps freed memory (release threshold = max), so repeated solves on the
-// same device do not pay cudaMalloc / cudaFree of the GB-scale buffers.
-struct PoolBuf {
-  void* p = nullptr;
-  cudaStream_t s = nullptr;
-  PoolBuf(std::size_t bytes, cudaStream_t stream) : s(stream) {
-    static bool configured[64] = {};
-    int dev = 0;
-    PVI_CUDA(cudaGetDevice(&dev));
-    if (dev < 64 && !configured[dev]) {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        std::uint64_t keep = ~0ull;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      }
-      cudaGetLastError();
-      configured[dev] = true;
-    }
-    if (bytes) PVI_CUDA(cudaMallocAsync(&p, bytes, stream));
-  }
-  PoolBuf(const PoolBuf&) = delete;
-  PoolBuf& operator=(const PoolBuf&) = delete;
-  ~PoolBuf() {
-    if (p) cudaFreeAsync(p, s);
-  }
-  template <typename U>
-  U* as() const {
-    return static_cast<U*>(p);
-  }
-};
-
 struct Stream {
   cudaStream_t s = nullptr;
   Stream() { PVI_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }

@@ -10,7 +10,9 @@
 // reduction then folds them in rollout-index order (sim.hpp:128-141).
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -251,13 +253,14 @@ struct DevPolicy {
 
 // policies.hpp:18-82; scenario_a.cpp:191-195; scenario_b.cpp:381-393;
 // scenario_c.cpp:361-370
-__device__ void apply_policy(const DevModel& dm, const DevPolicy& pol, const int* state, int arity,
-                             int* action) {
+template <int SC>
+__device__ __forceinline__ void apply_policy(const DevModel& dm, const DevPolicy& pol, const int* state,
+                                             int arity, int* action) {
   if (pol.kind == 0) {
     std::uint64_t idx = 0;
     for (int i = 0; i < arity; ++i) idx += static_cast<std::uint64_t>(state[i]) * dm.weight[i];
     const std::uint32_t a = pol.table[idx];
-    if (dm.scenario == PVI_SCENARIO_B) {
+    if (SC == PVI_SCENARIO_B) {
       action[0] = static_cast<int>(a) / dm.b_nb;
       action[1] = static_cast<int>(a) % dm.b_nb;
     } else {
@@ -265,7 +268,7 @@ __device__ void apply_policy(const DevModel& dm, const DevPolicy& pol, const int
     }
     return;
   }
-  switch (dm.scenario) {
+  switch (SC) {
     case PVI_SCENARIO_A: {
       int position = 0;
       for (int i = 0; i < arity; ++i) position += state[i];
@@ -308,8 +311,10 @@ struct SimError {
   int state[kMaxDigits];
 };
 
-// rollout (sim.hpp:68-124)
-__global__ void __launch_bounds__(128) k_rollouts(DevModel dm, const DevPolicy* __restrict__ pols,
+// rollout (sim.hpp:68-124); one instantiation per scenario (SC), so each
+// carries only its own step function and policy arithmetic
+template <int SC, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_rollouts(DevModel dm, const DevPolicy* __restrict__ pols,
                                                   int n_rollouts, int horizon, int warmup,
                                                   std::uint64_t base_seed, int arity, int products,
                                                   double gamma, double* __restrict__ out,
@@ -322,20 +327,20 @@ __global__ void __launch_bounds__(128) k_rollouts(DevModel dm, const DevPolicy* 
   for (int k = 0; k < arity; ++k) state[k] = 0;
   int action[2] = {0, 0};
   int bound[2];
-  if (dm.scenario == PVI_SCENARIO_B) {
+  if (SC == PVI_SCENARIO_B) {
     bound[0] = 2 * (dm.b_na - 1);
     bound[1] = 2 * (dm.b_nb - 1);
   } else {
     bound[0] = bound[1] = static_cast<int>(dm.n_actions) - 1;
   }
-  const int action_arity = dm.scenario == PVI_SCENARIO_B ? 2 : 1;
+  constexpr int action_arity = SC == PVI_SCENARIO_B ? 2 : 1;
   Rng rng(base_seed, static_cast<std::uint64_t>(i));
   const int total_days = warmup + horizon;
   double ret = 0.0, weight = 1.0;
   long long demand[2] = {0, 0}, filled[2] = {0, 0}, expired[2] = {0, 0}, received[2] = {0, 0},
             holding[2] = {0, 0};
   for (int day = 0; day < total_days; ++day) {
-    apply_policy(dm, pol, state, arity, action);
+    apply_policy<SC>(dm, pol, state, arity, action);
     for (int k = 0; k < action_arity; ++k) {
       if (action[k] < 0 || action[k] > bound[k]) {
         const unsigned long long key = static_cast<unsigned long long>(p) * n_rollouts + i;
@@ -354,11 +359,9 @@ __global__ void __launch_bounds__(128) k_rollouts(DevModel dm, const DevPolicy* 
     st.reward = 0.0;
     for (int k = 0; k < 2; ++k)
       st.demand[k] = st.filled[k] = st.expired[k] = st.received[k] = st.holding[k] = 0;
-    switch (dm.scenario) {
-      case PVI_SCENARIO_A: step_a(dm, state, action, rng, st); break;
-      case PVI_SCENARIO_B: step_b(dm, state, action, rng, st); break;
-      default: step_c(dm, state, action, rng, st); break;
-    }
+    if constexpr (SC == PVI_SCENARIO_A) step_a(dm, state, action, rng, st);
+    else if constexpr (SC == PVI_SCENARIO_B) step_b(dm, state, action, rng, st);
+    else step_c(dm, state, action, rng, st);
     if (day >= warmup) {
       ret += weight * st.reward;
       weight *= gamma;
@@ -422,17 +425,15 @@ __global__ void k_draws(std::uint64_t seed, std::uint64_t rollout, std::uint32_t
   for (int i = 0; i < n; ++i) out[i] = rng.next_u64();
 }
 
-struct Buf {
-  void* p = nullptr;
-  explicit Buf(std::size_t b) {
-    if (b) PVI_CUDA(cudaMalloc(&p, b));
-  }
-  ~Buf() {
-    if (p) cudaFree(p);
-  }
-  Buf(const Buf&) = delete;
-  Buf& operator=(const Buf&) = delete;
-};
+// one non-blocking stream per (host thread, device) for the evaluations
+cudaStream_t sim_stream(int device) {
+  static thread_local cudaStream_t streams[64] = {};
+  if (device < 0 || device >= 64) fail(PVI_ERR_DEVICE, "device ordinal out of range");
+  if (!streams[device]) PVI_CUDA(cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking));
+  return streams[device];
+}
+
+using Buf = PoolBuf;
 
 }  // namespace
 
@@ -450,8 +451,7 @@ void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_po
 
   std::vector<DevPolicy> hp(n_policies);
   std::vector<std::unique_ptr<Buf>> tables;
-  cudaStream_t stream;
-  PVI_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  cudaStream_t stream = sim_stream(device);
   for (std::uint32_t i = 0; i < n_policies; ++i) {
     const pvi_policy& p = policies[i];
     hp[i].kind = p.kind;
@@ -464,7 +464,7 @@ void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_po
       for (std::uint32_t j = 0; j < i; ++j)
         if (policies[j].kind == 0 && policies[j].table == p.table) found = hp[j].table;
       if (!found) {
-        tables.push_back(std::make_unique<Buf>(n_states * 4));
+        tables.push_back(std::make_unique<Buf>(n_states * 4, stream));
         PVI_CUDA(cudaMemcpyAsync(tables.back()->p, p.table, n_states * 4, cudaMemcpyHostToDevice, stream));
         found = static_cast<const std::uint32_t*>(tables.back()->p);
       }
@@ -475,22 +475,46 @@ void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_po
         fail(PVI_ERR_PARAMETER, "heuristic policy expects " + std::to_string(need) + " parameters");
     }
   }
-  Buf dpol(sizeof(DevPolicy) * n_policies);
+  Buf dpol(sizeof(DevPolicy) * n_policies, stream);
   PVI_CUDA(cudaMemcpyAsync(dpol.p, hp.data(), sizeof(DevPolicy) * n_policies, cudaMemcpyHostToDevice, stream));
   const std::size_t n_sum = static_cast<std::size_t>(n_policies) * cfg.n_rollouts;
-  Buf dsum(n_sum * 7 * sizeof(double));
-  Buf dstat(static_cast<std::size_t>(n_policies) * 14 * sizeof(double));
-  Buf derr(sizeof(SimError));
+  Buf dsum(n_sum * 7 * sizeof(double), stream);
+  Buf dstat(static_cast<std::size_t>(n_policies) * 14 * sizeof(double), stream);
+  Buf derr(sizeof(SimError), stream);
   SimError herr;
   std::memset(&herr, 0, sizeof(herr));
   herr.key = ~0ull;
   PVI_CUDA(cudaMemcpyAsync(derr.p, &herr, sizeof(herr), cudaMemcpyHostToDevice, stream));
   const dim3 grid((cfg.n_rollouts + 127) / 128, n_policies);
-  k_rollouts<<<grid, 128, 0, stream>>>(dm, static_cast<const DevPolicy*>(dpol.p), cfg.n_rollouts,
+  // CTAs per SM the register allocation is bounded for (measured per
+  // scenario on a B200: A 3, B 4, C 1; PVI_SIM_MINB overrides)
+  static const int minb_env = [] {
+    const char* e = std::getenv("PVI_SIM_MINB");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int minb = minb_env > 0 ? minb_env
+                   : m.scenario == PVI_SCENARIO_A ? 3 : m.scenario == PVI_SCENARIO_B ? 4 : 1;
+#define PVI_KR(MB)                                                                                   \
+  (m.scenario == PVI_SCENARIO_A ? k_rollouts<PVI_SCENARIO_A, MB>                                    \
+   : m.scenario == PVI_SCENARIO_B ? k_rollouts<PVI_SCENARIO_B, MB> : k_rollouts<PVI_SCENARIO_C, MB>)
+  auto kr = minb >= 5 ? PVI_KR(5) : minb >= 4 ? PVI_KR(4) : minb >= 3 ? PVI_KR(3) : minb >= 2 ? PVI_KR(2) : PVI_KR(1);
+#undef PVI_KR
+  static const bool trace = [] {
+    const char* e = std::getenv("PVI_SIM_TRACE");
+    return e && e[0] == '1';
+  }();
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (trace) {
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, stream);
+  }
+  kr<<<grid, 128, 0, stream>>>(dm, static_cast<const DevPolicy*>(dpol.p), cfg.n_rollouts,
                                        cfg.horizon_days, cfg.warmup_days, cfg.base_seed, arity,
                                        products, m.gamma, static_cast<double*>(dsum.p),
                                        static_cast<SimError*>(derr.p));
   PVI_CUDA(cudaGetLastError());
+  if (trace) cudaEventRecord(t1, stream);
   k_reduce_eval<<<(n_policies * 7 + 63) / 64, 64, 0, stream>>>(static_cast<const double*>(dsum.p), cfg.n_rollouts,
                                                               n_policies, static_cast<double*>(dstat.p));
   PVI_CUDA(cudaGetLastError());
@@ -500,7 +524,13 @@ void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_po
   if (per_rollout)
     PVI_CUDA(cudaMemcpyAsync(per_rollout, dsum.p, n_sum * 7 * sizeof(double), cudaMemcpyDeviceToHost, stream));
   PVI_CUDA(cudaStreamSynchronize(stream));
-  cudaStreamDestroy(stream);
+  if (trace) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    std::fprintf(stderr, "[pvi sim] k_rollouts %u x %d: %.3f ms\n", n_policies, cfg.n_rollouts, ms);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+  }
   if (herr.key != ~0ull) {
     std::string tuple;
     for (int q = 0; q < herr.arity; ++q) tuple += std::to_string(herr.state[q]) + " ";
@@ -529,20 +559,22 @@ void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_po
 }
 
 void philox_block_device(const std::uint32_t ctr[4], const std::uint32_t key[2], std::uint32_t out[4]) {
-  select_device(-1);
-  Buf d(16);
-  k_philox<<<1, 1>>>(ctr[0], ctr[1], ctr[2], ctr[3], key[0], key[1], static_cast<std::uint32_t*>(d.p));
+  const cudaStream_t st = sim_stream(select_device(-1));
+  Buf d(16, st);
+  k_philox<<<1, 1, 0, st>>>(ctr[0], ctr[1], ctr[2], ctr[3], key[0], key[1], static_cast<std::uint32_t*>(d.p));
   PVI_CUDA(cudaGetLastError());
-  PVI_CUDA(cudaMemcpy(out, d.p, 16, cudaMemcpyDeviceToHost));
+  PVI_CUDA(cudaMemcpyAsync(out, d.p, 16, cudaMemcpyDeviceToHost, st));
+  PVI_CUDA(cudaStreamSynchronize(st));
 }
 
 void rollout_draws_device(std::uint64_t seed, std::uint64_t rollout, std::uint32_t day, int n,
                           std::uint64_t* out) {
-  select_device(-1);
-  Buf d(static_cast<std::size_t>(n) * 8);
-  k_draws<<<1, 1>>>(seed, rollout, day, n, static_cast<std::uint64_t*>(d.p));
+  const cudaStream_t st = sim_stream(select_device(-1));
+  Buf d(static_cast<std::size_t>(n) * 8, st);
+  k_draws<<<1, 1, 0, st>>>(seed, rollout, day, n, static_cast<std::uint64_t*>(d.p));
   PVI_CUDA(cudaGetLastError());
-  PVI_CUDA(cudaMemcpy(out, d.p, static_cast<std::size_t>(n) * 8, cudaMemcpyDeviceToHost));
+  PVI_CUDA(cudaMemcpyAsync(out, d.p, static_cast<std::size_t>(n) * 8, cudaMemcpyDeviceToHost, st));
+  PVI_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace pvi_b200
