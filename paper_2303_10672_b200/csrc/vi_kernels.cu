@@ -2572,6 +2572,156 @@ __global__ void __launch_bounds__(256) k_c_bin_level(const double* __restrict__ 
   Hout[out_base + gid] = acc;
 }
 
+// The same pass with the (b, d_k) plane staged in shared memory.  A pass
+// only mixes the "units left" digit b and digit k, so for fixed tau, order a
+// and the other digits the outputs Hout(b, d_k) of all x_1 read one
+// [b' <= a][d'][x_1] block of Hin: the CTA stages that block (each input read
+// from global memory once instead of ~b times through L1/L2) and thread
+// (x_1, d_k) walks b.  Same terms in the same order as k_c_bin_level.
+__global__ void __launch_bounds__(448) k_c_bin_tile(const double* __restrict__ Hin,
+                                                    double* __restrict__ Hout,
+                                                    const double* __restrict__ binom_k,
+                                                    std::size_t binom_a_stride, int r, int m,
+                                                    int k, std::uint32_t wb, int endo, int in_is_g,
+                                                    int n_prof) {
+  extern __shared__ double tile[];  // [b][d_k][x_1]
+  __shared__ double s_bin[32 * 32];
+  const int a = endo ? r - 1 - static_cast<int>(blockIdx.z) : 0;  // heavy orders first
+  const int nb = endo ? a + 1 : r;
+  const int tau = static_cast<int>(blockIdx.y);
+  const int cap = r - 1;
+  // rest digits: positions 1..m-1 with weights r^(p-1); x_1 (p = 1) and
+  // digit k are the tile axes, the others come from blockIdx.x
+  std::uint32_t rest0 = 0, wk = 1;
+  {
+    std::uint32_t o = blockIdx.x, w = 1;
+    for (int p = 1; p <= m - 1; ++p) {
+      if (p == k) wk = w;
+      if (p != 1 && p != k) {
+        rest0 += (o % static_cast<std::uint32_t>(r)) * w;
+        o /= static_cast<std::uint32_t>(r);
+      }
+      w *= static_cast<std::uint32_t>(r);
+    }
+  }
+  const double* bt = binom_k + a * binom_a_stride;
+  for (int i = threadIdx.x; i < nb * r; i += blockDim.x) s_bin[i] = bt[i];
+  const std::size_t out_base =
+      endo ? c_tri_base(a, wb) + static_cast<std::size_t>(tau) * nb * wb
+           : static_cast<std::size_t>(tau) * n_prof;
+  const std::size_t in_base = (endo && !in_is_g) ? out_base : static_cast<std::size_t>(tau) * n_prof;
+  const int plane = r * r;
+  for (int i = threadIdx.x; i < nb * plane; i += blockDim.x) {
+    const int b = i / plane, e = i % plane, d = e / r, x1 = e % r;
+    tile[i] = __ldg(Hin + in_base + static_cast<std::size_t>(b) * wb + rest0 + d * wk + x1);
+  }
+  __syncthreads();
+  if (static_cast<int>(threadIdx.x) >= plane) return;
+  const int dk = threadIdx.x / r, x1 = threadIdx.x % r;
+  double* out = Hout + out_base + rest0 + dk * wk + x1;
+  for (int b = 0; b < nb; ++b) {
+    const double* w = s_bin + b * r;
+    double acc = 0.0;
+    for (int y = 0; y <= b; ++y) acc = fma(w[y], tile[((b - y) * r + min(dk + y, cap)) * r + x1], acc);
+    out[static_cast<std::size_t>(b) * wb] = acc;
+  }
+}
+
+// Persistent form of k_c_bin_tile: one CTA per SM walks the (order a,
+// tau, line) items with a stride of gridDim.x, heavy orders first; the next
+// item's [b][d_k][x_1] block lands by cp.async in the second buffer while
+// this one is computed, and 896 threads split each (d_k, x_1) column's b
+// values (even / odd) so two FMA chains run per column.
+__global__ void __launch_bounds__(896, 1) k_c_bin_tile_p(const double* __restrict__ Hin,
+                                                         double* __restrict__ Hout,
+                                                         const double* __restrict__ binom_k,
+                                                         std::size_t binom_a_stride, int r, int m,
+                                                         int k, std::uint32_t wb, int endo,
+                                                         int in_is_g, int n_prof, int n_lines) {
+  extern __shared__ double smem_t[];  // 2 x [b][d_k][x_1], then 2 x s_bin [b][y]
+  const int plane = r * r, cube = r * plane;
+  double* tiles = smem_t;
+  double* bins = smem_t + 2 * cube;
+  const int cap = r - 1;
+  const int n_a = endo ? r : 1;
+  const int n_items = n_a * 7 * n_lines;
+  struct Item {
+    int a, nb, tau;
+    std::uint32_t rest0, wk;
+    std::size_t in_base, out_base;
+  };
+  auto item = [&](int i) {
+    Item it;
+    const int ai = i / (7 * n_lines), rem = i % (7 * n_lines);
+    it.a = endo ? r - 1 - ai : 0;  // heavy orders first
+    it.nb = endo ? it.a + 1 : r;
+    it.tau = rem / n_lines;
+    std::uint32_t o = static_cast<std::uint32_t>(rem % n_lines), w = 1;
+    it.rest0 = 0;
+    it.wk = 1;
+    for (int p = 1; p <= m - 1; ++p) {
+      if (p == k) it.wk = w;
+      if (p != 1 && p != k) {
+        it.rest0 += (o % static_cast<std::uint32_t>(r)) * w;
+        o /= static_cast<std::uint32_t>(r);
+      }
+      w *= static_cast<std::uint32_t>(r);
+    }
+    it.out_base = endo ? c_tri_base(it.a, wb) + static_cast<std::size_t>(it.tau) * it.nb * wb
+                       : static_cast<std::size_t>(it.tau) * n_prof;
+    it.in_base = (endo && !in_is_g) ? it.out_base : static_cast<std::size_t>(it.tau) * n_prof;
+    return it;
+  };
+  const unsigned tbase = static_cast<unsigned>(__cvta_generic_to_shared(tiles));
+  const unsigned bbase = static_cast<unsigned>(__cvta_generic_to_shared(bins));
+  auto stage = [&](const Item& it, int buf) {
+    const unsigned dst = tbase + static_cast<unsigned>(buf * cube) * 8u;
+    for (int i = threadIdx.x; i < it.nb * plane; i += blockDim.x) {
+      const int b = i / plane, e = i % plane, d = e / r, x1 = e % r;
+      const double* src = Hin + it.in_base + static_cast<std::size_t>(b) * wb + it.rest0 + d * it.wk + x1;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * i), "l"(src));
+    }
+    const double* bt = binom_k + it.a * binom_a_stride;
+    const unsigned bdst = bbase + static_cast<unsigned>(buf * plane) * 8u;
+    for (int i = threadIdx.x; i < it.nb * r; i += blockDim.x)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(bdst + 8u * i), "l"(bt + i));
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  const int half = threadIdx.x / 448, e = threadIdx.x % 448;
+  const int dk = e / r, x1 = e % r;
+  const bool worker = e < plane;
+  int i = static_cast<int>(blockIdx.x);
+  if (i >= n_items) return;
+  Item cur = item(i);
+  stage(cur, 0);
+  for (int buf = 0; i < n_items; buf ^= 1) {
+    const int inext = i + static_cast<int>(gridDim.x);
+    Item nxt{};
+    if (inext < n_items) {
+      nxt = item(inext);
+      stage(nxt, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (worker) {
+      const double* tile = tiles + buf * cube;
+      const double* sb = bins + buf * plane;
+      double* out = Hout + cur.out_base + cur.rest0 + dk * cur.wk + x1;
+      for (int b = half; b < cur.nb; b += 2) {
+        const double* w = sb + b * r;
+        double acc = 0.0;
+        for (int y = 0; y <= b; ++y) acc = fma(w[y], tile[((b - y) * r + min(dk + y, cap)) * r + x1], acc);
+        out[static_cast<std::size_t>(b) * wb] = acc;
+      }
+    }
+    __syncthreads();  // the buffer is refilled two items later
+    cur = nxt;
+    i = inext;
+  }
+}
+
 // Last pass (k = 1) fused with the Q rows, the first max over the orders and
 // the finalize.  CTA = CQ_GROUPS groups of the A_max+1 states that differ
 // only in x_1; a group's H_2 entries (b, z_1) for b, z_1 in [0, A_max] are one
@@ -3036,6 +3186,15 @@ static int num_sms() {
   return n;
 }
 
+// PVI_C_TILE: 0 = k_c_bin_level, 1 = k_c_bin_tile, 2 = persistent k_c_bin_tile_p
+static int c_tile_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("PVI_C_TILE");
+    return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 2;
+  }();
+  return mode;
+}
+
 static bool a_group_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PVI_A_GROUP");
@@ -3360,9 +3519,26 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
         wk /= static_cast<std::uint32_t>(r);
         double* dst = Hb[i & 1];
         const unsigned blocks = grid_for(static_cast<std::uint64_t>(r) * wb, 256);
-        k_c_bin_level<<<dim3(blocks, 7, endo ? r : 1), 256, smem, stream>>>(
-            src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, endo ? a_stride : 0, r, wk,
-            wb, endo ? 1 : 0, src == G ? 1 : 0, static_cast<int>(n_prof));
+        if (c_tile_mode() == 2 && r <= 21) {
+          const int n_lines = static_cast<int>(wb / (static_cast<std::uint32_t>(r) * r));
+          const std::size_t smt = 2 * (static_cast<std::size_t>(r) * r * r + static_cast<std::size_t>(r) * r) * sizeof(double);
+          cudaFuncSetAttribute(k_c_bin_tile_p, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          const int n_items = (endo ? r : 1) * 7 * n_lines;
+          k_c_bin_tile_p<<<static_cast<unsigned>(std::min(n_items, num_sms())), 896, smt, stream>>>(
+              src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, endo ? a_stride : 0, r, M, k, wb,
+              endo ? 1 : 0, src == G ? 1 : 0, static_cast<int>(n_prof), n_lines);
+        } else if (c_tile_mode() == 1 && r <= 21) {
+          const std::size_t smt = static_cast<std::size_t>(r) * r * r * sizeof(double);
+          cudaFuncSetAttribute(k_c_bin_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          k_c_bin_tile<<<dim3(static_cast<unsigned>(wb / (static_cast<std::uint32_t>(r) * r)), 7, endo ? r : 1), 448,
+                         smt, stream>>>(src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k,
+                                        endo ? a_stride : 0, r, M, k, wb, endo ? 1 : 0, src == G ? 1 : 0,
+                                        static_cast<int>(n_prof));
+        } else {
+          k_c_bin_level<<<dim3(blocks, 7, endo ? r : 1), 256, smem, stream>>>(
+              src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, endo ? a_stride : 0, r, wk,
+              wb, endo ? 1 : 0, src == G ? 1 : 0, static_cast<int>(n_prof));
+        }
         src = dst;
       }
       if (qf_enabled() && !endo) {  // endogenous: per-order restaging loses to k_c_bin_q

@@ -1,6 +1,6 @@
 # per-kernel durations (ncu launch list) of the bench step under env settings
 mkdir -p gpurun_out
-P="python bench.py --steps 1 --warmup 3 --no-solve --no-e2e --no-cpu-baseline --no-alt --no-simopt"
+P="python bench.py --steps 1 --warmup 3 --no-solve --no-e2e --no-cpu-baseline --no-alt --no-simopt ${EXTRA:-}"
 for v in $VALS; do
   env $VAR=$v $P > gpurun_out/lt_plain_$v.log 2>&1 && \
   env $VAR=$v ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/lt_$v.csv $P > /dev/null 2>&1
