@@ -57,7 +57,11 @@ struct Workspace {
   cudaEvent_t done[kChunkEvents] = {};
   cudaEvent_t ev[3 * kChunkEvents] = {};
   Workspace() {
-    PVI_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    // `stream` carries the pipelined backup's stage-1 pieces: highest
+    // priority, so they are scheduled ahead of the stage-2 grids they feed
+    int least = 0, greatest = 0;
+    PVI_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    PVI_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, greatest));
     PVI_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
     PVI_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
     for (auto& x : s2) PVI_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
@@ -947,7 +951,7 @@ void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t
   a.algorithm = m.algorithm;
   a.want_values = out_values || out_actions;
   if (b_pipe && lo == 0 && hi == n && std::is_same<T, double>::value && e2e_pairs() &&
-      b_sweep_honours_xb_range(m, device) && m.b_na % 2 == 0 && m.b_na / 2 <= Workspace::kChunkEvents / 2) {
+      b_sweep_honours_xb_range(m, device) && m.b_na % 2 == 0 && m.b_na / 2 <= 8) {
     // Pipelined by x_3 pairs.  Stage 2 of the states with top A digit
     // x_3 in {2p, 2p+1} reads the W rows r = (o_a, x_3, x_2) of that pair
     // (and the constants' rows of lower x_3, done by earlier pairs); stage 1
@@ -973,45 +977,84 @@ void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t
       tev.push_back(e);
     };
     mark(st);
+    // piece 0 goes up in two halves (top digits t < na/2, then the rest) so
+    // the first stage-1 rows start after 1/16 of V instead of 1/8
+    const int th = na / 2;
+    const std::uint64_t n_r = static_cast<std::uint64_t>(na) * na * na;
     for (int p = 0; p < pairs; ++p) {
       const std::uint64_t off = static_cast<std::uint64_t>(p) * slab_run;
-      PVI_CUDA(cudaMemcpy2DAsync(v + off, pitch * sizeof(T), static_cast<const T*>(values) + off,
-                                 pitch * sizeof(T), slab_run * sizeof(T), na, cudaMemcpyHostToDevice, ws.up));
-      PVI_CUDA(cudaEventRecord(ws.done[Workspace::kChunkEvents / 2 + p], ws.up));
+      const T* src = static_cast<const T*>(values);
+      if (p == 0) {
+        PVI_CUDA(cudaMemcpy2DAsync(v + off, pitch * sizeof(T), src + off, pitch * sizeof(T), slab_run * sizeof(T), th,
+                                   cudaMemcpyHostToDevice, ws.up));
+        PVI_CUDA(cudaEventRecord(ws.ev[16], ws.up));
+        const std::uint64_t off2 = off + th * pitch;
+        PVI_CUDA(cudaMemcpy2DAsync(v + off2, pitch * sizeof(T), src + off2, pitch * sizeof(T), slab_run * sizeof(T),
+                                   na - th, cudaMemcpyHostToDevice, ws.up));
+        PVI_CUDA(cudaEventRecord(ws.ev[17], ws.up));
+      } else {
+        PVI_CUDA(cudaMemcpy2DAsync(v + off, pitch * sizeof(T), src + off, pitch * sizeof(T), slab_run * sizeof(T), na,
+                                   cudaMemcpyHostToDevice, ws.up));
+        PVI_CUDA(cudaEventRecord(ws.done[Workspace::kChunkEvents / 2 + p], ws.up));
+      }
       mark(ws.up);
     }
-    // stage 1 pieces in order on `st`; stage 2 of pair p on s2[p % 2] once
+    // stage 1 pieces in order on `st`; stage 2 of pair p on s2[] once
     // stage 1 of pieces <= p is done (it also reads the constants' rows of
-    // lower pairs), so consecutive pairs' stage-2 grids fill each other's tail
+    // lower pairs), so consecutive grids fill each other's tail
     for (int p = 0; p < pairs; ++p) {
-      PVI_CUDA(cudaStreamWaitEvent(st, ws.done[Workspace::kChunkEvents / 2 + p], 0));
       a.stages = 1;
       a.lo = 0;
       a.hi = n;
       a.x3_rows_lo = 2 * p;
       a.x3_rows_hi = 2 * p + 1;
+      if (p == 0) {
+        // rows r = (o_a = t, ...): the first half of the rows reads the first half-piece
+        PVI_CUDA(cudaStreamWaitEvent(st, ws.ev[16], 0));
+        a.r_lo = 0;
+        a.r_hi = n_r / na * th;
+        launch_sweep<T>(m, dm, a, ws.scratch, st);
+        PVI_CUDA(cudaStreamWaitEvent(st, ws.ev[17], 0));
+        a.r_lo = a.r_hi;
+        a.r_hi = ~0ull;
+      } else {
+        PVI_CUDA(cudaStreamWaitEvent(st, ws.done[Workspace::kChunkEvents / 2 + p], 0));
+      }
       launch_sweep<T>(m, dm, a, ws.scratch, st);
+      a.r_lo = 0;
+      a.r_hi = ~0ull;
       PVI_CUDA(cudaEventRecord(ws.ev[p], st));
       mark(st);
     }
+    // stage 2 of each pair in two x_b column halves: each half's V' / argmax
+    // (512 rows of 2,048 states) goes back with one 2-D copy as it finishes
+    const std::uint64_t xa_rows = 2ull * na * na;
     for (int p = 0; p < pairs; ++p) {
-      cudaStream_t cs = ws.s2[p % 2];
-      PVI_CUDA(cudaStreamWaitEvent(cs, ws.ev[p], 0));
-      a.stages = 2;
-      a.x3_rows_lo = a.x3_rows_hi = -1;
-      a.lo = p * per_pair;
-      a.hi = (p + 1) * per_pair;
-      launch_sweep<T>(m, dm, a, ws.scratch, cs);
-      mark(cs);
-      PVI_CUDA(cudaEventRecord(ws.done[p], cs));
-      PVI_CUDA(cudaStreamWaitEvent(ws.copy, ws.done[p], 0));
-      if (out_values)
-        PVI_CUDA(cudaMemcpyAsync(static_cast<T*>(out_values) + a.lo, vo + a.lo, per_pair * sizeof(T),
-                                 cudaMemcpyDeviceToHost, ws.copy));
-      if (out_actions)
-        PVI_CUDA(cudaMemcpyAsync(out_actions + a.lo, ao + a.lo, per_pair * 4, cudaMemcpyDeviceToHost, ws.copy));
-      mark(ws.copy);
+      for (int h = 0; h < 2; ++h) {
+        cudaStream_t cs = ws.s2[(2 * p + h) % 2];
+        PVI_CUDA(cudaStreamWaitEvent(cs, ws.ev[p], 0));
+        a.stages = 2;
+        a.x3_rows_lo = a.x3_rows_hi = -1;
+        a.lo = p * per_pair;
+        a.hi = (p + 1) * per_pair;
+        a.xb_lo = h * n_xb / 2;
+        a.xb_hi = (h + 1) * n_xb / 2;
+        launch_sweep<T>(m, dm, a, ws.scratch, cs);
+        mark(cs);
+        PVI_CUDA(cudaEventRecord(ws.ev[20 + 2 * p + h], cs));
+        PVI_CUDA(cudaStreamWaitEvent(ws.copy, ws.ev[20 + 2 * p + h], 0));
+        const std::uint64_t o = a.lo + a.xb_lo, w = a.xb_hi - a.xb_lo;
+        if (out_values)
+          PVI_CUDA(cudaMemcpy2DAsync(static_cast<T*>(out_values) + o, n_xb * sizeof(T), vo + o, n_xb * sizeof(T),
+                                     w * sizeof(T), xa_rows, cudaMemcpyDeviceToHost, ws.copy));
+        if (out_actions)
+          PVI_CUDA(cudaMemcpy2DAsync(out_actions + o, n_xb * 4, ao + o, n_xb * 4, w * 4, xa_rows,
+                                     cudaMemcpyDeviceToHost, ws.copy));
+        mark(ws.copy);
+      }
     }
+    a.xb_lo = 0;
+    a.xb_hi = ~0ull;
     PVI_CUDA(cudaStreamSynchronize(st));
     for (auto x : ws.s2) PVI_CUDA(cudaStreamSynchronize(x));
     PVI_CUDA(cudaStreamSynchronize(ws.copy));
