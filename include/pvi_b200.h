@@ -371,6 +371,21 @@ int pvi_rollout_draws(uint64_t base_seed, uint64_t rollout, uint32_t day, int n,
 int pvi_profile_enable(int on);
 int pvi_profile_read(double* kernel_ms, uint64_t* kernel_launches, uint64_t* all_launches);
 
+/* ---- policy CSV (runner.cpp:90-166, io.cpp:53-92) -----------------------
+ * Formatting and parsing run on the device, one thread per row.
+ * pvi_policy_csv_format writes the BODY of policy_to_csv (one row per state:
+ * the decoded tuple, then the action fields; no header line) into out;
+ * out = NULL returns the byte length in *length.
+ * pvi_policy_csv_parse is policy_from_csv after the metadata check: the
+ * whole file text (header included) -> |S| actions, with the reference's
+ * FormatError (row count, field count, non-numeric) and IndexingError
+ * (tuple range) for the first bad row in file order; a state named twice
+ * takes the last row's action, states never named take 0. */
+int pvi_policy_csv_format(const pvi_model* m, const uint32_t* actions, char* out, uint64_t capacity,
+                          uint64_t* length, char* err, size_t errlen);
+int pvi_policy_csv_parse(const pvi_model* m, const char* text, uint64_t length, uint32_t* actions,
+                         char* err, size_t errlen);
+
 /* ---- checkpoints (checkpoint.hpp:24-35) --------------------------------- */
 int pvi_checkpoint_save(const char* path, const double* values, uint64_t count, uint64_t iteration,
                         const uint8_t fingerprint[32], char* err, size_t errlen);

@@ -147,6 +147,8 @@ SIGNATURES = {
                                       _vp] + _E),
     "pvi_partition": (C.c_int, [_vp, C.c_int, _vp]),
     "pvi_sweep_read_runs": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(C.c_size_t)]),
+    "pvi_policy_csv_format": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]),
+    "pvi_policy_csv_parse": (C.c_int, [_vp, _vp, C.c_uint64, _vp, C.c_char_p, C.c_size_t]),
     "pvi_rollout_config_defaults": (None, [_vp]),
     "pvi_sim_evaluate": (C.c_int, [_vp, _vp, C.c_uint32, _vp, _vp, _vp] + _E),
     "pvi_philox_block": (C.c_int, [_vp, _vp, _vp]),

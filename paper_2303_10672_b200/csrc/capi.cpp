@@ -333,6 +333,25 @@ int pvi_partition(const pvi_model* m, int parts, uint64_t* bounds) {
   return guarded(nullptr, 0, nullptr, [&] { partition(M(m), parts, bounds); });
 }
 
+int pvi_policy_csv_format(const pvi_model* m, const uint32_t* actions, char* out, uint64_t capacity,
+                          uint64_t* length, char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if (!m || !m->impl) fail(PVI_ERR_PARAMETER, "null model");
+    if (!actions) fail(PVI_ERR_PARAMETER, "null actions");
+    const std::uint64_t l = policy_csv_format(M(m), actions, out, capacity);
+    if (length) *length = l;
+  });
+}
+
+int pvi_policy_csv_parse(const pvi_model* m, const char* text, uint64_t length, uint32_t* actions,
+                         char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if (!m || !m->impl) fail(PVI_ERR_PARAMETER, "null model");
+    if (!text || !actions) fail(PVI_ERR_PARAMETER, "null buffer");
+    policy_csv_parse(M(m), text, length, actions);
+  });
+}
+
 int pvi_sweep_read_runs(const pvi_model* m, uint64_t lo, uint64_t hi, uint64_t* runs, size_t capacity,
                         size_t* count) {
   return guarded(nullptr, 0, nullptr, [&] {

@@ -23,6 +23,11 @@ void vi_sweep_device(const Model& m, int precision, double gamma, const void* vp
                      const void* const* hist, int n_hist, int want_stats, double* stats,
                      void* stream);
 void partition(const Model& m, int parts, std::uint64_t* bounds);
+// policy CSV rows on the device (io_kernels.cu): the body (one row per
+// state) of runner.cpp's policy_to_csv; out = nullptr returns the length
+std::uint64_t policy_csv_format(const Model& m, const std::uint32_t* actions, char* out, std::uint64_t capacity);
+// policy_from_csv after the metadata check: whole file text -> actions
+void policy_csv_parse(const Model& m, const char* text, std::uint64_t len, std::uint32_t* out);
 void profile_enable(bool on);
 void profile_read(double* ms, std::uint64_t* main_launches, std::uint64_t* all_launches);
 void initial_values_host(const Model& m, double* out);

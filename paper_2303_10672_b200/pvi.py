@@ -280,6 +280,29 @@ class Model:
         _raise(L.load().pvi_partition(self._h, parts, _p(b)), None)
         return b
 
+    def policy_csv_body(self, actions: np.ndarray) -> bytes:
+        """The rows of runner.cpp's policy_to_csv (one per state, no header),
+        formatted on the device (pvi_policy_csv_format)."""
+        a = np.ascontiguousarray(actions, np.uint32)
+        if a.shape != (self.state_count(),):
+            raise ParameterError("policy must have one action per state")
+        ln = C.c_uint64()
+        err = _err_buf()
+        _raise(L.load().pvi_policy_csv_format(self._h, _p(a), None, 0, C.byref(ln), err, len(err)), err)
+        buf = np.empty(ln.value, np.uint8)
+        _raise(L.load().pvi_policy_csv_format(self._h, _p(a), _p(buf), ln.value, C.byref(ln), err, len(err)), err)
+        return buf.tobytes()
+
+    def policy_from_csv_text(self, text: bytes) -> np.ndarray:
+        """runner.cpp's policy_from_csv after the metadata check, parsed on
+        the device (pvi_policy_csv_parse)."""
+        out = np.zeros(self.state_count(), np.uint32)
+        buf = np.frombuffer(text, np.uint8)
+        err = _err_buf()
+        _raise(L.load().pvi_policy_csv_parse(self._h, _p(buf) if len(buf) else None, len(buf), _p(out), err,
+                                             len(err)), err)
+        return out
+
     def sweep_read_runs(self, lo: int, hi: int) -> list:
         """State runs [(a, b), ...] of V that a sweep of shard [lo, hi) reads
         (pvi_sweep_read_runs): what a multi-GPU driver must refresh."""

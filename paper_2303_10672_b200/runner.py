@@ -40,11 +40,16 @@ def csv_row(fields) -> str:
     return ",".join(csv_field(str(f)) for f in fields) + "\n"
 
 
-def atomic_write_text(path: str, text: str) -> None:
+def atomic_write_text(path: str, text) -> None:
+    """Temp file + rename (io.cpp atomic_write_text); text is str or bytes."""
     tmp = path + ".tmp"
     try:
-        with open(tmp, "w", newline="") as f:
-            f.write(text)
+        if isinstance(text, (bytes, bytearray, memoryview)):
+            with open(tmp, "wb") as f:
+                f.write(text)
+        else:
+            with open(tmp, "w", newline="") as f:
+                f.write(text)
         os.replace(tmp, path)
     except OSError as e:
         raise P.IoError(f"cannot write {path}: {e}") from e
@@ -123,28 +128,11 @@ def report_text(name: str, scenario: str, threads: int, extra) -> str:
 # policy CSV (runner.cpp:90-166)
 
 
-def policy_to_csv(model: P.Model, actions: np.ndarray) -> str:
-    n = model.state_count()
-    arity = model.state_arity()
-    last = model.decode(n - 1)  # the last state holds every digit's maximum
-    radices = [d + 1 for d in last]
-    idx = np.arange(n, dtype=np.int64)
-    digits = []
-    rem = idx
-    weights = [int(np.prod(radices[i + 1:])) for i in range(arity)]
-    for w in weights:
-        digits.append(rem // w)
-        rem = rem % w
-    cols = digits
-    if model.scenario() == "b":
-        nb = model.info.max_order_b + 1
-        cols = cols + [actions.astype(np.int64) // nb, actions.astype(np.int64) % nb]
-    else:
-        cols = cols + [actions.astype(np.int64)]
-    table = np.stack(cols, axis=1)
+def policy_to_csv(model: P.Model, actions: np.ndarray) -> bytes:
+    """runner.cpp:90-107: the header row, then one row per state formatted
+    on the device (pvi_policy_csv_format)."""
     header = csv_row(state_column_names(model) + action_column_names(model))
-    body = "\n".join(",".join(map(str, r)) for r in table.tolist())
-    return header + body + "\n"
+    return header.encode() + model.policy_csv_body(actions)
 
 
 def write_policy_outputs(model: P.Model, actions: np.ndarray, scenario: str, name: str,
@@ -167,31 +155,11 @@ def policy_from_csv(model: P.Model, csv_path: str) -> np.ndarray:
     if meta.get("fingerprint", "") != fp:
         raise P.FingerprintMismatch(f"policy fingerprint {meta.get('fingerprint', '')} does not "
                                     f"match the configured scenario's {fp}")
-    n = model.state_count()
-    arity = model.state_arity()
-    ncols = arity + len(action_column_names(model))
     try:
-        data = np.loadtxt(csv_path, delimiter=",", skiprows=1, dtype=np.int64, ndmin=2)
-    except ValueError as e:
-        raise P.FormatError(f"policy CSV is not numeric: {e}") from e
-    if data.shape[0] != n:
-        raise P.FormatError(f"policy CSV has {data.shape[0] + 1} rows, expected {n + 1}")
-    if data.shape[1] != ncols:
-        raise P.FormatError(f"policy CSV rows have {data.shape[1]} fields")
-    last = model.decode(n - 1)
-    radices = [d + 1 for d in last]
-    weights = np.array([int(np.prod(radices[i + 1:])) for i in range(arity)], np.int64)
-    digits = data[:, :arity]
-    if (digits < 0).any() or (digits >= np.array(radices)).any():
-        raise P.IndexingError("policy CSV tuple component out of range")
-    idx = digits @ weights
-    if model.scenario() == "b":
-        act = data[:, arity] * (model.info.max_order_b + 1) + data[:, arity + 1]
-    else:
-        act = data[:, arity]
-    out = np.zeros(n, np.uint32)
-    out[idx] = act
-    return out
+        text = open(csv_path, "rb").read()
+    except OSError as e:
+        raise P.IoError(f"cannot read {csv_path}: {e}") from e
+    return model.policy_from_csv_text(text)  # parsed on the device (pvi_policy_csv_parse)
 
 
 # ---------------------------------------------------------------------------
