@@ -276,9 +276,16 @@ def ours_arm(args, world, rank, local):
             dist.barrier()
         torch.cuda.synchronize()
 
+    exchange = os.environ.get("PVI_EXCHANGE", "peer")
+
     def timed(algorithm, steps, warmup, clocks=None):
+        nonlocal vprev, vnext
         model.set_algorithm(algorithm)
-        solver = ShardedValueIteration(model, cfg)
+        solver = ShardedValueIteration(model, cfg, exchange=exchange)
+        bufs = solver.buffers()
+        if bufs is not None:  # fused peer exchange: sweep into the IPC-shared replicas
+            bufs[0].copy_(vprev)
+            vprev, vnext = bufs
         for _ in range(warmup):
             solver.step(vprev, vnext, stats, test, hist)
         barrier()
@@ -365,6 +372,9 @@ def ours_arm(args, world, rank, local):
 
     if world > 1:
         roofline["exchange_bytes_per_rank"] = solver.read_set_bytes()
+        roofline["exchange"] = ("fused peer stores from the sweep (NVLink, IPC)" if solver.buffers() is not None
+                                else "NCCL all-to-all of the read set" if solver.plan is not None
+                                else "NCCL all-gather")
     line = {"metric": "bellman_evals_per_sec", "value": value, "unit": "evals/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",

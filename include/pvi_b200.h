@@ -258,6 +258,31 @@ int pvi_vi_sweep_device(const pvi_model* m, int precision, double gamma,
                         const void* const* hist_device, int n_hist, int want_stats,
                         double* stats_device, void* stream, char* err, size_t errlen);
 
+/* pvi_vi_sweep_device with the exchange fused into the sweep: for the
+ * factored Scenario B x_3-pair sweep (the only one whose read set is a
+ * function of the shard), the finalize of the stage-2 kernel also stores
+ * every V' entry of [lo, hi) into the replica of each peer whose next sweep
+ * reads it, over NVLink peer memory, as the state is finished.  peer_vnext:
+ * the peers' next-value buffers mapped into this process (pvi_ipc_open);
+ * peer_lo / peer_hi: the peers' shards.  After the peers' sweeps the caller
+ * synchronises the ranks (the convergence statistics' all-reduce does).
+ * PVI_ERR_PARAMETER for any other sweep, for periodic span, > 8 peers. */
+int pvi_vi_sweep_device_peers(const pvi_model* m, int precision, double gamma,
+                              const void* values_prev_device, void* values_next_device, uint64_t lo,
+                              uint64_t hi, int test, int want_stats, double* stats_device, void* stream,
+                              int n_peers, void* const* peer_values_next, const uint64_t* peer_lo,
+                              const uint64_t* peer_hi, char* err, size_t errlen);
+
+/* Device buffers shareable across processes (cudaMalloc, whole allocation)
+ * and their CUDA IPC handles (64 bytes): the peer buffers of
+ * pvi_vi_sweep_device_peers.  pvi_ipc_open maps a peer's buffer into this
+ * process (on the current device); pvi_ipc_close unmaps it. */
+int pvi_device_alloc(uint64_t bytes, void** out, char* err, size_t errlen);
+int pvi_device_free(void* p);
+int pvi_ipc_get_handle(void* device_ptr, uint8_t handle[64], char* err, size_t errlen);
+int pvi_ipc_open(const uint8_t handle[64], void** device_ptr, char* err, size_t errlen);
+int pvi_ipc_close(void* device_ptr);
+
 /* Cost-weighted contiguous partition of the state space into `parts`
  * shards (bounds has parts+1 entries), aligned to the kernel's state tiles. */
 int pvi_partition(const pvi_model* m, int parts, uint64_t* bounds);

@@ -333,6 +333,56 @@ int pvi_partition(const pvi_model* m, int parts, uint64_t* bounds) {
   return guarded(nullptr, 0, nullptr, [&] { partition(M(m), parts, bounds); });
 }
 
+int pvi_vi_sweep_device_peers(const pvi_model* m, int precision, double gamma,
+                              const void* values_prev_device, void* values_next_device, uint64_t lo,
+                              uint64_t hi, int test, int want_stats, double* stats_device, void* stream,
+                              int n_peers, void* const* peer_values_next, const uint64_t* peer_lo,
+                              const uint64_t* peer_hi, char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if (!m || !m->impl) fail(PVI_ERR_PARAMETER, "null model");
+    if (n_peers > 0 && (!peer_values_next || !peer_lo || !peer_hi)) fail(PVI_ERR_PARAMETER, "null peer arrays");
+    vi_sweep_device_peers(M(m), precision, gamma, values_prev_device, values_next_device, lo, hi, test,
+                          want_stats, stats_device, stream, n_peers, peer_values_next, peer_lo, peer_hi);
+  });
+}
+
+int pvi_device_alloc(uint64_t bytes, void** out, char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if (!out) fail(PVI_ERR_PARAMETER, "null out");
+    select_device(-1);
+    *out = nullptr;
+    PVI_CUDA(cudaMalloc(out, bytes));
+  });
+}
+
+int pvi_device_free(void* p) {
+  return guarded(nullptr, 0, nullptr, [&] {
+    if (p) PVI_CUDA(cudaFree(p));
+  });
+}
+
+int pvi_ipc_get_handle(void* device_ptr, uint8_t handle[64], char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    cudaIpcMemHandle_t h;
+    PVI_CUDA(cudaIpcGetMemHandle(&h, device_ptr));
+    static_assert(sizeof(h) == 64, "CUDA IPC handle size");
+    std::memcpy(handle, &h, 64);
+  });
+}
+
+int pvi_ipc_open(const uint8_t handle[64], void** device_ptr, char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    select_device(-1);
+    PVI_CUDA(cudaIpcOpenMemHandle(device_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int pvi_ipc_close(void* device_ptr) {
+  return guarded(nullptr, 0, nullptr, [&] { PVI_CUDA(cudaIpcCloseMemHandle(device_ptr)); });
+}
+
 int pvi_policy_csv_format(const pvi_model* m, const uint32_t* actions, char* out, uint64_t capacity,
                           uint64_t* length, char* err, size_t errlen) {
   return guarded(err, errlen, nullptr, [&] {

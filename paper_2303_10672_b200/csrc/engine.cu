@@ -1234,7 +1234,7 @@ template <typename T>
 void sweep_device_impl(const Model& m, double gamma, const void* vprev, void* vnext,
                        std::uint32_t* act, std::uint64_t lo, std::uint64_t hi, int test,
                        const void* const* hist, int n_hist, int want_stats, double* stats,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, const FinalizeArgs* peers = nullptr) {
   int device = 0;
   PVI_CUDA(cudaGetDevice(&device));
   const DevModel& dm = m.device_view(device);
@@ -1261,6 +1261,14 @@ void sweep_device_impl(const Model& m, double gamma, const void* vprev, void* vn
       for (int k = 0; k < 7; ++k) a.fa.hist[k] = hist[n_hist - 7 + k];
     }
   }
+  if (peers) {
+    a.fa.n_peers = peers->n_peers;
+    for (int q = 0; q < peers->n_peers; ++q) {
+      a.fa.peer_v[q] = peers->peer_v[q];
+      a.fa.peer_x3_lo[q] = peers->peer_x3_lo[q];
+      a.fa.peer_x3_hi[q] = peers->peer_x3_hi[q];
+    }
+  }
   launch_sweep<T>(m, dm, a, scratch, stream);
   if (want_stats && stats) k_stats_to_doubles<<<1, 1, 0, stream>>>(dstats->as<SweepStats>(), stats);
   PVI_CUDA(cudaGetLastError());
@@ -1277,6 +1285,36 @@ void vi_sweep_device(const Model& m, int precision, double gamma, const void* vp
     sweep_device_impl<float>(m, gamma, vprev, vnext, act, lo, hi, test, hist, n_hist, want_stats, stats, st);
   else
     sweep_device_impl<double>(m, gamma, vprev, vnext, act, lo, hi, test, hist, n_hist, want_stats, stats, st);
+}
+
+void vi_sweep_device_peers(const Model& m, int precision, double gamma, const void* vprev, void* vnext,
+                           std::uint64_t lo, std::uint64_t hi, int test, int want_stats, double* stats,
+                           void* stream, int n_peers, void* const* peer_vnext, const std::uint64_t* peer_lo,
+                           const std::uint64_t* peer_hi) {
+  if (lo > hi || hi > m.space.count) fail(PVI_ERR_PARAMETER, "state range out of bounds");
+  if (n_peers < 0 || n_peers > 8) fail(PVI_ERR_PARAMETER, "between 0 and 8 peers");
+  if (test == PVI_TEST_PERIODIC_SPAN) fail(PVI_ERR_PARAMETER, "peer sweep: periodic span not supported");
+  int device = 0;
+  PVI_CUDA(cudaGetDevice(&device));
+  if (!b_sweep_honours_xb_range(m, device))
+    fail(PVI_ERR_PARAMETER, "fused peer writes need the factored Scenario B x_3-pair sweep");
+  FinalizeArgs pf;
+  pf.n_peers = n_peers;
+  const int na = m.b_na;
+  const std::uint64_t n_xb = static_cast<std::uint64_t>(m.b_nb) * m.b_nb * m.b_nb;
+  const std::uint64_t per = static_cast<std::uint64_t>(na) * na * n_xb;
+  for (int q = 0; q < n_peers; ++q) {
+    if (!peer_vnext[q] || peer_lo[q] >= peer_hi[q] || peer_hi[q] > m.space.count)
+      fail(PVI_ERR_PARAMETER, "bad peer descriptor");
+    pf.peer_v[q] = peer_vnext[q];
+    pf.peer_x3_lo[q] = static_cast<int>(peer_lo[q] / per) / 2 * 2;
+    pf.peer_x3_hi[q] = std::min(na - 1, static_cast<int>((peer_hi[q] - 1) / per) / 2 * 2 + 1);
+  }
+  auto st = static_cast<cudaStream_t>(stream);
+  if (precision == 1)
+    sweep_device_impl<float>(m, gamma, vprev, vnext, nullptr, lo, hi, test, nullptr, 0, want_stats, stats, st, &pf);
+  else
+    sweep_device_impl<double>(m, gamma, vprev, vnext, nullptr, lo, hi, test, nullptr, 0, want_stats, stats, st, &pf);
 }
 
 // ---------------------------------------------------------------------------

@@ -22,6 +22,10 @@ void vi_sweep_device(const Model& m, int precision, double gamma, const void* vp
                      std::uint32_t* act, std::uint64_t lo, std::uint64_t hi, int test,
                      const void* const* hist, int n_hist, int want_stats, double* stats,
                      void* stream);
+void vi_sweep_device_peers(const Model& m, int precision, double gamma, const void* vprev, void* vnext,
+                           std::uint64_t lo, std::uint64_t hi, int test, int want_stats, double* stats,
+                           void* stream, int n_peers, void* const* peer_vnext, const std::uint64_t* peer_lo,
+                           const std::uint64_t* peer_hi);
 void partition(const Model& m, int parts, std::uint64_t* bounds);
 // policy CSV rows on the device (io_kernels.cu): the body (one row per
 // state) of runner.cpp's policy_to_csv; out = nullptr returns the length

@@ -59,6 +59,19 @@ __device__ __forceinline__ void state_stat(const FinalizeArgs& fa, std::uint64_t
   smin = fmin(smin, stat);
 }
 
+// Fused exchange: store V'[st] into each peer replica whose next sweep
+// reads it.  Slab r = x_a of the state; the peer's stage 1 reads row r when
+// r's x_3 digit is in its pair range, or r is a constants' row (x_2 = 0)
+// below its range's top (vi_kernels.cu sweep_read_runs).
+template <typename T>
+__device__ __forceinline__ void peer_store(const FinalizeArgs& fa, int xa, int na, int st, T v) {
+  const int ap = xa % (na * na), x2r = ap % na, x3r = ap / na;
+  for (int q = 0; q < fa.n_peers; ++q) {
+    const bool need = (x3r >= fa.peer_x3_lo[q] && x3r <= fa.peer_x3_hi[q]) || (x2r == 0 && x3r <= fa.peer_x3_hi[q]);
+    if (need) static_cast<T*>(fa.peer_v[q])[st] = v;
+  }
+}
+
 __device__ __forceinline__ void reduce_stats(double smax, double smin, unsigned long long bad,
                                              SweepStats* st) {
   if (st == nullptr) return;
@@ -2030,8 +2043,10 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw3(DevModel dm, const double
     const T best = static_cast<T>(__ldg(er_base + 2 * xa) + s_best[xl]);
     if (vout) vout[st - out_off] = best;
     if (WA && act) act[st - out_off] = s_arg[xl];
+    if (fa.n_peers) peer_store<T>(fa, xa, na, st, best);
     state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
   }
+  if (fa.n_peers) __threadfence_system();  // peer stores visible before the stats reach NCCL
   reduce_stats(smx, smn, bad, fa.stats);
 }
 
@@ -2292,8 +2307,10 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
     const T best = static_cast<T>(__ldg(er_base + 2 * xa) + s_best[xl]);
     if (vout) vout[st - out_off] = best;
     if (WA && act) act[st - out_off] = s_arg[xl];
+    if (fa.n_peers) peer_store<T>(fa, xa, na, st, best);
     state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
   }
+  if (fa.n_peers) __threadfence_system();  // peer stores visible before the stats reach NCCL
   reduce_stats(smx, smn, bad, fa.stats);
 }
 

@@ -19,6 +19,13 @@ struct FinalizeArgs {
   const void* hist[8] = {};      // device pointers, oldest..newest (newest = V_prev)
   double gamma = 0.0;
   SweepStats* stats = nullptr;   // device; nullptr disables the reduction
+  // Fused exchange over NVLink peer memory (factored B x_3-pair sweep): the
+  // finalize also stores each V' entry into the replica of every peer whose
+  // next sweep reads it (its x_3 rows, or its constants' rows x_2 = 0 with
+  // x_3 <= its x3_hi).  peer_v: IPC-mapped |S|-entry buffers of the peers.
+  int n_peers = 0;
+  void* peer_v[8] = {};
+  int peer_x3_lo[8] = {}, peer_x3_hi[8] = {};
 };
 
 template <typename T>

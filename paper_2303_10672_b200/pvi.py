@@ -494,6 +494,76 @@ def sweep_device(model: Model, precision: str, gamma: float, vprev_ptr: int, vne
                                         err, len(err)), err)
 
 
+def sweep_device_peers(model: Model, precision: str, gamma: float, vprev_ptr: int, vnext_ptr: int,
+                       lo: int, hi: int, peers: Sequence[tuple], test: Optional[str] = None,
+                       stats_ptr: Optional[int] = None, stream_ptr: Optional[int] = None):
+    """sweep_device with the exchange fused in (pvi_vi_sweep_device_peers):
+    `peers` = [(peer_vnext_ptr, peer_lo, peer_hi), ...], the peers' next-value
+    buffers mapped into this process (ipc_open) and their shards."""
+    t = -1 if test is None else _TEST_NAMES[test]
+    n = len(peers)
+    ptrs = (C.c_void_p * max(1, n))(*[int(p[0]) for p in peers])
+    plo = (C.c_uint64 * max(1, n))(*[int(p[1]) for p in peers])
+    phi = (C.c_uint64 * max(1, n))(*[int(p[2]) for p in peers])
+    err = _err_buf()
+    _raise(L.load().pvi_vi_sweep_device_peers(model.handle, int(precision == "f32"), gamma,
+                                              C.c_void_p(vprev_ptr), C.c_void_p(vnext_ptr), lo, hi, t,
+                                              int(stats_ptr is not None),
+                                              None if stats_ptr is None else C.c_void_p(stats_ptr),
+                                              None if stream_ptr is None else C.c_void_p(stream_ptr),
+                                              n, ptrs, plo, phi, err, len(err)), err)
+
+
+class DeviceBuffer:
+    """A cudaMalloc'd device buffer (pvi_device_alloc) that other processes
+    can map (ipc_handle / ipc_open); usable from torch through
+    __cuda_array_interface__ (torch.as_tensor(buf, device="cuda"))."""
+
+    def __init__(self, count: int, dtype=np.float64):
+        self.dtype = np.dtype(dtype)
+        self.count = int(count)
+        p = C.c_void_p()
+        err = _err_buf()
+        _raise(L.load().pvi_device_alloc(self.count * self.dtype.itemsize, C.byref(p), err, len(err)), err)
+        self.ptr = int(p.value)
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.count,), "typestr": self.dtype.str, "data": (self.ptr, False),
+                "version": 3, "strides": None}
+
+    def ipc_handle(self) -> bytes:
+        h = (C.c_uint8 * 64)()
+        err = _err_buf()
+        _raise(L.load().pvi_ipc_get_handle(C.c_void_p(self.ptr), h, err, len(err)), err)
+        return bytes(h)
+
+    def free(self):
+        if self.ptr:
+            L.load().pvi_device_free(C.c_void_p(self.ptr))
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map a peer process's DeviceBuffer (by its 64-byte handle) into this
+    process; returns the device pointer (ipc_close to unmap)."""
+    h = (C.c_uint8 * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    err = _err_buf()
+    _raise(L.load().pvi_ipc_open(h, C.byref(p), err, len(err)), err)
+    return int(p.value)
+
+
+def ipc_close(ptr: int):
+    _raise(L.load().pvi_ipc_close(C.c_void_p(ptr)), None)
+
+
 def profile_enable(on: bool = True):
     _raise(L.load().pvi_profile_enable(int(on)), None)
 

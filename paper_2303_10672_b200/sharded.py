@@ -21,6 +21,14 @@ ranks that is ~16 MiB received per rank per sweep instead of 112 MiB.
 The full replica is re-assembled (one all-gather) only where a caller needs
 all of V: checkpoints and the returned value vector.
 
+Fused exchange (exchange="peer").  The ranks' value buffers are CUDA-IPC
+shared (pvi_device_alloc / pvi_ipc_open), and the factored B sweep writes
+each finished V' entry straight into the replicas of the peers whose next
+sweep reads it, over NVLink peer memory, from the stage-2 finalize
+(pvi_vi_sweep_device_peers) -- the exchange overlaps the sweep instead of
+following it.  The MAX all-reduce of the statistics is the only collective
+left; it also orders every rank's stores before the next sweep.
+
 The per-slice sweep is injectable so the host logic (partition, exchange,
 reduction, history window, convergence) runs under `gloo` on CPU in tests;
 the default sweep is the device kernel through pvi_vi_sweep_device.
@@ -82,8 +90,13 @@ class ShardedValueIteration:
 
     def __init__(self, model: P.Model, config: Optional[P.ViConfig] = None,
                  device: Optional[torch.device] = None, sweep: Optional[SweepFn] = None,
-                 group=None):
+                 group=None, exchange: str = "auto"):
+        """exchange: "auto"/"runs" -- refresh the read set with one NCCL
+        all-to-all (all-gather when the sweep reads all of V); "peer" -- the
+        sweep itself stores V' into the peers' IPC-mapped replicas (factored
+        B x_3-pair sweep on CUDA devices; falls back to "runs" otherwise)."""
         self.model = model
+        self.exchange_mode = exchange
         self.cfg = config or P.ViConfig()
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -103,6 +116,46 @@ class ShardedValueIteration:
         self._send = torch.empty(self.maxlen, dtype=self.dtype, device=self.device)
         self._recv = torch.empty(self.maxlen * self.world, dtype=self.dtype, device=self.device)
         self._setup_read_sets()
+        self.peer = None
+        if (exchange == "peer" and self.world > 1 and self.plan is not None and sweep is None
+                and self.device.type == "cuda"):
+            self._setup_peers()
+
+    # -- fused peer exchange ---------------------------------------------------
+    def _setup_peers(self):
+        """Two IPC-shared value buffers per rank; map every peer's pair."""
+        bufs = [P.DeviceBuffer(self.n, np.float32 if self.dtype == torch.float32 else np.float64)
+                for _ in range(2)]
+        handles = [None] * self.world
+        dist.all_gather_object(handles, [b.ipc_handle() for b in bufs], group=self.group)
+        mapped = [[None] * self.world for _ in range(2)]
+        for q in range(self.world):
+            if q != self.rank:
+                for k in range(2):
+                    mapped[k][q] = P.ipc_open(handles[q][k])
+        self.peer = {"bufs": bufs, "tensors": [torch.as_tensor(b, device=self.device) for b in bufs],
+                     "mapped": mapped}
+
+    def buffers(self):
+        """The two value buffers the fused exchange writes into (peer mode),
+        else None: callers that step() with these get the fused path."""
+        return None if self.peer is None else tuple(self.peer["tensors"])
+
+    def _peer_slot(self, v: torch.Tensor):
+        if self.peer is None:
+            return None
+        for k, t in enumerate(self.peer["tensors"]):
+            if t.data_ptr() == v.data_ptr():
+                return k
+        return None
+
+    def close(self):
+        if self.peer is not None:
+            for k in range(2):
+                for q, ptr in enumerate(self.peer["mapped"][k]):
+                    if ptr:
+                        P.ipc_close(ptr)
+            self.peer = None
 
     # -- read sets -----------------------------------------------------------
     def _setup_read_sets(self):
@@ -184,10 +237,28 @@ class ShardedValueIteration:
              test: Optional[int] = None, hist: List[torch.Tensor] = ()):
         """One sweep + exchange.  `hist` holds the 7 previous vectors
         (oldest..newest, newest = vprev) when test is the periodic span."""
+        k = self._peer_slot(vnext)
+        if k is not None and test != P.PERIODIC_SPAN:
+            self._peer_sweep(vprev, vnext, k, test, stats)
+            return
         self.sweep(vprev, vnext, None, self.lo, self.hi, test, list(hist), stats)
         if stats is not None:
             self.reduce_stats(stats)
         self.refresh(vnext)
+
+    def _peer_sweep(self, vprev, vnext, k, test, stats):
+        names = {0: "value_span", 1: "change_span"}
+        peers = [(self.peer["mapped"][k][q], self.bounds[q], self.bounds[q + 1])
+                 for q in range(self.world) if q != self.rank]
+        P.sweep_device_peers(self.model, self.cfg.precision, self.gamma, vprev.data_ptr(),
+                             vnext.data_ptr(), self.lo, self.hi, peers,
+                             None if test is None else names[test],
+                             None if stats is None else stats.data_ptr(),
+                             torch.cuda.current_stream().cuda_stream)
+        if stats is not None:
+            self.reduce_stats(stats)  # also orders every rank's peer stores
+        else:
+            dist.barrier(group=self.group)
 
     # -- full solve ----------------------------------------------------------
     def solve(self, resume: Optional[P.Checkpoint] = None) -> ShardedResult:
@@ -198,7 +269,10 @@ class ShardedValueIteration:
                                   f"configured capacity of {cfg.max_states}", n)
         if not cfg.epsilon > 0:
             raise P.ParameterError("value iteration: epsilon must be > 0")
-        ring = [torch.empty(n, dtype=self.dtype, device=self.device) for _ in range(self.hist_cap)]
+        if self.peer is not None and self.hist_cap == 2:
+            ring = list(self.peer["tensors"])
+        else:
+            ring = [torch.empty(n, dtype=self.dtype, device=self.device) for _ in range(self.hist_cap)]
         if resume is not None:
             if resume.fingerprint != self.model.fingerprint():
                 raise P.FingerprintMismatch("resume checkpoint fingerprint does not match model")
@@ -233,10 +307,14 @@ class ShardedValueIteration:
             want = cfg.fixed_iterations == 0 and len(order) + 1 >= self.hist_cap
             hist = [ring[k] for k in order] if (want and self.test == P.PERIODIC_SPAN) else []
             ts = time.perf_counter()
-            self.sweep(ring[prev], ring[nxt], None, self.lo, self.hi,
-                       self.test if want else None, hist, stats)
-            self.reduce_stats(stats)
-            self.refresh(ring[nxt])
+            if self._peer_slot(ring[nxt]) is not None and self.test != P.PERIODIC_SPAN:
+                self._peer_sweep(ring[prev], ring[nxt], self._peer_slot(ring[nxt]),
+                                 self.test if want else None, stats)
+            else:
+                self.sweep(ring[prev], ring[nxt], None, self.lo, self.hi,
+                           self.test if want else None, hist, stats)
+                self.reduce_stats(stats)
+                self.refresh(ring[nxt])
             st = stats.cpu().numpy()  # the one host round trip per sweep
             sweep_s += time.perf_counter() - ts
             order.append(nxt)

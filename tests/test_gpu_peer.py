@@ -1,0 +1,178 @@
+"""Fused exchange over peer memory (pvi_vi_sweep_device_peers): the
+factored B stage-2 finalize stores each V' entry into the replica of every
+peer whose next sweep reads it.
+
+One GPU here, so the peers are (1) other buffers of the same process and
+(2) a second process on the same GPU mapping this one's buffer through CUDA
+IPC (ranks synchronised with gloo on the host; no kernel waits on another
+process).  Both check: the peer replica holds exactly this shard's V' on the
+peer's read set (pvi_sweep_read_runs) and nothing elsewhere."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _covered(runs, lo, hi, n):
+    mask = np.zeros(n, bool)
+    for a, b in runs:
+        mask[max(a, lo):min(b, hi)] = True
+    return mask
+
+
+def test_peer_stores_in_process(pvi):
+    m = pvi.make_preset("b/m3/exp1").set_algorithm("factored")
+    n = m.state_count()
+    b = [int(x) for x in m.partition(8)]
+    V = np.random.default_rng(6).uniform(-20.0, 20.0, n)
+    full, _ = pvi.bellman_backup_batch(m, V, 0, n)
+    vprev = torch.as_tensor(V, device="cuda")
+    r = 3
+    lo, hi = b[r], b[r + 1]
+    vnext = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+    peers = {q: pvi.DeviceBuffer(n) for q in (1, 6, 7)}
+    tens = {q: torch.as_tensor(buf, device="cuda") for q, buf in peers.items()}
+    for t in tens.values():
+        t.fill_(float("nan"))
+    stats = torch.empty(4, dtype=torch.float64, device="cuda")
+    pvi.sweep_device_peers(m, "f64", m.discount(), vprev.data_ptr(), vnext.data_ptr(), lo, hi,
+                           [(peers[q].ptr, b[q], b[q + 1]) for q in peers], test="change_span",
+                           stats_ptr=stats.data_ptr(), stream_ptr=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(vnext[lo:hi].cpu().numpy(), full[lo:hi])
+    for q, t in tens.items():
+        got = t.cpu().numpy()
+        want_mask = _covered(m.sweep_read_runs(b[q], b[q + 1]), lo, hi, n)
+        assert want_mask.any()
+        np.testing.assert_array_equal(got[want_mask], full[want_mask])
+        assert np.isnan(got[~want_mask]).all()  # nothing outside the peer's read set
+    # the same sweep without peers: identical values and statistics
+    vnext2 = torch.empty_like(vnext)
+    stats2 = torch.empty_like(stats)
+    pvi.sweep_device(m, "f64", m.discount(), vprev.data_ptr(), vnext2.data_ptr(), None, lo, hi,
+                     "change_span", (), stats2.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(vnext2[lo:hi], vnext[lo:hi]) and torch.equal(stats2, stats)
+
+
+def test_peer_sweep_refuses_other_sweeps(pvi):
+    m = pvi.make_preset("b/m3/exp4")  # exact: reads all of V
+    v = torch.zeros(m.state_count(), dtype=torch.float64, device="cuda")
+    with pytest.raises(pvi.ParameterError):
+        pvi.sweep_device_peers(m, "f64", m.discount(), v.data_ptr(), v.data_ptr(), 0, 10, [])
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _ipc_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2303_10672_b200 as pvi
+        m = pvi.make_preset("b/m3/exp1").set_algorithm("factored")
+        n = m.state_count()
+        b = [int(x) for x in m.partition(world)]
+        lo, hi = b[rank], b[rank + 1]
+        V = np.random.default_rng(6).uniform(-20.0, 20.0, n)
+        mine = pvi.DeviceBuffer(n)
+        tmine = torch.as_tensor(mine, device="cuda")
+        tmine.fill_(float("nan"))
+        torch.cuda.synchronize()
+        handles = [None] * world
+        dist.all_gather_object(handles, mine.ipc_handle())
+        peers = []
+        for p in range(world):
+            if p != rank:
+                peers.append((pvi.ipc_open(handles[p]), b[p], b[p + 1]))
+        vprev = torch.as_tensor(V, device="cuda")
+        pvi.sweep_device_peers(m, "f64", m.discount(), vprev.data_ptr(), tmine.data_ptr(), lo, hi, peers,
+                               stream_ptr=torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        dist.barrier()  # every rank's sweep (and its stores into the others) is done
+        got = tmine.cpu().numpy()
+        full, _ = pvi.bellman_backup_batch(m, V, 0, n)
+        own = np.zeros(n, bool)
+        own[lo:hi] = True
+        runs = m.sweep_read_runs(lo, hi)
+        need = np.zeros(n, bool)
+        for a, bb in runs:
+            need[a:bb] = True
+        ok_own = bool(np.array_equal(got[own], full[own]))
+        from_peers = need & ~own
+        ok_peer = bool(np.array_equal(got[from_peers], full[from_peers]))
+        untouched = bool(np.isnan(got[~(own | need)]).all())
+        dist.barrier()
+        for p in peers:
+            pvi.ipc_close(p[0])
+        q.put((rank, ok_own, ok_peer, untouched, int(from_peers.sum())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_stores_across_processes_ipc():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, ok_own, ok_peer, untouched, n_from_peers in res:
+        assert n_from_peers > 0
+        assert ok_own and ok_peer and untouched, (rank, ok_own, ok_peer, untouched)
+
+
+def _solve_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2303_10672_b200 as pvi
+        from paper_2303_10672_b200.sharded import ShardedValueIteration
+        m = pvi.make_preset("b/m3/exp1").set_algorithm("factored")
+        solver = ShardedValueIteration(m, pvi.ViConfig(), exchange="peer")
+        assert solver.buffers() is not None
+        res = solver.solve()
+        solver.close()
+        if rank == 0:
+            q.put((res.iterations, res.converged, res.values, res.policy))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_solve_with_fused_peer_exchange(pvi):
+    """The whole sharded solve with the exchange fused into the sweep (two
+    ranks on one GPU, IPC-mapped replicas, gloo for the statistics): the
+    same iterations, values and policy as the single-process solve."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_solve_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    it, conv, values, policy = q.get(timeout=900)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want = pvi.run_value_iteration(pvi.make_preset("b/m3/exp1").set_algorithm("factored"))
+    assert (it, conv) == (want.iterations, want.converged)
+    np.testing.assert_array_equal(values, want.values)
+    np.testing.assert_array_equal(policy, want.policy)
