@@ -377,7 +377,7 @@ struct BGeo {
 };
 
 template <typename T, int M, int NB, int NCH>
-__global__ void __launch_bounds__(256, NCH == 1 ? 2 : 3) k_sweep_b_geo(DevModel dm, const T* __restrict__ V,
+__global__ void __launch_bounds__(256, NCH == 1 ? 2 : 3) k_sweep_b_geo(DevModel dm, const double* __restrict__ GV,
                                                         T* __restrict__ part_v,
                                                         std::uint8_t* __restrict__ part_a,
                                                         T* __restrict__ qout, std::uint64_t lo,
@@ -474,11 +474,13 @@ __global__ void __launch_bounds__(256, NCH == 1 ? 2 : 3) k_sweep_b_geo(DevModel 
       }
       const double revenue = revenue_a + crb * hb;
       const double head = revenue - cva_oa;
-      const T* va = V + base + ob0 * WB;
+      // GV = gamma * V, formed once per sweep (k_scale_v) with the same
+      // rounding the reference's per-term gamma * V[next] has
+      const double* gva = GV + base + ob0 * WB;
 #pragma unroll
       for (int ob = 0; ob < OBC; ++ob) {
-        const double v = static_cast<double>(__ldg(va + ob * WB));
-        q[ob] += static_cast<T>(p * (head - cvb[ob] + gamma * v));
+        const double gv = __ldg(gva + ob * WB);
+        q[ob] += static_cast<T>(p * (head - cvb[ob] + gv));
       }
     }
   }
@@ -3018,6 +3020,15 @@ __global__ void __launch_bounds__(256) k_initial_b(DevModel dm, const double* __
   out[s] = tab[2 * b_pair_index(dm, s, imb)];
 }
 
+// GV[i] = gamma * V[i] in double: the factor of every reference backup
+// term, formed once per sweep instead of once per term (bit-identical).
+template <typename T>
+__global__ void __launch_bounds__(256) k_scale_v(const T* __restrict__ V, double gamma, double* __restrict__ gv,
+                                                 std::uint64_t n) {
+  const std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) gv[i] = gamma * static_cast<double>(V[i]);
+}
+
 template <typename T>
 __global__ void k_cast_from_f64(const double* __restrict__ in, T* __restrict__ out, std::uint64_t n) {
   const std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -3741,11 +3752,14 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
       (void)attr_set;
       cudaFuncSetAttribute(k_sweep_b<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(k_sweep_b<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      count_launches(a.want_values ? 2 : 1);
+      count_launches(a.want_values ? 3 : 2);
       {
       MainKernelScope prof(stream);
       const std::size_t sm_geo = sizeof(double) * (2 * (dm.b_len_a + dm.b_len_b + 1));
       bool done = false;
+      // gamma * V once per sweep: one FP64 multiply per reference term fewer
+      double* gv = scratch.get<double>(8, dm.n_states, stream);
+      k_scale_v<T><<<grid_for(dm.n_states, 256), 256, 0, stream>>>(a.v, a.gamma, gv, dm.n_states);
       // Two order_b chunks per (state, order_a) when NB is even: half the
       // accumulators per thread -> 3 CTAs/SM instead of 2 (K1-B).
 #define PVI_B_GEO(MM, NNB, NCH)                                                               \
@@ -3753,7 +3767,7 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
     const dim3 g2(grid.x, grid.y * NCH);                                                      \
     T* pv2 = a.want_values ? scratch.get<T>(0, static_cast<std::size_t>(dm.b_na) * NCH * nr, stream) : nullptr; \
     std::uint8_t* pa2 = a.want_values ? scratch.get<std::uint8_t>(1, static_cast<std::size_t>(dm.b_na) * NCH * nr, stream) : nullptr; \
-    k_sweep_b_geo<T, MM, NNB, NCH><<<g2, block, sm_geo, stream>>>(dm, a.v, pv2, pa2, a.qout, lo, hi, t0, a.gamma); \
+    k_sweep_b_geo<T, MM, NNB, NCH><<<g2, block, sm_geo, stream>>>(dm, gv, pv2, pa2, a.qout, lo, hi, t0, a.gamma); \
     pv = pv2;                                                                                 \
     pa = pa2;                                                                                 \
     n_chunks = dm.b_na * NCH;                                                                 \
