@@ -316,8 +316,9 @@ def ours_arm(args, world, rank, local):
     terms = model.terms_per_sweep()
     value = terms * args.steps / (total_ms * 1e-3)
 
-    # roofline of the dominant kernel (K1 backup) on this rank
-    shard_terms = state_terms(model, solver.lo, solver.hi)
+    # roofline of the dominant kernel (K1 backup) on this rank (its own states:
+    # a state range, or the (pair, x_b range) blocks of a unit shard)
+    shard_terms = sum(state_terms(model, a, b) for a, b in solver.own_runs[solver.rank])
     bpt = BYTES_PER_TERM[args.precision]
     achieved_gbs = bpt * shard_terms * k_launches / (kernel_ms * 1e-3) / 1e9 if kernel_ms else 0.0
     peaks = {}
@@ -375,6 +376,8 @@ def ours_arm(args, world, rank, local):
         roofline["exchange"] = ("fused peer stores from the sweep (NVLink, IPC)" if solver.buffers() is not None
                                 else "NCCL all-to-all of the read set" if solver.plan is not None
                                 else "NCCL all-gather")
+        roofline["shards"] = ("units: (x_3 pair, x_b column range) blocks" if solver.units is not None
+                              else "contiguous state ranges")
     line = {"metric": "bellman_evals_per_sec", "value": value, "unit": "evals/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",

@@ -273,6 +273,25 @@ int pvi_vi_sweep_device_peers(const pvi_model* m, int precision, double gamma,
                               int n_peers, void* const* peer_values_next, const uint64_t* peer_lo,
                               const uint64_t* peer_hi, char* err, size_t errlen);
 
+/* Unit shards (factored Scenario B x_3-pair sweep only): unit u = pair * G + g,
+ * G = |x_b| / 16 column groups; a shard is a contiguous unit range, i.e. a
+ * few (x_3 pair, x_b column range) blocks, so shards can be cut finer than
+ * whole pairs.  pvi_unit_partition: cost-weighted unit bounds (parts + 1).
+ * pvi_unit_runs: which = 0 the shard's own states, 1 the V runs its sweep
+ * reads (own states included); sorted disjoint runs[2i] .. runs[2i+1].
+ * pvi_vi_sweep_device_units: the shard's sweep (f64), with the optional
+ * fused peer stores of pvi_vi_sweep_device_peers (peers by unit range). */
+int pvi_unit_count(const pvi_model* m, uint64_t* count);
+int pvi_unit_partition(const pvi_model* m, int parts, uint64_t* bounds);
+int pvi_unit_runs(const pvi_model* m, uint64_t u_lo, uint64_t u_hi, int which, uint64_t* runs,
+                  size_t capacity, size_t* count);
+int pvi_vi_sweep_device_units(const pvi_model* m, int precision, double gamma,
+                              const void* values_prev_device, void* values_next_device,
+                              uint32_t* actions_device, uint64_t u_lo, uint64_t u_hi, int test,
+                              int want_stats, double* stats_device, void* stream, int n_peers,
+                              void* const* peer_values_next, const uint64_t* peer_u_lo,
+                              const uint64_t* peer_u_hi, char* err, size_t errlen);
+
 /* Device buffers shareable across processes (cudaMalloc, whole allocation)
  * and their CUDA IPC handles (64 bytes): the peer buffers of
  * pvi_vi_sweep_device_peers.  pvi_ipc_open maps a peer's buffer into this

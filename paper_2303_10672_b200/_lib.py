@@ -148,6 +148,10 @@ SIGNATURES = {
     "pvi_partition": (C.c_int, [_vp, C.c_int, _vp]),
     "pvi_sweep_read_runs": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(C.c_size_t)]),
     "pvi_vi_sweep_device_peers": (C.c_int, [_vp, C.c_int, C.c_double, _vp, _vp, C.c_uint64, C.c_uint64, C.c_int, C.c_int, _vp, _vp, C.c_int, _vp, _vp, _vp, C.c_char_p, C.c_size_t]),
+    "pvi_unit_count": (C.c_int, [_vp, C.POINTER(C.c_uint64)]),
+    "pvi_unit_partition": (C.c_int, [_vp, C.c_int, _vp]),
+    "pvi_unit_runs": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(C.c_size_t)]),
+    "pvi_vi_sweep_device_units": (C.c_int, [_vp, C.c_int, C.c_double, _vp, _vp, _vp, C.c_uint64, C.c_uint64, C.c_int, C.c_int, _vp, _vp, C.c_int, _vp, _vp, _vp, C.c_char_p, C.c_size_t]),
     "pvi_device_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]),
     "pvi_device_free": (C.c_int, [_vp]),
     "pvi_ipc_get_handle": (C.c_int, [_vp, _vp, C.c_char_p, C.c_size_t]),

@@ -346,6 +346,52 @@ int pvi_vi_sweep_device_peers(const pvi_model* m, int precision, double gamma,
   });
 }
 
+int pvi_unit_count(const pvi_model* m, uint64_t* count) {
+  return guarded(nullptr, 0, nullptr, [&] {
+    if (!m || !m->impl || !count) fail(PVI_ERR_PARAMETER, "null argument");
+    *count = unit_count(M(m));
+  });
+}
+
+int pvi_unit_partition(const pvi_model* m, int parts, uint64_t* bounds) {
+  return guarded(nullptr, 0, nullptr, [&] {
+    if (!m || !m->impl || !bounds) fail(PVI_ERR_PARAMETER, "null argument");
+    unit_partition(M(m), parts, bounds);
+  });
+}
+
+int pvi_unit_runs(const pvi_model* m, uint64_t u_lo, uint64_t u_hi, int which, uint64_t* runs,
+                  size_t capacity, size_t* count) {
+  return guarded(nullptr, 0, nullptr, [&] {
+    if (!m || !m->impl) fail(PVI_ERR_PARAMETER, "null model");
+    if (u_lo > u_hi || u_hi > unit_count(M(m))) fail(PVI_ERR_PARAMETER, "unit range out of bounds");
+    const auto r = which == 0 ? unit_own_runs(M(m), u_lo, u_hi) : unit_read_runs(M(m), u_lo, u_hi);
+    if (count) *count = r.size();
+    if (runs) {
+      if (capacity < r.size()) fail(PVI_ERR_PARAMETER, "unit_runs: capacity too small");
+      for (std::size_t i = 0; i < r.size(); ++i) {
+        runs[2 * i] = r[i].first;
+        runs[2 * i + 1] = r[i].second;
+      }
+    }
+  });
+}
+
+int pvi_vi_sweep_device_units(const pvi_model* m, int precision, double gamma,
+                              const void* values_prev_device, void* values_next_device,
+                              uint32_t* actions_device, uint64_t u_lo, uint64_t u_hi, int test,
+                              int want_stats, double* stats_device, void* stream, int n_peers,
+                              void* const* peer_values_next, const uint64_t* peer_u_lo,
+                              const uint64_t* peer_u_hi, char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if (!m || !m->impl) fail(PVI_ERR_PARAMETER, "null model");
+    if (n_peers > 0 && (!peer_values_next || !peer_u_lo || !peer_u_hi)) fail(PVI_ERR_PARAMETER, "null peer arrays");
+    vi_sweep_device_units(M(m), precision, gamma, values_prev_device, values_next_device, actions_device, u_lo,
+                          u_hi, test, want_stats, stats_device, stream, n_peers, peer_values_next, peer_u_lo,
+                          peer_u_hi);
+  });
+}
+
 int pvi_device_alloc(uint64_t bytes, void** out, char* err, size_t errlen) {
   return guarded(err, errlen, nullptr, [&] {
     if (!out) fail(PVI_ERR_PARAMETER, "null out");

@@ -1287,6 +1287,247 @@ void vi_sweep_device(const Model& m, int precision, double gamma, const void* vp
     sweep_device_impl<double>(m, gamma, vprev, vnext, act, lo, hi, test, hist, n_hist, want_stats, stats, st);
 }
 
+// ---------------------------------------------------------------------------
+// Unit shards of the factored B x_3-pair sweep.  Unit u = pair * G + g with
+// G = |x_b| / 16 column groups: a stage-2 CTA is (pair, x_b), so a shard of
+// consecutive units is a few (pair, column-group range) segments, and the
+// state space can be cut finer than whole pairs (8 pairs for 8 ranks left
+// the heaviest pair 36% above the lightest).
+
+namespace {
+
+struct UnitGeo {
+  int na, pairs;
+  std::uint64_t n_xb, groups, per_x3, per_pair;
+};
+
+UnitGeo unit_geo(const Model& m) {
+  if (!b_sweep_honours_xb_range(m, 0))
+    fail(PVI_ERR_PARAMETER, "unit shards need the factored Scenario B x_3-pair sweep");
+  UnitGeo g;
+  g.na = m.b_na;
+  g.pairs = (g.na + 1) / 2;
+  g.n_xb = static_cast<std::uint64_t>(m.b_nb) * m.b_nb * m.b_nb;
+  g.groups = g.n_xb / 16;
+  g.per_x3 = static_cast<std::uint64_t>(g.na) * g.na * g.n_xb;
+  g.per_pair = 2 * g.per_x3;
+  return g;
+}
+
+// A unit range as at most three launches' worth of work: a partial pair at
+// the head (a column range), a block of whole pairs, a partial pair at the
+// tail.  g_lo/g_hi are column groups, p_lo..p_hi pairs (equal for partials).
+struct UnitSeg {
+  int p_lo, p_hi;
+  std::uint32_t g_lo, g_hi;
+};
+
+std::vector<UnitSeg> unit_segments(const UnitGeo& g, std::uint64_t u_lo, std::uint64_t u_hi) {
+  std::vector<UnitSeg> out;
+  const std::uint32_t G = static_cast<std::uint32_t>(g.groups);
+  std::uint64_t u = u_lo;
+  while (u < u_hi) {
+    const int p = static_cast<int>(u / G);
+    const std::uint64_t p_start = static_cast<std::uint64_t>(p) * G;
+    const std::uint64_t p_end = p_start + G;
+    if (u == p_start && u_hi >= p_end) {
+      // whole pairs p .. p1 - 1
+      const int p1 = static_cast<int>(u_hi / G);
+      out.push_back({p, p1 - 1, 0u, G});
+      u = static_cast<std::uint64_t>(p1) * G;
+    } else {
+      const std::uint64_t end = std::min(u_hi, p_end);
+      out.push_back({p, p, static_cast<std::uint32_t>(u - p_start), static_cast<std::uint32_t>(end - p_start)});
+      u = end;
+    }
+  }
+  return out;
+}
+
+void merge_runs(std::vector<std::pair<std::uint64_t, std::uint64_t>>& runs) {
+  std::sort(runs.begin(), runs.end());
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> out;
+  for (const auto& r : runs) {
+    if (r.first >= r.second) continue;
+    if (!out.empty() && out.back().second >= r.first)
+      out.back().second = std::max(out.back().second, r.second);
+    else
+      out.push_back(r);
+  }
+  runs.swap(out);
+}
+
+// x_3 rows a unit range's stage 1 builds: its pairs' digits, and the
+// constants' rows below
+std::pair<int, int> unit_x3_range(const UnitGeo& g, std::uint64_t u_lo, std::uint64_t u_hi) {
+  const int p0 = static_cast<int>(u_lo / g.groups), p1 = static_cast<int>((u_hi - 1) / g.groups);
+  return {2 * p0, std::min(g.na - 1, 2 * p1 + 1)};
+}
+
+}  // namespace
+
+std::uint64_t unit_count(const Model& m) {
+  const UnitGeo g = unit_geo(m);
+  return static_cast<std::uint64_t>(g.pairs) * g.groups;
+}
+
+void unit_partition(const Model& m, int parts, std::uint64_t* bounds) {
+  if (parts < 1) fail(PVI_ERR_PARAMETER, "partition: parts must be >= 1");
+  const UnitGeo g = unit_geo(m);
+  const std::uint64_t nu = static_cast<std::uint64_t>(g.pairs) * g.groups;
+  // per-unit cost: the pair's stage-2 diagonal work plus its constants
+  // (Model::state_cost of the x_3-pair sweep)
+  std::vector<double> prefix(nu + 1, 0.0);
+  for (std::uint64_t u = 0; u < nu; ++u) {
+    const int p = static_cast<int>(u / g.groups);
+    prefix[u + 1] = prefix[u] + 34.4 + 2.0 * (p + 1);
+  }
+  bounds[0] = 0;
+  for (int k = 1; k < parts; ++k) {
+    const double target = prefix[nu] * k / parts;
+    const std::uint64_t u = static_cast<std::uint64_t>(
+        std::lower_bound(prefix.begin(), prefix.end(), target) - prefix.begin());
+    bounds[k] = std::max(bounds[k - 1], std::min(u, nu));
+  }
+  bounds[parts] = nu;
+}
+
+std::vector<std::pair<std::uint64_t, std::uint64_t>> unit_own_runs(const Model& m, std::uint64_t u_lo,
+                                                                   std::uint64_t u_hi) {
+  const UnitGeo g = unit_geo(m);
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> runs;
+  for (const UnitSeg& sg : unit_segments(g, u_lo, u_hi)) {
+    const std::uint64_t xa0 = static_cast<std::uint64_t>(2 * sg.p_lo) * g.na * g.na;
+    const std::uint64_t xa1 = std::min<std::uint64_t>(static_cast<std::uint64_t>(2 * sg.p_hi + 2) * g.na * g.na,
+                                                      static_cast<std::uint64_t>(g.na) * g.na * g.na);
+    for (std::uint64_t xa = xa0; xa < xa1; ++xa)
+      runs.emplace_back(xa * g.n_xb + 16ull * sg.g_lo, xa * g.n_xb + 16ull * sg.g_hi);
+  }
+  merge_runs(runs);
+  return runs;
+}
+
+std::vector<std::pair<std::uint64_t, std::uint64_t>> unit_read_runs(const Model& m, std::uint64_t u_lo,
+                                                                    std::uint64_t u_hi) {
+  const UnitGeo g = unit_geo(m);
+  auto runs = unit_own_runs(m, u_lo, u_hi);
+  if (u_lo >= u_hi) return runs;
+  const auto x3 = unit_x3_range(g, u_lo, u_hi);
+  const int n_r = g.na * g.na * g.na;
+  for (int r = 0; r < n_r; ++r) {
+    const int ap = r % (g.na * g.na), x2r = ap % g.na, x3r = ap / g.na;
+    if ((x3r >= x3.first && x3r <= x3.second) || (x2r == 0 && x3r <= x3.second))
+      runs.emplace_back(static_cast<std::uint64_t>(r) * g.n_xb, static_cast<std::uint64_t>(r + 1) * g.n_xb);
+  }
+  merge_runs(runs);
+  return runs;
+}
+
+namespace {
+
+template <typename T>
+void sweep_units_impl(const Model& m, double gamma, const void* vprev, void* vnext, std::uint32_t* act,
+                      std::uint64_t u_lo, std::uint64_t u_hi, int test, int want_stats, double* stats,
+                      cudaStream_t stream, const FinalizeArgs& peers) {
+  const UnitGeo g = unit_geo(m);
+  int device = 0;
+  PVI_CUDA(cudaGetDevice(&device));
+  const DevModel& dm = m.device_view(device);
+  static thread_local Scratch scratch;
+  static thread_local DevBuf* dstats = nullptr;
+  if (!dstats) dstats = new DevBuf(sizeof(SweepStats));
+  const std::uint64_t n = m.space.count;
+  bool first = true;
+  const bool st_on = want_stats && stats;
+  if (st_on && test == PVI_TEST_PERIODIC_SPAN) fail(PVI_ERR_PARAMETER, "unit sweep: periodic span not supported");
+  if (st_on) {
+    // the reduction of an empty range still has to publish its identity
+    init_stats_device(dstats->as<SweepStats>(), stream);
+    first = false;
+  }
+  const auto segs = unit_segments(g, u_lo, u_hi);
+  if (!segs.empty()) {
+    const UnitSeg& s0 = segs.front();
+    const UnitSeg& s1 = segs.back();
+    const std::uint32_t G = static_cast<std::uint32_t>(g.groups);
+    // stage 1: every row of the shard's pairs and the constants' rows below,
+    // in one launch; the non-constant rows of a partial head / tail pair
+    // only for its columns
+    SweepArgs<T> a;
+    a.v = static_cast<const T*>(vprev);
+    a.vout = static_cast<T*>(vnext);
+    a.out_off = 0;
+    a.gamma = gamma;
+    a.algorithm = PVI_ALGO_FACTORED;
+    a.want_values = true;
+    a.stages = 1;
+    a.lo = 0;
+    a.hi = n;
+    a.x3_rows_lo = 2 * s0.p_lo;
+    a.x3_rows_hi = std::min(g.na - 1, 2 * s1.p_hi + 1);
+    a.x3_rows_strict = 0;
+    if (s0.g_lo > 0 || (s0.p_lo == s1.p_hi && s0.g_hi < G)) {
+      a.head_pair = s0.p_lo;
+      a.head_g_lo = static_cast<int>(s0.g_lo);
+    }
+    if (s1.g_hi < G) {
+      a.tail_pair = s1.p_hi;
+      a.tail_g_hi = static_cast<int>(s1.g_hi);
+    }
+    launch_sweep<T>(m, dm, a, scratch, stream);
+    // stage 2: one 1-D grid over the shard's (pair, x_b) units, fused
+    // finalize (+ peer stores)
+    SweepArgs<T> b;
+    b.v = a.v;
+    b.vout = a.vout;
+    b.act = act;
+    b.out_off = 0;
+    b.gamma = gamma;
+    b.algorithm = PVI_ALGO_FACTORED;
+    b.want_values = true;
+    b.stages = 2;
+    b.lo = 0;
+    b.hi = n;
+    b.flat_lo = u_lo * 16;
+    b.flat_hi = u_hi * 16;
+    b.fa = peers;
+    if (st_on) {
+      b.fa.stats = dstats->as<SweepStats>();
+      b.fa.test = test;
+      b.fa.gamma = gamma;
+    }
+    b.init_stats = first;
+    launch_sweep<T>(m, dm, b, scratch, stream);
+  }
+  if (st_on) k_stats_to_doubles<<<1, 1, 0, stream>>>(dstats->as<SweepStats>(), stats);
+  PVI_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+void vi_sweep_device_units(const Model& m, int precision, double gamma, const void* vprev, void* vnext,
+                           std::uint32_t* act, std::uint64_t u_lo, std::uint64_t u_hi, int test, int want_stats,
+                           double* stats, void* stream, int n_peers, void* const* peer_vnext,
+                           const std::uint64_t* peer_u_lo, const std::uint64_t* peer_u_hi) {
+  const UnitGeo g = unit_geo(m);
+  const std::uint64_t nu = static_cast<std::uint64_t>(g.pairs) * g.groups;
+  if (u_lo > u_hi || u_hi > nu) fail(PVI_ERR_PARAMETER, "unit range out of bounds");
+  if (n_peers < 0 || n_peers > 8) fail(PVI_ERR_PARAMETER, "between 0 and 8 peers");
+  if (precision == 1) fail(PVI_ERR_PARAMETER, "unit shards run the f64 sweep");
+  FinalizeArgs pf;
+  pf.n_peers = n_peers;
+  for (int q = 0; q < n_peers; ++q) {
+    if (!peer_vnext[q] || peer_u_lo[q] >= peer_u_hi[q] || peer_u_hi[q] > nu)
+      fail(PVI_ERR_PARAMETER, "bad peer descriptor");
+    const auto x3 = unit_x3_range(g, peer_u_lo[q], peer_u_hi[q]);
+    pf.peer_v[q] = peer_vnext[q];
+    pf.peer_x3_lo[q] = x3.first;
+    pf.peer_x3_hi[q] = x3.second;
+  }
+  sweep_units_impl<double>(m, gamma, vprev, vnext, act, u_lo, u_hi, test, want_stats, stats,
+                           static_cast<cudaStream_t>(stream), pf);
+}
+
 void vi_sweep_device_peers(const Model& m, int precision, double gamma, const void* vprev, void* vnext,
                            std::uint64_t lo, std::uint64_t hi, int test, int want_stats, double* stats,
                            void* stream, int n_peers, void* const* peer_vnext, const std::uint64_t* peer_lo,

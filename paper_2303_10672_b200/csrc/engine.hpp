@@ -3,6 +3,8 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "model.hpp"
 
@@ -27,6 +29,17 @@ void vi_sweep_device_peers(const Model& m, int precision, double gamma, const vo
                            void* stream, int n_peers, void* const* peer_vnext, const std::uint64_t* peer_lo,
                            const std::uint64_t* peer_hi);
 void partition(const Model& m, int parts, std::uint64_t* bounds);
+// unit shards of the factored B x_3-pair sweep (engine.cu)
+std::uint64_t unit_count(const Model& m);
+void unit_partition(const Model& m, int parts, std::uint64_t* bounds);
+std::vector<std::pair<std::uint64_t, std::uint64_t>> unit_own_runs(const Model& m, std::uint64_t u_lo,
+                                                                   std::uint64_t u_hi);
+std::vector<std::pair<std::uint64_t, std::uint64_t>> unit_read_runs(const Model& m, std::uint64_t u_lo,
+                                                                    std::uint64_t u_hi);
+void vi_sweep_device_units(const Model& m, int precision, double gamma, const void* vprev, void* vnext,
+                           std::uint32_t* act, std::uint64_t u_lo, std::uint64_t u_hi, int test, int want_stats,
+                           double* stats, void* stream, int n_peers, void* const* peer_vnext,
+                           const std::uint64_t* peer_u_lo, const std::uint64_t* peer_u_hi);
 // policy CSV rows on the device (io_kernels.cu): the body (one row per
 // state) of runner.cpp's policy_to_csv; out = nullptr returns the length
 std::uint64_t policy_csv_format(const Model& m, const std::uint32_t* actions, char* out, std::uint64_t capacity);

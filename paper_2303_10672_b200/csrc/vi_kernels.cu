@@ -1145,17 +1145,22 @@ __device__ __forceinline__ void w16_row(const double* __restrict__ slab, double*
                                         double* __restrict__ v0t,
                                         const std::uint16_t* __restrict__ group_order,
                                         int n_groups, int n_r, int r, int tiled,
-                                        const double* s_pmf_b, const double* s_cdf_b) {
+                                        const double* s_pmf_b, const double* s_cdf_b,
+                                        int g_lo = 0, int g_cnt = -1) {
   constexpr int NB = 16, S8 = 8, OB4 = 4;
   const int stride = slab_stride(NB);
   if (threadIdx.x < NB) v0t[static_cast<std::size_t>(r) * NB + threadIdx.x] = slab[threadIdx.x];
   const int sub = threadIdx.x & 7;
   const int x1b = (sub >> 2) * S8;
   const int ob0 = (sub & 3) * OB4;
-  for (int gbase = 0; gbase < n_groups; gbase += blockDim.x >> 3) {
+  // a sub-range of groups (unit shards) runs in index order, the whole
+  // row in the stock-sorted order
+  const bool all_groups = g_cnt < 0 || g_cnt >= n_groups;
+  const int n_iter = all_groups ? n_groups : g_cnt;
+  for (int gbase = 0; gbase < n_iter; gbase += blockDim.x >> 3) {
     const int gi = gbase + (threadIdx.x >> 3);
-    const bool active = gi < n_groups;
-    const int grp = group_order[active ? gi : 0];
+    const bool active = gi < n_iter;
+    const int grp = all_groups ? group_order[active ? gi : 0] : g_lo + (active ? gi : 0);
     int xg[M + 1];
     int S = 0;
     {
@@ -1274,7 +1279,8 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16p(DevModel dm, const doubl
                                                         const std::uint16_t* __restrict__ group_order,
                                                         int n_groups, int n_xb, int n_bp, int n_r,
                                                         int x3_lo, int x3_hi, int tiled, int r_base,
-                                                        int r_count, int strict) {
+                                                        int r_count, int strict, int g_lo, int g_cnt,
+                                                        int hp, int hg_lo, int tp, int tg_hi) {
   constexpr int NB = 16;
   extern __shared__ double slabs[];  // 2 x [bp][ob]
   const int stride = slab_stride(NB);
@@ -1318,8 +1324,25 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16p(DevModel dm, const doubl
       asm volatile("cp.async.wait_all;\n" ::: "memory");
     }
     __syncthreads();
+    // unit shards: the main rows (x_2 != 0) of a partial head / tail pair
+    // only for that pair's columns; every other row for all columns
+    int rg_lo = g_lo, rg_cnt = g_cnt;
+    if (hp >= 0 || tp >= 0) {
+      const int ap = (r_base + t) % (na * na), x2r = ap % na, pr = (ap / na) / 2;
+      rg_lo = 0;
+      rg_cnt = -1;
+      if (x2r != 0 && pr == hp && pr == tp) {
+        rg_lo = hg_lo;
+        rg_cnt = tg_hi - hg_lo;
+      } else if (x2r != 0 && pr == hp) {
+        rg_lo = hg_lo;
+        rg_cnt = n_groups - hg_lo;
+      } else if (x2r != 0 && pr == tp) {
+        rg_cnt = tg_hi;
+      }
+    }
     w16_row<M>(slabs + buf * slab_sz, W, v0t, group_order, n_groups, n_r, r_base + t, tiled, s_pmf_b,
-               s_cdf_b);
+               s_cdf_b, rg_lo, rg_cnt);
     __syncthreads();  // the slab is refilled two rows later
     t = tn;
   }
@@ -1904,12 +1927,16 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw3(DevModel dm, const double
                                                        T* __restrict__ vout,
                                                        std::uint32_t* __restrict__ act,
                                                        std::uint64_t out_off, FinalizeArgs fa,
-                                                       int xb_base, int pr_base) {
+                                                       int xb_base, int pr_base, int flat_lo) {
   constexpr int NB = 16;
   extern __shared__ double sm[];
   const int na = dm.b_na, dn = dm.b_dn;
   const int n_xa = na * na * na;
-  const int pr = pr_base + static_cast<int>(blockIdx.x), xbi = xb_base + static_cast<int>(blockIdx.y);
+  // flat_lo >= 0: a 1-D grid over the (pair, x_b) units flat_lo.. (unit shards)
+  const int pr = flat_lo >= 0 ? (flat_lo + static_cast<int>(blockIdx.x)) / n_xb
+                              : pr_base + static_cast<int>(blockIdx.x);
+  const int xbi = flat_lo >= 0 ? (flat_lo + static_cast<int>(blockIdx.x)) % n_xb
+                               : xb_base + static_cast<int>(blockIdx.y);
   const int x3_0 = 2 * pr, n_x3 = min(2, na - x3_0);   // this CTA's x_3 values
   const int n_f = min(x3_0 + n_x3 - 1, na - 1) + 1;    // R(0, j) rows, j = 0..n_f-1
   const int n_rows = n_x3 * na + n_f;
@@ -2078,12 +2105,16 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
                                                        T* __restrict__ vout,
                                                        std::uint32_t* __restrict__ act,
                                                        std::uint64_t out_off, FinalizeArgs fa,
-                                                       int xb_base, int pr_base) {
+                                                       int xb_base, int pr_base, int flat_lo) {
   constexpr int NB = 16;
   extern __shared__ double sm[];
   const int na = dm.b_na, dn = dm.b_dn;
   const int n_xa = na * na * na;
-  const int pr = pr_base + static_cast<int>(blockIdx.x), xbi = xb_base + static_cast<int>(blockIdx.y);
+  // flat_lo >= 0: a 1-D grid over the (pair, x_b) units flat_lo.. (unit shards)
+  const int pr = flat_lo >= 0 ? (flat_lo + static_cast<int>(blockIdx.x)) / n_xb
+                              : pr_base + static_cast<int>(blockIdx.x);
+  const int xbi = flat_lo >= 0 ? (flat_lo + static_cast<int>(blockIdx.x)) % n_xb
+                               : xb_base + static_cast<int>(blockIdx.y);
   const int x3_0 = 2 * pr, n_x3 = min(2, na - x3_0);  // this CTA's x_3 values
   const int n_rows = n_x3 * na;
   // main rows R(u, x_3) [n_x3*na][ob] of W and V0; DB: two buffers (the
@@ -3090,6 +3121,11 @@ void count_launches(int n) {
 }
 }  // namespace
 
+void init_stats_device(SweepStats* st, cudaStream_t stream) {
+  k_init_stats<<<1, 1, 0, stream>>>(st);
+  count_launches(1);
+}
+
 bool profiling_enabled() {
   std::lock_guard<std::mutex> lock(g_prof.mu);
   return g_prof.on;
@@ -3345,8 +3381,15 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
   }
   // stage-1 row filter: the shard's rows (+ constants' rows), or exactly the
   // caller's x_3 rows (pipelined host-buffer backup)
-  const bool s1_strict = a.x3_rows_lo >= 0 && qw && M == 3 && std::is_same<T, double>::value && w16p_enabled();
-  const int s1_x3_lo = s1_strict ? a.x3_rows_lo : x3_lo, s1_x3_hi = s1_strict ? a.x3_rows_hi : x3_hi;
+  const bool s1_rows = a.x3_rows_lo >= 0 && qw && M == 3 && std::is_same<T, double>::value && w16p_enabled();
+  const bool s1_strict = s1_rows && a.x3_rows_strict;
+  const int s1_x3_lo = s1_rows ? a.x3_rows_lo : x3_lo, s1_x3_hi = s1_rows ? a.x3_rows_hi : x3_hi;
+  // x_b digit-group range of stage 1 (w16p only)
+  const std::uint32_t n_grp_all = static_cast<std::uint32_t>(n_bp);
+  const std::uint32_t g0 = std::min(a.xg_lo, n_grp_all), g1 = std::min(a.xg_hi, n_grp_all);
+  if ((g0 > 0 || g1 < n_grp_all) && !(std::is_same<T, double>::value && w16p_enabled()))
+    fail(PVI_ERR_PARAMETER, "factored b: x_b group ranges need the f64 persistent stage 1");
+  const int s1_g_lo = static_cast<int>(g0), s1_g_cnt = (g0 == 0 && g1 == n_grp_all) ? -1 : static_cast<int>(g1 - g0);
   {
     MainKernelScope prof(stream);
 #define PVI_BF(MM, NBX)                                                                            \
@@ -3365,7 +3408,8 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
               dm, reinterpret_cast<const double*>(a.v), W, v0t, dc.b_group_order_b,                \
               static_cast<int>(n_bp), static_cast<int>(n_xb), static_cast<int>(n_bp),               \
               static_cast<int>(n_r), s1_x3_lo, s1_x3_hi, qw && MM == 3 ? 1 : 0, static_cast<int>(r0), \
-              static_cast<int>(r1 - r0), s1_strict);                                               \
+              static_cast<int>(r1 - r0), s1_strict ? 1 : 0, s1_g_lo, s1_g_cnt, a.head_pair,       \
+              a.head_g_lo, a.tail_pair, a.tail_g_hi);                                              \
         } else {                                                                                   \
           k_b_fact_w16<T, MM><<<static_cast<unsigned>(r1 - r0), 256, sm0, stream>>>(               \
               dm, a.v, W, v0t, dc.b_group_order_b, static_cast<int>(n_bp), static_cast<int>(n_xb),  \
@@ -3398,11 +3442,16 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
         const std::uint64_t per_pr = 2ull * na * na * n_xb;                                       \
         const std::uint64_t pr0 = lo / per_pr;                                                    \
         const std::uint64_t pr1 = std::min<std::uint64_t>((hi + per_pr - 1) / per_pr, (na + 1) / 2); \
-        if (xb1 > xb0 && pr1 > pr0)                                                                \
+        if (a.flat_hi > a.flat_lo)                                                                  \
+          kq<<<dim3(static_cast<unsigned>(a.flat_hi - a.flat_lo), 1), 32, smq, stream>>>(          \
+              dm, W, v0t, dc.b_erpt, lo, hi, a.gamma, static_cast<int>(n_xb),                      \
+              static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa,  \
+              0, 0, static_cast<int>(a.flat_lo));                                                  \
+        else if (xb1 > xb0 && pr1 > pr0)                                                           \
           kq<<<dim3(static_cast<unsigned>(pr1 - pr0), static_cast<unsigned>(xb1 - xb0)), 32, smq, stream>>>( \
               dm, W, v0t, dc.b_erpt, lo, hi, a.gamma, static_cast<int>(n_xb),                      \
               static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa,  \
-              static_cast<int>(xb0), static_cast<int>(pr0));                                       \
+              static_cast<int>(xb0), static_cast<int>(pr0), -1);                                   \
       } else if (fused && dc.b_pt_unit && qp_enabled()) {                                          \
         auto kq = a.act ? k_b_fact_qp3<T, true> : k_b_fact_qp3<T, false>;                          \
         const std::size_t smp = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(double) + 1);       \
@@ -3601,7 +3650,7 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
   const std::uint64_t lo = a.lo, hi = a.hi, nr = hi - lo;
   if (nr == 0) return;
   FinalizeArgs fa = a.fa;
-  if (fa.stats) {
+  if (fa.stats && a.init_stats) {
     k_init_stats<<<1, 1, 0, stream>>>(fa.stats);
     count_launches(1);
   }

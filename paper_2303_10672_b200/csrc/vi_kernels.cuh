@@ -50,6 +50,18 @@ struct SweepArgs {
   // factored B stage 1 (m = 3, f64): when >= 0, only the W rows whose x_3
   // digit lies in [x3_rows_lo, x3_rows_hi] (no constants' rows of lower x_3)
   int x3_rows_lo = -1, x3_rows_hi = -1;
+  int x3_rows_strict = 1;  // 0: also the constants' rows (x_2 = 0, x_3 <= x3_rows_hi)
+  // factored B stage 1 (f64): only the x_b digit groups [xg_lo, xg_hi) (16
+  // consecutive x_b each) of the rows -- the x_b columns of a unit shard
+  std::uint32_t xg_lo = 0, xg_hi = ~0u;
+  // false: accumulate into fa.stats without resetting them first (the
+  // second and later launches of one multi-segment sweep)
+  bool init_stats = true;
+  // unit shards: stage 2 as a 1-D grid over the flat (pair, x_b) indices
+  // [flat_lo, flat_hi); stage 1 restricts the non-constant rows of a partial
+  // head pair to groups >= head_g_lo and of a partial tail pair to < tail_g_hi
+  std::uint64_t flat_lo = 0, flat_hi = 0;
+  int head_pair = -1, head_g_lo = 0, tail_pair = -1, tail_g_hi = 0;
 };
 
 // Grow-only device scratch buffers, keyed by slot.
@@ -91,6 +103,7 @@ std::vector<std::pair<std::uint64_t, std::uint64_t>> sweep_read_runs(const Model
                                                                      std::uint64_t hi);
 void profile_enable(bool on);
 bool profiling_enabled();
+void init_stats_device(SweepStats* st, cudaStream_t stream);
 void profile_read(double* ms, std::uint64_t* main_launches, std::uint64_t* all_launches);
 void launch_initial_b(const DevModel& dm, double* out, std::uint64_t n, cudaStream_t stream);
 template <typename T>

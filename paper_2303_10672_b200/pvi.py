@@ -303,6 +303,28 @@ class Model:
                                              len(err)), err)
         return out
 
+    def unit_count(self) -> int:
+        """Units of the factored B x_3-pair sweep (pvi_unit_count)."""
+        c = C.c_uint64()
+        _raise(L.load().pvi_unit_count(self._h, C.byref(c)), None)
+        return int(c.value)
+
+    def unit_partition(self, parts: int) -> np.ndarray:
+        b = np.zeros(parts + 1, np.uint64)
+        _raise(L.load().pvi_unit_partition(self._h, parts, _p(b)), None)
+        return b
+
+    def unit_runs(self, u_lo: int, u_hi: int, read: bool = False) -> list:
+        """State runs of a unit shard: its own states, or (read=True) what its
+        sweep reads (pvi_unit_runs)."""
+        cnt = C.c_size_t()
+        w = 1 if read else 0
+        _raise(L.load().pvi_unit_runs(self._h, u_lo, u_hi, w, None, 0, C.byref(cnt)), None)
+        buf = np.zeros(2 * cnt.value, np.uint64)
+        _raise(L.load().pvi_unit_runs(self._h, u_lo, u_hi, w, buf.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                      cnt.value, C.byref(cnt)), None)
+        return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(cnt.value)]
+
     def sweep_read_runs(self, lo: int, hi: int) -> list:
         """State runs [(a, b), ...] of V that a sweep of shard [lo, hi) reads
         (pvi_sweep_read_runs): what a multi-GPU driver must refresh."""
@@ -509,6 +531,27 @@ def sweep_device_peers(model: Model, precision: str, gamma: float, vprev_ptr: in
     _raise(L.load().pvi_vi_sweep_device_peers(model.handle, int(precision == "f32"), gamma,
                                               C.c_void_p(vprev_ptr), C.c_void_p(vnext_ptr), lo, hi, t,
                                               int(stats_ptr is not None),
+                                              None if stats_ptr is None else C.c_void_p(stats_ptr),
+                                              None if stream_ptr is None else C.c_void_p(stream_ptr),
+                                              n, ptrs, plo, phi, err, len(err)), err)
+
+
+def sweep_device_units(model: Model, gamma: float, vprev_ptr: int, vnext_ptr: int, u_lo: int, u_hi: int,
+                       peers: Sequence[tuple] = (), test: Optional[str] = None,
+                       stats_ptr: Optional[int] = None, stream_ptr: Optional[int] = None,
+                       actions_ptr: Optional[int] = None):
+    """The sweep of unit shard [u_lo, u_hi) (pvi_vi_sweep_device_units, f64),
+    optionally storing into peers' replicas: peers = [(ptr, peer_u_lo, peer_u_hi)]."""
+    t = -1 if test is None else _TEST_NAMES[test]
+    n = len(peers)
+    ptrs = (C.c_void_p * max(1, n))(*[int(p[0]) for p in peers])
+    plo = (C.c_uint64 * max(1, n))(*[int(p[1]) for p in peers])
+    phi = (C.c_uint64 * max(1, n))(*[int(p[2]) for p in peers])
+    err = _err_buf()
+    _raise(L.load().pvi_vi_sweep_device_units(model.handle, 0, gamma, C.c_void_p(vprev_ptr),
+                                              C.c_void_p(vnext_ptr),
+                                              None if actions_ptr is None else C.c_void_p(actions_ptr),
+                                              u_lo, u_hi, t, int(stats_ptr is not None),
                                               None if stats_ptr is None else C.c_void_p(stats_ptr),
                                               None if stream_ptr is None else C.c_void_p(stream_ptr),
                                               n, ptrs, plo, phi, err, len(err)), err)

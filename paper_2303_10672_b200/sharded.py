@@ -90,7 +90,7 @@ class ShardedValueIteration:
 
     def __init__(self, model: P.Model, config: Optional[P.ViConfig] = None,
                  device: Optional[torch.device] = None, sweep: Optional[SweepFn] = None,
-                 group=None, exchange: str = "auto"):
+                 group=None, exchange: str = "auto", shards: str = "auto"):
         """exchange: "auto"/"runs" -- refresh the read set with one NCCL
         all-to-all (all-gather when the sweep reads all of V); "peer" -- the
         sweep itself stores V' into the peers' IPC-mapped replicas (factored
@@ -107,10 +107,32 @@ class ShardedValueIteration:
         self.bounds = [int(b) for b in model.partition(self.world)]
         self.lo, self.hi = self.bounds[self.rank], self.bounds[self.rank + 1]
         self.maxlen = max(self.bounds[r + 1] - self.bounds[r] for r in range(self.world))
+        # Unit shards (factored B x_3-pair sweep): rank r owns the (pair, x_b
+        # column range) blocks of units [ub[r], ub[r+1]) -- balanced finer
+        # than whole pairs.  shards: "auto" (units where the sweep supports
+        # them and there is more than one rank), "units", "range".
+        self.units = None
+        if shards != "range" and self.world > 1:
+            try:
+                nu = model.unit_count()
+            except P.Error:
+                nu = 0
+            if nu and (shards == "units" or sweep is None):
+                self.units = [int(b) for b in model.unit_partition(self.world)]
+        if self.units is not None:
+            ub = self.units
+            self.u_lo, self.u_hi = ub[self.rank], ub[self.rank + 1]
+            self.own_runs = [model.unit_runs(ub[r], ub[r + 1]) for r in range(self.world)]
+            self.read_runs = [model.unit_runs(ub[r], ub[r + 1], read=True) for r in range(self.world)]
+        else:
+            self.own_runs = [[(self.bounds[r], self.bounds[r + 1])] for r in range(self.world)]
+            self.read_runs = None
+        self._own_idx = None
         self.dtype = torch.float32 if self.cfg.precision == "f32" else torch.float64
         self.gamma = self.cfg.gamma if self.cfg.gamma is not None else model.discount()
         self.test = (model.default_convergence_test() if self.cfg.convergence_test is None
                      else P._TEST_NAMES[self.cfg.convergence_test])
+        self.injected = sweep is not None
         self.sweep = sweep or device_sweep(model, self.cfg.precision, self.gamma)
         self.hist_cap = 8 if self.test == P.PERIODIC_SPAN else 2
         self._send = torch.empty(self.maxlen, dtype=self.dtype, device=self.device)
@@ -157,28 +179,53 @@ class ShardedValueIteration:
                         P.ipc_close(ptr)
             self.peer = None
 
+    # -- the rank's sweep --------------------------------------------------------
+    def _sweep(self, vprev, vnext, actions, test, hist, stats, peers=None):
+        """This rank's sweep: its state range, or its unit shard."""
+        if self.units is None:
+            self.sweep(vprev, vnext, actions, self.lo, self.hi, test, list(hist), stats)
+            return
+        if self.injected:
+            self.sweep(vprev, vnext, actions, self.u_lo, self.u_hi, test, list(hist), stats)
+            return
+        names = {0: "value_span", 1: "change_span"}
+        P.sweep_device_units(self.model, self.gamma, vprev.data_ptr(), vnext.data_ptr(), self.u_lo, self.u_hi,
+                             peers or (), None if test is None else names[test],
+                             None if stats is None else stats.data_ptr(),
+                             torch.cuda.current_stream().cuda_stream,
+                             None if actions is None else actions.data_ptr())
+
     # -- read sets -----------------------------------------------------------
+    @staticmethod
+    def _intersect(ra, rb):
+        """Indices in both run lists (sorted, disjoint runs)."""
+        out, i, j = [], 0, 0
+        while i < len(ra) and j < len(rb):
+            a, b = max(ra[i][0], rb[j][0]), min(ra[i][1], rb[j][1])
+            if a < b:
+                out.append(np.arange(a, b, dtype=np.int64))
+            if ra[i][1] < rb[j][1]:
+                i += 1
+            else:
+                j += 1
+        return np.concatenate(out) if out else np.zeros(0, np.int64)
+
     def _setup_read_sets(self):
         """Index plan of the read-set all-to-all (or None: every rank reads
         all of V, so the refresh is the all-gather)."""
         self.plan = None
         if self.world == 1:
             return
-        runs = [self.model.sweep_read_runs(self.bounds[r], self.bounds[r + 1])
-                for r in range(self.world)]
-        if all(rr == [(0, self.n)] for rr in runs):
+        runs = self.read_runs or [self.model.sweep_read_runs(self.bounds[r], self.bounds[r + 1])
+                                  for r in range(self.world)]
+        if self.units is None and all(rr == [(0, self.n)] for rr in runs):
             return
-
-        def clip(rr, a, b):
-            parts = [np.arange(max(x, a), min(y, b), dtype=np.int64) for x, y in rr
-                     if max(x, a) < min(y, b)]
-            return np.concatenate(parts) if parts else np.zeros(0, np.int64)
-
         me = self.rank
-        send = [clip(runs[q], self.lo, self.hi) if q != me else np.zeros(0, np.int64)
+        own = self.own_runs
+        send = [self._intersect(runs[q], own[me]) if q != me else np.zeros(0, np.int64)
                 for q in range(self.world)]
-        recv = [clip(runs[me], self.bounds[q], self.bounds[q + 1]) if q != me
-                else np.zeros(0, np.int64) for q in range(self.world)]
+        recv = [self._intersect(runs[me], own[q]) if q != me else np.zeros(0, np.int64)
+                for q in range(self.world)]
         dev = self.device
         self.plan = {
             "send_idx": torch.from_numpy(np.concatenate(send)).to(dev),
@@ -198,10 +245,16 @@ class ShardedValueIteration:
             return (self.n - (self.hi - self.lo)) * item
         return sum(self.plan["recv_splits"]) * item
 
+    def own_states(self) -> int:
+        return sum(b - a for a, b in self.own_runs[self.rank])
+
     # -- collectives ---------------------------------------------------------
     def exchange(self, v: torch.Tensor, send=None, recv=None):
         """All-gather every rank's slice of `v` into every replica."""
         if self.world == 1:
+            return
+        if self.units is not None:
+            self._exchange_units(v)
             return
         send = self._send if send is None else send
         recv = self._recv if recv is None else recv
@@ -212,6 +265,22 @@ class ShardedValueIteration:
             a, b = self.bounds[r], self.bounds[r + 1]
             if r != self.rank and b > a:
                 v[a:b].copy_(recv[r * self.maxlen:r * self.maxlen + (b - a)])
+
+    def _exchange_units(self, v: torch.Tensor):
+        """Full-replica all-gather for unit shards (own states are index sets)."""
+        if self._own_idx is None:
+            idx = [torch.from_numpy(np.concatenate([np.arange(a, b, dtype=np.int64) for a, b in rr]))
+                   .to(self.device) for rr in self.own_runs]
+            self._own_idx = idx
+        idx = self._own_idx
+        maxc = max(len(x) for x in idx)
+        send = torch.zeros(maxc, dtype=v.dtype, device=v.device)
+        send[:len(idx[self.rank])] = v.index_select(0, idx[self.rank])
+        recv = torch.empty(maxc * self.world, dtype=v.dtype, device=v.device)
+        dist.all_gather_into_tensor(recv, send, group=self.group)
+        for q in range(self.world):
+            if q != self.rank:
+                v.index_copy_(0, idx[q], recv[q * maxc:q * maxc + len(idx[q])])
 
     def refresh(self, v: torch.Tensor):
         """Make every entry the next sweep of this rank reads current: the
@@ -241,20 +310,25 @@ class ShardedValueIteration:
         if k is not None and test != P.PERIODIC_SPAN:
             self._peer_sweep(vprev, vnext, k, test, stats)
             return
-        self.sweep(vprev, vnext, None, self.lo, self.hi, test, list(hist), stats)
+        self._sweep(vprev, vnext, None, test, hist, stats)
         if stats is not None:
             self.reduce_stats(stats)
         self.refresh(vnext)
 
     def _peer_sweep(self, vprev, vnext, k, test, stats):
         names = {0: "value_span", 1: "change_span"}
-        peers = [(self.peer["mapped"][k][q], self.bounds[q], self.bounds[q + 1])
-                 for q in range(self.world) if q != self.rank]
-        P.sweep_device_peers(self.model, self.cfg.precision, self.gamma, vprev.data_ptr(),
-                             vnext.data_ptr(), self.lo, self.hi, peers,
-                             None if test is None else names[test],
-                             None if stats is None else stats.data_ptr(),
-                             torch.cuda.current_stream().cuda_stream)
+        if self.units is not None:
+            ub = self.units
+            peers = [(self.peer["mapped"][k][q], ub[q], ub[q + 1]) for q in range(self.world) if q != self.rank]
+            self._sweep(vprev, vnext, None, test, (), stats, peers)
+        else:
+            peers = [(self.peer["mapped"][k][q], self.bounds[q], self.bounds[q + 1])
+                     for q in range(self.world) if q != self.rank]
+            P.sweep_device_peers(self.model, self.cfg.precision, self.gamma, vprev.data_ptr(),
+                                 vnext.data_ptr(), self.lo, self.hi, peers,
+                                 None if test is None else names[test],
+                                 None if stats is None else stats.data_ptr(),
+                                 torch.cuda.current_stream().cuda_stream)
         if stats is not None:
             self.reduce_stats(stats)  # also orders every rank's peer stores
         else:
@@ -311,8 +385,7 @@ class ShardedValueIteration:
                 self._peer_sweep(ring[prev], ring[nxt], self._peer_slot(ring[nxt]),
                                  self.test if want else None, stats)
             else:
-                self.sweep(ring[prev], ring[nxt], None, self.lo, self.hi,
-                           self.test if want else None, hist, stats)
+                self._sweep(ring[prev], ring[nxt], None, self.test if want else None, hist, stats)
                 self.reduce_stats(stats)
                 self.refresh(ring[nxt])
             st = stats.cpu().numpy()  # the one host round trip per sweep
@@ -336,8 +409,8 @@ class ShardedValueIteration:
                 break
         vfinal = ring[order[-1]]
         actions = torch.zeros(n, dtype=torch.int32, device=self.device)
-        self.sweep(vfinal, ring[order[0]] if len(order) > 1 else torch.empty_like(vfinal),
-                   actions, self.lo, self.hi, None, [], None)
+        self._sweep(vfinal, ring[order[0]] if len(order) > 1 else torch.empty_like(vfinal),
+                    actions, None, [], None)
         self.exchange(actions, send=torch.empty(self.maxlen, dtype=torch.int32, device=self.device),
                       recv=torch.empty(self.maxlen * self.world, dtype=torch.int32,
                                        device=self.device))

@@ -176,3 +176,48 @@ def test_sharded_solve_with_fused_peer_exchange(pvi):
     assert (it, conv) == (want.iterations, want.converged)
     np.testing.assert_array_equal(values, want.values)
     np.testing.assert_array_equal(policy, want.policy)
+
+
+# --- unit shards: (x_3 pair, x_b column range) blocks ------------------------
+
+@pytest.mark.parametrize("parts", [8, 5, 3])
+def test_unit_shards_equal_full_sweep(pvi, parts):
+    """Every rank's unit-shard sweep (a few (pair, x_b range) segments) is
+    bit-identical to its states of one full sweep, reads only its read
+    runs (all else NaN), and the shards' statistics combine to the full
+    sweep's."""
+    m = pvi.make_preset("b/m3/exp1").set_algorithm("factored")
+    n = m.state_count()
+    V = np.random.default_rng(9).uniform(-20.0, 20.0, n)
+    vprev = torch.as_tensor(V, device="cuda")
+    full = torch.empty_like(vprev)
+    fst = torch.empty(4, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    pvi.sweep_device(m, "f64", m.discount(), vprev.data_ptr(), full.data_ptr(), None, 0, n, "change_span",
+                     (), fst.data_ptr(), st)
+    b = [int(x) for x in m.unit_partition(parts)]
+    assert b[0] == 0 and b[-1] == m.unit_count() and len(set(b)) == parts + 1
+    covered = np.zeros(n, np.int32)
+    agg = np.array([-np.inf, -np.inf, -np.inf])
+    for r in range(parts):
+        own = m.unit_runs(b[r], b[r + 1])
+        rd = m.unit_runs(b[r], b[r + 1], read=True)
+        Vp = torch.full_like(vprev, float("nan"))
+        for x, y in rd:
+            Vp[x:y] = vprev[x:y]
+        out = torch.full_like(vprev, float("nan"))
+        sts = torch.empty(4, dtype=torch.float64, device="cuda")
+        pvi.sweep_device_units(m, m.discount(), Vp.data_ptr(), out.data_ptr(), b[r], b[r + 1],
+                               test="change_span", stats_ptr=sts.data_ptr(), stream_ptr=st)
+        torch.cuda.synchronize()
+        o = out.cpu().numpy()
+        f = full.cpu().numpy()
+        mask = np.zeros(n, bool)
+        for x, y in own:
+            mask[x:y] = True
+        covered += mask
+        np.testing.assert_array_equal(o[mask], f[mask])
+        assert np.isnan(o[~mask]).all()
+        agg = np.maximum(agg, sts.cpu().numpy()[:3])
+    assert (covered == 1).all()  # the shards tile the state space
+    np.testing.assert_array_equal(agg, fst.cpu().numpy()[:3])

@@ -183,3 +183,74 @@ def test_read_set_exchange_delivers_every_read(world):
         np.testing.assert_array_equal(full, want)
         # the read set is a fraction of the all-gather's volume
         assert received < 0.5 * (n - (bounds[rank + 1] - bounds[rank])) * 8
+
+
+def _fake_unit_sweep(model):
+    """_fake_sweep over a unit shard: writes its own (pair, x_b range) runs
+    from a checksum of its whole read set."""
+    def sweep(vprev, vnext, actions, u_lo, u_hi, test, hist, stats):
+        c = _runs_checksum(vprev, model.unit_runs(u_lo, u_hi, read=True))
+        for a, b in model.unit_runs(u_lo, u_hi):
+            s = torch.arange(a, b, dtype=torch.float64)
+            vnext[a:b] = torch.remainder(3.0 * vprev[a:b] + c + s, MOD)
+        if stats is not None:
+            stats[:] = torch.tensor([0.0, 0.0, NEG, 0.0], dtype=torch.float64)
+    return sweep
+
+
+def _unit_worker(rank, world, port, preset, steps, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2303_10672_b200 as P
+        from paper_2303_10672_b200.sharded import ShardedValueIteration
+        m = P.make_preset(preset).set_algorithm("factored")
+        n = m.state_count()
+        solver = ShardedValueIteration(m, P.ViConfig(), device=torch.device("cpu"),
+                                       sweep=_fake_unit_sweep(m), shards="units")
+        assert solver.units is not None and solver.plan is not None
+        v = torch.remainder(torch.arange(n, dtype=torch.float64) * 7.0, MOD)
+        w = torch.empty_like(v)
+        for _ in range(steps):
+            solver.step(v, w)
+            v, w = w, v
+        ub = solver.units
+        runs = m.unit_runs(ub[rank], ub[rank + 1], read=True)
+        mine = {(a, b): v[a:b].clone().numpy() for a, b in runs}
+        solver.exchange(v)
+        out_q.put((rank, mine, v.numpy().copy(), solver.read_set_bytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [3, 4])
+def test_unit_shard_exchange_delivers_every_read(world):
+    import paper_2303_10672_b200 as P
+    preset, steps = "b/m3/exp1", 2
+    m = P.make_preset(preset).set_algorithm("factored")
+    n = m.state_count()
+    ub = [int(b) for b in m.unit_partition(world)]
+    v = torch.remainder(torch.arange(n, dtype=torch.float64) * 7.0, MOD)
+    for _ in range(steps):
+        w = v.clone()
+        for r in range(world):
+            c = _runs_checksum(v, m.unit_runs(ub[r], ub[r + 1], read=True))
+            for a, b in m.unit_runs(ub[r], ub[r + 1]):
+                w[a:b] = torch.remainder(3.0 * v[a:b] + c + torch.arange(a, b, dtype=torch.float64), MOD)
+        v = w
+    want = v.numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_unit_worker, args=(r, world, port, preset, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=900) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, mine, full, received in got:
+        for (a, b), vals in mine.items():
+            np.testing.assert_array_equal(vals, want[a:b])
+        np.testing.assert_array_equal(full, want)
+        assert 0 < received < 0.6 * n * 8
