@@ -376,6 +376,8 @@ def ours_arm(args, world, rank, local):
         roofline["exchange"] = ("fused peer stores from the sweep (NVLink, IPC)" if solver.buffers() is not None
                                 else "NCCL all-to-all of the read set" if solver.plan is not None
                                 else "NCCL all-gather")
+        if solver.peer_error:
+            roofline["peer_fallback"] = solver.peer_error
         roofline["shards"] = ("units: (x_3 pair, x_b column range) blocks" if solver.units is not None
                               else "contiguous state ranges")
     line = {"metric": "bellman_evals_per_sec", "value": value, "unit": "evals/s",

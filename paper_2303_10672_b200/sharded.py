@@ -139,22 +139,45 @@ class ShardedValueIteration:
         self._recv = torch.empty(self.maxlen * self.world, dtype=self.dtype, device=self.device)
         self._setup_read_sets()
         self.peer = None
+        self.peer_error = None
         if (exchange == "peer" and self.world > 1 and self.plan is not None and sweep is None
                 and self.device.type == "cuda"):
             self._setup_peers()
 
     # -- fused peer exchange ---------------------------------------------------
     def _setup_peers(self):
-        """Two IPC-shared value buffers per rank; map every peer's pair."""
-        bufs = [P.DeviceBuffer(self.n, np.float32 if self.dtype == torch.float32 else np.float64)
-                for _ in range(2)]
-        handles = [None] * self.world
-        dist.all_gather_object(handles, [b.ipc_handle() for b in bufs], group=self.group)
+        """Two IPC-shared value buffers per rank; map every peer's pair.
+        Every rank must take the same exchange path, so the ranks agree (one
+        MIN all-reduce) and all fall back to the read-set all-to-all if any
+        of them could not map its peers (e.g. no peer access)."""
+        bufs, handles, why = [], [None] * self.world, ""
+        try:
+            bufs = [P.DeviceBuffer(self.n, np.float32 if self.dtype == torch.float32 else np.float64)
+                    for _ in range(2)]
+            mine = [b.ipc_handle() for b in bufs]
+        except P.Error as e:
+            mine, why = None, str(e)
+        dist.all_gather_object(handles, mine, group=self.group)
         mapped = [[None] * self.world for _ in range(2)]
-        for q in range(self.world):
-            if q != self.rank:
-                for k in range(2):
-                    mapped[k][q] = P.ipc_open(handles[q][k])
+        ok = all(h is not None for h in handles)
+        if ok:
+            try:
+                for q in range(self.world):
+                    if q != self.rank:
+                        for k in range(2):
+                            mapped[k][q] = P.ipc_open(handles[q][k])
+            except P.Error as e:
+                ok, why = False, str(e)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=self.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        if int(flag.item()) == 0:
+            for k in range(2):
+                for ptr in mapped[k]:
+                    if ptr:
+                        P.ipc_close(ptr)
+            self.peer_error = why or "a peer rank could not map the IPC buffers"
+            self.exchange_mode = "runs"
+            return
         self.peer = {"bufs": bufs, "tensors": [torch.as_tensor(b, device=self.device) for b in bufs],
                      "mapped": mapped}
 
