@@ -430,9 +430,13 @@ def ours_arm(args, world, rank, local):
             if world == 1:  # the product API: pvi_vi_solve, V resident on the device throughout
                 res = P.run_value_iteration(model, cfg)
                 api = "pvi_vi_solve (run_value_iteration)"
-            else:           # one process per GPU, NCCL exchange per sweep
-                res = ShardedValueIteration(model, cfg).solve()
-                api = "sharded.ShardedValueIteration"
+            else:           # one process per GPU; the bench step's exchange per sweep
+                sv = ShardedValueIteration(model, cfg, exchange=exchange)
+                try:
+                    res = sv.solve()
+                finally:
+                    sv.close()
+                api = f"sharded.ShardedValueIteration (exchange={sv.exchange_mode})"
             calls.append(time.perf_counter() - t0)
             runs.append(res)
         best = min(range(2), key=lambda i: runs[i].wall_seconds)

@@ -148,7 +148,7 @@ class ShardedValueIteration:
     def _setup_peers(self):
         """Two IPC-shared value buffers per rank; map every peer's pair.
         Every rank must take the same exchange path, so the ranks agree (one
-        MIN all-reduce) and all fall back to the read-set all-to-all if any
+        all-gather of their flags) and all fall back to the read-set all-to-all if any
         of them could not map its peers (e.g. no peer access)."""
         bufs, handles, why = [], [None] * self.world, ""
         try:
@@ -168,9 +168,9 @@ class ShardedValueIteration:
                             mapped[k][q] = P.ipc_open(handles[q][k])
             except P.Error as e:
                 ok, why = False, str(e)
-        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=self.device)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
-        if int(flag.item()) == 0:
+        oks = [None] * self.world
+        dist.all_gather_object(oks, ok, group=self.group)
+        if not all(oks):
             for k in range(2):
                 for ptr in mapped[k]:
                     if ptr:
@@ -195,7 +195,10 @@ class ShardedValueIteration:
         return None
 
     def close(self):
+        """Unmap the peers' buffers (collective in peer mode: every rank's
+        stores into them are done before any rank unmaps or frees)."""
         if self.peer is not None:
+            dist.barrier(group=self.group)
             for k in range(2):
                 for q, ptr in enumerate(self.peer["mapped"][k]):
                     if ptr:

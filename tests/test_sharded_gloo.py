@@ -254,3 +254,65 @@ def test_unit_shard_exchange_delivers_every_read(world):
             np.testing.assert_array_equal(vals, want[a:b])
         np.testing.assert_array_equal(full, want)
         assert 0 < received < 0.6 * n * 8
+
+
+# --- fused peer exchange setup: all ranks agree ------------------------------
+
+def _peer_setup_worker(rank, world, port, fail_rank, fail_where, out_q):
+    """_setup_peers with the device calls stubbed: one rank cannot allocate
+    or map; every rank must fall back to the read-set exchange together."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2303_10672_b200 as P
+        from paper_2303_10672_b200 import sharded as S
+
+        class FakeBuf:
+            def __init__(self, count, dtype):
+                if rank == fail_rank and fail_where == "alloc":
+                    raise P.DeviceError("cudaMalloc failed (stub)")
+
+            def ipc_handle(self):
+                return bytes([rank]) * 64
+
+        opened, closed = [], []
+
+        def fake_open(h):
+            if rank == fail_rank and fail_where == "open":
+                raise P.DeviceError("peer access unavailable (stub)")
+            opened.append(h[0])
+            return 1000 + h[0]
+
+        S.P.DeviceBuffer = FakeBuf
+        S.P.ipc_open = fake_open
+        S.P.ipc_close = lambda ptr: closed.append(ptr)
+        m = P.make_preset("b/m2/exp1").set_algorithm("factored")
+        solver = S.ShardedValueIteration(m, P.ViConfig(), device=torch.device("cpu"),
+                                         sweep=_fake_sweep(m.sweep_read_runs))
+        solver._setup_peers()
+        out_q.put((rank, solver.peer is None, solver.exchange_mode, solver.peer_error,
+                   sorted(opened), sorted(closed)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_where", ["alloc", "open"])
+def test_peer_setup_falls_back_on_every_rank(fail_where):
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_setup_worker, args=(r, world, port, 1, fail_where, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, no_peer, mode, why, opened, closed in res:
+        assert no_peer and mode == "runs" and why, (rank, no_peer, mode, why)
+        # whatever a healthy rank mapped before the vote is unmapped again
+        assert [1000 + q for q in opened] == closed
+    if fail_where == "open":  # the healthy ranks had mapped both peers' two buffers
+        assert [len(r[4]) for r in res] == [4, 0, 4]
