@@ -19,6 +19,15 @@ namespace pvi_b200 {
                                            " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
   } while (0)
 
+// Host -> device copy of a one-off table that is complete when this returns.
+// A plain cudaMemcpy from pageable memory may return before its DMA lands,
+// and every kernel here runs on a non-blocking stream, which does not wait
+// for the legacy stream the copy was queued on.
+inline void upload_bytes(void* dst, const void* src, std::size_t bytes) {
+  PVI_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+  PVI_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+}
+
 __host__ __device__ inline int ipos(int x) { return x > 0 ? x : 0; }
 
 // Order-preserving map from double to u64 so that atomicMax/atomicMin on

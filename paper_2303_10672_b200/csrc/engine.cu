@@ -36,7 +36,7 @@ const U* upload(DeviceCopy& dc, const std::vector<U>& host) {
   if (host.empty()) return nullptr;
   void* p = nullptr;
   PVI_CUDA(cudaMalloc(&p, host.size() * sizeof(U)));
-  PVI_CUDA(cudaMemcpy(p, host.data(), host.size() * sizeof(U), cudaMemcpyHostToDevice));
+  upload_bytes(p, host.data(), host.size() * sizeof(U));
   dc.allocations.push_back(p);
   return static_cast<const U*>(p);
 }

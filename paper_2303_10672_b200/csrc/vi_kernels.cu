@@ -109,6 +109,24 @@ __device__ __forceinline__ void reduce_stats(double smax, double smin, unsigned 
   }
 }
 
+// reduce_stats for one-warp CTAs: shuffles only (reduce_stats' 768 bytes of
+// static shared memory would cost k_b_fact_qw4 one resident CTA per SM)
+__device__ __forceinline__ void reduce_stats_warp(double smax, double smin, unsigned long long bad,
+                                                  SweepStats* st) {
+  if (st == nullptr) return;
+  for (int o = 16; o > 0; o >>= 1) {
+    smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+    smin = fmin(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+    const unsigned long long ob = __shfl_xor_sync(0xffffffffu, bad, o);
+    bad = ob < bad ? ob : bad;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (smax != -DBL_MAX) atomicMax(&st->max_key, dkey(smax));
+    if (smin != DBL_MAX) atomicMin(&st->min_key, dkey(smin));
+    if (bad != ~0ull) atomicMin(&st->first_bad, bad);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // FIFO / LIFO ageing of a stock profile x[1..m] (scenario_a.cpp:18-40,
 // scenario_b.cpp:18-26).  Writes next[1..m-1]; returns units expiring.
@@ -2344,7 +2362,7 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
     state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
   }
   if (fa.n_peers) __threadfence_system();  // peer stores visible before the stats reach NCCL
-  reduce_stats(smx, smn, bad, fa.stats);
+  reduce_stats_warp(smx, smn, bad, fa.stats);
 }
 
 // ---------------------------------------------------------------------------
@@ -3324,8 +3342,8 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
       void* q2 = nullptr;
       PVI_CUDA(cudaMalloc(&q1, oa_h.size() * 2));
       PVI_CUDA(cudaMalloc(&q2, ob_h.size() * 2));
-      PVI_CUDA(cudaMemcpy(q1, oa_h.data(), oa_h.size() * 2, cudaMemcpyHostToDevice));
-      PVI_CUDA(cudaMemcpy(q2, ob_h.data(), ob_h.size() * 2, cudaMemcpyHostToDevice));
+      upload_bytes(q1, oa_h.data(), oa_h.size() * 2);
+      upload_bytes(q2, ob_h.data(), ob_h.size() * 2);
       dc.allocations.push_back(q1);
       dc.allocations.push_back(q2);
       dc.b_order_a = static_cast<std::uint16_t*>(q1);
@@ -3348,7 +3366,7 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
         std::stable_sort(go.begin(), go.end(), [&](int x, int y) { return gs[x] < gs[y]; });
         void* q = nullptr;
         PVI_CUDA(cudaMalloc(&q, go.size() * 2));
-        PVI_CUDA(cudaMemcpy(q, go.data(), go.size() * 2, cudaMemcpyHostToDevice));
+        upload_bytes(q, go.data(), go.size() * 2);
         dc.allocations.push_back(q);
         return static_cast<std::uint16_t*>(q);
       };
@@ -3697,7 +3715,7 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
             }
             void* q = nullptr;
             PVI_CUDA(cudaMalloc(&q, tab.size() * sizeof(double)));
-            PVI_CUDA(cudaMemcpy(q, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+            upload_bytes(q, tab.data(), tab.size() * sizeof(double));
             dc.allocations.push_back(q);
             dc.a_cdf_sf = static_cast<double*>(q);
             dc.a_pd = pdh;
