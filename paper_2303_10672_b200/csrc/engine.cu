@@ -1375,12 +1375,14 @@ void unit_partition(const Model& m, int parts, std::uint64_t* bounds) {
   if (parts < 1) fail(PVI_ERR_PARAMETER, "partition: parts must be >= 1");
   const UnitGeo g = unit_geo(m);
   const std::uint64_t nu = static_cast<std::uint64_t>(g.pairs) * g.groups;
-  // per-unit cost: the pair's stage-2 diagonal work plus its constants
-  // (Model::state_cost of the x_3-pair sweep)
+  // per-unit cost: the pair's stage-2 diagonal work plus its constants,
+  // fitted to per-shard stage-2 times on a B200 (8 unit shards: a pair-7
+  // CTA costs ~1.15x a pair-0 CTA, not the 1.38x the FMA counts give: the
+  // constants' j loop overlaps the row copies)
   std::vector<double> prefix(nu + 1, 0.0);
   for (std::uint64_t u = 0; u < nu; ++u) {
     const int p = static_cast<int>(u / g.groups);
-    prefix[u + 1] = prefix[u] + 34.4 + 2.0 * (p + 1);
+    prefix[u + 1] = prefix[u] + 34.4 + 0.8 * (p + 1);
   }
   bounds[0] = 0;
   for (int k = 1; k < parts; ++k) {

@@ -114,6 +114,10 @@ struct DeviceCopy {
   bool b_pt_unit = false;
   std::uint16_t* b_group_order = nullptr;    // A-side x_2..x_M digit groups by stock
   std::uint16_t* b_group_order_b = nullptr;  // B-side x_2..x_M digit groups by stock
+  // Stage-1 work lists of shard sweeps (k_b_fact_w16p): (row, group range,
+  // flags) items balanced over the persistent CTAs, keyed by the launch's
+  // row filter and column ranges; built once per key.
+  std::map<std::vector<int>, std::pair<void*, int>> b_s1_items;
   // Per-device workspace reused by the host-buffer entry points
   // (engine.cu Workspace: device copies of V / outputs, scratch, a stream).
   void* workspace = nullptr;

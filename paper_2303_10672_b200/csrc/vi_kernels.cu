@@ -1164,21 +1164,25 @@ __device__ __forceinline__ void w16_row(const double* __restrict__ slab, double*
                                         const std::uint16_t* __restrict__ group_order,
                                         int n_groups, int n_r, int r, int tiled,
                                         const double* s_pmf_b, const double* s_cdf_b,
-                                        int g_lo = 0, int g_cnt = -1) {
+                                        int g_lo = 0, int g_cnt = -1, bool sorted = false,
+                                        bool write_v0 = true) {
   constexpr int NB = 16, S8 = 8, OB4 = 4;
   const int stride = slab_stride(NB);
-  if (threadIdx.x < NB) v0t[static_cast<std::size_t>(r) * NB + threadIdx.x] = slab[threadIdx.x];
+  if (write_v0 && threadIdx.x < NB) v0t[static_cast<std::size_t>(r) * NB + threadIdx.x] = slab[threadIdx.x];
   const int sub = threadIdx.x & 7;
   const int x1b = (sub >> 2) * S8;
   const int ob0 = (sub & 3) * OB4;
   // a sub-range of groups (unit shards) runs in index order, the whole
-  // row in the stock-sorted order
+  // row in the stock-sorted order; `sorted`: [g_lo, g_lo + g_cnt) are
+  // positions in the stock-sorted order (a chunk of a whole row)
   const bool all_groups = g_cnt < 0 || g_cnt >= n_groups;
+  const bool by_order = all_groups || sorted;
+  const int g_base = all_groups ? 0 : g_lo;
   const int n_iter = all_groups ? n_groups : g_cnt;
   for (int gbase = 0; gbase < n_iter; gbase += blockDim.x >> 3) {
     const int gi = gbase + (threadIdx.x >> 3);
     const bool active = gi < n_iter;
-    const int grp = all_groups ? group_order[active ? gi : 0] : g_lo + (active ? gi : 0);
+    const int grp = by_order ? group_order[g_base + (active ? gi : 0)] : g_lo + (active ? gi : 0);
     int xg[M + 1];
     int S = 0;
     {
@@ -1298,7 +1302,9 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16p(DevModel dm, const doubl
                                                         int n_groups, int n_xb, int n_bp, int n_r,
                                                         int x3_lo, int x3_hi, int tiled, int r_base,
                                                         int r_count, int strict, int g_lo, int g_cnt,
-                                                        int hp, int hg_lo, int tp, int tg_hi) {
+                                                        int hp, int hg_lo, int tp, int tg_hi,
+                                                        const int4* __restrict__ items = nullptr,
+                                                        int n_items = 0) {
   constexpr int NB = 16;
   extern __shared__ double slabs[];  // 2 x [bp][ob]
   const int stride = slab_stride(NB);
@@ -1331,6 +1337,31 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16p(DevModel dm, const doubl
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };
+  if (items) {
+    // shard sweeps: a host-built list of (row, group range, flags) items of
+    // similar cost, so the wanted rows of a sparse row set spread evenly
+    // over the CTAs instead of landing on the few CTAs whose stride hits
+    // them; each item stages its row's slab (L2-resident V)
+    int i = static_cast<int>(blockIdx.x);
+    if (i >= n_items) return;
+    stage(items[i].x - r_base, 0);
+    for (int buf = 0; i < n_items; buf ^= 1) {
+      const int in = i + static_cast<int>(gridDim.x);
+      if (in < n_items) {
+        stage(items[in].x - r_base, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+      }
+      __syncthreads();
+      const int4 it = items[i];
+      w16_row<M>(slabs + buf * slab_sz, W, v0t, group_order, n_groups, n_r, it.x, tiled, s_pmf_b, s_cdf_b,
+                 it.y, it.z, (it.w & 1) != 0, (it.w & 2) != 0);
+      __syncthreads();  // the slab is refilled two items later
+      i = in;
+    }
+    return;
+  }
   int t = next_row(static_cast<int>(blockIdx.x));
   if (t < r_count) stage(t, 0);
   for (int buf = 0; t < r_count; buf ^= 1) {
@@ -3239,6 +3270,70 @@ static bool qw_enabled() {
   return on;
 }
 
+// PVI_B_S1ITEMS=0: shard sweeps' stage 1 walks its rows with a plain stride
+static bool s1_items_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PVI_B_S1ITEMS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// The stage-1 work list of one k_b_fact_w16p launch: exactly the rows and
+// group ranges its row-stride loop would process (same filter and column
+// rules), each row cut into chunks of `chunk` groups so that every
+// persistent CTA gets a similar share.  Flags: 1 = the range indexes the
+// stock-sorted group order (whole rows), 2 = write the row's V0 entries.
+static std::vector<int4> b_s1_items(int M, int na, int n_groups, int r0, int r1, int x3_lo, int x3_hi,
+                                    int strict, int g_lo, int g_cnt, int hp, int hg_lo, int tp, int tg_hi,
+                                    int grid) {
+  struct Row {
+    int r, lo, cnt, all;
+  };
+  std::vector<Row> rows;
+  long long total = 0;
+  for (int r = r0; r < r1; ++r) {
+    const int ap = r % (na * na), x2r = ap % na, x3r = ap / na;
+    if (M == 3) {
+      const bool want = strict ? (x3r >= x3_lo && x3r <= x3_hi)
+                               : !((x3r < x3_lo || x3r > x3_hi) && !(x2r == 0 && x3r <= x3_hi));
+      if (!want) continue;
+    }
+    int rg_lo = g_lo, rg_cnt = g_cnt;
+    if (hp >= 0 || tp >= 0) {
+      const int pr = x3r / 2;
+      rg_lo = 0;
+      rg_cnt = -1;
+      if (x2r != 0 && pr == hp && pr == tp) {
+        rg_lo = hg_lo;
+        rg_cnt = tg_hi - hg_lo;
+      } else if (x2r != 0 && pr == hp) {
+        rg_lo = hg_lo;
+        rg_cnt = n_groups - hg_lo;
+      } else if (x2r != 0 && pr == tp) {
+        rg_cnt = tg_hi;
+      }
+    }
+    const bool all = rg_cnt < 0 || rg_cnt >= n_groups;
+    rows.push_back({r, all ? 0 : rg_lo, all ? n_groups : std::max(rg_cnt, 0), all ? 1 : 0});
+    total += rows.back().cnt;
+  }
+  // ~8 items per CTA, in multiples of the 32 groups a CTA pass covers
+  long long chunk = (total + 8ll * grid - 1) / (8ll * grid);
+  chunk = std::min<long long>(std::max<long long>((chunk + 31) / 32 * 32, 32), n_groups);
+  std::vector<int4> out;
+  for (const Row& w : rows) {
+    if (w.cnt == 0) {
+      out.push_back(make_int4(w.r, w.lo, 0, 2));
+      continue;
+    }
+    for (int c = 0; c < w.cnt; c += static_cast<int>(chunk))
+      out.push_back(make_int4(w.r, w.lo + c, std::min(static_cast<int>(chunk), w.cnt - c),
+                              w.all | (c == 0 ? 2 : 0)));
+  }
+  return out;
+}
+
 // PVI_B_QW4: 0 = k_b_fact_qw3, 1 = k_b_fact_qw4, 2 = k_b_fact_qw4 with
 // double-buffered row staging, 3 = k_b_fact_qw4 with the constants' rows
 // prefetched into shared memory
@@ -3421,13 +3516,39 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
         if (std::is_same<T, double>::value && w16p_enabled()) {                                    \
           auto kp = k_b_fact_w16p<MM>;                                                             \
           cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sm0);          \
-          const unsigned g = static_cast<unsigned>(std::min<std::uint64_t>(r1 - r0, 2 * num_sms())); \
+          unsigned g = static_cast<unsigned>(std::min<std::uint64_t>(r1 - r0, 2 * num_sms()));     \
+          /* a shard's sparse row set: the balanced work list */                                   \
+          const int4* s1_items = nullptr;                                                          \
+          int s1_n = 0;                                                                            \
+          if (s1_items_enabled() && !s1_strict &&                                                  \
+              (a.head_pair >= 0 || a.tail_pair >= 0 || s1_g_cnt >= 0 || s1_x3_lo > 0 || s1_x3_hi < na - 1)) { \
+            const std::vector<int> key{MM, static_cast<int>(r0), static_cast<int>(r1), s1_x3_lo,   \
+                                       s1_x3_hi, s1_strict ? 1 : 0, s1_g_lo, s1_g_cnt, a.head_pair, \
+                                       a.head_g_lo, a.tail_pair, a.tail_g_hi, static_cast<int>(g)}; \
+            auto it = dc.b_s1_items.find(key);                                                     \
+            if (it == dc.b_s1_items.end()) {                                                       \
+              const auto v = b_s1_items(MM, na, static_cast<int>(n_bp), static_cast<int>(r0),      \
+                                        static_cast<int>(r1), s1_x3_lo, s1_x3_hi, s1_strict ? 1 : 0, \
+                                        s1_g_lo, s1_g_cnt, a.head_pair, a.head_g_lo, a.tail_pair, \
+                                        a.tail_g_hi, static_cast<int>(g));                         \
+              void* q = nullptr;                                                                   \
+              if (!v.empty()) {                                                                    \
+                PVI_CUDA(cudaMalloc(&q, v.size() * sizeof(int4)));                                 \
+                upload_bytes(q, v.data(), v.size() * sizeof(int4));                                \
+                dc.allocations.push_back(q);                                                       \
+              }                                                                                    \
+              it = dc.b_s1_items.emplace(key, std::make_pair(q, static_cast<int>(v.size()))).first; \
+            }                                                                                      \
+            s1_items = static_cast<const int4*>(it->second.first);                                 \
+            s1_n = it->second.second;                                                              \
+            g = static_cast<unsigned>(std::min<long long>(std::max(s1_n, 1), 2ll * num_sms()));    \
+          }                                                                                        \
           kp<<<g, 256, 2 * sm0, stream>>>(                                                         \
               dm, reinterpret_cast<const double*>(a.v), W, v0t, dc.b_group_order_b,                \
               static_cast<int>(n_bp), static_cast<int>(n_xb), static_cast<int>(n_bp),               \
               static_cast<int>(n_r), s1_x3_lo, s1_x3_hi, qw && MM == 3 ? 1 : 0, static_cast<int>(r0), \
               static_cast<int>(r1 - r0), s1_strict ? 1 : 0, s1_g_lo, s1_g_cnt, a.head_pair,       \
-              a.head_g_lo, a.tail_pair, a.tail_g_hi);                                              \
+              a.head_g_lo, a.tail_pair, a.tail_g_hi, s1_items, s1_n);                              \
         } else {                                                                                   \
           k_b_fact_w16<T, MM><<<static_cast<unsigned>(r1 - r0), 256, sm0, stream>>>(               \
               dm, a.v, W, v0t, dc.b_group_order_b, static_cast<int>(n_bp), static_cast<int>(n_xb),  \
