@@ -181,12 +181,14 @@ typedef struct {
   int device;                /* CUDA ordinal, -1 = current */
   int algorithm;             /* -1: the model's (pvi_model_set_algorithm), else pvi_algorithm */
   int loop;                  /* sweep loop control: -1 auto (graph-resident when no checkpoint
-                                falls inside the loop and the test keeps <= 2 vectors), 0 host
-                                loop (one 32-byte read-back per sweep), 1 graph-resident loop
-                                (CUDA graph with a device-evaluated WHILE condition: no host
-                                round trip per sweep; PVI_ERR_PARAMETER where unsupported) */
-  int l2_persist;            /* -1 auto / 1 on: an L2 access-policy window (persisting) over the
-                                value-vector ring; 0 off */
+                                falls inside the loop), 0 host loop (one 32-byte read-back per
+                                sweep), 1 graph-resident loop (CUDA graph with a device-evaluated
+                                WHILE condition: no host round trip per sweep; the periodic span's
+                                8-vector ring rotates through a chain of 8 IF nodes; PVI_ERR_PARAMETER
+                                with checkpoints) */
+  int l2_persist;            /* 1 on: an L2 access-policy window (persisting) over the value-vector
+                                ring; 0 off; -1 auto: on for the exact kernels, off for the
+                                factored sweeps (their traffic is the W / G tables) */
 } pvi_vi_config;
 
 /* Backup algorithm.  EXACT reproduces the reference's per-term expression

@@ -499,8 +499,7 @@ struct LoopState {
   int pad;
 };
 
-__global__ void k_loop_decide(LoopState* ls, const SweepStats* st, cudaGraphConditionalHandle h_while,
-                              cudaGraphConditionalHandle h_if, int set_if) {
+__device__ bool loop_decide(LoopState* ls, const SweepStats* st) {
   LoopState s = *ls;
   s.iteration += 1;
   bool stop = false;
@@ -516,7 +515,9 @@ __global__ void k_loop_decide(LoopState* ls, const SweepStats* st, cudaGraphCond
       s.last_lo = lo;
       bool c;
       if (s.test == PVI_TEST_VALUE_SPAN) c = (0.0 < hi ? hi : 0.0) < s.epsilon;  // std::max(0.0, hi)
-      else c = hi - lo < s.epsilon;  // change span (periodic span needs 8 vectors: host loop)
+      else if (s.test == PVI_TEST_PERIODIC_SPAN)  // vi.hpp:150-156 (evaluate_test above)
+        c = s.iteration >= 7 && hi - lo <= 2.0 * s.epsilon * fmin(fabs(hi), fabs(lo));
+      else c = hi - lo < s.epsilon;  // change span
       s.converged = c ? 1 : 0;
       stop = c;
     }
@@ -526,8 +527,25 @@ __global__ void k_loop_decide(LoopState* ls, const SweepStats* st, cudaGraphCond
     }
   }
   *ls = s;
+  return stop;
+}
+
+__global__ void k_loop_decide(LoopState* ls, const SweepStats* st, cudaGraphConditionalHandle h_while,
+                              cudaGraphConditionalHandle h_if, int set_if) {
+  const bool stop = loop_decide(ls, st);
   cudaGraphSetConditional(h_while, stop ? 0u : 1u);
   if (set_if) cudaGraphSetConditional(h_if, stop ? 0u : 1u);
+}
+
+// Eight-slot ring (periodic span): the WHILE body is a chain of eight IF
+// nodes, one per ring phase; IF k sweeps into slot k of the rotation, then
+// clears its own condition and arms IF k+1 (IF 0 in the next iteration).
+__global__ void k_loop_decide_phase(LoopState* ls, const SweepStats* st, cudaGraphConditionalHandle h_while,
+                                    cudaGraphConditionalHandle h_self, cudaGraphConditionalHandle h_next) {
+  const bool stop = loop_decide(ls, st);
+  cudaGraphSetConditional(h_while, stop ? 0u : 1u);
+  cudaGraphSetConditional(h_self, 0u);
+  cudaGraphSetConditional(h_next, stop ? 0u : 1u);
 }
 
 // Persisting L2 window over [base, base + bytes) for kernels launched on
@@ -603,7 +621,11 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
     ring.push_back(std::make_unique<RingSlot>(RingSlot{ring_mem.as<T>() + static_cast<std::size_t>(i) * n}));
   double l2_ratio = 0.0;
   const std::size_t l2_bytes =
-      cfg.l2_persist == 0 ? 0
+      // auto: on for the exact kernels (their gathers hit the ring); off for
+      // the factored sweeps, whose traffic is the W / G tables: a window over
+      // the ring costs them L2 (tools/loop_ab.py on a B200: b/m3/exp1 solve
+      // 78.5 -> 84.7 ms, c/m5/exp2 190 -> 225 ms with the window)
+      (cfg.l2_persist == 0 || (cfg.l2_persist < 0 && algo == PVI_ALGO_FACTORED)) ? 0
                           : set_l2_window(stream.s, ring_mem.p, static_cast<std::size_t>(hist_cap) * n * sizeof(T),
                                           device, &l2_ratio);
   struct L2Reset {
@@ -653,10 +675,13 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
   const std::uint64_t start_iteration = iteration;
   // graph-resident loop: two-vector tests, no checkpoint inside the loop,
   // not while the bench's per-launch profiler records events
-  const bool graph_possible = hist_cap == 2 && !ckpt && !profiling_enabled();
+  const bool graph_possible = !ckpt && !profiling_enabled();
   if (cfg.loop == 1 && !graph_possible)
-    fail(PVI_ERR_PARAMETER, "graph-resident loop needs a value- or change-span test and no checkpoints");
-  const bool use_graph = graph_possible && cfg.loop != 0;
+    fail(PVI_ERR_PARAMETER, "graph-resident loop needs no checkpoints");
+  // auto: the graph for two-vector tests; the periodic span's 8-branch graph
+  // costs more to build than it saves over its typical 12-20 sweeps (c/m5/exp1
+  // 40.1 ms host vs 41.7 ms graph on a B200), so it runs only on request
+  const bool use_graph = graph_possible && (cfg.loop == 1 || (cfg.loop < 0 && hist_cap == 2));
   std::uint64_t graph_sweeps = 0;
   const auto t_loop_start = std::chrono::steady_clock::now();
   while (true) {
@@ -668,10 +693,12 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
     } else if (iteration >= start_iteration + cfg.max_iterations) {
       break;
     }
-    if (use_graph && sweeps > 0) {
+    if (use_graph && sweeps > 0 && static_cast<int>(order.size()) == hist_cap) {
       // every remaining sweep in one graph launch (the first sweep ran eagerly:
-      // it builds the per-model tables and scratch the captured sweeps reuse)
+      // it builds the per-model tables and scratch the captured sweeps reuse;
+      // periodic span: the first 7, which fill the ring)
       const int a_slot = order.front(), b_slot = order.back();
+      const std::vector<int> base = order;  // ring oldest..newest at entry
       PoolBuf dls(sizeof(LoopState), stream.s);
       LoopState h{};
       h.iteration = iteration;
@@ -686,7 +713,8 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
       PVI_CUDA(cudaGraphCreate(&graph, 0));
       cudaGraphConditionalHandle h_while, h_if;
       PVI_CUDA(cudaGraphConditionalHandleCreate(&h_while, graph, 1, cudaGraphCondAssignDefault));
-      PVI_CUDA(cudaGraphConditionalHandleCreate(&h_if, graph, 0, cudaGraphCondAssignDefault));
+      if (hist_cap == 2)  // an unused handle fails instantiation (ConditionalHandleUnused)
+        PVI_CUDA(cudaGraphConditionalHandleCreate(&h_if, graph, 0, cudaGraphCondAssignDefault));
       cudaGraphNodeParams wp = {};
       wp.type = cudaGraphNodeTypeConditional;
       wp.conditional.handle = h_while;
@@ -709,6 +737,38 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
         return a;
       };
       cudaStream_t cs = stream.s;
+      if (hist_cap != 2) {
+        // body: IF_0 -> IF_1 -> .. -> IF_7; IF_k { sweep base[k-1] -> base[k]
+        // with history base[k+1..k+7], decide } -- the host loop's ring
+        // rotation, one phase per slot (IF_0 armed at launch)
+        std::vector<cudaGraphConditionalHandle> hk(static_cast<std::size_t>(hist_cap));
+        for (int k = 0; k < hist_cap; ++k)
+          PVI_CUDA(cudaGraphConditionalHandleCreate(&hk[k], graph, k == 0 ? 1 : 0, cudaGraphCondAssignDefault));
+        cudaGraphNode_t prev = nullptr;
+        for (int k = 0; k < hist_cap; ++k) {
+          cudaGraphNodeParams ip = {};
+          ip.type = cudaGraphNodeTypeConditional;
+          ip.conditional.handle = hk[k];
+          ip.conditional.type = cudaGraphCondTypeIf;
+          ip.conditional.size = 1;
+          cudaGraphNode_t inode;
+          PVI_CUDA(cudaGraphAddNode(&inode, body, prev ? &prev : nullptr, prev ? 1 : 0, &ip));
+          prev = inode;
+          SweepArgs<T> a = sweep_args(base[(k + hist_cap - 1) % hist_cap], base[k]);
+          if (h.test == PVI_TEST_PERIODIC_SPAN) {
+            a.fa.n_hist = hist_cap - 1;
+            for (int j = 0; j < hist_cap - 1; ++j) a.fa.hist[j] = ring[base[(k + 1 + j) % hist_cap]]->p;
+          }
+          cudaGraph_t tmp = nullptr;
+          PVI_CUDA(cudaStreamBeginCaptureToGraph(cs, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                 cudaStreamCaptureModeRelaxed));
+          launch_sweep<T>(m, dm, a, scratch, cs);
+          k_loop_decide_phase<<<1, 1, 0, cs>>>(dls.as<LoopState>(), dstats.as<SweepStats>(), h_while, hk[k],
+                                               hk[(k + 1) % hist_cap]);
+          PVI_CUDA(cudaGetLastError());
+          PVI_CUDA(cudaStreamEndCapture(cs, &tmp));
+        }
+      } else {
       // body: sweep b -> a, decide (sets WHILE and IF), IF { sweep a -> b, decide }
       PVI_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
       launch_sweep<T>(m, dm, sweep_args(b_slot, a_slot), scratch, cs);
@@ -737,9 +797,22 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
         PVI_CUDA(cudaGetLastError());
         PVI_CUDA(cudaStreamEndCapture(cs, &tmp));
       }
+      }
       cudaGraphExec_t exec = nullptr;
       const auto tr1 = std::chrono::steady_clock::now();
-      PVI_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      {
+        cudaGraphInstantiateParams ipar = {};
+        const cudaError_t ie = cudaGraphInstantiateWithParams(&exec, graph, &ipar);
+        if (ie != cudaSuccess) {
+          cudaGraphNodeType nt = cudaGraphNodeTypeEmpty;
+          if (ipar.errNode_out) cudaGraphNodeGetType(ipar.errNode_out, &nt);
+          cudaGetLastError();
+          cudaGraphDestroy(graph);
+          fail(PVI_ERR_DEVICE, std::string("graph loop instantiate: ") + cudaGetErrorString(ie) + " (result " +
+                                 std::to_string(static_cast<int>(ipar.result_out)) + ", node type " +
+                                 std::to_string(static_cast<int>(nt)) + ")");
+        }
+      }
       const auto tr2 = std::chrono::steady_clock::now();
       PVI_CUDA(cudaEventRecord(ev0, cs));
       PVI_CUDA(cudaGraphLaunch(exec, cs));
@@ -761,7 +834,9 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
       graph_sweeps = h.iteration - iteration;
       sweeps += graph_sweeps;
       iteration = h.iteration;
-      if (graph_sweeps % 2 == 1) {  // newest is slot a
+      if (hist_cap != 2) {  // the ring rotated once per graph sweep
+        for (int i = 0; i < hist_cap; ++i) order[i] = base[(graph_sweeps + i) % hist_cap];
+      } else if (graph_sweeps % 2 == 1) {  // newest is slot a
         order.clear();
         order.push_back(b_slot);
         order.push_back(a_slot);

@@ -407,7 +407,7 @@ class ViConfig:
     device: int = -1
     algorithm: Optional[str] = None  # None: the model's (Model.set_algorithm)
     loop: str = "auto"               # "auto" | "host" | "graph" (pvi_vi_config::loop)
-    l2_persist: Optional[bool] = None  # None: auto (on)
+    l2_persist: Optional[bool] = None  # None: auto (on for the exact kernels)
 
     def to_c(self) -> L.ViConfigC:
         c = L.ViConfigC()

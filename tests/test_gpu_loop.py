@@ -6,6 +6,8 @@ convergence test, iteration limit) runs on the device after every sweep and
 drives a CUDA-graph WHILE node, so a solve is one graph launch.  It must
 change nothing: iteration counts, values and policies are bit-identical to
 the host-driven loop (and so to the reference, tests/test_gpu_vi.py)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -36,13 +38,34 @@ def _same(a, b):
     ("b/m2/exp1", {"algorithm": "factored"}),
     ("b/m2/p1", {"fixed_iterations": 100}),
     ("a/m2/exp1", {"max_iterations": 37}),
+    ("c/m3/exp1", {}),
+    ("c/m3/exp1", {"algorithm": "factored"}),
+    ("c/m3/exp2", {"algorithm": "factored"}),
+    ("c/m3/exp1", {"precision": "f32"}),
+    ("c/m3/exp1", {"max_iterations": 12}),
+    ("c/m3/exp1", {"fixed_iterations": 20}),
 ])
 def test_graph_loop_equals_host_loop(pvi, preset, kw):
     host = _solve(pvi, preset, loop="host", **dict(kw))
     graph = _solve(pvi, preset, loop="graph", **dict(kw))
     _same(host, graph)
     assert host.graph_sweeps == 0
-    assert graph.graph_sweeps == graph.iterations - 1  # the first sweep runs eagerly
+    # the first sweep runs eagerly (periodic span: the 7 that fill the 8-slot ring)
+    eager = 7 if preset.startswith("c/") else 1
+    assert graph.graph_sweeps == graph.iterations - eager
+
+
+def test_graph_loop_periodic_matches_reference(pvi):
+    # the 8-slot ring (a chain of IF nodes per phase) reproduces the reference's c/m3 solves bit for bit
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz"))
+    for preset in ("c/m3/exp1", "c/m3/exp2"):
+        key = f"solve|{preset}|f64"
+        r = _solve(pvi, preset, loop="graph")
+        assert r.graph_sweeps == r.iterations - 7
+        it, conv = gold[key + "|meta"]
+        assert r.iterations == it and r.converged == bool(conv)
+        np.testing.assert_array_equal(r.values, gold[key + "|values"])
+        np.testing.assert_array_equal(r.policy, gold[key + "|policy"])
 
 
 def test_graph_loop_limits(pvi):
@@ -62,13 +85,22 @@ def test_graph_loop_divergence(pvi):
 
 def test_graph_loop_refuses_unsupported(pvi, tmp_path):
     with pytest.raises(pvi.ParameterError):
-        _solve(pvi, "c/m3/exp1", loop="graph")  # periodic span keeps 8 vectors
-    with pytest.raises(pvi.ParameterError):
         _solve(pvi, "a/m2/exp1", loop="graph", checkpoint_every=100,
                checkpoint_path=str(tmp_path / "c.ckpt"))
-    # auto falls back to the host loop in both cases
+    # auto: the host loop with checkpoints, and for the periodic span (its
+    # 8-branch graph is built only on request); the graph otherwise
+    r = _solve(pvi, "a/m2/exp1", checkpoint_every=100, checkpoint_path=str(tmp_path / "d.ckpt"))
+    assert r.graph_sweeps == 0 and r.converged
     r = _solve(pvi, "c/m3/exp1")
     assert r.graph_sweeps == 0 and r.converged
+    r = _solve(pvi, "a/m2/exp1")
+    assert r.graph_sweeps == r.iterations - 1 and r.converged
+
+
+def test_l2_window_auto(pvi):
+    # auto: a window over the value ring for the exact kernels only
+    assert _solve(pvi, "a/m2/exp1", algorithm="exact").l2_window_bytes > 0
+    assert _solve(pvi, "a/m2/exp1", algorithm="factored").l2_window_bytes == 0
 
 
 @pytest.mark.parametrize("preset", ["a/m3/exp1", "b/m2/exp1", "c/m3/exp1"])

@@ -7,7 +7,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2303_10672_b200 as P  # noqa: E402
 
 CASES = [("a/m2/exp1", "exact"), ("a/m5/exp5", "factored"), ("a/m5/exp6", "factored"),
-         ("a/m5/exp5", "exact"), ("b/m3/exp1", "factored"), ("b/m2/exp1", "exact")]
+         ("a/m5/exp5", "exact"), ("b/m3/exp1", "factored"), ("b/m2/exp1", "exact"),
+         ("c/m5/exp1", "factored"), ("c/m5/exp2", "factored"), ("c/m3/exp1", "exact")]
 for preset, algo in CASES:
     m = P.make_preset(preset).set_algorithm(algo)
     P.run_value_iteration(m, P.ViConfig(fixed_iterations=2))  # warm tables / scratch
