@@ -2731,12 +2731,16 @@ __global__ void __launch_bounds__(448) k_c_bin_tile(const double* __restrict__ H
 // item's [b][d_k][x_1] block lands by cp.async in the second buffer while
 // this one is computed, and 896 threads split each (d_k, x_1) column's b
 // values (even / odd) so two FMA chains run per column.
+// RC > 0: the radix r = A_max + 1 as a compile-time constant (21 for every
+// C preset), so the staging and tile index arithmetic divides by constants.
+template <int RC>
 __global__ void __launch_bounds__(896, 1) k_c_bin_tile_p(const double* __restrict__ Hin,
                                                          double* __restrict__ Hout,
                                                          const double* __restrict__ binom_k,
-                                                         std::size_t binom_a_stride, int r, int m,
+                                                         std::size_t binom_a_stride, int r_in, int m,
                                                          int k, std::uint32_t wb, int endo,
                                                          int in_is_g, int n_prof, int n_lines) {
+  const int r = RC > 0 ? RC : r_in;
   extern __shared__ double smem_t[];  // 2 x [b][d_k][x_1], then 2 x s_bin [b][y]
   const int plane = r * r, cube = r * plane;
   double* tiles = smem_t;
@@ -3738,9 +3742,10 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
         if (c_tile_mode() == 2 && r <= 21) {
           const int n_lines = static_cast<int>(wb / (static_cast<std::uint32_t>(r) * r));
           const std::size_t smt = 2 * (static_cast<std::size_t>(r) * r * r + static_cast<std::size_t>(r) * r) * sizeof(double);
-          cudaFuncSetAttribute(k_c_bin_tile_p, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
           const int n_items = (endo ? r : 1) * 7 * n_lines;
-          k_c_bin_tile_p<<<static_cast<unsigned>(std::min(n_items, num_sms())), 896, smt, stream>>>(
+          auto kern = r == 21 ? k_c_bin_tile_p<21> : k_c_bin_tile_p<0>;
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          kern<<<static_cast<unsigned>(std::min(n_items, num_sms())), 896, smt, stream>>>(
               src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, endo ? a_stride : 0, r, M, k, wb,
               endo ? 1 : 0, src == G ? 1 : 0, static_cast<int>(n_prof), n_lines);
         } else if (c_tile_mode() == 1 && r <= 21) {
