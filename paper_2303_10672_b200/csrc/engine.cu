@@ -905,6 +905,18 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
   const auto t_loop_end = std::chrono::steady_clock::now();
   // Policy extraction (vi.hpp:267-280): one more argmax sweep.
   const T* vfinal = ring[order.back()]->as<T>();
+  // The value read-back overlaps the extraction sweep (which only reads
+  // vfinal): widened on the solve stream, copied out on a side stream.
+  std::unique_ptr<PoolBuf> wide;
+  std::unique_ptr<Stream> side;
+  cudaEvent_t ev_wide = nullptr;
+  if (out_values) {
+    wide = std::make_unique<PoolBuf>(n * sizeof(double), stream.s);
+    launch_widen<T>(vfinal, wide->as<double>(), n, stream.s);
+    side = std::make_unique<Stream>();
+    PVI_CUDA(cudaEventCreateWithFlags(&ev_wide, cudaEventDisableTiming));
+    PVI_CUDA(cudaEventRecord(ev_wide, stream.s));
+  }
   PoolBuf policy(n * sizeof(std::uint32_t), stream.s);
   {
     SweepArgs<T> a;
@@ -917,19 +929,20 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
     PVI_CUDA(cudaEventRecord(ev0, stream.s));
     launch_sweep<T>(m, dm, a, scratch, stream.s);
     PVI_CUDA(cudaEventRecord(ev1, stream.s));
+    if (out_values) {
+      PVI_CUDA(cudaStreamWaitEvent(side->s, ev_wide, 0));
+      PVI_CUDA(cudaMemcpyAsync(out_values, wide->p, n * 8, cudaMemcpyDeviceToHost, side->s));
+      PVI_CUDA(cudaStreamSynchronize(side->s));
+      cudaEventDestroy(ev_wide);
+    }
     PVI_CUDA(cudaStreamSynchronize(stream.s));
     float ms = 0.f;
     PVI_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
     sweep_ms += ms;
     ++sweeps;
   }
+  wide.reset();  // freed on the solve stream, after the side copy completed
   if (writer) writer->finish();  // every checkpoint on disk before returning
-  if (out_values) {
-    PoolBuf w(n * sizeof(double), stream.s);
-    launch_widen<T>(vfinal, w.as<double>(), n, stream.s);
-    PVI_CUDA(cudaMemcpyAsync(out_values, w.p, n * 8, cudaMemcpyDeviceToHost, stream.s));
-    PVI_CUDA(cudaStreamSynchronize(stream.s));
-  }
   if (out_policy) {
     PVI_CUDA(cudaMemcpyAsync(out_policy, policy.p, n * 4, cudaMemcpyDeviceToHost, stream.s));
     PVI_CUDA(cudaStreamSynchronize(stream.s));
