@@ -470,6 +470,25 @@ def ours_arm(args, world, rank, local):
                           "candidates": len(so.log), "wall_seconds": so.wall_seconds,
                           "device_seconds": so.device_seconds,
                           "rollout_days_per_s": days / max(so.device_seconds, 1e-9)}
+        # the whole 21 x 21 grid in one batch (GPU-only extra mode) and the
+        # optimality gap of the GA's best against the VI policy, both scored
+        # over 10,000 rollouts on common random numbers (runner cmd_evaluate)
+        mb = P.make_preset("b/m2/exp1")
+        ex = P.simopt(mb, sampler="exhaustive", rollouts_per_candidate=4096, base_seed=42)
+        vi = P.run_value_iteration(mb, P.ViConfig())
+        evs, _ = P.evaluate_policies(mb, [P.make_vi_policy(mb, vi.policy),
+                                          P.make_heuristic_policy(mb, so.best),
+                                          P.make_heuristic_policy(mb, ex.best)],
+                                     P.RolloutConfig(n_rollouts=10_000, base_seed=42))
+        vi_mean = evs[0].ret.mean
+        line["simopt"]["exhaustive"] = {
+            "candidates": len(ex.log), "best": ex.best, "best_mean": ex.best_mean,
+            "device_seconds": ex.device_seconds,
+            "rollout_days_per_s": len(ex.log) * 4096 * 465 / max(ex.device_seconds, 1e-9)}
+        line["simopt"]["optimality_gap_pct"] = {
+            "vi_policy_mean": vi_mean, "rollouts": 10_000,
+            "ga_best": 100.0 * (vi_mean - evs[1].ret.mean) / abs(vi_mean),
+            "exhaustive_best": 100.0 * (vi_mean - evs[2].ret.mean) / abs(vi_mean)}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import refbind as R

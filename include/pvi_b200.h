@@ -374,7 +374,9 @@ int pvi_sim_evaluate(const pvi_model* m, const pvi_policy* policies, uint32_t n_
  * with each generation's fresh candidates scored in ONE batched device
  * evaluation (pvi_sim_evaluate) instead of one evaluate_policy per candidate. */
 typedef struct {
-  int sampler;                 /* 0 auto (grid if 1-D, else GA), 1 grid, 2 GA */
+  int sampler;                 /* 0 auto (grid if 1-D, else GA), 1 grid, 2 GA, 3 exhaustive
+                                  grid over the whole product space in one batch (GPU-only
+                                  extra mode; PVI_ERR_PARAMETER above 1e6 candidates) */
   int population;              /* 50 */
   int max_generations;         /* 100 */
   int patience;                /* 5 */

@@ -515,6 +515,7 @@ int pvi_simopt(const pvi_model* m, const pvi_simopt_config* cfg, int* best, doub
       c = *cfg;
     else
       pvi_simopt_config_defaults(&c);
+    if (c.sampler < 0 || c.sampler > 3) fail(PVI_ERR_PARAMETER, "simopt: unknown sampler");
     simopt_run(M(m), c, best, best_mean, best_sd, generations, log, log ? log_capacity : 0, n_logged,
                dimension, device_seconds);
   });

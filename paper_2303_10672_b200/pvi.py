@@ -826,7 +826,7 @@ def simopt(model: Model, sampler: str = "auto", population: int = 50, max_genera
     c = L.SimoptConfigC()
     lib = L.load()
     lib.pvi_simopt_config_defaults(C.byref(c))
-    c.sampler = {"auto": 0, "grid": 1, "ga": 2}[sampler]
+    c.sampler = {"auto": 0, "grid": 1, "ga": 2, "exhaustive": 3}[sampler]
     c.population, c.max_generations, c.patience = population, max_generations, patience
     c.crossover_rate, c.mutation_rate, c.seed = crossover_rate, mutation_rate, seed
     c.rollouts_per_candidate, c.horizon_days, c.warmup_days = (rollouts_per_candidate,

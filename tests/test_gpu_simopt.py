@@ -31,3 +31,23 @@ def test_simopt_published_parameters(pvi):
     # PAPER Table 8 / Table 12: A base stock S = 5; B (S_a, S_b) = (13, 12)
     assert pvi.simopt(pvi.make_preset("a/m2/exp1"), rollouts_per_candidate=4096).best == [5]
     assert pvi.simopt(pvi.make_preset("b/m2/exp1"), rollouts_per_candidate=4096).best == [13, 12]
+
+
+def test_simopt_exhaustive_grid(pvi):
+    # GPU-only extra mode: all 21 x 21 (S_a, S_b) in one batch.
+    # Common random numbers: every candidate the reference's GA scored has the
+    # same (mean, sd) bit for bit, and the grid's best is the global optimum
+    # of the GA's ordering (higher mean, then the smaller vector).
+    m = pvi.make_preset("b/m2/exp1")
+    r = pvi.simopt(m, sampler="exhaustive", rollouts_per_candidate=4096, base_seed=42)
+    assert len(r.log) == 441 and r.generations == 1
+    vals = [tuple(e[1]) for e in r.log]
+    assert vals == sorted(vals) and len(set(vals)) == 441
+    score = {tuple(e[1]): (e[2], e[3]) for e in r.log}
+    for v, (_, mean, sd) in zip(G["simopt|b/m2/exp1|log_values"], G["simopt|b/m2/exp1|log_scores"]):
+        assert score[tuple(int(x) for x in v)] == (mean, sd)
+    top = max(r.log, key=lambda e: (e[2], [-x for x in e[1]]))
+    assert r.best == list(top[1]) and r.best_mean == top[2]
+    assert r.best_mean >= G["simopt|b/m2/exp1|score"][0]
+    with pytest.raises(pvi.ParameterError):  # 21^14 candidates
+        pvi.simopt(pvi.make_preset("c/m3/exp1"), sampler="exhaustive", rollouts_per_candidate=16)
