@@ -2510,14 +2510,33 @@ __global__ void __launch_bounds__(128) k_sweep_c(DevModel dm, const T* __restric
 // (2.9e7 for c/m5, 21 demands each); stage 2 is one gather of G per
 // (state, order, composition): 7.2e10 instead of the reference's 1.5e12 terms.
 
-template <typename T, int M>
+// DN > 0: the demand count (A_max + 1 = 21 for every C preset) and the radix
+// are compile-time, the d loop is unrolled, and the reward is read from two
+// exact tables, RA[x + D] = -C_h x^+ - C_s (-x)^+ and CW[w] = C_w w (the same
+// IEEE operations in the same order as the inline expression, so G is
+// bit-identical), instead of three int->double conversions and five FP64
+// operations per term.
+template <typename T, int M, int DN = 0>
 __global__ void __launch_bounds__(256) k_c_fact_g(DevModel dm, const T* __restrict__ V,
                                                   double* __restrict__ G, int n_prof,
                                                   double gamma) {
-  const std::uint64_t gid = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  constexpr int NRA = DN > 0 ? M * (DN - 1) + DN : 1;  // x = total - d in [-(DN-1), M (DN-1)]
+  __shared__ double s_ra[NRA], s_cw[DN > 0 ? DN : 1], s_pmf[DN > 0 ? DN : 1];
   const int tau = blockIdx.y;
+  if (DN > 0) {
+    for (int i = threadIdx.x; i < NRA; i += blockDim.x) {
+      const int x = i - (DN - 1);
+      s_ra[i] = -dm.c_ch * ipos(x) - dm.c_cs * ipos(-x);
+    }
+    for (int i = threadIdx.x; i < DN; i += blockDim.x) {
+      s_cw[i] = dm.c_cw * i;
+      s_pmf[i] = dm.c_pmf[tau * DN + i];
+    }
+    __syncthreads();
+  }
+  const std::uint64_t gid = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gid >= static_cast<std::uint64_t>(n_prof)) return;
-  const int cap = dm.c_max_order, r = cap + 1, dn = dm.c_dmax + 1;
+  const int cap = DN > 0 ? DN - 1 : dm.c_max_order, r = cap + 1, dn = DN > 0 ? DN : dm.c_dmax + 1;
   // profile digits: zi = y_M r^(M-1) + sum_{j<M} z_j r^(j-1)
   int z[M + 1];
   {
@@ -2549,8 +2568,22 @@ __global__ void __launch_bounds__(256) k_c_fact_g(DevModel dm, const T* __restri
     w[0] = wk;
   }
   const std::uint32_t tau_base = static_cast<std::uint32_t>((tau + 1) % 7) * w[0];
-  const double* pmf = dm.c_pmf + tau * dn;
   double acc = 0.0;
+  if (DN > 0) {
+#pragma unroll
+    for (int d = 0; d < (DN > 0 ? DN : 1); ++d) {
+      std::uint32_t idx = tau_base;
+#pragma unroll
+      for (int j = 1; j <= M - 2; ++j)
+        idx += static_cast<std::uint32_t>(max(min(sp[j + 1] - d, z[j + 1]), 0)) * w[M - j];
+      idx += static_cast<std::uint32_t>(max(min(total - d, fresh), 0)) * w[1];
+      const double r0 = s_ra[total - d + (DN - 1)] - s_cw[max(z[1] - d, 0)];
+      acc = fma(s_pmf[d], fma(gamma, static_cast<double>(__ldg(V + idx)), r0), acc);
+    }
+    G[static_cast<std::size_t>(tau) * n_prof + gid] = acc;
+    return;
+  }
+  const double* pmf = dm.c_pmf + tau * dn;
   for (int d = 0; d < dn; ++d) {
     std::uint32_t idx = tau_base;
 #pragma unroll
@@ -3720,7 +3753,10 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     MainKernelScope prof(stream);
 #define PVI_CF(MM)                                                                               \
   if (!done && M == MM) {                                                                        \
-    k_c_fact_g<T, MM><<<dim3(grid_for(n_prof, 256), 7), 256, 0, stream>>>(dm, a.v, G, static_cast<int>(n_prof), a.gamma); \
+    if (dm.c_max_order == 20 && dm.c_dmax == 20)                                                  \
+      k_c_fact_g<T, MM, 21><<<dim3(grid_for(n_prof, 256), 7), 256, 0, stream>>>(dm, a.v, G, static_cast<int>(n_prof), a.gamma); \
+    else                                                                                           \
+      k_c_fact_g<T, MM><<<dim3(grid_for(n_prof, 256), 7), 256, 0, stream>>>(dm, a.v, G, static_cast<int>(n_prof), a.gamma); \
     if (!bin)                                                                                    \
       k_c_fact_q<T, MM><<<dim3(grid_for(nr, 128), na), 128, 0, stream>>>(dm, G, pv, a.qout, lo, hi, static_cast<int>(n_prof)); \
     done = true;                                                                                 \
