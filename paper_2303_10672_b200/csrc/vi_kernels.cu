@@ -2848,7 +2848,18 @@ __global__ void __launch_bounds__(896, 1) k_c_bin_tile_p(const double* __restric
       for (int b = half; b < cur.nb; b += 2) {
         const double* w = sb + b * r;
         double acc = 0.0;
-        for (int y = 0; y <= b; ++y) acc = fma(w[y], tile[((b - y) * r + min(dk + y, cap)) * r + x1], acc);
+        if (RC > 0) {
+          // y unrolled (b is warp-uniform, so the exit is a uniform branch):
+          // tile row b - y is an immediate offset from the row-b base
+          const double* tb = tile + b * plane + x1;
+#pragma unroll
+          for (int y = 0; y < (RC > 0 ? RC : 1); ++y) {
+            if (y > b) break;
+            acc = fma(w[y], tb[min(dk + y, cap) * r - y * plane], acc);
+          }
+        } else {
+          for (int y = 0; y <= b; ++y) acc = fma(w[y], tile[((b - y) * r + min(dk + y, cap)) * r + x1], acc);
+        }
         out[static_cast<std::size_t>(b) * wb] = acc;
       }
     }
