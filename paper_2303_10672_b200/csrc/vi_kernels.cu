@@ -2810,12 +2810,26 @@ __global__ void __launch_bounds__(896, 1) k_c_bin_tile_p(const double* __restric
   };
   const unsigned tbase = static_cast<unsigned>(__cvta_generic_to_shared(tiles));
   const unsigned bbase = static_cast<unsigned>(__cvta_generic_to_shared(bins));
+  const int s_rows = static_cast<int>(blockDim.x) / r;
+  const int s_x1 = static_cast<int>(threadIdx.x) % r, s_row0 = static_cast<int>(threadIdx.x) / r;
   auto stage = [&](const Item& it, int buf) {
     const unsigned dst = tbase + static_cast<unsigned>(buf * cube) * 8u;
-    for (int i = threadIdx.x; i < it.nb * plane; i += blockDim.x) {
-      const int b = i / plane, e = i % plane, d = e / r, x1 = e % r;
-      const double* src = Hin + it.in_base + static_cast<std::size_t>(b) * wb + it.rest0 + d * it.wk + x1;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * i), "l"(src));
+    if (RC > 0) {
+      // thread t < 42 r: x_1 = t % r of rows (b, d) = t / r, t / r + 42, ..
+      if (s_row0 < s_rows) {
+        const double* src0 = Hin + it.in_base + it.rest0 + s_x1;
+        for (int row = s_row0; row < it.nb * r; row += s_rows) {
+          const int b = row / r, d = row - b * r;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * (row * r + s_x1)),
+                       "l"(src0 + static_cast<std::size_t>(b) * wb + d * it.wk));
+        }
+      }
+    } else {
+      for (int i = threadIdx.x; i < it.nb * plane; i += blockDim.x) {
+        const int b = i / plane, e = i % plane, d = e / r, x1 = e % r;
+        const double* src = Hin + it.in_base + static_cast<std::size_t>(b) * wb + it.rest0 + d * it.wk + x1;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * i), "l"(src));
+      }
     }
     const double* bt = binom_k + it.a * binom_a_stride;
     const unsigned bdst = bbase + static_cast<unsigned>(buf * plane) * 8u;
