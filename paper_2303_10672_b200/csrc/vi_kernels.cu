@@ -2889,7 +2889,7 @@ __global__ void __launch_bounds__(896, 1) k_c_bin_tile_p(const double* __restric
 // 21 x 21 tile, staged in shared memory once (per order for the endogenous
 // per-order tables) instead of being re-read per (state, order) from L2/DRAM.
 constexpr int CQ_GROUPS = 12;
-template <typename T>
+template <typename T, int RC = 0>
 __global__ void __launch_bounds__(256) k_c_bin_qf(DevModel dm, const double* __restrict__ H2,
                                                   const T* __restrict__ V, T* __restrict__ vout,
                                                   std::uint32_t* __restrict__ act,
@@ -2900,7 +2900,7 @@ __global__ void __launch_bounds__(256) k_c_bin_qf(DevModel dm, const double* __r
                                                   FinalizeArgs fa) {
   extern __shared__ double sm[];
   const int na = static_cast<int>(dm.n_actions), dn = dm.c_dmax + 1;
-  const int r = dm.c_max_order + 1, cap = r - 1, m = dm.c_m;
+  const int r = RC > 0 ? RC : dm.c_max_order + 1, cap = r - 1, m = dm.c_m;
   double* s_bin = sm;                       // [a][y] = Bin(y; a, q_1(a))
   double* s_pd = s_bin + r * r;             // PD(tau), 7 values
   double* s_tile = s_pd + 8;                // [group][b][z_1]
@@ -2933,7 +2933,8 @@ __global__ void __launch_bounds__(256) k_c_bin_qf(DevModel dm, const double* __r
         const std::uint64_t gq = grp_lo + gg;
         if (gq >= n_groups) continue;
         const std::uint64_t s0 = gq * r;
-        const int tq = static_cast<int>(s0 / wb);
+        // RC > 0: state indices fit 32 bits (checked at launch)
+        const int tq = RC > 0 ? static_cast<int>(static_cast<std::uint32_t>(s0) / wb) : static_cast<int>(s0 / wb);
         const std::size_t rest0 = static_cast<std::size_t>(s0 - static_cast<std::uint64_t>(tq) * wb);
         const std::size_t base = (endo && !in_is_g)
                                      ? c_tri_base(a, wb) + static_cast<std::size_t>(tq) * (a + 1) * wb
@@ -2945,7 +2946,18 @@ __global__ void __launch_bounds__(256) k_c_bin_qf(DevModel dm, const double* __r
     if (!live) continue;
     const double* w = s_bin + a * r;
     double acc = 0.0;
-    for (int y = 0; y <= a; ++y) acc = fma(w[y], tile[(a - y) * r + min(x1 + y, cap)], acc);
+    if (RC > 0) {
+      // y unrolled, a is CTA-uniform: the exit is a uniform branch and the
+      // tile row a - y an immediate offset from the row-a base
+      const double* ta = tile + a * r;
+#pragma unroll
+      for (int y = 0; y < (RC > 0 ? RC : 1); ++y) {
+        if (y > a) break;
+        acc = fma(w[y], ta[min(x1 + y, cap) - y * r], acc);
+      }
+    } else {
+      for (int y = 0; y <= a; ++y) acc = fma(w[y], tile[(a - y) * r + min(x1 + y, cap)], acc);
+    }
     const double fixed = a > 0 ? -dm.c_cf : 0.0;
     const T qa = static_cast<T>(fma(fixed, s_pd[tau], acc));
     if (a == 0 || qa > best) {
@@ -3827,8 +3839,9 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
         const std::uint64_t n_groups = dm.n_states / static_cast<std::uint64_t>(r);
         const std::size_t smq = sizeof(double) * (static_cast<std::size_t>(r) * r + 8 +
                                                   static_cast<std::size_t>(CQ_GROUPS) * r * r);
-        cudaFuncSetAttribute(k_c_bin_qf<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        k_c_bin_qf<T><<<static_cast<unsigned>((n_groups + CQ_GROUPS - 1) / CQ_GROUPS), 256, smq, stream>>>(
+        auto kq = r == 21 && dm.n_states < (1ull << 32) ? k_c_bin_qf<T, 21> : k_c_bin_qf<T, 0>;
+        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        kq<<<static_cast<unsigned>((n_groups + CQ_GROUPS - 1) / CQ_GROUPS), 256, smq, stream>>>(
             dm, src, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, static_cast<int>(n_prof), wb,
             endo ? 1 : 0, src == G ? 1 : 0, n_groups, a.fa);
         qf_done = true;
