@@ -66,32 +66,65 @@ def init_dist():
 
 
 # ---------------------------------------------------------------------------
-# work model (SURVEY §8d closed forms, per state)
+# work model (SURVEY §8d closed forms).  Built from the product model for our
+# arm and from the reference library (oracle/_ref) alone for the reference
+# arm, which must not load this repo's package.
 
 
-def state_terms(model, lo: int, hi: int) -> float:
-    """Reference backup terms of states [lo, hi)."""
+class Work:
+    """Reference backup terms (state, action, outcome) of a preset, per range."""
+
+    def __init__(self, scenario: str, life: int, na: int, nb: int, states: int, actions: int,
+                 terms: float):
+        self.scenario, self.life, self.na, self.nb = scenario, life, na, nb
+        self.states, self.actions, self.terms = states, actions, terms
+
+    def range_terms(self, lo: int, hi: int) -> float:
+        if self.scenario != "b":
+            return self.terms * (hi - lo) / self.states
+        m, na, nb = self.life, self.na, self.nb
+        rem = np.arange(lo, hi, dtype=np.int64)
+        ia = np.zeros(hi - lo, np.int64)
+        ib = np.zeros(hi - lo, np.int64)
+        for i, w in enumerate([na ** (m - 1 - k) * nb ** m for k in range(m)] +
+                              [nb ** (m - 1 - k) for k in range(m)]):
+            d = rem // w
+            rem = rem % w
+            if i < m:
+                ia += d
+            else:
+                ib += d
+        return float(np.sum((ia + 1) * (ib + 1), dtype=np.float64)) * self.actions
+
+    def b_group(self) -> int:
+        """States sharing the product-A digits (one contiguous block)."""
+        return self.nb ** self.life
+
+
+def work_from_model(model) -> Work:
     sc = model.scenario()
-    n = hi - lo
-    if sc != "b":
-        return model.terms_per_sweep() * n / model.state_count()
-    m = (model.state_arity()) // 2
-    na = model.info.max_order_a + 1
-    nb = model.info.max_order_b + 1
-    s = np.arange(lo, hi, dtype=np.int64)
-    ia = np.zeros(n, np.int64)
-    ib = np.zeros(n, np.int64)
-    rem = s.copy()
-    radices = [na] * m + [nb] * m
-    weights = [int(np.prod(radices[i + 1:])) for i in range(2 * m)]
-    for i in range(2 * m):
-        d = rem // weights[i]
-        rem = rem % weights[i]
-        if i < m:
-            ia += d
-        else:
-            ib += d
-    return float(np.sum((ia + 1) * (ib + 1), dtype=np.float64)) * model.action_count()
+    life = model.state_arity() // 2 if sc == "b" else 0
+    na = model.info.max_order_a + 1 if sc == "b" else 0
+    nb = model.info.max_order_b + 1 if sc == "b" else 0
+    return Work(sc, life, na, nb, model.state_count(), model.action_count(), model.terms_per_sweep())
+
+
+def work_from_reference(preset: str) -> Work:
+    """The same closed forms from the reference's own model (refbind), SURVEY §8d:
+    A |S||A|(D+1) = |S||A||Omega|; C |S|(D+1)C(A_max+m, m) = |S||Omega|;
+    B |A| sum_s (I_a+1)(I_b+1)."""
+    from oracle import refbind as R
+    c = R.counts(preset)
+    sc = preset[0]
+    if sc == "a":
+        return Work("a", 0, 0, 0, c.states, c.actions, float(c.states) * c.actions * c.outcomes)
+    if sc == "c":
+        return Work("c", 0, 0, 0, c.states, c.actions, float(c.states) * c.outcomes)
+    t = R.b_tables(preset)
+    life = int(preset.split("/")[1][1:])
+    na, nb = t["max_order_a"] + 1, t["max_order_b"] + 1
+    per = lambda r: r ** life * (life * (r - 1) / 2.0 + 1.0)  # noqa: E731  sum over one product's digits of (I+1)
+    return Work("b", life, na, nb, c.states, c.actions, float(c.actions) * per(na) * per(nb))
 
 
 # ---------------------------------------------------------------------------
@@ -153,33 +186,30 @@ class Clocks:
 # CPU reference (oracle/_ref = the unmodified reference, compiled here)
 
 
-def cpu_sample_plan(model, budget_s: float, calib_rate: float):
+def cpu_sample_plan(work: Work, budget_s: float, calib_rate: float):
     """Contiguous state ranges spread over the space, sized to ~budget_s of CPU work."""
-    n = model.state_count()
-    if model.scenario() == "b":
-        group = int(model.info.max_order_b + 1) ** ((model.state_arity()) // 2)
-    else:
-        group = max(1, n // 4096)
+    n = work.states
+    group = work.b_group() if work.scenario == "b" else max(1, n // 4096)
     n_groups = max(1, n // group)
-    per_group = model.terms_per_sweep() / n_groups  # mean group size
+    per_group = work.terms / n_groups  # mean group size
     want = max(1, int(budget_s * calib_rate / max(per_group, 1.0)))
     want = min(want, n_groups)
     stride = max(1, n_groups // want)
     return [(g * group, min(n, (g + 1) * group)) for g in range(0, n_groups, stride)][:want]
 
 
-def run_cpu_reference(model, preset: str, precision: str, budget_s: float, V: np.ndarray,
+def run_cpu_reference(work: Work, preset: str, precision: str, budget_s: float, V: np.ndarray,
                       offset: int = 0):
     """Time the reference's bellman_backup_batch (threads = all host cores) on a bounded
     sample; returns (terms/s, seconds, terms, description, threads)."""
     from oracle import refbind as R
     threads = os.cpu_count() or 1
     # calibrate with one small range
-    plan = cpu_sample_plan(model, budget_s, 3e9)
+    plan = cpu_sample_plan(work, budget_s, 3e9)
     lo, hi = plan[len(plan) // 2]
     _, _, secs = R.backup_range(preset, V, lo, hi, f32=precision == "f32", threads=threads)
-    rate = state_terms(model, lo, hi) / max(secs, 1e-6)
-    plan = cpu_sample_plan(model, budget_s, rate)
+    rate = work.range_terms(lo, hi) / max(secs, 1e-6)
+    plan = cpu_sample_plan(work, budget_s, rate)
     if offset:
         plan = plan[offset % len(plan):] + plan[:offset % len(plan)]
     terms = 0.0
@@ -188,12 +218,13 @@ def run_cpu_reference(model, preset: str, precision: str, budget_s: float, V: np
     for lo, hi in plan:
         _, _, secs = R.backup_range(preset, V, lo, hi, f32=precision == "f32", threads=threads)
         total += secs
-        terms += state_terms(model, lo, hi)
+        terms += work.range_terms(lo, hi)
         used += hi - lo
         if total > budget_s * 1.5:
             break
-    desc = (f"reference bellman_backup_batch over {used} of {model.state_count()} states "
-            f"({terms:.3e} terms) in contiguous tiles spread across the space")
+    desc = (f"reference bellman_backup_batch over {used} of {work.states} states "
+            f"({terms:.3e} terms, {100.0 * terms / work.terms:.2f}% of a sweep) in contiguous "
+            f"tiles spread across the space")
     return terms / total, total, terms, desc, threads
 
 
@@ -202,7 +233,10 @@ def run_cpu_reference(model, preset: str, precision: str, budget_s: float, V: np
 
 
 def reference_arm(args, world, rank):
-    import paper_2303_10672_b200 as P
+    """The reference's own CPU implementation (oracle/_ref = the unmodified
+    reference sources) through its bellman_backup_batch, on all host cores.
+    Nothing from this repo's package is loaded here.  One step = one bounded
+    sample (~4 s) of the workload's sweep; value = terms/s over the samples."""
     from oracle import refbind as R
     if rank != 0:
         return
@@ -210,27 +244,29 @@ def reference_arm(args, world, rank):
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/libpvi_ref.so was not built (needs /root/reference)"}))
         return
-    model = P.make_preset(args.workload)
+    work = work_from_reference(args.workload)
     V = R.initial_values(args.workload)
     step_budget = 4.0
-    rates = []
-    times = []
+    rates, times, descs = [], [], []
     for k in range(args.warmup + args.steps):
-        rate, secs, terms, desc, threads = run_cpu_reference(model, args.workload, args.precision,
+        rate, secs, terms, desc, threads = run_cpu_reference(work, args.workload, args.precision,
                                                              step_budget, V, offset=k)
         if k >= args.warmup:
             rates.append(rate)
             times.append(secs)
+            descs.append(desc)
     value = float(sum(r * t for r, t in zip(rates, times)) / sum(times))
     line = {
         "metric": "bellman_evals_per_sec", "value": value, "unit": "evals/s",
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * model.terms_per_sweep() / value,
+        "ms_per_step": 1e3 * sum(times) / len(times),
+        "full_sweep_ms_extrapolated": 1e3 * work.terms / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": args.precision, "data": "synthetic (deterministic preset tables; V = initial value)",
-        "config": workload_config(model, args, world),
+        "config": workload_config(work, args, world),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference",
-                         "sample": desc + f"; {step_budget:.0f} s per step"},
+                         "sample": descs[0] + f"; one step = one ~{step_budget:.0f} s sample, "
+                                              f"rotated through the space step by step"},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -238,14 +274,95 @@ def reference_arm(args, world, rank):
     print(json.dumps(line))
 
 
-def workload_config(model, args, world):
-    return {"workload": f"{args.workload} Bellman sweep ({model.state_count():,} states, "
-                        f"{model.action_count()} actions, {args.precision})",
-            "preset": args.workload, "states": model.state_count(),
-            "actions": model.action_count(), "terms_per_sweep": model.terms_per_sweep(),
+def workload_config(work: Work, args, world):
+    return {"workload": f"{args.workload} Bellman sweep ({work.states:,} states, "
+                        f"{work.actions} actions, {args.precision})",
+            "preset": args.workload, "states": work.states,
+            "actions": work.actions, "terms_per_sweep": work.terms,
             "l2_flush": "256 MiB write between timed steps (V is 128 MiB, partials 2.4 GB)",
             "parallelism": f"state-shards x{world} (cost-weighted; per sweep the V runs each shard "
                            f"reads: NCCL all-to-all for factored B, all-gather otherwise)"}
+
+
+def _load_json(rel):
+    try:
+        with open(os.path.join(ROOT, rel)) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+def fp64_peak_tflops():
+    """Measured FP64 FMA peak (tools/fp64_peak.cu on a B200, profiles/r2_fp64_peak.json),
+    else the nominal 148 SMs x 64 FMA/clk x 2 x 1965 MHz."""
+    j = _load_json("profiles/r2_fp64_peak.json")
+    if j:
+        best = max(r["tflops"] for r in j["results"] if r["kernel"] == "dfma")
+        return best, "profiles/r2_fp64_peak.json (tools/fp64_peak.cu, DFMA, measured on a B200)"
+    return 148 * 64 * 2 * 1.965e9 / 1e12, "nominal 148 SMs x 64 FMA/clk x 2 x 1965 MHz (no measurement)"
+
+
+def essential_bytes(model, precision: str, states: int) -> float:
+    """Bytes a sweep of `states` states cannot avoid moving: V in, V' and the
+    argmax out, plus the per-state model table the kernel must read (factored
+    B: ER / PT, 2 doubles per state)."""
+    t = BYTES_PER_TERM[precision]
+    per = 2 * t + 4
+    if model.scenario() == "b" and getattr(model, "algorithm", "exact") == "factored":
+        per += 16
+    return float(per) * states
+
+
+def compute_roofline(model, args, work, shard_terms, shard_states, kernel_ms, k_launches, step_ms):
+    """The sweep is bound by the FP64 pipe, not by HBM: V and every table are
+    L2-resident or staged in shared memory, and no stage is a dense contraction
+    (no tensor-core form; B200's FP64 DMMA peak equals its FP64 FMA peak).
+    `achieved` = the FP64 flops the kernels execute (factored: FMAs from the loop
+    bounds, Model::factored_fmas; exact: the reference's 5 unfused ops per term)
+    / the measured K1 time; `peak` = the measured DFMA peak.  `hbm` holds the
+    memory side: the sweep's essential bytes and the ncu-measured DRAM traffic
+    per sweep (profiles/k1_traffic.json)."""
+    kernel_s = kernel_ms * 1e-3 / max(k_launches, 1)
+    frac_of_sweep = shard_terms / work.terms
+    if args.algorithm == "factored":
+        flops = 2.0 * model.info.factored_fmas * frac_of_sweep
+        flop_src = "2 x Model::factored_fmas (FMAs from the factored kernels' loop bounds)"
+    else:
+        flops = 5.0 * shard_terms
+        flop_src = "5 unfused FP64 ops per reference term (the reference's expression)"
+    peak, peak_src = fp64_peak_tflops()
+    achieved = flops / kernel_s / 1e12 if kernel_ms else 0.0
+    traffic = None
+    for tj in _load_json("profiles/k1_traffic.json") or []:
+        if (tj.get("workload"), tj.get("precision"), tj.get("algorithm")) == \
+                (args.workload, args.precision, args.algorithm):
+            traffic = tj.get("dram_bytes_per_launch")
+            if traffic is not None:
+                traffic *= frac_of_sweep
+    peaks = _load_json("MEASURED_PEAKS.json") or {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    ess = essential_bytes(model, args.precision, shard_states)
+    hbm = {"essential_bytes": ess,
+           "achieved_gbs": ess / kernel_s / 1e9 if kernel_ms else 0.0, "peak": hbm_peak,
+           "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+           "traffic_bytes": traffic}
+    hbm["frac"] = hbm["achieved_gbs"] / hbm_peak
+    if traffic:
+        hbm["traffic_gbs"] = traffic / kernel_s / 1e9
+        hbm["traffic_frac"] = hbm["traffic_gbs"] / hbm_peak
+        hbm["traffic_over_essential"] = traffic / ess
+    # the reference enumeration's gather bytes, for comparison only (L1/L2 hits)
+    ref_terms = {"bytes_per_term": BYTES_PER_TERM[args.precision], "terms_per_launch": shard_terms,
+                 "gbs": BYTES_PER_TERM[args.precision] * shard_terms / kernel_s / 1e9 if kernel_ms else 0.0,
+                 "note": "one V[next] gather per reference term (SURVEY 8d); these are L1/L2 hits "
+                         "or not performed at all by the factored kernels, so not a roofline"}
+    return {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "kernel": "K1 launches of one sweep (factored B: k_b_fact_w16p + k_b_fact_qw4)",
+            "flops_per_launch": flops, "flops_source": flop_src, "peak_source": peak_src,
+            "kernel_ms_per_launch": kernel_ms / max(k_launches, 1),
+            "kernel_share_of_step": kernel_ms / max(sum(step_ms), 1e-9),
+            "hbm": hbm, "reference_term_gather": ref_terms}
 
 
 def ours_arm(args, world, rank, local):
@@ -316,61 +433,13 @@ def ours_arm(args, world, rank, local):
     terms = model.terms_per_sweep()
     value = terms * args.steps / (total_ms * 1e-3)
 
-    # roofline of the dominant kernel (K1 backup) on this rank (its own states:
-    # a state range, or the (pair, x_b range) blocks of a unit shard)
-    shard_terms = sum(state_terms(model, a, b) for a, b in solver.own_runs[solver.rank])
-    bpt = BYTES_PER_TERM[args.precision]
-    achieved_gbs = bpt * shard_terms * k_launches / (kernel_ms * 1e-3) / 1e9 if kernel_ms else 0.0
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except OSError:
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
-            for tj in json.load(f):
-                if (tj.get("workload"), tj.get("precision"), tj.get("algorithm")) == \
-                        (args.workload, args.precision, args.algorithm):
-                    traffic = tj.get("dram_bytes_per_launch")
-    except (OSError, ValueError, AttributeError):
-        pass
-    kernel_s = kernel_ms * 1e-3 / max(k_launches, 1)
-    roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
-                "frac": achieved_gbs / peak, "traffic": traffic,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)" if peaks else
-                "fallback 6650 GB/s (B200_PROFILING.md)",
-                "algorithmic_bytes": f"{bpt} B (one V[next] gather) per reference term "
-                                     f"(SURVEY 8d); {shard_terms:.4e} terms per launch",
-                "kernel_ms_per_launch": kernel_ms / max(k_launches, 1),
-                "kernel_share_of_step": (kernel_ms / max(sum(step_ms), 1e-9)),
-                "note": "V is L1/L2-resident (re-read ~141k times per element per sweep); "
-                        "frac > 1 means the reference-term bytes never reach HBM. With the "
-                        "factored algorithm the kernel also does far fewer operations than "
-                        "reference terms; compute_roofline below is its real work. DESIGN.md 4-5."}
-    # also against the measured L2 random-gather bandwidth
-    # (tools/gather_peak.cu, 8-byte gathers from a 64 MiB buffer)
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_gather_peak.json")) as f:
-            gp = {r["buffer_mib"]: r for r in json.load(f)["results"]}
-        l2g = float(gp[64]["random_gather_gbs"])
-        roofline["l2_gather_peak"] = l2g
-        roofline["frac_vs_l2_gather"] = achieved_gbs / l2g
-        roofline["l2_gather_source"] = "profiles/r1_gather_peak.json (64 MiB, measured on a B200)"
-    except (OSError, ValueError, KeyError):
-        pass
-    fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12  # 2:1 FP32:FP64 (ncu), nominal clock
-    if args.algorithm == "factored":
-        flops = 2.0 * model.info.factored_fmas * (shard_terms / terms)
-    else:
-        flops = 5.0 * shard_terms  # the reference's 5 unfused f64 ops per term
-    compute = {"unit": "TFLOP/s (FP64)", "achieved": flops / kernel_s / 1e12 if kernel_ms else 0.0,
-               "peak": fp64_peak, "flops_per_launch": flops,
-               "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (nominal, not measured)"}
-    compute["frac"] = compute["achieved"] / fp64_peak
-
+    # roofline of the dominant kernels (the sweep's K1 launches: factored B =
+    # k_b_fact_w16p + k_b_fact_qw4) on this rank's own states
+    work = work_from_model(model)
+    shard_terms = sum(work.range_terms(a, b) for a, b in solver.own_runs[solver.rank])
+    shard_states = sum(b - a for a, b in solver.own_runs[solver.rank])
+    roofline = compute_roofline(model, args, work, shard_terms, shard_states, kernel_ms, k_launches,
+                                step_ms)
     if world > 1:
         roofline["exchange_bytes_per_rank"] = solver.read_set_bytes()
         roofline["exchange"] = ("fused peer stores from the sweep (NVLink, IPC)" if solver.buffers() is not None
@@ -385,9 +454,8 @@ def ours_arm(args, world, rank, local):
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": args.precision,
             "data": "synthetic (deterministic preset tables; V = initial value)",
-            "config": dict(workload_config(model, args, world), algorithm=args.algorithm),
-            "clocks": clk, "gpu_launches": int(all_launches), "roofline": roofline,
-            "compute_roofline": compute}
+            "config": dict(workload_config(work, args, world), algorithm=args.algorithm),
+            "clocks": clk, "gpu_launches": int(all_launches), "roofline": roofline}
 
     # the other algorithm on the same data (exact = bit-identical to the reference)
     if not args.no_alt:
@@ -493,7 +561,7 @@ def ours_arm(args, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import refbind as R
         if R.available():
-            rate, secs, sterms, desc, threads = run_cpu_reference(model, args.workload,
+            rate, secs, sterms, desc, threads = run_cpu_reference(work, args.workload,
                                                                   args.precision,
                                                                   args.cpu_budget, v0)
             line["cpu_baseline"] = {"value": rate, "unit": "evals/s", "cores": threads,

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "model.hpp"
@@ -26,6 +27,23 @@ namespace pvi_b200 {
 inline void upload_bytes(void* dst, const void* src, std::size_t bytes) {
   PVI_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
   PVI_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+}
+
+// Debug aid standing in for compute-sanitizer's initcheck (closed on this
+// GPU pool): with PVI_POISON=1 every sweep scratch buffer and every output
+// slice is filled with 0xFF bytes (NaN for f64/f32, 255 for the u8 partial
+// argmax) before a sweep, so a kernel that reads an element nobody wrote, or
+// leaves an output element unwritten, produces NaN / a wrong action that the
+// parity tests see (tests/test_gpu_poison.py).
+inline bool poison_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PVI_POISON");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+inline void maybe_poison(void* p, std::size_t bytes, cudaStream_t stream) {
+  if (p && bytes && poison_enabled()) PVI_CUDA(cudaMemsetAsync(p, 0xFF, bytes, stream));
 }
 
 __host__ __device__ inline int ipos(int x) { return x > 0 ? x : 0; }

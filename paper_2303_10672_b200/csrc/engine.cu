@@ -1029,6 +1029,9 @@ void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t
   T* vo = out_values ? ws.io.get<T>(1, nr, st) : nullptr;
   std::uint32_t* ao = out_actions ? ws.io.get<std::uint32_t>(2, nr, st) : nullptr;
   T* qo = out_q ? ws.io.get<T>(3, nr * m.n_actions, st) : nullptr;
+  maybe_poison(vo, nr * sizeof(T), st);  // debug (PVI_POISON=1): unwritten outputs show up
+  maybe_poison(ao, nr * sizeof(std::uint32_t), st);
+  maybe_poison(qo, nr * m.n_actions * sizeof(T), st);
   SweepArgs<T> a;
   a.v = v;
   a.vout = vo;

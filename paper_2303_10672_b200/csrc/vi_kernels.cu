@@ -3835,7 +3835,8 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
         }
         src = dst;
       }
-      if (qf_enabled() && !endo) {  // endogenous: per-order restaging loses to k_c_bin_q
+      // k_c_bin_qf maps 256 threads onto CQ_GROUPS groups of r states: r <= 21
+      if (qf_enabled() && !endo && r * CQ_GROUPS <= 256) {  // endogenous: per-order restaging loses to k_c_bin_q
         const std::uint64_t n_groups = dm.n_states / static_cast<std::uint64_t>(r);
         const std::size_t smq = sizeof(double) * (static_cast<std::size_t>(r) * r + 8 +
                                                   static_cast<std::size_t>(CQ_GROUPS) * r * r);
@@ -3867,6 +3868,9 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
                   Scratch& scratch, cudaStream_t stream) {
   const std::uint64_t lo = a.lo, hi = a.hi, nr = hi - lo;
   if (nr == 0) return;
+  // a complete sweep (not one stage / row block of a pipelined one) owns
+  // every scratch buffer: poison them all (debug, PVI_POISON=1)
+  if (a.stages == 3 && a.r_lo == 0 && a.r_hi == ~0ull && a.x3_rows_lo < 0) scratch.poison(stream);
   FinalizeArgs fa = a.fa;
   if (fa.stats && a.init_stats) {
     k_init_stats<<<1, 1, 0, stream>>>(fa.stats);

@@ -83,8 +83,13 @@ struct Scratch {
       ptr[slot] = nullptr;
       PVI_CUDA(cudaMalloc(&ptr[slot], need));
       bytes[slot] = need;
+      maybe_poison(ptr[slot], need, stream);
     }
     return static_cast<U*>(ptr[slot]);
+  }
+  // PVI_POISON=1: refill every buffer (called at the start of a full sweep)
+  void poison(cudaStream_t stream) {
+    for (std::size_t i = 0; i < ptr.size(); ++i) maybe_poison(ptr[i], bytes[i], stream);
   }
   ~Scratch() {
     for (void* p : ptr)
