@@ -192,10 +192,14 @@ typedef struct {
 } pvi_vi_config;
 
 /* Backup algorithm.  EXACT reproduces the reference's per-term expression
- * and summation order (bit-identical results).  FACTORED (Scenario B only;
- * others fall back to EXACT) contracts the separable issued-pair law first,
- * doing ~16x fewer operations per sweep; results agree with the reference to
- * rounding (the north-star 1e-9 contract), not bit for bit. */
+ * and summation order (bit-identical results).  FACTORED (all three
+ * scenarios; tabular models keep EXACT) regroups the sums -- B: the separable
+ * issued-pair law contracted first, with diagonal running sums; C: the
+ * demand summed per post-delivery profile, then the multinomial receipt as a
+ * chain of binomial passes; A: demand values that leave the same carried
+ * stock merged -- doing 10^2-10^4x fewer operations per sweep; results agree
+ * with the reference to rounding (V within 1e-12 per sweep, the north-star
+ * 1e-9 contract at convergence), not bit for bit. */
 typedef enum { PVI_ALGO_EXACT = 0, PVI_ALGO_FACTORED = 1 } pvi_algorithm;
 /* Default algorithm of every sweep on this model (pvi_vi_backup, pvi_q_rows,
  * pvi_vi_sweep_device, and pvi_vi_solve with algorithm = -1). */
@@ -250,9 +254,13 @@ int pvi_check_convergence(const pvi_model* m, int precision, int test, const voi
  * entries, only [lo, hi) written; actions_device: NULL or |S| u32.
  * hist_device: NULL, or an array of `n_hist` device pointers (oldest..newest,
  * the newest being values_prev) for the periodic-span statistic.
- * stats_device: 4 doubles written by the fused reduction kernel:
- *   [0] max(stat), [1] -min(stat), [2] first non-finite state (as double, or -1), [3] unused;
- * stat is |dV| (value span), dV (change span) or D(s) (periodic span).
+ * stats_device: 4 doubles written by the fused reduction kernel, encoded so
+ * that ONE element-wise MAX all-reduce over ranks combines shards:
+ *   [0] max(stat), [1] -min(stat), [2] -(first non-finite state), [3] 0.
+ * Sentinels: [0] and [1] are -DBL_MAX for an empty range; [2] is -DBL_MAX
+ * when every state is finite (a bad state s arrives as -s, so after the
+ * MAX the smallest bad state wins).  stat is |dV| (value span), dV (change
+ * span) or D(s) (periodic span).
  * want_stats = 0 skips the reduction.  stream: cudaStream_t or NULL. */
 int pvi_vi_sweep_device(const pvi_model* m, int precision, double gamma,
                         const void* values_prev_device, void* values_next_device,
@@ -367,12 +375,31 @@ int pvi_sim_evaluate(const pvi_model* m, const pvi_policy* policies, uint32_t n_
                      const pvi_rollout_config* cfg, pvi_rollout_summary* per_rollout,
                      pvi_evaluation* evals, char* err, size_t errlen);
 
+/* detail::reduce (sim.hpp:128-141) on the host: per policy and KPI, the mean
+ * (sequential sum in rollout-index order / n) and the two-pass sample sd,
+ * the same operations as the device reduction inside pvi_sim_evaluate, so
+ * per-rollout summaries gathered from several devices (rollout shards:
+ * rollout i of a shard starting at rollout f is rollout f + i of the whole
+ * evaluation when its base_seed is base_seed + f, rng.hpp:37-44) reduce to
+ * the single-device Evaluation bit for bit.  per_rollout: n_policies x
+ * n_rollouts summaries. */
+int pvi_sim_reduce(const pvi_rollout_summary* per_rollout, uint32_t n_policies, int n_rollouts, int products,
+                   pvi_evaluation* evals, char* err, size_t errlen);
+
 /* ---- simulation optimisation (simopt.hpp, runner.cpp:352-403) ----------
  * The reference's grid search / generational GA (simopt.cpp:22-161), run on
  * the host exactly as the reference runs it (std::mt19937_64 and the
  * libstdc++ distributions, so the search trajectory is the reference's),
  * with each generation's fresh candidates scored in ONE batched device
  * evaluation (pvi_sim_evaluate) instead of one evaluate_policy per candidate. */
+/* Scores a batch of heuristic candidates (n x dimension ints, row-major) into
+ * means[n] / sds[n]; returns 0, or nonzero to abort the search.  Lets a
+ * caller put the batch point on other devices: the multi-GPU driver
+ * (sharded_sim.py) runs the same GA on every rank and shards each
+ * generation's candidates (or rollouts) across the ranks inside it. */
+typedef int (*pvi_score_batch_fn)(void* user, const int* candidates, int n, int dimension, double* means,
+                                  double* sds);
+
 typedef struct {
   int sampler;                 /* 0 auto (grid if 1-D, else GA), 1 grid, 2 GA, 3 exhaustive
                                   grid over the whole product space in one batch (GPU-only
@@ -388,6 +415,8 @@ typedef struct {
   int warmup_days;             /* 100 */
   uint64_t base_seed;          /* eval.base_seed, 42 */
   int device;                  /* -1 = current */
+  pvi_score_batch_fn score_batch; /* NULL: pvi_sim_evaluate on `device` (the default) */
+  void* score_user;            /* passed to score_batch */
 } pvi_simopt_config;
 
 void pvi_simopt_config_defaults(pvi_simopt_config* c);

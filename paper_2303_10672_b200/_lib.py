@@ -96,7 +96,13 @@ class SimoptConfigC(C.Structure):
                 ("patience", C.c_int), ("crossover_rate", C.c_double),
                 ("mutation_rate", C.c_double), ("seed", C.c_uint64),
                 ("rollouts_per_candidate", C.c_int), ("horizon_days", C.c_int),
-                ("warmup_days", C.c_int), ("base_seed", C.c_uint64), ("device", C.c_int)]
+                ("warmup_days", C.c_int), ("base_seed", C.c_uint64), ("device", C.c_int),
+                ("score_batch", C.c_void_p), ("score_user", C.c_void_p)]
+
+
+# int (*)(void* user, const int* candidates, int n, int dimension, double* means, double* sds)
+SCORE_BATCH_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int), C.c_int, C.c_int,
+                             C.POINTER(C.c_double), C.POINTER(C.c_double))
 
 
 class ScoredCandidateC(C.Structure):
@@ -161,6 +167,7 @@ SIGNATURES = {
     "pvi_policy_csv_parse": (C.c_int, [_vp, _vp, C.c_uint64, _vp, C.c_char_p, C.c_size_t]),
     "pvi_rollout_config_defaults": (None, [_vp]),
     "pvi_sim_evaluate": (C.c_int, [_vp, _vp, C.c_uint32, _vp, _vp, _vp] + _E),
+    "pvi_sim_reduce": (C.c_int, [_vp, C.c_uint32, C.c_int, C.c_int, _vp] + _E),
     "pvi_philox_block": (C.c_int, [_vp, _vp, _vp]),
     "pvi_rollout_draws": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_int, _vp]),
     "pvi_checkpoint_save": (C.c_int, [C.c_char_p, _vp, C.c_uint64, C.c_uint64, _vp] + _E),

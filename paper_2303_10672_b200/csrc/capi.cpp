@@ -504,6 +504,16 @@ void pvi_simopt_config_defaults(pvi_simopt_config* c) {
   c->device = -1;
 }
 
+int pvi_sim_reduce(const pvi_rollout_summary* per_rollout, uint32_t n_policies, int n_rollouts, int products,
+                   pvi_evaluation* evals, char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if (n_rollouts < 1) fail(PVI_ERR_PARAMETER, "evaluation needs at least one rollout");
+    if (products < 1 || products > 2) fail(PVI_ERR_PARAMETER, "products must be 1 or 2");
+    if (n_policies && (!per_rollout || !evals)) fail(PVI_ERR_PARAMETER, "null argument");
+    sim_reduce_host(reinterpret_cast<const double*>(per_rollout), n_policies, n_rollouts, products, evals);
+  });
+}
+
 int pvi_simopt(const pvi_model* m, const pvi_simopt_config* cfg, int* best, double* best_mean,
                double* best_sd, int* generations, pvi_scored_candidate* log, int log_capacity,
                int* n_logged, int* dimension, double* device_seconds, char* err, size_t errlen) {

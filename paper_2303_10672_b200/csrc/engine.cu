@@ -15,6 +15,8 @@
 #include <exception>
 #include <filesystem>
 #include <fstream>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -1313,6 +1315,19 @@ bool check_convergence(const Model& m, int precision, int test, const void* cons
 // Device-resident sweep of one shard (multi-GPU driver)
 
 namespace {
+struct DeviceSweepBufs {
+  Scratch scratch;
+  std::unique_ptr<DevBuf> st;
+  DevBuf* stats() {
+    if (!st) st.reset(new DevBuf(sizeof(SweepStats)));
+    return st.get();
+  }
+};
+DeviceSweepBufs& device_sweep_bufs(int device) {
+  static thread_local std::map<int, DeviceSweepBufs> bufs;
+  return bufs[device];
+}
+
 __global__ void k_stats_to_doubles(const SweepStats* st, double* out) {
   const SweepStats s = *st;
   out[0] = s.max_key == 0ull ? -1.7976931348623157e308 : dkey_inv(s.max_key);
@@ -1329,9 +1344,12 @@ void sweep_device_impl(const Model& m, double gamma, const void* vprev, void* vn
   int device = 0;
   PVI_CUDA(cudaGetDevice(&device));
   const DevModel& dm = m.device_view(device);
-  static thread_local Scratch scratch;
-  static thread_local DevBuf* dstats = nullptr;
-  if (!dstats) dstats = new DevBuf(sizeof(SweepStats));
+  // per (thread, device) scratch and statistics: the device-resident sweeps
+  // of one thread run one at a time per device (they share these buffers;
+  // the sharded driver issues them from one thread on one stream)
+  DeviceSweepBufs& bufs = device_sweep_bufs(device);
+  Scratch& scratch = bufs.scratch;
+  DevBuf* dstats = bufs.stats();
   SweepArgs<T> a;
   a.v = static_cast<const T*>(vprev);
   a.vout = static_cast<T*>(vnext);
@@ -1526,9 +1544,12 @@ void sweep_units_impl(const Model& m, double gamma, const void* vprev, void* vne
   int device = 0;
   PVI_CUDA(cudaGetDevice(&device));
   const DevModel& dm = m.device_view(device);
-  static thread_local Scratch scratch;
-  static thread_local DevBuf* dstats = nullptr;
-  if (!dstats) dstats = new DevBuf(sizeof(SweepStats));
+  // per (thread, device) scratch and statistics: the device-resident sweeps
+  // of one thread run one at a time per device (they share these buffers;
+  // the sharded driver issues them from one thread on one stream)
+  DeviceSweepBufs& bufs = device_sweep_bufs(device);
+  Scratch& scratch = bufs.scratch;
+  DevBuf* dstats = bufs.stats();
   const std::uint64_t n = m.space.count;
   bool first = true;
   const bool st_on = want_stats && stats;

@@ -59,6 +59,8 @@ void load_checkpoint(const std::string& path, const std::uint8_t* expected, doub
 void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_policies,
                   const pvi_rollout_config& cfg, pvi_rollout_summary* per_rollout,
                   pvi_evaluation* evals);
+// detail::reduce on the host (pvi_sim_reduce): summ is n_policies x n x 7
+void sim_reduce_host(const double* summ, std::uint32_t n_policies, int n, int products, pvi_evaluation* evals);
 void simopt_run(const Model& m, const pvi_simopt_config& cfg, int* best, double* best_mean,
                 double* best_sd, int* generations, pvi_scored_candidate* log, int log_capacity,
                 int* n_logged, int* dimension, double* device_seconds);

@@ -435,6 +435,27 @@ cudaStream_t sim_stream(int device) {
 
 using Buf = PoolBuf;
 
+void fill_evaluations(const double* stat, std::uint32_t n_policies, int n_rollouts, int products,
+                      pvi_evaluation* evals) {
+  for (std::uint32_t p = 0; p < n_policies; ++p) {
+    const double* s = stat + static_cast<std::size_t>(p) * 14;
+    pvi_evaluation& e = evals[p];
+    std::memset(&e, 0, sizeof(e));
+    e.products = products;
+    e.n_rollouts = n_rollouts;
+    e.ret_mean = s[0];
+    e.ret_sd = s[1];
+    for (int k = 0; k < products; ++k) {
+      e.service_mean[k] = s[2 * (1 + k)];
+      e.service_sd[k] = s[2 * (1 + k) + 1];
+      e.wastage_mean[k] = s[2 * (3 + k)];
+      e.wastage_sd[k] = s[2 * (3 + k) + 1];
+      e.holding_mean[k] = s[2 * (5 + k)];
+      e.holding_sd[k] = s[2 * (5 + k) + 1];
+    }
+  }
+}
+
 }  // namespace
 
 void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_policies,
@@ -537,25 +558,33 @@ void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_po
     fail(PVI_ERR_CONTRACT, "policy returned out-of-range order " + std::to_string(herr.action) +
                                " in state [ " + tuple + "]");
   }
-  if (evals) {
-    for (std::uint32_t p = 0; p < n_policies; ++p) {
-      const double* s = &hstat[static_cast<std::size_t>(p) * 14];
-      pvi_evaluation& e = evals[p];
-      std::memset(&e, 0, sizeof(e));
-      e.products = products;
-      e.n_rollouts = cfg.n_rollouts;
-      e.ret_mean = s[0];
-      e.ret_sd = s[1];
-      for (int k = 0; k < products; ++k) {
-        e.service_mean[k] = s[2 * (1 + k)];
-        e.service_sd[k] = s[2 * (1 + k) + 1];
-        e.wastage_mean[k] = s[2 * (3 + k)];
-        e.wastage_sd[k] = s[2 * (3 + k) + 1];
-        e.holding_mean[k] = s[2 * (5 + k)];
-        e.holding_sd[k] = s[2 * (5 + k) + 1];
+  if (evals) fill_evaluations(hstat.data(), n_policies, cfg.n_rollouts, products, evals);
+}
+
+void sim_reduce_host(const double* summ, std::uint32_t n_policies, int n, int products, pvi_evaluation* evals) {
+  // the operations of k_reduce_eval (and of the reference's detail::reduce),
+  // compiled without FMA contraction: the same bits
+  std::vector<double> stat(static_cast<std::size_t>(n_policies) * 14);
+  for (std::uint32_t p = 0; p < n_policies; ++p)
+    for (int f = 0; f < 7; ++f) {
+      const double* base = summ + static_cast<std::size_t>(p) * n * 7 + f;
+      double sum = 0.0;
+      for (int i = 0; i < n; ++i) sum += base[static_cast<std::size_t>(i) * 7];
+      const double mean = sum / static_cast<double>(n);
+      double sd = 0.0;
+      if (n > 1) {
+        double ss = 0.0;
+        for (int i = 0; i < n; ++i) {
+          const double x = base[static_cast<std::size_t>(i) * 7];
+          const double d = x - mean;
+          ss += d * d;
+        }
+        sd = std::sqrt(ss / static_cast<double>(n - 1));
       }
+      stat[(static_cast<std::size_t>(p) * 7 + f) * 2] = mean;
+      stat[(static_cast<std::size_t>(p) * 7 + f) * 2 + 1] = sd;
     }
-  }
+  fill_evaluations(stat.data(), n_policies, n, products, evals);
 }
 
 void philox_block_device(const std::uint32_t ctr[4], const std::uint32_t key[2], std::uint32_t out[4]) {

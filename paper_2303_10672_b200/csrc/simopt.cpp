@@ -57,7 +57,7 @@ bool better(const std::vector<int>& a, double ma, const std::vector<int>& b, dou
 
 class Evaluator {
  public:
-  Evaluator(const Model& m, const pvi_simopt_config& c) : m_(m) {
+  Evaluator(const Model& m, const pvi_simopt_config& c) : m_(m), fn_(c.score_batch), user_(c.score_user) {
     rc_.horizon_days = c.horizon_days;
     rc_.warmup_days = c.warmup_days;
     rc_.n_rollouts = c.rollouts_per_candidate;
@@ -67,6 +67,19 @@ class Evaluator {
   std::vector<Score> operator()(const std::vector<const std::vector<int>*>& batch) {
     std::vector<Score> out(batch.size());
     if (batch.empty()) return out;
+    if (fn_) {  // the caller's batch point (e.g. sharded over several GPUs)
+      const int dim = static_cast<int>(batch[0]->size());
+      std::vector<int> flat;
+      flat.reserve(batch.size() * dim);
+      for (const auto* c : batch) flat.insert(flat.end(), c->begin(), c->end());
+      std::vector<double> means(batch.size()), sds(batch.size());
+      const auto t0 = std::chrono::steady_clock::now();
+      const int rc = fn_(user_, flat.data(), static_cast<int>(batch.size()), dim, means.data(), sds.data());
+      seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (rc != 0) fail(PVI_ERR_FAILURE, "simopt: score_batch callback failed (" + std::to_string(rc) + ")");
+      for (std::size_t i = 0; i < batch.size(); ++i) out[i] = {means[i], sds[i]};
+      return out;
+    }
     std::vector<pvi_policy> pols(batch.size());
     for (std::size_t i = 0; i < batch.size(); ++i) {
       pols[i] = pvi_policy{};
@@ -85,6 +98,8 @@ class Evaluator {
 
  private:
   const Model& m_;
+  pvi_score_batch_fn fn_ = nullptr;
+  void* user_ = nullptr;
   pvi_rollout_config rc_{};
 };
 

@@ -6,7 +6,7 @@
 // per-(state, action) accumulation visits its terms in the reference's
 // order with the reference's expression tree (cited per kernel).  The
 // device therefore reproduces the reference CPU solver's value vectors bit
-// for bit in both f64 and f32 modes (tests/test_gpu_parity.py).
+// for bit in both f64 and f32 modes (tests/test_gpu_vi.py, test_gpu_headline.py).
 //
 // Layout in HBM: V is a flat |S| array of T in mixed-radix index order
 // (digit 0 most significant, tuple_space.hpp:12-13), exactly the

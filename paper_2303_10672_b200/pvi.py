@@ -801,6 +801,26 @@ def evaluate_policies(model: Model, policies: Sequence[Policy], config: RolloutC
     return out, summ
 
 
+def _evaluation(e) -> "Evaluation":
+    return Evaluation(KpiStat(e.ret_mean, e.ret_sd),
+                      [KpiStat(e.service_mean[k], e.service_sd[k]) for k in range(2)],
+                      [KpiStat(e.wastage_mean[k], e.wastage_sd[k]) for k in range(2)],
+                      [KpiStat(e.holding_mean[k], e.holding_sd[k]) for k in range(2)],
+                      e.products, e.n_rollouts)
+
+
+def sim_reduce(summaries: np.ndarray, products: int) -> list:
+    """detail::reduce (sim.hpp:128-141) of per-rollout summaries shaped
+    (n_policies, n_rollouts, 7), in rollout-index order, on the host
+    (pvi_sim_reduce): bit-identical to pvi_sim_evaluate's own reduction."""
+    a = np.ascontiguousarray(summaries, np.float64)
+    n_pol, n = a.shape[0], a.shape[1]
+    ev = (L.EvaluationC * max(1, n_pol))()
+    err = _err_buf()
+    _raise(L.load().pvi_sim_reduce(_p(a), n_pol, n, products, ev, err, len(err)), err)
+    return [_evaluation(ev[i]) for i in range(n_pol)]
+
+
 def evaluate_policy(model: Model, policy: Policy, config: RolloutConfig) -> Evaluation:
     return evaluate_policies(model, [policy], config)[0][0]
 
@@ -820,8 +840,12 @@ def simopt(model: Model, sampler: str = "auto", population: int = 50, max_genera
            patience: int = 5, crossover_rate: float = 0.9, mutation_rate: float = 0.0,
            seed: int = 1, rollouts_per_candidate: int = 4000, horizon_days: int = 365,
            warmup_days: int = 100, base_seed: int = 42, device: int = -1,
-           log_capacity: int = 20000) -> SimoptResult:
-    """cmd_simopt's search (runner.cpp:352-403): grid (1-D) or GA, batched on the GPU."""
+           log_capacity: int = 20000, score_batch=None) -> SimoptResult:
+    """cmd_simopt's search (runner.cpp:352-403): grid (1-D) or GA, batched on the GPU.
+
+    score_batch: optional callable (candidates: int array n x dim) -> (means, sds)
+    that replaces the single-device evaluator as the batch point (the sharded
+    multi-GPU driver passes one; sharded_sim.py)."""
     import time
     c = L.SimoptConfigC()
     lib = L.load()
@@ -832,15 +856,35 @@ def simopt(model: Model, sampler: str = "auto", population: int = 50, max_genera
     c.rollouts_per_candidate, c.horizon_days, c.warmup_days = (rollouts_per_candidate,
                                                               horizon_days, warmup_days)
     c.base_seed, c.device = base_seed, device
+    cb = None
+    failure = []
+    if score_batch is not None:
+        def _cb(user, cands, n, dim, means, sds):
+            try:
+                arr = np.ctypeslib.as_array(cands, shape=(n * dim,)).reshape(n, dim).copy()
+                mu, sd = score_batch(arr)
+                for i in range(n):
+                    means[i] = float(mu[i])
+                    sds[i] = float(sd[i])
+                return 0
+            except BaseException as e:  # noqa: BLE001 -- reported after the C call returns
+                failure.append(e)
+                return 1
+        cb = L.SCORE_BATCH_FN(_cb)
+        c.score_batch = C.cast(cb, C.c_void_p)
     best = (C.c_int * 14)()
     bm, bsd, dev_s = C.c_double(), C.c_double(), C.c_double()
     gens, nlog, dim = C.c_int(), C.c_int(), C.c_int()
     logs = (L.ScoredCandidateC * log_capacity)()
     err = _err_buf()
     t0 = time.perf_counter()
-    _raise(lib.pvi_simopt(model.handle, C.byref(c), best, C.byref(bm), C.byref(bsd),
-                          C.byref(gens), logs, log_capacity, C.byref(nlog), C.byref(dim),
-                          C.byref(dev_s), err, len(err)), err)
+    rc = lib.pvi_simopt(model.handle, C.byref(c), best, C.byref(bm), C.byref(bsd),
+                        C.byref(gens), logs, log_capacity, C.byref(nlog), C.byref(dim),
+                        C.byref(dev_s), err, len(err))
+    if failure:
+        raise failure[0]
+    _raise(rc, err)
+    del cb
     wall = time.perf_counter() - t0
     d = dim.value
     entries = [(logs[i].generation, list(logs[i].values[:d]), logs[i].mean, logs[i].sd)

@@ -112,7 +112,12 @@ class ShardedValueIteration:
         # than whole pairs.  shards: "auto" (units where the sweep supports
         # them and there is more than one rank), "units", "range".
         self.units = None
-        if shards != "range" and self.world > 1:
+        test0 = (model.default_convergence_test() if (config is None or config.convergence_test is None)
+                 else P._TEST_NAMES[config.convergence_test])
+        if shards == "units" and test0 == P.PERIODIC_SPAN:
+            raise P.ParameterError("unit shards: the periodic-span statistic needs range shards")
+        # the unit sweep has no periodic-span statistic: range shards then
+        if shards != "range" and self.world > 1 and test0 != P.PERIODIC_SPAN:
             try:
                 nu = model.unit_count()
             except P.Error:
