@@ -268,15 +268,19 @@ int pvi_vi_sweep_device(const pvi_model* m, int precision, double gamma,
                         const void* const* hist_device, int n_hist, int want_stats,
                         double* stats_device, void* stream, char* err, size_t errlen);
 
-/* pvi_vi_sweep_device with the exchange fused into the sweep: for the
- * factored Scenario B x_3-pair sweep (the only one whose read set is a
- * function of the shard), the finalize of the stage-2 kernel also stores
- * every V' entry of [lo, hi) into the replica of each peer whose next sweep
- * reads it, over NVLink peer memory, as the state is finished.  peer_vnext:
- * the peers' next-value buffers mapped into this process (pvi_ipc_open);
+/* pvi_vi_sweep_device with the exchange fused into the sweep: the kernel
+ * that finishes a state's V' also stores it into peers' replicas over
+ * NVLink peer memory, so the refresh overlaps the sweep instead of
+ * following it.  For the factored Scenario B x_3-pair sweep (whose read set
+ * is a function of the shard) each entry goes only to the peers whose next
+ * sweep reads it; for every other sweep (which gathers from all of V) every
+ * entry of [lo, hi) goes to every peer (full replicas).  peer_vnext: the
+ * peers' next-value buffers mapped into this process (pvi_ipc_open);
  * peer_lo / peer_hi: the peers' shards.  After the peers' sweeps the caller
- * synchronises the ranks (the convergence statistics' all-reduce does).
- * PVI_ERR_PARAMETER for any other sweep, for periodic span, > 8 peers. */
+ * synchronises the ranks (the convergence statistics' all-reduce does; the
+ * kernels fence their peer stores system-wide before it).
+ * PVI_ERR_PARAMETER for periodic span (its 8-vector ring is refreshed by the
+ * caller) and for > 8 peers. */
 int pvi_vi_sweep_device_peers(const pvi_model* m, int precision, double gamma,
                               const void* values_prev_device, void* values_next_device, uint64_t lo,
                               uint64_t hi, int test, int want_stats, double* stats_device, void* stream,

@@ -1372,6 +1372,7 @@ void sweep_device_impl(const Model& m, double gamma, const void* vprev, void* vn
   }
   if (peers) {
     a.fa.n_peers = peers->n_peers;
+    a.fa.peer_all = peers->peer_all;
     for (int q = 0; q < peers->n_peers; ++q) {
       a.fa.peer_v[q] = peers->peer_v[q];
       a.fa.peer_x3_lo[q] = peers->peer_x3_lo[q];
@@ -1651,10 +1652,23 @@ void vi_sweep_device_peers(const Model& m, int precision, double gamma, const vo
   if (test == PVI_TEST_PERIODIC_SPAN) fail(PVI_ERR_PARAMETER, "peer sweep: periodic span not supported");
   int device = 0;
   PVI_CUDA(cudaGetDevice(&device));
-  if (!b_sweep_honours_xb_range(m, device))
-    fail(PVI_ERR_PARAMETER, "fused peer writes need the factored Scenario B x_3-pair sweep");
   FinalizeArgs pf;
   pf.n_peers = n_peers;
+  if (!b_sweep_honours_xb_range(m, device)) {
+    // every other sweep gathers from all of V: broadcast each finished V'
+    // entry of [lo, hi) into every peer's replica
+    pf.peer_all = 1;
+    for (int q = 0; q < n_peers; ++q) {
+      if (!peer_vnext[q] || peer_hi[q] > m.space.count) fail(PVI_ERR_PARAMETER, "bad peer descriptor");
+      pf.peer_v[q] = peer_vnext[q];
+    }
+    auto st = static_cast<cudaStream_t>(stream);
+    if (precision == 1)
+      sweep_device_impl<float>(m, gamma, vprev, vnext, nullptr, lo, hi, test, nullptr, 0, want_stats, stats, st, &pf);
+    else
+      sweep_device_impl<double>(m, gamma, vprev, vnext, nullptr, lo, hi, test, nullptr, 0, want_stats, stats, st, &pf);
+    return;
+  }
   const int na = m.b_na;
   const std::uint64_t n_xb = static_cast<std::uint64_t>(m.b_nb) * m.b_nb * m.b_nb;
   const std::uint64_t per = static_cast<std::uint64_t>(na) * na * n_xb;
@@ -1678,6 +1692,15 @@ void vi_sweep_device_peers(const Model& m, int precision, double gamma, const vo
 void partition(const Model& m, int parts, std::uint64_t* bounds) {
   if (parts < 1) fail(PVI_ERR_PARAMETER, "partition: parts must be >= 1");
   const std::uint64_t n = m.space.count;
+  if (c_weekday_local(m)) {
+    // factored C: whole weekdays (a shard's tables are its weekdays' rows,
+    // launch_c_factored); 7 weekdays over `parts` ranks, sizes differ by <= 1
+    const std::uint64_t w = n / 7;
+    bounds[0] = 0;
+    for (int p = 1; p <= parts; ++p) bounds[p] = std::min<std::uint64_t>(7, (7ull * p + parts - 1) / parts) * w;
+    bounds[parts] = n;
+    return;
+  }
   const std::uint64_t tile = std::max<std::uint64_t>(1, m.tile_states());
   const std::uint64_t n_tiles = (n + tile - 1) / tile;
   std::vector<double> cost(n_tiles, 0.0);

@@ -35,6 +35,11 @@ template <typename T>
 __device__ __forceinline__ void state_stat(const FinalizeArgs& fa, std::uint64_t s, T vnew,
                                            const T* __restrict__ vprev, double& smax,
                                            double& smin, unsigned long long& bad) {
+  // fused exchange, broadcast form (every sweep but factored B's x_3-pair
+  // sweep, whose readers are a function of the shard: peer_store): each
+  // finished V' entry goes straight into every peer's replica over NVLink
+  if (fa.peer_all)
+    for (int q = 0; q < fa.n_peers; ++q) static_cast<T*>(fa.peer_v[q])[s] = vnew;
   const double cur = static_cast<double>(vnew);
   if (!isfinite(cur)) bad = s < bad ? s : bad;
   if (fa.test < 0) return;
@@ -65,6 +70,7 @@ __device__ __forceinline__ void state_stat(const FinalizeArgs& fa, std::uint64_t
 // below its range's top (vi_kernels.cu sweep_read_runs).
 template <typename T>
 __device__ __forceinline__ void peer_store(const FinalizeArgs& fa, int xa, int na, int st, T v) {
+  if (fa.peer_all) return;  // state_stat stores to every peer
   const int ap = xa % (na * na), x2r = ap % na, x3r = ap / na;
   for (int q = 0; q < fa.n_peers; ++q) {
     const bool need = (x3r >= fa.peer_x3_lo[q] && x3r <= fa.peer_x3_hi[q]) || (x2r == 0 && x3r <= fa.peer_x3_hi[q]);
@@ -73,7 +79,11 @@ __device__ __forceinline__ void peer_store(const FinalizeArgs& fa, int xa, int n
 }
 
 __device__ __forceinline__ void reduce_stats(double smax, double smin, unsigned long long bad,
-                                             SweepStats* st) {
+                                             const FinalizeArgs& fa) {
+  // peer stores of this CTA visible system-wide before the statistics (and
+  // the all-reduce that follows the kernel) are
+  if (fa.n_peers) __threadfence_system();
+  SweepStats* st = fa.stats;
   if (st == nullptr) return;
   for (int o = 16; o > 0; o >>= 1) {
     smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
@@ -112,7 +122,9 @@ __device__ __forceinline__ void reduce_stats(double smax, double smin, unsigned 
 // reduce_stats for one-warp CTAs: shuffles only (reduce_stats' 768 bytes of
 // static shared memory would cost k_b_fact_qw4 one resident CTA per SM)
 __device__ __forceinline__ void reduce_stats_warp(double smax, double smin, unsigned long long bad,
-                                                  SweepStats* st) {
+                                                  const FinalizeArgs& fa) {
+  if (fa.n_peers) __threadfence_system();
+  SweepStats* st = fa.stats;
   if (st == nullptr) return;
   for (int o = 16; o > 0; o >>= 1) {
     smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
@@ -254,7 +266,7 @@ __global__ void __launch_bounds__(256) k_sweep_a(DevModel dm, const T* __restric
     if (act) act[s - out_off] = besta;
     state_stat<T>(fa, s, best, V, smax, smin, bad);
   }
-  reduce_stats(smax, smin, bad, fa.stats);
+  reduce_stats(smax, smin, bad, fa);
 }
 
 // ---------------------------------------------------------------------------
@@ -651,7 +663,7 @@ __global__ void __launch_bounds__(256) k_a_fact(DevModel dm, const T* __restrict
     if (act) act[s - out_off] = besta;
     state_stat<T>(fa, s, best, V, smax, smin, bad);
   }
-  reduce_stats(smax, smin, bad, fa.stats);
+  reduce_stats(smax, smin, bad, fa);
 }
 
 // LIFO: the carried stock's fate does not depend on the oldest bucket x_1
@@ -743,7 +755,7 @@ __global__ void __launch_bounds__(128) k_a_fact_lifo(DevModel dm, const T* __res
       state_stat<T>(fa, s, best, V, smax, smin, bad);
     }
   }
-  reduce_stats(smax, smin, bad, fa.stats);
+  reduce_stats(smax, smin, bad, fa);
 }
 
 // FIFO by diagonals (the K1-B stage-2 construction on the A side): with
@@ -861,7 +873,7 @@ __global__ void __launch_bounds__(128) k_a_fact_fifo(DevModel dm, const T* __res
       for (int a = 0; a < NA; ++a) acc[a] = fma(p, rv[a], acc[a]);
     }
   }
-  reduce_stats(smax, smin, bad, fa.stats);
+  reduce_stats(smax, smin, bad, fa);
 }
 
 // ---------------------------------------------------------------------------
@@ -1800,7 +1812,7 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qd3(DevModel dm, const double
       if (WA && act) act[st - out_off] = s_arg[xa];
       state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
     }
-    reduce_stats(smx, smn, bad, fa.stats);
+    reduce_stats(smx, smn, bad, fa);
   }
 }
 
@@ -1959,7 +1971,7 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qp3(DevModel dm, const double
     if (WA && act) act[st - out_off] = s_arg[xa];
     state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
   }
-  reduce_stats(smx, smn, bad, fa.stats);
+  reduce_stats(smx, smn, bad, fa);
 }
 
 // k_b_fact_qp3 with one warp per CTA: CTA = (x_3 pair, x_b).  The CTA stages
@@ -2124,8 +2136,7 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw3(DevModel dm, const double
     if (fa.n_peers) peer_store<T>(fa, xa, na, st, best);
     state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
   }
-  if (fa.n_peers) __threadfence_system();  // peer stores visible before the stats reach NCCL
-  reduce_stats(smx, smn, bad, fa.stats);
+  reduce_stats(smx, smn, bad, fa);
 }
 
 // k_b_fact_qw3 with three changes:
@@ -2392,8 +2403,7 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
     if (fa.n_peers) peer_store<T>(fa, xa, na, st, best);
     state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
   }
-  if (fa.n_peers) __threadfence_system();  // peer stores visible before the stats reach NCCL
-  reduce_stats_warp(smx, smn, bad, fa.stats);
+  reduce_stats_warp(smx, smn, bad, fa);
 }
 
 // ---------------------------------------------------------------------------
@@ -2519,10 +2529,10 @@ __global__ void __launch_bounds__(128) k_sweep_c(DevModel dm, const T* __restric
 template <typename T, int M, int DN = 0>
 __global__ void __launch_bounds__(256) k_c_fact_g(DevModel dm, const T* __restrict__ V,
                                                   double* __restrict__ G, int n_prof,
-                                                  double gamma) {
+                                                  double gamma, int tau0) {
   constexpr int NRA = DN > 0 ? M * (DN - 1) + DN : 1;  // x = total - d in [-(DN-1), M (DN-1)]
   __shared__ double s_ra[NRA], s_cw[DN > 0 ? DN : 1], s_pmf[DN > 0 ? DN : 1];
-  const int tau = blockIdx.y;
+  const int tau = tau0 + static_cast<int>(blockIdx.y);  // a shard computes its weekdays' rows only
   if (DN > 0) {
     for (int i = threadIdx.x; i < NRA; i += blockDim.x) {
       const int x = i - (DN - 1);
@@ -2678,7 +2688,7 @@ __global__ void __launch_bounds__(256) k_c_bin_level(const double* __restrict__ 
                                                      const double* __restrict__ binom_k,
                                                      std::size_t binom_a_stride, int r,
                                                      std::uint32_t wk, std::uint32_t wb,
-                                                     int endo, int in_is_g, int n_prof) {
+                                                     int endo, int in_is_g, int n_prof, int tau0) {
   extern __shared__ double s_bin[];
   const int a = static_cast<int>(blockIdx.z);
   const int nb = endo ? a + 1 : r;
@@ -2687,7 +2697,7 @@ __global__ void __launch_bounds__(256) k_c_bin_level(const double* __restrict__ 
   __syncthreads();
   const int gid = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gid >= nb * static_cast<int>(wb)) return;
-  const int tau = static_cast<int>(blockIdx.y);
+  const int tau = tau0 + static_cast<int>(blockIdx.y);
   const int b = gid / static_cast<int>(wb);
   const int dk = (gid / static_cast<int>(wk)) % r;
   const std::size_t out_base =
@@ -2704,66 +2714,18 @@ __global__ void __launch_bounds__(256) k_c_bin_level(const double* __restrict__ 
   Hout[out_base + gid] = acc;
 }
 
-// The same pass with the (b, d_k) plane staged in shared memory.  A pass
-// only mixes the "units left" digit b and digit k, so for fixed tau, order a
-// and the other digits the outputs Hout(b, d_k) of all x_1 read one
-// [b' <= a][d'][x_1] block of Hin: the CTA stages that block (each input read
+// The pass with the (b, d_k) plane staged in shared memory.  A pass only
+// mixes the "units left" digit b and digit k, so for fixed tau, order a and
+// the other digits the outputs Hout(b, d_k) of all x_1 read one
+// [b' <= a][d'][x_1] block of Hin: a CTA stages that block (each input read
 // from global memory once instead of ~b times through L1/L2) and thread
-// (x_1, d_k) walks b.  Same terms in the same order as k_c_bin_level.
-__global__ void __launch_bounds__(448) k_c_bin_tile(const double* __restrict__ Hin,
-                                                    double* __restrict__ Hout,
-                                                    const double* __restrict__ binom_k,
-                                                    std::size_t binom_a_stride, int r, int m,
-                                                    int k, std::uint32_t wb, int endo, int in_is_g,
-                                                    int n_prof) {
-  extern __shared__ double tile[];  // [b][d_k][x_1]
-  __shared__ double s_bin[32 * 32];
-  const int a = endo ? r - 1 - static_cast<int>(blockIdx.z) : 0;  // heavy orders first
-  const int nb = endo ? a + 1 : r;
-  const int tau = static_cast<int>(blockIdx.y);
-  const int cap = r - 1;
-  // rest digits: positions 1..m-1 with weights r^(p-1); x_1 (p = 1) and
-  // digit k are the tile axes, the others come from blockIdx.x
-  std::uint32_t rest0 = 0, wk = 1;
-  {
-    std::uint32_t o = blockIdx.x, w = 1;
-    for (int p = 1; p <= m - 1; ++p) {
-      if (p == k) wk = w;
-      if (p != 1 && p != k) {
-        rest0 += (o % static_cast<std::uint32_t>(r)) * w;
-        o /= static_cast<std::uint32_t>(r);
-      }
-      w *= static_cast<std::uint32_t>(r);
-    }
-  }
-  const double* bt = binom_k + a * binom_a_stride;
-  for (int i = threadIdx.x; i < nb * r; i += blockDim.x) s_bin[i] = bt[i];
-  const std::size_t out_base =
-      endo ? c_tri_base(a, wb) + static_cast<std::size_t>(tau) * nb * wb
-           : static_cast<std::size_t>(tau) * n_prof;
-  const std::size_t in_base = (endo && !in_is_g) ? out_base : static_cast<std::size_t>(tau) * n_prof;
-  const int plane = r * r;
-  for (int i = threadIdx.x; i < nb * plane; i += blockDim.x) {
-    const int b = i / plane, e = i % plane, d = e / r, x1 = e % r;
-    tile[i] = __ldg(Hin + in_base + static_cast<std::size_t>(b) * wb + rest0 + d * wk + x1);
-  }
-  __syncthreads();
-  if (static_cast<int>(threadIdx.x) >= plane) return;
-  const int dk = threadIdx.x / r, x1 = threadIdx.x % r;
-  double* out = Hout + out_base + rest0 + dk * wk + x1;
-  for (int b = 0; b < nb; ++b) {
-    const double* w = s_bin + b * r;
-    double acc = 0.0;
-    for (int y = 0; y <= b; ++y) acc = fma(w[y], tile[((b - y) * r + min(dk + y, cap)) * r + x1], acc);
-    out[static_cast<std::size_t>(b) * wb] = acc;
-  }
-}
-
-// Persistent form of k_c_bin_tile: one CTA per SM walks the (order a,
-// tau, line) items with a stride of gridDim.x, heavy orders first; the next
-// item's [b][d_k][x_1] block lands by cp.async in the second buffer while
-// this one is computed, and 896 threads split each (d_k, x_1) column's b
-// values (even / odd) so two FMA chains run per column.
+// (x_1, d_k) walks b; same terms in the same order as k_c_bin_level.
+// Persistent: one CTA per SM walks the (order a, tau, line) items with a
+// stride of gridDim.x, heavy orders first; the next item's [b][d_k][x_1]
+// block lands by cp.async in the second buffer while this one is computed,
+// and 896 threads split each (d_k, x_1) column's b values (even / odd) so
+// two FMA chains run per column.  Items cover the weekdays
+// [tau0, tau0 + n_tau) only (a weekday shard's rows).
 // RC > 0: the radix r = A_max + 1 as a compile-time constant (21 for every
 // C preset), so the staging and tile index arithmetic divides by constants.
 template <int RC>
@@ -2772,7 +2734,8 @@ __global__ void __launch_bounds__(896, 1) k_c_bin_tile_p(const double* __restric
                                                          const double* __restrict__ binom_k,
                                                          std::size_t binom_a_stride, int r_in, int m,
                                                          int k, std::uint32_t wb, int endo,
-                                                         int in_is_g, int n_prof, int n_lines) {
+                                                         int in_is_g, int n_prof, int n_lines, int tau0,
+                                                         int n_tau) {
   const int r = RC > 0 ? RC : r_in;
   extern __shared__ double smem_t[];  // 2 x [b][d_k][x_1], then 2 x s_bin [b][y]
   const int plane = r * r, cube = r * plane;
@@ -2780,7 +2743,7 @@ __global__ void __launch_bounds__(896, 1) k_c_bin_tile_p(const double* __restric
   double* bins = smem_t + 2 * cube;
   const int cap = r - 1;
   const int n_a = endo ? r : 1;
-  const int n_items = n_a * 7 * n_lines;
+  const int n_items = n_a * n_tau * n_lines;
   struct Item {
     int a, nb, tau;
     std::uint32_t rest0, wk;
@@ -2788,10 +2751,10 @@ __global__ void __launch_bounds__(896, 1) k_c_bin_tile_p(const double* __restric
   };
   auto item = [&](int i) {
     Item it;
-    const int ai = i / (7 * n_lines), rem = i % (7 * n_lines);
+    const int ai = i / (n_tau * n_lines), rem = i % (n_tau * n_lines);
     it.a = endo ? r - 1 - ai : 0;  // heavy orders first
     it.nb = endo ? it.a + 1 : r;
-    it.tau = rem / n_lines;
+    it.tau = tau0 + rem / n_lines;
     std::uint32_t o = static_cast<std::uint32_t>(rem % n_lines), w = 1;
     it.rest0 = 0;
     it.wk = 1;
@@ -2897,7 +2860,7 @@ __global__ void __launch_bounds__(256) k_c_bin_qf(DevModel dm, const double* __r
                                                   std::uint64_t hi, std::uint64_t out_off,
                                                   int n_prof, std::uint32_t wb, int endo,
                                                   int in_is_g, std::uint64_t n_groups,
-                                                  FinalizeArgs fa) {
+                                                  std::uint64_t grp0, FinalizeArgs fa) {
   extern __shared__ double sm[];
   const int na = static_cast<int>(dm.n_actions), dn = dm.c_dmax + 1;
   const int r = RC > 0 ? RC : dm.c_max_order + 1, cap = r - 1, m = dm.c_m;
@@ -2914,7 +2877,7 @@ __global__ void __launch_bounds__(256) k_c_bin_qf(DevModel dm, const double* __r
     s_pd[threadIdx.x] = pd;
   }
   const int g = threadIdx.x / r, x1 = threadIdx.x % r;
-  const std::uint64_t grp = static_cast<std::uint64_t>(blockIdx.x) * CQ_GROUPS + g;
+  const std::uint64_t grp = grp0 + static_cast<std::uint64_t>(blockIdx.x) * CQ_GROUPS + g;
   const bool live = g < CQ_GROUPS && grp < n_groups;
   const std::uint64_t s = grp * r + x1;
   const int tau = live ? static_cast<int>(s / wb) : 0;
@@ -2922,7 +2885,7 @@ __global__ void __launch_bounds__(256) k_c_bin_qf(DevModel dm, const double* __r
   T best = T(0);
   std::uint32_t besta = 0;
   double* tile = s_tile + (g < CQ_GROUPS ? g : 0) * r * r;
-  const std::uint64_t grp_lo = static_cast<std::uint64_t>(blockIdx.x) * CQ_GROUPS;
+  const std::uint64_t grp_lo = grp0 + static_cast<std::uint64_t>(blockIdx.x) * CQ_GROUPS;
   for (int a = 0; a < na; ++a) {
     // stage the tiles: exogenous once (a == 0, all b); endogenous per order
     if (a == 0 || (endo && !in_is_g)) {
@@ -2973,7 +2936,7 @@ __global__ void __launch_bounds__(256) k_c_bin_qf(DevModel dm, const double* __r
     if (act) act[s - out_off] = besta;
     state_stat<T>(fa, s, best, V, smx, smn, bad);
   }
-  reduce_stats(smx, smn, bad, fa.stats);
+  reduce_stats(smx, smn, bad, fa);
 }
 
 // Pass k = 1 fused with the Q output: thread = (state, order).
@@ -3115,7 +3078,7 @@ __global__ void __launch_bounds__(256) k_sweep_tab(DevModel dm, const T* __restr
     if (act) act[s - out_off] = besta;
     state_stat<T>(fa, s, best, V, smax, smin, bad);
   }
-  reduce_stats(smax, smin, bad, fa.stats);
+  reduce_stats(smax, smin, bad, fa);
 }
 
 // ---------------------------------------------------------------------------
@@ -3151,7 +3114,7 @@ __global__ void __launch_bounds__(256) k_finalize(const T* __restrict__ part_v,
     if (act) act[s - out_off] = arg;
     state_stat<T>(fa, s, best, V, smax, smin, bad);
   }
-  reduce_stats(smax, smin, bad, fa.stats);
+  reduce_stats(smax, smin, bad, fa);
 }
 
 // Statistic over explicit vectors (pvi_check_convergence).
@@ -3162,7 +3125,7 @@ __global__ void __launch_bounds__(256) k_stats(const T* __restrict__ vnew, const
   double smax = -DBL_MAX, smin = DBL_MAX;
   unsigned long long bad = ~0ull;
   if (s < n) state_stat<T>(fa, s, vnew[s], vprev, smax, smin, bad);
-  reduce_stats(smax, smin, bad, fa.stats);
+  reduce_stats(smax, smin, bad, fa);
 }
 
 // ---------------------------------------------------------------------------
@@ -3437,15 +3400,6 @@ static int num_sms() {
   return n;
 }
 
-// PVI_C_TILE: 0 = k_c_bin_level, 1 = k_c_bin_tile, 2 = persistent k_c_bin_tile_p
-static int c_tile_mode() {
-  static const int mode = [] {
-    const char* e = std::getenv("PVI_C_TILE");
-    return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 2;
-  }();
-  return mode;
-}
-
 static bool a_group_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PVI_A_GROUP");
@@ -3712,6 +3666,15 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
   return true;
 }
 
+// True when the factored C sweep of this model runs launch_c_factored (whose
+// tables are weekday-local; the exact kernels gather from all of V).
+bool c_weekday_local(const Model& model) {
+  if (model.scenario != PVI_SCENARIO_C || model.algorithm != PVI_ALGO_FACTORED) return false;
+  long long n_prof = 1;
+  for (int i = 0; i < model.pc.useful_life; ++i) n_prof *= model.pc.max_order + 1;
+  return model.pc.useful_life >= 2 && model.pc.useful_life <= 6 && n_prof * 7 <= (1ll << 31);
+}
+
 // True when the factored B sweep of this model runs k_b_fact_qw3 (which
 // honours SweepArgs::xb_lo/xb_hi).  Valid after the first factored launch
 // (the law-mass check runs there).
@@ -3735,6 +3698,25 @@ std::vector<std::pair<std::uint64_t, std::uint64_t>> sweep_read_runs(const Model
   const std::uint64_t n = model.space.count;
   std::vector<std::pair<std::uint64_t, std::uint64_t>> runs;
   if (lo >= hi) return runs;
+  if (model.scenario == PVI_SCENARIO_C && model.algorithm == PVI_ALGO_FACTORED && c_weekday_local(model)) {
+    // weekday tau reads only V's slice (tau + 1) mod 7 (launch_c_factored)
+    const std::uint64_t w = n / 7;
+    const std::uint64_t t0 = lo / w, t1 = (hi - 1) / w + 1;
+    for (std::uint64_t t = t0; t < t1; ++t) {
+      const std::uint64_t nt = (t + 1) % 7;
+      runs.emplace_back(nt * w, (nt + 1) * w);
+    }
+    runs.emplace_back(lo, hi);  // own states (convergence statistic)
+    std::sort(runs.begin(), runs.end());
+    std::vector<std::pair<std::uint64_t, std::uint64_t>> out;
+    for (const auto& r : runs) {
+      if (!out.empty() && out.back().second >= r.first)
+        out.back().second = std::max(out.back().second, r.second);
+      else
+        out.push_back(r);
+    }
+    return out;
+  }
   if (!b_sweep_honours_xb_range(model, 0)) {
     runs.emplace_back(0, n);
     return runs;
@@ -3762,6 +3744,13 @@ std::vector<std::pair<std::uint64_t, std::uint64_t>> sweep_read_runs(const Model
   return out;
 }
 
+// Factored C sweep of the states [lo, hi).  Everything a state of weekday
+// tau needs is weekday-local: G[tau] reads only V's next-weekday slice
+// (tau + 1) mod 7, and every binomial pass and the Q pass of tau read only
+// rows of tau.  So the sweep computes the tables for the weekdays
+// [tau0, tau1) that [lo, hi) touches and nothing else: a weekday shard of
+// the multi-GPU driver does 1/7 of the whole-space work per weekday it owns
+// and reads one V slice it does not own (sweep_read_runs).
 template <typename T>
 bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
                        Scratch& scratch, cudaStream_t stream) {
@@ -3772,11 +3761,13 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
   if (n_prof * 7 > (1ll << 31)) return false;
   const std::uint64_t lo = a.lo, hi = a.hi, nr = hi - lo;
   const int na = static_cast<int>(dm.n_actions);
+  const std::uint32_t wb = static_cast<std::uint32_t>(n_prof / r);  // r^(M-1) = states per weekday
+  const int tau0 = static_cast<int>(lo / wb), tau1 = static_cast<int>((hi - 1) / wb) + 1;
+  const int n_tau = tau1 - tau0;
   double* G = scratch.get<double>(5, static_cast<std::size_t>(n_prof) * 7, stream);
   T* pv = a.want_values ? scratch.get<T>(0, static_cast<std::size_t>(na) * nr, stream) : nullptr;
   const bool bin = dm.c_binom != nullptr && c_bin_enabled();
   const bool endo = bin && !dm.c_exogenous;
-  const std::uint32_t wb = static_cast<std::uint32_t>(n_prof / r);  // r^(M-1)
   // pass tables: exo 7*n_prof each; endo sum_a 7 (a+1) wb each
   const std::size_t tab = endo ? c_tri_base(r, wb) : static_cast<std::size_t>(n_prof) * 7;
   double* Hb[2] = {nullptr, nullptr};
@@ -3788,12 +3779,13 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
   int launches = 0;
   {
     MainKernelScope prof(stream);
+    const dim3 ggrid(grid_for(n_prof, 256), static_cast<unsigned>(n_tau));
 #define PVI_CF(MM)                                                                               \
   if (!done && M == MM) {                                                                        \
     if (dm.c_max_order == 20 && dm.c_dmax == 20)                                                  \
-      k_c_fact_g<T, MM, 21><<<dim3(grid_for(n_prof, 256), 7), 256, 0, stream>>>(dm, a.v, G, static_cast<int>(n_prof), a.gamma); \
+      k_c_fact_g<T, MM, 21><<<ggrid, 256, 0, stream>>>(dm, a.v, G, static_cast<int>(n_prof), a.gamma, tau0); \
     else                                                                                           \
-      k_c_fact_g<T, MM><<<dim3(grid_for(n_prof, 256), 7), 256, 0, stream>>>(dm, a.v, G, static_cast<int>(n_prof), a.gamma); \
+      k_c_fact_g<T, MM><<<ggrid, 256, 0, stream>>>(dm, a.v, G, static_cast<int>(n_prof), a.gamma, tau0); \
     if (!bin)                                                                                    \
       k_c_fact_q<T, MM><<<dim3(grid_for(nr, 128), na), 128, 0, stream>>>(dm, G, pv, a.qout, lo, hi, static_cast<int>(n_prof)); \
     done = true;                                                                                 \
@@ -3811,40 +3803,34 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
       for (int k = M - 1, i = 0; k >= 2; --k, ++i) {
         wk /= static_cast<std::uint32_t>(r);
         double* dst = Hb[i & 1];
-        const unsigned blocks = grid_for(static_cast<std::uint64_t>(r) * wb, 256);
-        if (c_tile_mode() == 2 && r <= 21) {
+        if (r <= 21) {
           const int n_lines = static_cast<int>(wb / (static_cast<std::uint32_t>(r) * r));
           const std::size_t smt = 2 * (static_cast<std::size_t>(r) * r * r + static_cast<std::size_t>(r) * r) * sizeof(double);
-          const int n_items = (endo ? r : 1) * 7 * n_lines;
+          const int n_items = (endo ? r : 1) * n_tau * n_lines;
           auto kern = r == 21 ? k_c_bin_tile_p<21> : k_c_bin_tile_p<0>;
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
           kern<<<static_cast<unsigned>(std::min(n_items, num_sms())), 896, smt, stream>>>(
               src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, endo ? a_stride : 0, r, M, k, wb,
-              endo ? 1 : 0, src == G ? 1 : 0, static_cast<int>(n_prof), n_lines);
-        } else if (c_tile_mode() == 1 && r <= 21) {
-          const std::size_t smt = static_cast<std::size_t>(r) * r * r * sizeof(double);
-          cudaFuncSetAttribute(k_c_bin_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-          k_c_bin_tile<<<dim3(static_cast<unsigned>(wb / (static_cast<std::uint32_t>(r) * r)), 7, endo ? r : 1), 448,
-                         smt, stream>>>(src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k,
-                                        endo ? a_stride : 0, r, M, k, wb, endo ? 1 : 0, src == G ? 1 : 0,
-                                        static_cast<int>(n_prof));
-        } else {
-          k_c_bin_level<<<dim3(blocks, 7, endo ? r : 1), 256, smem, stream>>>(
+              endo ? 1 : 0, src == G ? 1 : 0, static_cast<int>(n_prof), n_lines, tau0, n_tau);
+        } else {  // radix > 21: the tile does not fit shared memory
+          const unsigned blocks = grid_for(static_cast<std::uint64_t>(r) * wb, 256);
+          k_c_bin_level<<<dim3(blocks, static_cast<unsigned>(n_tau), endo ? r : 1), 256, smem, stream>>>(
               src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, endo ? a_stride : 0, r, wk,
-              wb, endo ? 1 : 0, src == G ? 1 : 0, static_cast<int>(n_prof));
+              wb, endo ? 1 : 0, src == G ? 1 : 0, static_cast<int>(n_prof), tau0);
         }
         src = dst;
       }
       // k_c_bin_qf maps 256 threads onto CQ_GROUPS groups of r states: r <= 21
       if (qf_enabled() && !endo && r * CQ_GROUPS <= 256) {  // endogenous: per-order restaging loses to k_c_bin_q
         const std::uint64_t n_groups = dm.n_states / static_cast<std::uint64_t>(r);
+        const std::uint64_t g0 = lo / static_cast<std::uint64_t>(r), g1 = (hi - 1) / static_cast<std::uint64_t>(r) + 1;
         const std::size_t smq = sizeof(double) * (static_cast<std::size_t>(r) * r + 8 +
                                                   static_cast<std::size_t>(CQ_GROUPS) * r * r);
         auto kq = r == 21 && dm.n_states < (1ull << 32) ? k_c_bin_qf<T, 21> : k_c_bin_qf<T, 0>;
         cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        kq<<<static_cast<unsigned>((n_groups + CQ_GROUPS - 1) / CQ_GROUPS), 256, smq, stream>>>(
+        kq<<<static_cast<unsigned>((g1 - g0 + CQ_GROUPS - 1) / CQ_GROUPS), 256, smq, stream>>>(
             dm, src, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, static_cast<int>(n_prof), wb,
-            endo ? 1 : 0, src == G ? 1 : 0, n_groups, a.fa);
+            endo ? 1 : 0, src == G ? 1 : 0, n_groups, g0, a.fa);
         qf_done = true;
       } else {
         k_c_bin_q<T><<<dim3(grid_for(nr, 256), na), 256, 0, stream>>>(

@@ -24,6 +24,7 @@ struct FinalizeArgs {
   // next sweep reads it (its x_3 rows, or its constants' rows x_2 = 0 with
   // x_3 <= its x3_hi).  peer_v: IPC-mapped |S|-entry buffers of the peers.
   int n_peers = 0;
+  int peer_all = 0;              // 1: every V' entry to every peer (full replicas; state_stat)
   void* peer_v[8] = {};
   int peer_x3_lo[8] = {}, peer_x3_hi[8] = {};
 };
@@ -104,6 +105,7 @@ template <typename T>
 void launch_stats(const T* vnew, const T* vprev, std::uint64_t n, const FinalizeArgs& fa,
                   cudaStream_t stream);
 bool b_sweep_honours_xb_range(const Model& model, int device);
+bool c_weekday_local(const Model& model);
 std::vector<std::pair<std::uint64_t, std::uint64_t>> sweep_read_runs(const Model& model, std::uint64_t lo,
                                                                      std::uint64_t hi);
 void profile_enable(bool on);

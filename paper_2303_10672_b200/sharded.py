@@ -145,8 +145,10 @@ class ShardedValueIteration:
         self._setup_read_sets()
         self.peer = None
         self.peer_error = None
-        if (exchange == "peer" and self.world > 1 and self.plan is not None and sweep is None
-                and self.device.type == "cuda"):
+        # fused peer stores: factored B sends each entry to the peers that read
+        # it; every other sweep (value / change span) broadcasts its slice
+        if (exchange == "peer" and self.world > 1 and sweep is None and self.device.type == "cuda"
+                and self.test != P.PERIODIC_SPAN):
             self._setup_peers()
 
     # -- fused peer exchange ---------------------------------------------------
@@ -388,7 +390,16 @@ class ShardedValueIteration:
             iteration = 0
         ring[0].copy_(torch.as_tensor(v0, dtype=torch.float64).to(self.dtype))
         order = [0]
-        stats = torch.empty(4, dtype=torch.float64, device=self.device)
+        # Statistics of sweep i are read on the host one sweep late: sweep i+1
+        # is already enqueued when the host waits for sweep i's (reduced)
+        # statistics, so the device never idles on the host decision.  When
+        # sweep i converged (or diverged), sweep i+1 was speculative: its
+        # vector is dropped and V_i (another ring slot) is the result, so the
+        # iteration count and values are exactly the eager loop's.
+        pinned = self.device.type == "cuda"
+        dstats = [torch.empty(4, dtype=torch.float64, device=self.device) for _ in range(2)]
+        hstats = [torch.empty(4, dtype=torch.float64, pin_memory=pinned) for _ in range(2)]
+        pending = None  # (iteration, want, event, host stats, order after the sweep)
         sweep_s = 0.0
         converged = False
         start = iteration
@@ -396,48 +407,70 @@ class ShardedValueIteration:
         fp = self.model.fingerprint()
         if ckpt and resume is None and self.rank == 0:
             P.save_checkpoint(cfg.checkpoint_path, ring[0].double().cpu().numpy(), iteration, fp)
+        result_order = None
+        ts = time.perf_counter()
         while True:
-            if cfg.fixed_iterations > 0:
-                if iteration >= cfg.fixed_iterations:
+            stop = (iteration >= cfg.fixed_iterations if cfg.fixed_iterations > 0
+                    else iteration >= start + cfg.max_iterations)
+            launched = None
+            if not stop:
+                it = iteration + 1
+                prev = order[-1]
+                if len(order) < self.hist_cap:
+                    nxt = len(order)
+                else:
+                    nxt = order.pop(0)
+                want = cfg.fixed_iterations == 0 and len(order) + 1 >= self.hist_cap
+                hist = [ring[k] for k in order] if (want and self.test == P.PERIODIC_SPAN) else []
+                st = dstats[it & 1]
+                if self._peer_slot(ring[nxt]) is not None and self.test != P.PERIODIC_SPAN:
+                    self._peer_sweep(ring[prev], ring[nxt], self._peer_slot(ring[nxt]),
+                                     self.test if want else None, st)
+                else:
+                    self._sweep(ring[prev], ring[nxt], None, self.test if want else None, hist, st)
+                    self.reduce_stats(st)
+                    self.refresh(ring[nxt])
+                order.append(nxt)
+                hs = hstats[it & 1]
+                hs.copy_(st, non_blocking=pinned)
+                ev = None
+                if pinned:
+                    ev = torch.cuda.Event()
+                    ev.record()
+                launched = (it, want, ev, hs, list(order))
+                iteration = it
+            if pending is not None:
+                p_it, p_want, p_ev, p_hs, p_order = pending
+                if p_ev is not None:
+                    p_ev.synchronize()
+                stv = p_hs.numpy()
+                if stv[2] > NEG_INF:
+                    bad = int(-stv[2])
+                    raise P.NumericDivergence(f"non-finite value for state {bad} at iteration "
+                                              f"{p_it}", p_it)
+                done = False
+                if p_want:
+                    hi = stv[0]
+                    lo = 0.0 if self.test == P.VALUE_SPAN else -stv[1]
+                    done = bool(evaluate_test(self.test, float(hi), float(lo), cfg.epsilon, p_it))
+                if ckpt and p_it % cfg.checkpoint_every == 0:
+                    if self.plan is not None:
+                        self.exchange(ring[p_order[-1]])  # a checkpoint holds all of V
+                    if self.rank == 0:
+                        P.save_checkpoint(cfg.checkpoint_path, ring[p_order[-1]].double().cpu().numpy(),
+                                          p_it, fp)
+                if done:
                     converged = True
+                    iteration = p_it
+                    result_order = p_order
                     break
-            elif iteration >= start + cfg.max_iterations:
+            if launched is None:  # the iteration limit: the last launched sweep is the result
+                converged = cfg.fixed_iterations > 0
+                result_order = pending[4] if pending is not None else order
                 break
-            iteration += 1
-            prev = order[-1]
-            if len(order) < self.hist_cap:
-                nxt = len(order)
-            else:
-                nxt = order.pop(0)
-            want = cfg.fixed_iterations == 0 and len(order) + 1 >= self.hist_cap
-            hist = [ring[k] for k in order] if (want and self.test == P.PERIODIC_SPAN) else []
-            ts = time.perf_counter()
-            if self._peer_slot(ring[nxt]) is not None and self.test != P.PERIODIC_SPAN:
-                self._peer_sweep(ring[prev], ring[nxt], self._peer_slot(ring[nxt]),
-                                 self.test if want else None, stats)
-            else:
-                self._sweep(ring[prev], ring[nxt], None, self.test if want else None, hist, stats)
-                self.reduce_stats(stats)
-                self.refresh(ring[nxt])
-            st = stats.cpu().numpy()  # the one host round trip per sweep
-            sweep_s += time.perf_counter() - ts
-            order.append(nxt)
-            if st[2] > NEG_INF:
-                bad = int(-st[2])
-                raise P.NumericDivergence(f"non-finite value for state {bad} at iteration "
-                                          f"{iteration}", iteration)
-            if want:
-                hi = st[0]
-                lo = 0.0 if self.test == P.VALUE_SPAN else -st[1]
-                converged = bool(evaluate_test(self.test, float(hi), float(lo), cfg.epsilon, iteration))
-            if ckpt and iteration % cfg.checkpoint_every == 0:
-                if self.plan is not None:
-                    self.exchange(ring[order[-1]])  # a checkpoint holds all of V
-                if self.rank == 0:
-                    P.save_checkpoint(cfg.checkpoint_path, ring[order[-1]].double().cpu().numpy(),
-                                      iteration, fp)
-            if converged:
-                break
+            pending = launched
+        sweep_s += time.perf_counter() - ts
+        order = result_order
         vfinal = ring[order[-1]]
         actions = torch.zeros(n, dtype=torch.int32, device=self.device)
         self._sweep(vfinal, ring[order[0]] if len(order) > 1 else torch.empty_like(vfinal),

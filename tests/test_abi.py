@@ -238,7 +238,10 @@ def test_partition_is_cost_weighted_and_tile_aligned():
     import sys
     sys.argv = ["x"]
     import bench
-    costs = [bench.state_terms(m, b[i], b[i + 1]) for i in range(8)]
+    work = bench.work_from_model(m)
+    assert work.terms == m.terms_per_sweep()
+    assert abs(work.range_terms(0, m.state_count()) - work.terms) <= 1e-9 * work.terms
+    costs = [work.range_terms(b[i], b[i + 1]) for i in range(8)]
     assert max(costs) / (sum(costs) / 8) < 1.01  # equal-count sharding gives 1.30
 
 
@@ -259,3 +262,42 @@ def test_sweep_read_runs_host_logic(pvi):
         want = (16 * (32 + 2 * r) + 256 * 2 - 2 * (32 + 2 * r)) * slab
         assert cover == want, (r, cover, want)
     assert pvi.make_preset("b/m3/exp1").sweep_read_runs(0, 5) == [(0, n)]
+
+
+def test_factored_c_weekday_shards_host_logic(pvi):
+    """Factored C: shards are whole weekdays and a weekday shard reads only
+    V's next-weekday slices plus its own states (launch_c_factored)."""
+    for preset in ["c/m5/exp1", "c/m3/exp2"]:
+        m = pvi.make_preset(preset).set_algorithm("factored")
+        n = m.state_count()
+        w = n // 7
+        for parts, sizes in [(2, [4, 3]), (3, [3, 2, 2]), (4, [2, 2, 2, 1]), (7, [1] * 7), (8, [1] * 7 + [0])]:
+            b = [int(x) for x in m.partition(parts)]
+            assert [(b[i + 1] - b[i]) // w for i in range(parts)] == sizes and b[-1] == n
+        for t in range(7):
+            nt = (t + 1) % 7
+            runs = m.sweep_read_runs(t * w, (t + 1) * w)
+            want = sorted([(t * w, (t + 1) * w), (nt * w, (nt + 1) * w)])
+            if want[0][1] == want[1][0]:
+                want = [(want[0][0], want[1][1])]
+            assert runs == want, (preset, t, runs)
+        # the exact kernels gather from anywhere
+        assert pvi.make_preset(preset).sweep_read_runs(0, w) == [(0, n)]
+
+
+def test_reference_arm_work_model_matches_product():
+    """bench.py's reference arm derives the term counts from oracle/_ref alone
+    (it must not load this package): same closed forms as the product's."""
+    import sys
+    sys.argv = ["x"]
+    import bench
+    from oracle import refbind
+    if not refbind.available():
+        pytest.skip("oracle/_ref not built")
+    for preset in ["b/m3/exp1", "b/m2/exp1", "c/m5/exp1", "a/m5/exp5", "b/m3/exp4"]:
+        a = bench.work_from_reference(preset)
+        b = bench.work_from_model(P.make_preset(preset))
+        assert (a.states, a.actions) == (b.states, b.actions)
+        assert abs(a.terms - b.terms) <= 1e-9 * b.terms, preset
+        lo, hi = b.states // 3, b.states // 3 + 4096
+        assert a.range_terms(lo, hi) == b.range_terms(lo, hi)

@@ -61,11 +61,50 @@ def test_peer_stores_in_process(pvi):
     assert torch.equal(vnext2[lo:hi], vnext[lo:hi]) and torch.equal(stats2, stats)
 
 
-def test_peer_sweep_refuses_other_sweeps(pvi):
-    m = pvi.make_preset("b/m3/exp4")  # exact: reads all of V
+@pytest.mark.parametrize("preset,algo,test", [("b/m3/exp4", "exact", "change_span"),
+                                               ("a/m5/exp5", "factored", "value_span"),
+                                               ("c/m5/exp1", "factored", "change_span"),
+                                               ("a/m3/exp6", "exact", "value_span")])
+def test_peer_broadcast_for_whole_v_sweeps(pvi, preset, algo, test):
+    """Every sweep but factored B's gathers from all of V: its finalize
+    broadcasts each V' entry of [lo, hi) into every peer replica (and
+    nothing else), with the same values and statistics as without peers."""
+    m = pvi.make_preset(preset).set_algorithm(algo)
+    n = m.state_count()
+    b = [int(x) for x in m.partition(4)]
+    V = np.random.default_rng(12).uniform(-20.0, 20.0, n)
+    vprev = torch.as_tensor(V, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    r = 1
+    lo, hi = b[r], b[r + 1]
+    peers = {q: pvi.DeviceBuffer(n) for q in (0, 2, 3)}
+    tens = {q: torch.as_tensor(buf, device="cuda") for q, buf in peers.items()}
+    for t in tens.values():
+        t.fill_(float("nan"))
+    vnext = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+    stats = torch.empty(4, dtype=torch.float64, device="cuda")
+    pvi.sweep_device_peers(m, "f64", m.discount(), vprev.data_ptr(), vnext.data_ptr(), lo, hi,
+                           [(peers[q].ptr, b[q], b[q + 1]) for q in peers], test=test,
+                           stats_ptr=stats.data_ptr(), stream_ptr=st)
+    vnext2 = torch.full_like(vnext, float("nan"))
+    stats2 = torch.empty_like(stats)
+    pvi.sweep_device(m, "f64", m.discount(), vprev.data_ptr(), vnext2.data_ptr(), None, lo, hi, test, (),
+                     stats2.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert torch.equal(vnext[lo:hi], vnext2[lo:hi]) and torch.equal(stats, stats2)
+    want = vnext2[lo:hi].cpu().numpy()
+    for q, t in tens.items():
+        got = t.cpu().numpy()
+        np.testing.assert_array_equal(got[lo:hi], want)
+        assert np.isnan(got[:lo]).all() and np.isnan(got[hi:]).all()
+
+
+def test_peer_sweep_refuses_periodic_span(pvi):
+    m = pvi.make_preset("c/m3/exp1")
     v = torch.zeros(m.state_count(), dtype=torch.float64, device="cuda")
     with pytest.raises(pvi.ParameterError):
-        pvi.sweep_device_peers(m, "f64", m.discount(), v.data_ptr(), v.data_ptr(), 0, 10, [])
+        pvi.sweep_device_peers(m, "f64", m.discount(), v.data_ptr(), v.data_ptr(), 0, 10, [],
+                               test="periodic_span")
 
 
 def _free_port():
@@ -139,43 +178,56 @@ def test_peer_stores_across_processes_ipc():
         assert ok_own and ok_peer and untouched, (rank, ok_own, ok_peer, untouched)
 
 
-def _solve_worker(rank, world, port, q):
+def _solve_worker(rank, world, port, preset, algo, exchange, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
         import paper_2303_10672_b200 as pvi
         from paper_2303_10672_b200.sharded import ShardedValueIteration
-        m = pvi.make_preset("b/m3/exp1").set_algorithm("factored")
-        solver = ShardedValueIteration(m, pvi.ViConfig(), exchange="peer")
-        assert solver.buffers() is not None
+        m = pvi.make_preset(preset).set_algorithm(algo)
+        solver = ShardedValueIteration(m, pvi.ViConfig(), exchange=exchange)
+        if exchange == "peer":
+            assert solver.buffers() is not None
         res = solver.solve()
         solver.close()
         if rank == 0:
-            q.put((res.iterations, res.converged, res.values, res.policy))
+            q.put((res.iterations, res.converged, res.values, res.policy, solver.read_set_bytes()))
     finally:
         dist.destroy_process_group()
 
 
-def test_sharded_solve_with_fused_peer_exchange(pvi):
-    """The whole sharded solve with the exchange fused into the sweep (two
-    ranks on one GPU, IPC-mapped replicas, gloo for the statistics): the
-    same iterations, values and policy as the single-process solve."""
-    world = 2
+@pytest.mark.parametrize("preset,algo,exchange,world", [("b/m3/exp1", "factored", "peer", 2),
+                                                        ("a/m2/exp1", "factored", "peer", 2),
+                                                        ("b/m2/exp1", "exact", "peer", 3),
+                                                        ("c/m5/exp2", "factored", "runs", 2),
+                                                        ("c/m3/exp1", "factored", "runs", 3)])
+def test_sharded_solve_multi_process(pvi, preset, algo, exchange, world):
+    """The whole sharded solve, ranks as processes on this one GPU (gloo for
+    the statistics; no kernel waits on another rank): the fused peer stores
+    (factored B: to the readers; other sweeps: broadcast into full replicas)
+    and the weekday shards of factored C (read set: one next-weekday slice,
+    all-to-all) give the same iterations, values and policy as the
+    single-process solve.  The host reads each sweep's statistics one sweep
+    late (speculative next sweep), which must not change the result."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_solve_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_solve_worker, args=(r, world, port, preset, algo, exchange, q))
+             for r in range(world)]
     for p in procs:
         p.start()
-    it, conv, values, policy = q.get(timeout=900)
+    it, conv, values, policy, rbytes = q.get(timeout=900)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    want = pvi.run_value_iteration(pvi.make_preset("b/m3/exp1").set_algorithm("factored"))
+    want = pvi.run_value_iteration(pvi.make_preset(preset).set_algorithm(algo))
     assert (it, conv) == (want.iterations, want.converged)
     np.testing.assert_array_equal(values, want.values)
     np.testing.assert_array_equal(policy, want.policy)
+    if preset.startswith("c/"):
+        n = len(values)
+        assert rbytes <= 8 * (n // 7) * 3  # a weekday shard refreshes ~one weekday slice
 
 
 # --- unit shards: (x_3 pair, x_b column range) blocks ------------------------
