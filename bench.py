@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--algorithm", default="factored", choices=["exact", "factored"])
     ap.add_argument("--no-alt", action="store_true", help="skip timing the other algorithm")
     ap.add_argument("--no-simopt", action="store_true")
+    ap.add_argument("--no-others", action="store_true", help="skip the a/m5 and c/m5 workloads")
     ap.add_argument("--no-ckpt-solve", action="store_true",
                     help="skip the second solve with the preset's checkpoint cadence")
     ap.add_argument("--no-solve", action="store_true", help="skip the time-to-converge solve")
@@ -365,6 +366,127 @@ def compute_roofline(model, args, work, shard_terms, shard_states, kernel_ms, k_
             "hbm": hbm, "reference_term_gather": ref_terms}
 
 
+def philox_peak():
+    j = _load_json("profiles/r2_philox_peak.json")
+    if not j:
+        return None
+    return max(r["gblocks_per_s"] for r in j["results"]) * 1e9
+
+
+def simopt_section(P, world, rank, barrier):
+    """Config 5: the GA on b/m2/exp1 (4096 rollouts per candidate), the
+    exhaustive 21 x 21 grid, the optimality gap against the VI policy; with
+    the rollout kernel's Philox blocks/s against the measured Philox peak."""
+    import torch
+    import torch.distributed as dist
+    from paper_2303_10672_b200.sharded_sim import ShardedEvaluator
+    mb = P.make_preset("b/m2/exp1")
+    ev = ShardedEvaluator(mb)
+    ev.simopt(rollouts_per_candidate=256, base_seed=42, seed=1, max_generations=2)  # warm-up
+    ev.device_seconds = 0.0
+    barrier()
+    P.profile_enable(True)
+    P.profile_sim_read()
+    t0 = time.perf_counter()
+    so = ev.simopt(rollouts_per_candidate=4096, base_seed=42, seed=1)
+    wall = time.perf_counter() - t0
+    blocks, days, kms = P.profile_sim_read()
+    P.profile_enable(False)
+    t = torch.tensor([wall, ev.device_seconds], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    wall_max, dev_max = float(t[0]), float(t[1])
+    all_days = len(so.log) * 4096 * 465
+    out = {"preset": "b/m2/exp1", "sampler": "ga", "best": so.best, "best_mean": so.best_mean,
+           "generations": so.generations, "candidates": len(so.log), "n_gpus": world,
+           "sharding": "candidates of each generation over the ranks" if world > 1 else "one device",
+           "wall_seconds": wall_max, "device_seconds": dev_max,
+           "rollout_days_per_s": all_days / max(dev_max, 1e-9)}
+    peak = philox_peak()
+    if kms > 0:
+        out["k5_roofline"] = {
+            "bound": "int (Philox4x32-10)", "philox_blocks_per_rollout_day": blocks / max(days, 1),
+            "achieved_blocks_per_s": blocks / (kms * 1e-3), "kernel_ms": kms,
+            "rollout_days_per_s_kernel": days / (kms * 1e-3),
+            "peak_blocks_per_s": peak, "frac": (blocks / (kms * 1e-3) / peak) if peak else None,
+            "peak_source": "profiles/r2_philox_peak.json (tools/philox_peak.cu on a B200)" if peak else None,
+            "note": "rank-local counts: this rank's rollout kernels only"}
+    if world == 1:
+        ex = P.simopt(mb, sampler="exhaustive", rollouts_per_candidate=4096, base_seed=42)
+        vi = P.run_value_iteration(mb, P.ViConfig())
+        evs, _ = P.evaluate_policies(mb, [P.make_vi_policy(mb, vi.policy),
+                                          P.make_heuristic_policy(mb, so.best),
+                                          P.make_heuristic_policy(mb, ex.best)],
+                                     P.RolloutConfig(n_rollouts=10_000, base_seed=42))
+        vi_mean = evs[0].ret.mean
+        out["exhaustive"] = {
+            "candidates": len(ex.log), "best": ex.best, "best_mean": ex.best_mean,
+            "device_seconds": ex.device_seconds,
+            "rollout_days_per_s": len(ex.log) * 4096 * 465 / max(ex.device_seconds, 1e-9)}
+        out["optimality_gap_pct"] = {
+            "vi_policy_mean": vi_mean, "rollouts": 10_000,
+            "ga_best": 100.0 * (vi_mean - evs[1].ret.mean) / abs(vi_mean),
+            "exhaustive_best": 100.0 * (vi_mean - evs[2].ret.mean) / abs(vi_mean)}
+    return out
+
+
+OTHERS = ["a/m5/exp5", "c/m5/exp1", "c/m5/exp2"]
+
+
+def other_workloads(P, args, barrier):
+    """The other BASELINE configs: one factored f64 sweep (device events, L2
+    flushed between steps), the solve to the reference's criterion, and the
+    reference CPU solver on the host's cores (bounded sample) for each."""
+    import torch
+    out = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for preset in OTHERS:
+        m = P.make_preset(preset).set_algorithm("factored")
+        n = m.state_count()
+        v = torch.as_tensor(np.random.default_rng(7).uniform(-5.0, 5.0, n), device="cuda")
+        vn = torch.empty_like(v)
+        stats = torch.empty(4, dtype=torch.float64, device="cuda")
+        test = m.default_convergence_test()
+        hist = [v.clone() for _ in range(6)] + [v] if test == P.PERIODIC_SPAN else []
+        names = {0: "value_span", 1: "change_span", 2: "periodic_span"}
+        st = torch.cuda.current_stream().cuda_stream
+
+        def sweep():
+            P.sweep_device(m, "f64", m.discount(), v.data_ptr(), vn.data_ptr(), None, 0, n, names[test],
+                           [h.data_ptr() for h in hist], stats.data_ptr(), st)
+        for _ in range(3):
+            sweep()
+        barrier()
+        ms = []
+        for _ in range(5):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            sweep()
+            e1.record()
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        sweep_ms = statistics.median(ms)
+        terms = m.terms_per_sweep()
+        res = min((P.run_value_iteration(m) for _ in range(2)), key=lambda r: r.wall_seconds)
+        entry = {"states": n, "terms_per_sweep": terms, "algorithm": "factored", "sweep_ms": sweep_ms,
+                 "evals_per_s": terms / (sweep_ms * 1e-3), "solve_iterations": res.iterations,
+                 "solve_wall_seconds": res.wall_seconds, "data": "V ~ U(-5, 5) seed 7 for the sweep"}
+        if not args.no_cpu_baseline:
+            from oracle import refbind as R
+            if R.available():
+                work = work_from_reference(preset)
+                V = np.random.default_rng(7).uniform(-5.0, 5.0, n)
+                rate, secs, sterms, desc, threads = run_cpu_reference(work, preset, "f64", 4.0, V)
+                entry["cpu_baseline"] = {"value": rate, "unit": "evals/s", "cores": threads,
+                                         "kind": "reference", "sample": desc, "seconds": secs,
+                                         "extrapolated_solve_seconds": (res.iterations + 1) * terms / rate}
+                entry["speedup_sweep"] = entry["evals_per_s"] / rate
+                entry["speedup_solve"] = entry["cpu_baseline"]["extrapolated_solve_seconds"] / res.wall_seconds
+        out[preset] = entry
+    return out
+
+
 def ours_arm(args, world, rank, local):
     import torch
     import torch.distributed as dist
@@ -528,35 +650,17 @@ def ours_arm(args, world, rank, local):
                     "writer": "async PVI1 (pinned double buffer + writer thread)"}
 
     # simulation optimisation (config 5): the reference GA on b/m2/exp1 with
-    # 4096 rollouts per candidate, every generation scored in one device batch
-    if rank == 0 and world == 1 and not args.no_simopt:
-        so = P.simopt(P.make_preset("b/m2/exp1"), rollouts_per_candidate=4096, base_seed=42,
-                      seed=1)
-        days = len(so.log) * 4096 * 465
-        line["simopt"] = {"preset": "b/m2/exp1", "sampler": "ga", "best": so.best,
-                          "best_mean": so.best_mean, "generations": so.generations,
-                          "candidates": len(so.log), "wall_seconds": so.wall_seconds,
-                          "device_seconds": so.device_seconds,
-                          "rollout_days_per_s": days / max(so.device_seconds, 1e-9)}
-        # the whole 21 x 21 grid in one batch (GPU-only extra mode) and the
-        # optimality gap of the GA's best against the VI policy, both scored
-        # over 10,000 rollouts on common random numbers (runner cmd_evaluate)
-        mb = P.make_preset("b/m2/exp1")
-        ex = P.simopt(mb, sampler="exhaustive", rollouts_per_candidate=4096, base_seed=42)
-        vi = P.run_value_iteration(mb, P.ViConfig())
-        evs, _ = P.evaluate_policies(mb, [P.make_vi_policy(mb, vi.policy),
-                                          P.make_heuristic_policy(mb, so.best),
-                                          P.make_heuristic_policy(mb, ex.best)],
-                                     P.RolloutConfig(n_rollouts=10_000, base_seed=42))
-        vi_mean = evs[0].ret.mean
-        line["simopt"]["exhaustive"] = {
-            "candidates": len(ex.log), "best": ex.best, "best_mean": ex.best_mean,
-            "device_seconds": ex.device_seconds,
-            "rollout_days_per_s": len(ex.log) * 4096 * 465 / max(ex.device_seconds, 1e-9)}
-        line["simopt"]["optimality_gap_pct"] = {
-            "vi_policy_mean": vi_mean, "rollouts": 10_000,
-            "ga_best": 100.0 * (vi_mean - evs[1].ret.mean) / abs(vi_mean),
-            "exhaustive_best": 100.0 * (vi_mean - evs[2].ret.mean) / abs(vi_mean)}
+    # 4096 rollouts per candidate, every generation scored in one device
+    # batch; at N > 1 every generation's candidates are sharded over the ranks
+    # (sharded_sim.ShardedEvaluator), timed as the max over ranks
+    if not args.no_simopt:
+        line_so = simopt_section(P, world, rank, barrier)
+        if rank == 0:
+            line["simopt"] = line_so
+
+    # the other BASELINE configs, each against its own CPU baseline
+    if rank == 0 and world == 1 and not args.no_others:
+        line["other_workloads"] = other_workloads(P, args, barrier)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import refbind as R
@@ -574,6 +678,8 @@ def ours_arm(args, world, rank, local):
                 r = R.simopt("b/m2/exp1", rollouts=4096, eval_seed=42, ga_seed=1,
                              threads=threads)
                 line["cpu_baseline"]["simopt_b_m2_exp1_seconds"] = r["wall"]
+                line["simopt"]["cpu_wall_seconds"] = r["wall"]
+                line["simopt"]["speedup_vs_cpu"] = r["wall"] / max(line["simopt"]["wall_seconds"], 1e-9)
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

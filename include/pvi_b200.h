@@ -451,6 +451,12 @@ int pvi_rollout_draws(uint64_t base_seed, uint64_t rollout, uint32_t day, int n,
  * resets them (it synchronises on the recorded events). */
 int pvi_profile_enable(int on);
 int pvi_profile_read(double* kernel_ms, uint64_t* kernel_launches, uint64_t* all_launches);
+/* Simulation side of the hook: while enabled, every pvi_sim_evaluate counts
+ * the Philox4x32-10 blocks its rollouts draw (one per uniform, rng.hpp:37-60)
+ * and times its rollout kernel with CUDA events.  Returns the sums since the
+ * last read (rollout_days = policies x rollouts x (warm-up + horizon)) and
+ * resets them. */
+int pvi_profile_sim_read(uint64_t* philox_blocks, uint64_t* rollout_days, double* kernel_ms);
 
 /* ---- policy CSV (runner.cpp:90-166, io.cpp:53-92) -----------------------
  * Formatting and parsing run on the device, one thread per row.

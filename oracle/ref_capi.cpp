@@ -485,6 +485,21 @@ int ref_cmd(const char* preset, int which, const char* out_dir, int threads, int
   });
 }
 
+// cmd_solve with vi.fixed_iterations overridden and optionally resuming from
+// the directory's checkpoint (acceptance_main.cpp:303-325 flow).
+int ref_cmd_solve_fixed(const char* preset, const char* out_dir, int threads, std::uint64_t fixed_iterations,
+                        int resume, char* err, std::size_t errlen) {
+  return guarded(err, errlen, [&] {
+    ExperimentConfig cfg = make_preset(preset);
+    cfg.vi.fixed_iterations = fixed_iterations;
+    RunnerOptions opt;
+    opt.output_dir = out_dir;
+    opt.threads = threads;
+    opt.resume = resume != 0;
+    (void)cmd_solve(cfg, opt);
+  });
+}
+
 // Raw Philox block (rng.hpp:15-33) and RolloutRng draws (rng.hpp:37-60).
 void ref_philox_block(const std::uint32_t* ctr, const std::uint32_t* key, std::uint32_t* out) {
   const auto o = Philox4x32::block({ctr[0], ctr[1], ctr[2], ctr[3]}, {key[0], key[1]});

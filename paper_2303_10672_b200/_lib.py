@@ -176,6 +176,7 @@ SIGNATURES = {
     "pvi_simopt_config_defaults": (None, [_vp]),
     "pvi_simopt": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp] + _E),
     "pvi_profile_enable": (C.c_int, [C.c_int]),
+    "pvi_profile_sim_read": (C.c_int, [_vp, _vp, _vp]),
     "pvi_profile_read": (C.c_int, [_vp, _vp, _vp]),
 }
 

@@ -564,6 +564,10 @@ int pvi_profile_read(double* kernel_ms, uint64_t* kernel_launches, uint64_t* all
   return guarded(nullptr, 0, nullptr, [&] { profile_read(kernel_ms, kernel_launches, all_launches); });
 }
 
+int pvi_profile_sim_read(uint64_t* philox_blocks, uint64_t* rollout_days, double* kernel_ms) {
+  return guarded(nullptr, 0, nullptr, [&] { sim_profile_read(philox_blocks, rollout_days, kernel_ms); });
+}
+
 int pvi_sha256(const void* data, size_t len, uint8_t out[32]) {
   return guarded(nullptr, 0, nullptr, [&] { sha256(data, len, out); });
 }

@@ -46,6 +46,11 @@ std::uint64_t policy_csv_format(const Model& m, const std::uint32_t* actions, ch
 // policy_from_csv after the metadata check: whole file text -> actions
 void policy_csv_parse(const Model& m, const char* text, std::uint64_t len, std::uint32_t* out);
 void profile_enable(bool on);
+bool profiling_enabled();
+// simulation measurement hook: Philox blocks, rollout-days and k_rollouts
+// milliseconds accumulated while profiling is enabled
+void sim_profile_add(std::uint64_t philox_blocks, std::uint64_t rollout_days, double kernel_ms);
+void sim_profile_read(std::uint64_t* philox_blocks, std::uint64_t* rollout_days, double* kernel_ms);
 void profile_read(double* ms, std::uint64_t* main_launches, std::uint64_t* all_launches);
 void initial_values_host(const Model& m, double* out);
 

@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(128, MINB) k_rollouts(DevModel dm, const DevPo
                                                   int n_rollouts, int horizon, int warmup,
                                                   std::uint64_t base_seed, int arity, int products,
                                                   double gamma, double* __restrict__ out,
-                                                  SimError* err) {
+                                                  SimError* err, unsigned long long* blocks_out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int p = blockIdx.y;
   if (i >= n_rollouts) return;
@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(128, MINB) k_rollouts(DevModel dm, const DevPo
   Rng rng(base_seed, static_cast<std::uint64_t>(i));
   const int total_days = warmup + horizon;
   double ret = 0.0, weight = 1.0;
+  unsigned long long blocks = 0;
   long long demand[2] = {0, 0}, filled[2] = {0, 0}, expired[2] = {0, 0}, received[2] = {0, 0},
             holding[2] = {0, 0};
   for (int day = 0; day < total_days; ++day) {
@@ -354,6 +355,7 @@ __global__ void __launch_bounds__(128, MINB) k_rollouts(DevModel dm, const DevPo
         return;
       }
     }
+    blocks += rng.draw;  // Philox blocks drawn the previous day (measurement hook)
     rng.begin_day(static_cast<std::uint32_t>(day));
     Step st;
     st.reward = 0.0;
@@ -374,6 +376,7 @@ __global__ void __launch_bounds__(128, MINB) k_rollouts(DevModel dm, const DevPo
       }
     }
   }
+  if (blocks_out) atomicAdd(blocks_out, blocks + rng.draw);
   double* o = out + (static_cast<std::size_t>(p) * n_rollouts + i) * 7;
   o[0] = ret;
   for (int k = 0; k < 2; ++k) {
@@ -530,11 +533,24 @@ void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_po
     cudaEventCreate(&t1);
     cudaEventRecord(t0, stream);
   }
+  // measurement hook (pvi_profile_enable): Philox blocks drawn, kernel time
+  const bool prof = profiling_enabled();
+  std::unique_ptr<Buf> dblocks;
+  cudaEvent_t p0 = nullptr, p1 = nullptr;
+  if (prof) {
+    dblocks = std::make_unique<Buf>(sizeof(unsigned long long), stream);
+    PVI_CUDA(cudaMemsetAsync(dblocks->p, 0, sizeof(unsigned long long), stream));
+    PVI_CUDA(cudaEventCreate(&p0));
+    PVI_CUDA(cudaEventCreate(&p1));
+    PVI_CUDA(cudaEventRecord(p0, stream));
+  }
   kr<<<grid, 128, 0, stream>>>(dm, static_cast<const DevPolicy*>(dpol.p), cfg.n_rollouts,
                                        cfg.horizon_days, cfg.warmup_days, cfg.base_seed, arity,
                                        products, m.gamma, static_cast<double*>(dsum.p),
-                                       static_cast<SimError*>(derr.p));
+                                       static_cast<SimError*>(derr.p),
+                                       prof ? static_cast<unsigned long long*>(dblocks->p) : nullptr);
   PVI_CUDA(cudaGetLastError());
+  if (prof) PVI_CUDA(cudaEventRecord(p1, stream));
   if (trace) cudaEventRecord(t1, stream);
   k_reduce_eval<<<(n_policies * 7 + 63) / 64, 64, 0, stream>>>(static_cast<const double*>(dsum.p), cfg.n_rollouts,
                                                               n_policies, static_cast<double*>(dstat.p));
@@ -544,7 +560,18 @@ void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_po
   PVI_CUDA(cudaMemcpyAsync(hstat.data(), dstat.p, hstat.size() * 8, cudaMemcpyDeviceToHost, stream));
   if (per_rollout)
     PVI_CUDA(cudaMemcpyAsync(per_rollout, dsum.p, n_sum * 7 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  unsigned long long hblocks = 0;
+  if (prof) PVI_CUDA(cudaMemcpyAsync(&hblocks, dblocks->p, sizeof(hblocks), cudaMemcpyDeviceToHost, stream));
   PVI_CUDA(cudaStreamSynchronize(stream));
+  if (prof) {
+    float ms = 0.f;
+    PVI_CUDA(cudaEventElapsedTime(&ms, p0, p1));
+    cudaEventDestroy(p0);
+    cudaEventDestroy(p1);
+    sim_profile_add(hblocks, static_cast<std::uint64_t>(n_policies) * cfg.n_rollouts *
+                                 static_cast<std::uint64_t>(cfg.horizon_days + cfg.warmup_days),
+                    ms);
+  }
   if (trace) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, t0, t1);

@@ -388,17 +388,6 @@ __global__ void __launch_bounds__(256) k_sweep_b(DevModel dm, const T* __restric
 // becomes an immediate load offset, and the per-term work is exactly one
 // L1-resident gather plus the reference's five f64 operations.  Same term
 // order and expression as k_sweep_b, hence the same bits.
-// Read-only gather that the compiler may not move or drop.
-__device__ __forceinline__ double ldg_keep(const double* p) {
-  double v;
-  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ float ldg_keep(const float* p) {
-  float v;
-  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
-  return v;
-}
 
 template <int M, int NB>
 struct BGeo {
@@ -570,100 +559,6 @@ __global__ void __launch_bounds__(256) k_a_reward(DevModel dm, double* __restric
     acc = fma(dm.a_pmf[d], r, acc);
   }
   out[s] = acc;
-}
-
-template <typename T, int NA, int ML>
-__global__ void __launch_bounds__(256) k_a_fact(DevModel dm, const T* __restrict__ V,
-                                                const double* __restrict__ reward,
-                                                const double* __restrict__ cdf_sf, double pd,
-                                                T* __restrict__ vout, std::uint32_t* __restrict__ act,
-                                                T* __restrict__ qout, std::uint64_t lo,
-                                                std::uint64_t hi, std::uint64_t out_off,
-                                                double gamma, FinalizeArgs fa) {
-  extern __shared__ double s_tab[];  // pmf | cdf | sf
-  const int dn = dm.a_dmax + 1;
-  double* s_pmf = s_tab;
-  double* s_cdf = s_pmf + dn;
-  double* s_sf = s_cdf + dn;
-  for (int i = threadIdx.x; i < dn; i += blockDim.x) {
-    s_pmf[i] = dm.a_pmf[i];
-    s_cdf[i] = cdf_sf[i];
-  }
-  for (int i = threadIdx.x; i <= dn; i += blockDim.x) s_sf[i] = cdf_sf[dn + i];
-  __syncthreads();
-  const std::uint64_t s = lo + static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  double smax = -DBL_MAX, smin = DBL_MAX;
-  unsigned long long bad = ~0ull;
-  if (s < hi) {
-    constexpr int MC = ML / 10, LC = ML % 10;
-    const int m = ML ? MC : dm.a_m, lead = ML ? LC : dm.a_lead;
-    const int na = static_cast<int>(dm.n_actions);
-    constexpr int ND = ML ? MC + LC - 1 : kMaxDigits;
-    int st[ND];
-    if (ML) {
-      const std::uint32_t r = static_cast<std::uint32_t>(dm.a_max_order + 1);
-      std::uint64_t rem = s;
-#pragma unroll
-      for (int i = ND - 1; i >= 0; --i) {
-        st[i] = static_cast<int>(rem % r);
-        rem /= r;
-      }
-    } else {
-      decode(dm, s, st);
-    }
-    int x[ML ? MC + 1 : 14], aged[ML ? MC + 1 : 14];
-    int xt = 0;
-#pragma unroll
-    for (int j = 1; j <= m; ++j) {
-      x[j] = st[lead - 1 + m - j];
-      xt += x[j];
-    }
-    std::uint64_t base_static = 0;
-#pragma unroll
-    for (int k = 1; k <= lead - 2; ++k) base_static += st[k - 1] * dm.weight[k];
-    if (lead >= 2) base_static += st[lead - 2] * dm.weight[lead - 1];
-    const std::uint64_t w0 = dm.weight[0];
-    double u[NA];
-#pragma unroll
-    for (int a = 0; a < NA; ++a) u[a] = 0.0;
-    const int carried = xt - x[1];  // x_2 + .. + x_m
-    auto add_profile = [&](int d, double w) {
-      if (dm.a_lifo) age_lifo(x, m, d, aged);
-      else age_fifo(x, m, d, aged);
-      std::uint64_t base = base_static;
-      for (int j = 1; j <= m - 1; ++j) base += aged[j] * dm.weight[lead + m - 1 - j];
-      const T* vb = V + base;
-#pragma unroll
-      for (int a = 0; a < NA; ++a)
-        if (a < na) u[a] = fma(w, static_cast<double>(__ldg(vb + a * w0)), u[a]);
-    };
-    if (dm.a_lifo) {
-      for (int d = 0; d < carried; ++d) add_profile(d, s_pmf[d]);
-      add_profile(carried, s_sf[carried]);  // every d >= x_2 + .. + x_m empties the carried stock
-    } else {
-      add_profile(x[1], s_cdf[x[1]]);  // d <= x_1: (x_2, .., x_m) unchanged
-      for (int d = x[1] + 1; d < xt; ++d) add_profile(d, s_pmf[d]);
-      add_profile(xt, s_sf[max(xt, x[1] + 1)]);  // the rest empties the stock
-    }
-    const double rs = reward[s];
-    T best = T(0);
-    std::uint32_t besta = 0;
-#pragma unroll
-    for (int a = 0; a < NA; ++a) {
-      if (a < na) {
-        const T qa = static_cast<T>(fma(gamma, u[a], fma(-dm.a_cv * a, pd, rs)));
-        if (a == 0 || qa > best) {
-          best = qa;
-          besta = a;
-        }
-        if (qout) qout[(s - lo) * na + a] = qa;
-      }
-    }
-    if (vout) vout[s - out_off] = best;
-    if (act) act[s - out_off] = besta;
-    state_stat<T>(fa, s, best, V, smax, smin, bad);
-  }
-  reduce_stats(smax, smin, bad, fa);
 }
 
 // LIFO: the carried stock's fate does not depend on the oldest bucket x_1
@@ -1084,7 +979,6 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_q(DevModel dm, const double* 
     s_cg[i] = dm.b_pz_cum[ib * dnp + i];
   }
   __syncthreads();
-  const std::uint64_t n = dm.n_states;
   const std::uint64_t nr = hi - lo;
   const double cva_oa = dm.b_cva * oa;
   for (int t = threadIdx.x; t < n_xa; t += blockDim.x) {
@@ -1277,7 +1171,7 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16(DevModel dm, const T* __r
                                                        const std::uint16_t* __restrict__ group_order,
                                                        int n_groups, int n_xb, int n_bp, int n_r,
                                                        int x3_lo, int x3_hi, int tiled, int r_base) {
-  constexpr int NB = 16, S8 = 8, OB4 = 4;
+  constexpr int NB = 16;
   extern __shared__ double slab[];  // [bp][ob]
   const int stride = slab_stride(NB);
   const int r = r_base + static_cast<int>(blockIdx.x);
@@ -1406,216 +1300,6 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16p(DevModel dm, const doubl
                s_cdf_b, rg_lo, rg_cnt);
     __syncthreads();  // the slab is refilled two rows later
     t = tn;
-  }
-}
-
-// Stage 2, register-blocked (order_b radix 16, order_a radix <= 16).
-// The 16 states of an x_a "group" (same digits x_2..x_M, x_1 = 0..15) walk
-// the SAME sequence of aged profiles: after the merged h_a <= x_1 block,
-// step j consumes the j-th unit above x_1, so ap(j) does not depend on x_1,
-// and every state reaches its stock-out step j = S = x_2+..+x_M together.
-// Only the weights differ (pmf_a(x_1 + j), pz(I_b, x_1 + j)).  A thread
-// therefore owns 8 states x 4 order_b values of one group: each W / V0 row
-// element it reads from shared memory feeds 8 FMAs (vs 1 in k_b_fact_q),
-// which lifts the shared-memory delivery limit (16 doubles/clk/SM) above the
-// FP64 pipe.  Lanes: 32 groups x (2 state halves x 4 order_b quarters).
-template <typename T, int M>
-__global__ void __launch_bounds__(256, 2) k_b_fact_q16(DevModel dm, const double* __restrict__ W,
-                                                       const double* __restrict__ v0t,
-                                                       const double* __restrict__ erpt,
-                                                       const std::uint16_t* __restrict__ group_order,
-                                                       T* __restrict__ part_v,
-                                                       std::uint8_t* __restrict__ part_a,
-                                                       T* __restrict__ qout, std::uint64_t lo,
-                                                       std::uint64_t hi, double gamma,
-                                                       int n_groups, int n_xb, int n_ap, int n_r) {
-  constexpr int NB = 16, S8 = 8, OB4 = 4;
-  extern __shared__ double sm[];
-  const int na = dm.b_na;
-  const int stride = slab_stride(NB);
-  const int rows = slab_rows(n_ap);
-  double* w_sl = sm;
-  double* v0_sl = sm + rows * stride;
-  double* s_al = v0_sl + rows * stride;  // pmf_a
-  double* s_g = s_al + dm.b_dn;           // pz(I_b, .)
-  double* s_cal = s_g + dm.b_dn;          // cdf_a
-  double* s_cg = s_cal + dm.b_dn;         // pz_cum(I_b, .)
-  double* s_sfa = s_cg + dm.b_dn;         // sf_a
-  const int xbi = blockIdx.y;  // order_a fastest: the 16 CTAs of one x_b share its L2-resident rows
-  const int oa = blockIdx.x;
-  int ib = 0;
-  {
-    int rem = xbi;
-#pragma unroll
-    for (int j = 1; j <= M; ++j) {
-      ib += rem % NB;
-      rem /= NB;
-    }
-  }
-  const double sfb = dm.b_sf_b[ib];
-  const int dnp = dm.b_dn;
-  const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
-  for (int i = threadIdx.x; i < n_ap * NB; i += blockDim.x) {
-    const int ap = i / NB, ob = i % NB;
-    w_sl[slab_row(ap) * stride + ob] = W[(static_cast<std::size_t>(xbi) * n_r + r0 + ap) * NB + ob];
-    v0_sl[slab_row(ap) * stride + ob] = sfb * v0t[(r0 + ap) * NB + ob];
-  }
-  for (int i = threadIdx.x; i < dnp; i += blockDim.x) {
-    s_al[i] = dm.b_pmf_a[i];
-    s_g[i] = dm.b_pz[ib * dnp + i];
-    s_cal[i] = dm.b_cdf_a[i];
-    s_cg[i] = dm.b_pz_cum[ib * dnp + i];
-    s_sfa[i] = dm.b_sf_a[i];
-  }
-  __syncthreads();
-  const std::uint64_t n = dm.n_states;
-  const std::uint64_t nr = hi - lo;
-  const int sub = threadIdx.x & 7;
-  const int x1b = (sub >> 2) * S8;  // first x_1 of this thread's 8 states
-  const int ob0 = (sub & 3) * OB4;   // first order_b of this thread's 4
-  const double cva_oa = dm.b_cva * oa;
-  for (int gbase = 0; gbase < n_groups; gbase += blockDim.x >> 3) {
-    // whole warps stay in the loop (the epilogue shuffles across lanes)
-    const int gi = gbase + (threadIdx.x >> 3);
-    const bool active = gi < n_groups;
-    const int grp = group_order[active ? gi : 0];
-    // group digits x_2..x_M (grp = sum_{j>=2} x_j na^(j-2))
-    int xg[M + 1];
-    int S = 0;
-    {
-      int rem = grp;
-#pragma unroll
-      for (int j = 2; j <= M; ++j) {
-        xg[j] = rem % na;
-        rem /= na;
-        S += xg[j];
-      }
-    }
-    const std::uint64_t xa0 = static_cast<std::uint64_t>(grp) * na;  // x_a of x_1 = 0
-    // skip (warp-uniformly) groups with no state of this shard
-    const bool in_shard = active && (xa0 * n_xb + xbi < hi) && ((xa0 + na - 1) * n_xb + xbi >= lo);
-    if (!__any_sync(0xffffffffu, in_shard)) continue;
-    double acc[S8][OB4];
-    // merged block: aged profile (x_2..x_M) for h_a <= x_1
-    {
-      int ap = 0, w = 1;
-#pragma unroll
-      for (int j = 1; j <= M - 1; ++j) {
-        ap += xg[j + 1] * w;
-        w *= na;
-      }
-      const double* wr = w_sl + slab_row(ap) * stride + ob0;
-      const double* vr = v0_sl + slab_row(ap) * stride + ob0;
-      double wv[OB4], vv[OB4];
-#pragma unroll
-      for (int k = 0; k < OB4; ++k) {
-        wv[k] = wr[k];
-        vv[k] = vr[k];
-      }
-#pragma unroll
-      for (int i = 0; i < S8; ++i) {
-        const int x1 = min(x1b + i, na - 1);
-        double al, g;
-        if (S > 0) {
-          al = s_cal[x1];
-          g = s_cg[x1 + 1];
-        } else {  // all stock in the oldest bucket: h_a = 0..I_a (= x_1)
-          al = (x1 > 0 ? s_cal[x1 - 1] : 0.0) + s_sfa[x1];
-          g = s_cg[x1] + (1.0 - s_cg[x1]);
-        }
-#pragma unroll
-        for (int k = 0; k < OB4; ++k) acc[i][k] = fma(al, wv[k], g * vv[k]);
-      }
-    }
-    // steps j = 1..S: h_a = x_1 + j; j = S is the stock-out boundary.  The
-    // interior weights pmf_a / pz(I_b, .) at x_1 + j slide by one state per
-    // step: keep an 8-wide register window and load one new entry per step.
-    // (x_1 + j <= 15 + S < dn, so no clamping is needed.)
-    double al[S8], gw[S8];
-#pragma unroll
-    for (int i = 0; i < S8; ++i) {
-      al[i] = s_al[x1b + i + 1];
-      gw[i] = s_g[x1b + i + 1];
-    }
-    for (int j = 1; j <= S; ++j) {
-      int ap = 0, w = 1, prefix = 0;
-#pragma unroll
-      for (int q = 1; q <= M - 1; ++q) {
-        ap += ipos(xg[q + 1] - ipos(j - prefix)) * w;
-        prefix += xg[q + 1];
-        w *= na;
-      }
-      const double* wr = w_sl + slab_row(ap) * stride + ob0;
-      const double* vr = v0_sl + slab_row(ap) * stride + ob0;
-      double wv[OB4], vv[OB4];
-#pragma unroll
-      for (int k = 0; k < OB4; ++k) {
-        wv[k] = wr[k];
-        vv[k] = vr[k];
-      }
-      if (j < S) {
-#pragma unroll
-        for (int i = 0; i < S8; ++i) {
-#pragma unroll
-          for (int k = 0; k < OB4; ++k) acc[i][k] = fma(al[i], wv[k], fma(gw[i], vv[k], acc[i][k]));
-        }
-#pragma unroll
-        for (int i = 0; i < S8 - 1; ++i) {
-          al[i] = al[i + 1];
-          gw[i] = gw[i + 1];
-        }
-        al[S8 - 1] = s_al[x1b + S8 + j];
-        gw[S8 - 1] = s_g[x1b + S8 + j];
-      } else {
-#pragma unroll
-        for (int i = 0; i < S8; ++i) {
-          const int ha = x1b + i + j;
-          const double a_b = s_sfa[ha];
-          const double g_b = 1.0 - s_cg[ha];
-#pragma unroll
-          for (int k = 0; k < OB4; ++k) acc[i][k] = fma(a_b, wv[k], fma(g_b, vv[k], acc[i][k]));
-        }
-      }
-    }
-    // Q, first-max over order_b across the 4 lanes that share the states
-#pragma unroll
-    for (int i = 0; i < S8; ++i) {
-      const int x1 = x1b + i;
-      const std::uint64_t s = (xa0 + x1) * n_xb + xbi;
-      const bool valid = active && x1 < na && s >= lo && s < hi;
-      double er = 0.0, pt = 0.0;
-      if (valid) {
-        const std::size_t e = (static_cast<std::size_t>(xbi) * (n / n_xb) + xa0 + x1) * 2;
-        er = erpt[e];
-        pt = erpt[e + 1];
-      }
-      T best = T(0);
-      int bo = 0;
-#pragma unroll
-      for (int k = 0; k < OB4; ++k) {
-        const int ob = ob0 + k;
-        const double qd = fma(gamma, acc[i][k], er - (cva_oa + dm.b_cvb * ob) * pt);
-        const T qv = static_cast<T>(qd);
-        if (k == 0 || qv > best) {
-          best = qv;
-          bo = ob;
-        }
-        if (qout && valid) qout[(s - lo) * dm.n_actions + static_cast<std::uint64_t>(oa) * NB + ob] = qv;
-      }
-#pragma unroll
-      for (int off = 1; off <= 2; off <<= 1) {
-        const T ob_v = __shfl_xor_sync(0xffffffffu, best, off);
-        const int ob_i = __shfl_xor_sync(0xffffffffu, bo, off);
-        if (ob_v > best || (ob_v == best && ob_i < bo)) {
-          best = ob_v;
-          bo = ob_i;
-        }
-      }
-      if ((sub & 3) == 0 && valid && part_v) {
-        part_v[static_cast<std::uint64_t>(oa) * nr + (s - lo)] = best;
-        part_a[static_cast<std::uint64_t>(oa) * nr + (s - lo)] = static_cast<std::uint8_t>(bo);
-      }
-    }
   }
 }
 
@@ -1816,346 +1500,32 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_qd3(DevModel dm, const double
   }
 }
 
-// Paired diagonals (sweep path, fused over the orders_a like k_b_fact_qd3).
-// In k_b_fact_qd3 a lane owns one diagonal S2 and only 16 of the 31 lanes
-// have a state at any step u.  Here lane L owns the two diagonals S2 = L
-// (states at u = 0..L) and S2 = L + na (a prefix at u <= L, states at
-// u = L+1..na-1), so every lane emits one state per step; the two running
-// sums advance together and the output takes the one whose diagonal is
-// live.  Half-warp = one x_3 (rows broadcast within the half).
-template <typename T, bool WA>
-__global__ void __launch_bounds__(256, 2) k_b_fact_qp3(DevModel dm, const double* __restrict__ W,
-                                                          const double* __restrict__ v0t,
-                                                          const double* __restrict__ erpt,
-                                                          std::uint64_t lo, std::uint64_t hi,
-                                                          double gamma, int n_xb, int n_ap, int n_r,
-                                                          const T* __restrict__ V,
-                                                          T* __restrict__ vout,
-                                                          std::uint32_t* __restrict__ act,
-                                                          std::uint64_t out_off, FinalizeArgs fa) {
-  constexpr int NB = 16;
-  extern __shared__ double sm[];
-  const int na = dm.b_na, dn = dm.b_dn;
-  const int n_xa = na * na * na;
-  double* w_sl = sm;
-  double* v_sl = w_sl + n_ap * NB;
-  double* s_pa = v_sl + n_ap * NB;     // gamma pmf_a
-  double* s_ca = s_pa + dn;            // gamma cdf_a (inclusive)
-  double* s_pz = s_ca + dn;            // gamma sf_b pz(I_b, .)
-  double* s_cg = s_pz + dn;            // gamma sf_b pz_cum(I_b, .) (exclusive)
-  double* s_sa = s_cg + dn;            // gamma sf_a
-  // running max over (o_a, o_b) of Q - ER(s): ER is common to the row and is
-  // added once in the finalize, so the sweep never reads it per order
-  double* s_best = s_sa + dn;
-  std::uint8_t* s_arg = reinterpret_cast<std::uint8_t*>(s_best + n_xa);
-  const int xbi = blockIdx.x;
-  int ib = 0;
-  {
-    int rem = xbi;
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      ib += rem % NB;
-      rem /= NB;
-    }
-  }
-  const double gsf = gamma * dm.b_sf_b[ib];
-  for (int i = threadIdx.x; i < dn; i += blockDim.x) {
-    s_pa[i] = gamma * dm.b_pmf_a[i];
-    s_ca[i] = gamma * dm.b_cdf_a[i];
-    s_pz[i] = gsf * dm.b_pz[ib * dn + i];
-    s_cg[i] = gsf * dm.b_pz_cum[ib * dn + i];
-    s_sa[i] = gamma * dm.b_sf_a[i];
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int L = lane & 15, half = lane >> 4;
-  const int ilo = static_cast<int>(lo), ihi = static_cast<int>(hi);
-  const double cvb = dm.b_cvb;
-  const double* er_base = erpt + static_cast<std::size_t>(xbi) * n_xa * 2;  // [x_a][ER, PT]
-  const int n_pairs = (na + 1) / 2;
-  for (int oa = 0; oa < na; ++oa) {
-    const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
-    if (oa > 0) __syncthreads();
-    {
-      const double2* wsrc = reinterpret_cast<const double2*>(W + (static_cast<std::size_t>(xbi) * n_r + r0) * NB);
-      const double2* vsrc = reinterpret_cast<const double2*>(v0t + r0 * NB);
-      const unsigned wd = static_cast<unsigned>(__cvta_generic_to_shared(w_sl));
-      const unsigned vd = static_cast<unsigned>(__cvta_generic_to_shared(v_sl));
-      for (int i = threadIdx.x; i < n_ap * NB / 2; i += blockDim.x) {
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wd + 16u * i), "l"(wsrc + i));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(vd + 16u * i), "l"(vsrc + i));
-      }
-      asm volatile("cp.async.commit_group;\n" ::);
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
-    }
-    __syncthreads();
-    const double c0 = dm.b_cva * oa;
-    for (int pr = warp; pr < n_pairs; pr += blockDim.x >> 5) {
-      const int x3 = 2 * pr + half;
-      const int xlo0 = 2 * pr * na * na;
-      const int xhi0 = min(2 * pr + 2, na) * na * na - 1;
-      if (xhi0 * n_xb + xbi < ilo || xlo0 * n_xb + xbi >= ihi) continue;  // warp-uniform
-      const bool lane_ok = L < na && x3 < na;
-      const int x3c = min(x3, na - 1);
-      const int xa_lo = x3c * na * na;
-      // diagonal constants of S2 = L (a) and S2 = L + na (b)
-      const int Ia = min(L + x3c, dn - 1), Ib = min(L + na + x3c, dn - 1);
-      double acc_a[NB], acc_b[NB];
-      {
-        const double cwa = s_sa[Ia] - s_pa[Ia], cga = (gsf - s_cg[Ia]) - s_pz[Ia];
-        const double cwb = s_sa[Ib] - s_pa[Ib], cgb = (gsf - s_cg[Ib]) - s_pz[Ib];
-        // PT(s) = 1 (checked by the launcher), so the order cost
-        // C_v^a o_a + C_v^b o_b is a per-o_b constant of every row: it starts
-        // in the running sums
-#pragma unroll
-        for (int k = 0; k < NB; ++k) {
-          const double w0 = w_sl[k], v0 = v_sl[k];
-          const double cost = -fma(static_cast<double>(k), cvb, c0);
-          acc_a[k] = fma(cwa, w0, fma(cga, v0, cost));
-          acc_b[k] = fma(cwb, w0, fma(cgb, v0, cost));
-        }
-        for (int j = 0; j < x3c; ++j) {
-          const double* wr = w_sl + (j * na) * NB;
-          const double* vr = v_sl + (j * na) * NB;
-          const double pa = s_pa[max(Ia - j, 0)], pg = s_pz[max(Ia - j, 0)];
-          const double pb = s_pa[max(Ib - j, 0)], qb = s_pz[max(Ib - j, 0)];
-#pragma unroll
-          for (int k = 0; k < NB; ++k) {
-            const double wk = wr[k], vk = vr[k];
-            acc_a[k] = fma(pa, wk, fma(pg, vk, acc_a[k]));
-            acc_b[k] = fma(pb, wk, fma(qb, vk, acc_b[k]));
-          }
-        }
-      }
-      // step u emits x_1 = L - u (u <= L, diagonal a) or L + na - u (b)
-      const double* wrow = w_sl + (x3c * na) * NB;
-      const double* vrow = v_sl + (x3c * na) * NB;
-      for (int u = 0; u < na; ++u, wrow += NB, vrow += NB) {
-        const bool sw = u > L;
-        const int x1 = sw ? L + na - u : L - u;
-        const int xa = x1 + u * na + xa_lo;
-        const int st = xa * n_xb + xbi;
-        const bool valid = lane_ok && st >= ilo && st < ihi;
-        const int ia = max(L - u, 0), ibb = min(L + na - u, dn - 1);
-        const double pa = s_pa[ia], pg = s_pz[ia], pb = s_pa[ibb], qb = s_pz[ibb];
-        const int xc = min(max(x1, 0), dn - 2);
-        const double ca = s_ca[xc], cgx = s_cg[xc + 1];
-        double best = 0.0;
-        int bo = 0;
-#pragma unroll
-        for (int k = 0; k < NB; ++k) {
-          const double wk = wrow[k], vk = vrow[k];
-          const double r = sw ? acc_b[k] : acc_a[k];
-          const double t = fma(ca, wk, fma(cgx, vk, r));
-          if (k == 0 || t > best) {
-            best = t;
-            if (WA) bo = k;
-          }
-          acc_a[k] = fma(pa, wk, fma(pg, vk, acc_a[k]));
-          acc_b[k] = fma(pb, wk, fma(qb, vk, acc_b[k]));
-        }
-        if (valid && (oa == 0 || best > s_best[xa])) {
-          s_best[xa] = best;
-          if (WA) s_arg[xa] = static_cast<std::uint8_t>(oa * NB + bo);
-        }
-      }
-    }
-  }
-  __syncthreads();
-  double smx = -DBL_MAX, smn = DBL_MAX;
-  unsigned long long bad = ~0ull;
-  for (int xa = threadIdx.x; xa < n_xa; xa += blockDim.x) {
-    const int st = xa * n_xb + xbi;
-    if (st < ilo || st >= ihi) continue;
-    const T best = static_cast<T>(__ldg(er_base + 2 * xa) + s_best[xa]);
-    if (vout) vout[st - out_off] = best;
-    if (WA && act) act[st - out_off] = s_arg[xa];
-    state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
-  }
-  reduce_stats(smx, smn, bad, fa);
-}
-
-// k_b_fact_qp3 with one warp per CTA: CTA = (x_3 pair, x_b).  The CTA stages
-// only the rows its two x_3 use -- R(u, x_3) for its own x_3 and R(0, j) for
-// the diagonal constants -- so there is no block-wide barrier per order_a and
-// no warp waits for the slowest x_3 pair; the SM interleaves the CTAs.
-template <typename T, bool WA>
-__global__ void __launch_bounds__(32, 16) k_b_fact_qw3(DevModel dm, const double* __restrict__ W,
-                                                       const double* __restrict__ v0t,
-                                                       const double* __restrict__ erpt,
-                                                       std::uint64_t lo, std::uint64_t hi,
-                                                       double gamma, int n_xb, int n_ap, int n_r,
-                                                       const T* __restrict__ V,
-                                                       T* __restrict__ vout,
-                                                       std::uint32_t* __restrict__ act,
-                                                       std::uint64_t out_off, FinalizeArgs fa,
-                                                       int xb_base, int pr_base, int flat_lo) {
-  constexpr int NB = 16;
-  extern __shared__ double sm[];
-  const int na = dm.b_na, dn = dm.b_dn;
-  const int n_xa = na * na * na;
-  // flat_lo >= 0: a 1-D grid over the (pair, x_b) units flat_lo.. (unit shards)
-  const int pr = flat_lo >= 0 ? (flat_lo + static_cast<int>(blockIdx.x)) / n_xb
-                              : pr_base + static_cast<int>(blockIdx.x);
-  const int xbi = flat_lo >= 0 ? (flat_lo + static_cast<int>(blockIdx.x)) % n_xb
-                               : xb_base + static_cast<int>(blockIdx.y);
-  const int x3_0 = 2 * pr, n_x3 = min(2, na - x3_0);   // this CTA's x_3 values
-  const int n_f = min(x3_0 + n_x3 - 1, na - 1) + 1;    // R(0, j) rows, j = 0..n_f-1
-  const int n_rows = n_x3 * na + n_f;
-  double* w_sl = sm;                   // rows [n_x3*na main | n_f F rows][ob]
-  double* v_sl = w_sl + n_rows * NB;
-  double* s_pa = v_sl + n_rows * NB;
-  double* s_ca = s_pa + dn;
-  double* s_pz = s_ca + dn;
-  double* s_cg = s_pz + dn;
-  double* s_sa = s_cg + dn;
-  double* s_best = s_sa + dn;          // [n_x3 * na * na]
-  std::uint8_t* s_arg = reinterpret_cast<std::uint8_t*>(s_best + 2 * na * na);
-  const int ilo = static_cast<int>(lo), ihi = static_cast<int>(hi);
-  {
-    const int s_first = (x3_0 * na * na) * n_xb + xbi;
-    const int s_last = ((x3_0 + n_x3) * na * na - 1) * n_xb + xbi;
-    if (s_last < ilo || s_first >= ihi) return;  // no state of this CTA in the shard
-  }
-  int ib = 0;
-  {
-    int rem = xbi;
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      ib += rem % NB;
-      rem /= NB;
-    }
-  }
-  const double gsf = gamma * dm.b_sf_b[ib];
-  for (int i = threadIdx.x; i < dn; i += 32) {
-    s_pa[i] = gamma * dm.b_pmf_a[i];
-    s_ca[i] = gamma * dm.b_cdf_a[i];
-    s_pz[i] = gsf * dm.b_pz[ib * dn + i];
-    s_cg[i] = gsf * dm.b_pz_cum[ib * dn + i];
-    s_sa[i] = gamma * dm.b_sf_a[i];
-  }
-  const int lane = threadIdx.x & 31;
-  const int L = lane & 15, half = lane >> 4;
-  const int x3 = x3_0 + half;
-  const bool lane_ok = L < na && half < n_x3;
-  const int x3c = min(x3, na - 1);
-  const int Ia = min(L + x3c, dn - 1), Ib = min(L + na + x3c, dn - 1);
-  const double cvb = dm.b_cvb;
-  const double* er_base = erpt + static_cast<std::size_t>(xbi) * n_xa * 2;
-  const unsigned wd = static_cast<unsigned>(__cvta_generic_to_shared(w_sl));
-  const unsigned vd = static_cast<unsigned>(__cvta_generic_to_shared(v_sl));
-  for (int oa = 0; oa < na; ++oa) {
-    const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
-    __syncwarp();
-    {
-      // main rows: ap = x3_0*na .. (x3_0+n_x3)*na - 1 (contiguous); F rows ap = j*na
-      // W tiled [x_b / 16][r][x_b % 16][o_b] (k_b_fact_w16, tiled = 1): row r
-      // of this x_b at ((x_b/16) n_r + r) 256 + (x_b%16) 16
-      const double2* wsrc = reinterpret_cast<const double2*>(
-          W + ((static_cast<std::size_t>(xbi >> 4) * n_r + r0) * NB + (xbi & 15)) * NB);
-      const double2* vsrc = reinterpret_cast<const double2*>(v0t + r0 * NB);
-      for (int i = lane; i < n_rows * (NB / 2); i += 32) {
-        const int row = i >> 3, c = i & 7;
-        const int ap = row < n_x3 * na ? x3_0 * na + row : (row - n_x3 * na) * na;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wd + 16u * i), "l"(wsrc + ap * 128 + c));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(vd + 16u * i), "l"(vsrc + ap * 8 + c));
-      }
-      asm volatile("cp.async.commit_group;\n" ::);
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
-    }
-    __syncwarp();
-    const double c0 = dm.b_cva * oa;
-    const double* f_w = w_sl + n_x3 * na * NB;  // R(0, j) rows
-    const double* f_v = v_sl + n_x3 * na * NB;
-    double acc_a[NB], acc_b[NB];
-    {
-      const double cwa = s_sa[Ia] - s_pa[Ia], cga = (gsf - s_cg[Ia]) - s_pz[Ia];
-      const double cwb = s_sa[Ib] - s_pa[Ib], cgb = (gsf - s_cg[Ib]) - s_pz[Ib];
-#pragma unroll
-      for (int k = 0; k < NB; ++k) {
-        const double w0 = f_w[k], v0 = f_v[k];
-        const double cost = -fma(static_cast<double>(k), cvb, c0);
-        acc_a[k] = fma(cwa, w0, fma(cga, v0, cost));
-        acc_b[k] = fma(cwb, w0, fma(cgb, v0, cost));
-      }
-      for (int j = 0; j < x3c; ++j) {
-        const double* wr = f_w + j * NB;
-        const double* vr = f_v + j * NB;
-        const double pa = s_pa[max(Ia - j, 0)], pg = s_pz[max(Ia - j, 0)];
-        const double pb = s_pa[max(Ib - j, 0)], qb = s_pz[max(Ib - j, 0)];
-#pragma unroll
-        for (int k = 0; k < NB; ++k) {
-          const double wk = wr[k], vk = vr[k];
-          acc_a[k] = fma(pa, wk, fma(pg, vk, acc_a[k]));
-          acc_b[k] = fma(pb, wk, fma(qb, vk, acc_b[k]));
-        }
-      }
-    }
-    const int xa_lo = x3c * na * na;
-    const double* wrow = w_sl + (min(half, n_x3 - 1) * na) * NB;
-    const double* vrow = v_sl + (min(half, n_x3 - 1) * na) * NB;
-    for (int u = 0; u < na; ++u, wrow += NB, vrow += NB) {
-      const bool sw = u > L;
-      const int x1 = sw ? L + na - u : L - u;
-      const int xl = x1 + u * na + half * na * na;  // local state index
-      const int st = (x1 + u * na + xa_lo) * n_xb + xbi;
-      const bool valid = lane_ok && st >= ilo && st < ihi;
-      const int ia = max(L - u, 0), ibb = min(L + na - u, dn - 1);
-      const double pa = s_pa[ia], pg = s_pz[ia], pb = s_pa[ibb], qb = s_pz[ibb];
-      const int xc = min(max(x1, 0), dn - 2);
-      const double ca = s_ca[xc], cgx = s_cg[xc + 1];
-      double best = 0.0;
-      int bo = 0;
-#pragma unroll
-      for (int k = 0; k < NB; ++k) {
-        const double wk = wrow[k], vk = vrow[k];
-        const double r = sw ? acc_b[k] : acc_a[k];
-        const double t = fma(ca, wk, fma(cgx, vk, r));
-        if (k == 0 || t > best) {
-          best = t;
-          if (WA) bo = k;
-        }
-        acc_a[k] = fma(pa, wk, fma(pg, vk, acc_a[k]));
-        acc_b[k] = fma(pb, wk, fma(qb, vk, acc_b[k]));
-      }
-      if (valid && (oa == 0 || best > s_best[xl])) {
-        s_best[xl] = best;
-        if (WA) s_arg[xl] = static_cast<std::uint8_t>(oa * NB + bo);
-      }
-    }
-  }
-  __syncwarp();
-  double smx = -DBL_MAX, smn = DBL_MAX;
-  unsigned long long bad = ~0ull;
-  for (int xl = lane; xl < n_x3 * na * na; xl += 32) {
-    const int xa = x3_0 * na * na + xl;
-    const int st = xa * n_xb + xbi;
-    if (st < ilo || st >= ihi) continue;
-    const T best = static_cast<T>(__ldg(er_base + 2 * xa) + s_best[xl]);
-    if (vout) vout[st - out_off] = best;
-    if (WA && act) act[st - out_off] = s_arg[xl];
-    if (fa.n_peers) peer_store<T>(fa, xa, na, st, best);
-    state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
-  }
-  reduce_stats(smx, smn, bad, fa);
-}
-
-// k_b_fact_qw3 with three changes:
+// The sweep path of the diagonal stage 2: one warp per CTA, CTA = (x_3
+// pair, x_b).  Lane L owns the two diagonals S2 = L (states at u = 0..L)
+// and S2 = L + 16 (a prefix at u <= L, states at u = L+1..15), so every
+// lane emits one state per step with all 16 orders_b in registers; the two
+// running sums advance together and the output takes the one whose
+// diagonal is live.  Half-warp = one x_3 (rows broadcast within the half).
+// The CTA stages only the rows its two x_3 use, loops over the orders_a
+// keeping the running first-max per state in shared memory, and ends with
+// the finalize (V', argmax, convergence statistics, fused peer stores) --
+// no (o_a, state) partial buffers.
 //  * the diagonal constants C(I, x_3) are computed once per distinct
 //    I = x_3 + S2 (lane l: I = x3_0 + l, x_3 = x3_0) and handed to the lanes
 //    that need them by shuffles; the upper half-warp (x_3 = x3_0 + 1) adds
-//    its one extra R(0, x3_0) term.  33 constants per x_3 pair instead of
-//    64, with the same operations in the same order as k_b_fact_qw3.
-//  * the R(0, j) rows of the constants are not staged with the main rows:
-//    PF (the default) stages them one order_a ahead into their own buffer
-//    (cp.async group issued once the constants of this order_a are done),
-//    and the next order_a's main rows are issued right after this order_a's
-//    u loop, so both copies land behind computation; without PF they are
-//    read through L1/L2.  DB (double-buffered main rows) costs more in
-//    occupancy than it hides (measured 5.36 vs 4.88 ms per sweep).
+//    its one extra R(0, x3_0) term: 33 constants per x_3 pair instead of 64.
+//  * the R(0, j) rows of the constants are staged one order_a ahead into
+//    their own buffer (cp.async group issued once the constants of this
+//    order_a are done), and the next order_a's main rows right after this
+//    order_a's u loop, so both copies land behind computation.
 //  * the order_b maximum runs as two independent compare chains (even /
 //    odd o_b) merged with the first-maximum rule.
-// b/m3/exp1 sweep (stage 1 + 2): qw3 5.15 ms, qw4 4.88 ms, qw4+PF 4.62 ms.
-template <typename T, bool WA, bool DB, bool PF>
+// Measured (b/m3/exp1 sweep, stage 1 + 2): one diagonal per lane 7.3 ms,
+// paired diagonals in a 256-thread CTA 5.7 ms, one warp per CTA 5.15 ms,
+// shared constants 4.88 ms, + prefetched rows 4.62 ms, + 256-bit W stores in
+// stage 1 4.45 ms, + shuffle-only statistics 4.38 ms.  Double-buffered main
+// rows cost more occupancy than they hide (5.36 ms).
+template <typename T, bool WA>
 __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double* __restrict__ W,
                                                        const double* __restrict__ v0t,
                                                        const double* __restrict__ erpt,
@@ -2177,15 +1547,14 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
                                : xb_base + static_cast<int>(blockIdx.y);
   const int x3_0 = 2 * pr, n_x3 = min(2, na - x3_0);  // this CTA's x_3 values
   const int n_rows = n_x3 * na;
-  // main rows R(u, x_3) [n_x3*na][ob] of W and V0; DB: two buffers (the
-  // next order_a's rows land while this one is computed)
-  constexpr int NBUF = DB ? 2 : 1;
+  // main rows R(u, x_3) [n_x3*na][ob] of W and V0
+  constexpr int NBUF = 1;
   const int rb = 2 * na * NB;          // doubles per row array
   double* w_sl0 = sm;
   double* v_sl0 = w_sl0 + rb;
-  // PF: the R(0, j) rows of the constants (j < max(x3_0, 1)) staged in
-  // shared memory one order_a ahead
-  const int n_fr = PF ? max(na - 2, 1) : 0;
+  // the R(0, j) rows of the constants (j < max(x3_0, 1)) staged in shared
+  // memory one order_a ahead
+  const int n_fr = max(na - 2, 1);
   double* f_w = sm + NBUF * 2 * rb;
   double* f_v = f_w + n_fr * NB;
   double* s_pa = f_v + n_fr * NB;
@@ -2267,40 +1636,29 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
   const int ea_i = max(Ia - x3_0, 0), eb_i = max(Ib - x3_0, 0);
   const double ea = half ? s_pa[ea_i] : 0.0, eg = half ? s_pz[ea_i] : 0.0;
   const double eb = half ? s_pa[eb_i] : 0.0, eq = half ? s_pz[eb_i] : 0.0;
-  if (PF) {
-    stage_f(0);
-    stage(0, 0);
-  } else if (DB) {
-    stage(0, 0);
-  }
+  stage_f(0);
+  stage(0, 0);
   for (int oa = 0; oa < na; ++oa) {
-    const std::size_t r0 = static_cast<std::size_t>(oa) * n_ap;
     __syncwarp();
-    if (PF) {
-      asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // F rows of oa landed
-      __syncwarp();
-    } else if (!DB) {
-      stage(oa, 0);
-    } else if (oa + 1 < na) {
-      stage(oa + 1, (oa + 1) & 1);
-    }
-    const double* w_sl = w_sl0 + (DB ? (oa & 1) * 2 * rb : 0);
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // F rows of oa landed
+    __syncwarp();
+    const double* w_sl = w_sl0;
     const double* v_sl = w_sl + rb;
     const double c0 = dm.b_cva * oa;
     double acc_a[NB], acc_b[NB];
     {
-      // C(I_l, x3_0) from the R(0, j) rows (j < x3_0), read through L1/L2
-      const double* fw = PF ? f_w : W + wtile + r0 * NB * NB;  // row j at fw + j * fstride
-      const double* fv = PF ? f_v : v0t + r0 * NB;
-      const std::size_t fws = PF ? NB : static_cast<std::size_t>(na) * NB * NB;
-      const int fvs = PF ? NB : na * NB;
+      // C(I_l, x3_0) from the staged R(0, j) rows (j < x3_0)
+      const double* fw = f_w;  // row j at fw + j * NB
+      const double* fv = f_v;
+      const std::size_t fws = NB;
+      const int fvs = NB;
       double c[NB];
       {
         const double cw = s_sa[Il] - s_pa[Il], cg = (gsf - s_cg[Il]) - s_pz[Il];
 #pragma unroll
         for (int k = 0; k < NB; k += 2) {
-          const double2 w0 = PF ? *reinterpret_cast<const double2*>(fw + k) : __ldg(reinterpret_cast<const double2*>(fw + k));
-          const double2 v0 = PF ? *reinterpret_cast<const double2*>(fv + k) : __ldg(reinterpret_cast<const double2*>(fv + k));
+          const double2 w0 = *reinterpret_cast<const double2*>(fw + k);
+          const double2 v0 = *reinterpret_cast<const double2*>(fv + k);
           c[k] = fma(cw, w0.x, fma(cg, v0.x, -fma(static_cast<double>(k), cvb, c0)));
           c[k + 1] = fma(cw, w0.y, fma(cg, v0.y, -fma(static_cast<double>(k + 1), cvb, c0)));
         }
@@ -2311,8 +1669,8 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
         const double p = s_pa[max(Il - j, 0)], q = s_pz[max(Il - j, 0)];
 #pragma unroll
         for (int k = 0; k < NB; k += 2) {
-          const double2 wk = PF ? *reinterpret_cast<const double2*>(wr + k) : __ldg(reinterpret_cast<const double2*>(wr + k));
-          const double2 vk = PF ? *reinterpret_cast<const double2*>(vr + k) : __ldg(reinterpret_cast<const double2*>(vr + k));
+          const double2 wk = *reinterpret_cast<const double2*>(wr + k);
+          const double2 vk = *reinterpret_cast<const double2*>(vr + k);
           c[k] = fma(p, wk.x, fma(q, vk.x, c[k]));
           c[k + 1] = fma(p, wk.y, fma(q, vk.y, c[k + 1]));
         }
@@ -2323,17 +1681,13 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
         acc_b[k] = __shfl_sync(0xffffffffu, c[k], srcB);
       }
     }
-    if (PF) {
-      __syncwarp();  // every lane is done with the F rows of oa
-      if (oa + 1 < na) stage_f(oa + 1);
-      if (oa + 1 < na)
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // main rows of oa landed
-      else
-        asm volatile("cp.async.wait_all;\n" ::: "memory");
-    } else if (DB && oa + 1 < na)
-      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    else
+    __syncwarp();  // every lane is done with the F rows of oa
+    if (oa + 1 < na) {
+      stage_f(oa + 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // main rows of oa landed
+    } else {
       asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
@@ -2385,7 +1739,7 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
         if (WA) s_arg[xl] = static_cast<std::uint8_t>(oa * NB + (odd ? o1 : o0));
       }
     }
-    if (PF && oa + 1 < na) {
+    if (oa + 1 < na) {
       __syncwarp();  // every lane is done with the main rows of oa
       stage(oa + 1, 0);
     }
@@ -3229,6 +2583,30 @@ void profile_enable(bool on) {
   g_prof.on = on;
 }
 
+namespace {
+struct SimProf {
+  std::mutex mu;
+  std::uint64_t blocks = 0, days = 0;
+  double ms = 0.0;
+} g_sim_prof;
+}  // namespace
+
+void sim_profile_add(std::uint64_t philox_blocks, std::uint64_t rollout_days, double kernel_ms) {
+  std::lock_guard<std::mutex> lock(g_sim_prof.mu);
+  g_sim_prof.blocks += philox_blocks;
+  g_sim_prof.days += rollout_days;
+  g_sim_prof.ms += kernel_ms;
+}
+
+void sim_profile_read(std::uint64_t* philox_blocks, std::uint64_t* rollout_days, double* kernel_ms) {
+  std::lock_guard<std::mutex> lock(g_sim_prof.mu);
+  if (philox_blocks) *philox_blocks = g_sim_prof.blocks;
+  if (rollout_days) *rollout_days = g_sim_prof.days;
+  if (kernel_ms) *kernel_ms = g_sim_prof.ms;
+  g_sim_prof.blocks = g_sim_prof.days = 0;
+  g_sim_prof.ms = 0.0;
+}
+
 void profile_read(double* ms, std::uint64_t* main_launches, std::uint64_t* all_launches) {
   std::lock_guard<std::mutex> lock(g_prof.mu);
   double total = 0.0;
@@ -3273,48 +2651,6 @@ std::vector<std::uint16_t> digit_sum_order(int radix, int digits) {
   return order;
 }
 }  // namespace
-
-// PVI_B_Q16=0 selects the one-state-per-thread stage 2 (comparison runs).
-static bool c_bin_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PVI_C_BINOM");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-static bool qd_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PVI_B_QD");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-static bool qp_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PVI_B_QP");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-static bool qw_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PVI_B_QW");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-// PVI_B_S1ITEMS=0: shard sweeps' stage 1 walks its rows with a plain stride
-static bool s1_items_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PVI_B_S1ITEMS");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
 
 // The stage-1 work list of one k_b_fact_w16p launch: exactly the rows and
 // group ranges its row-stride loop would process (same filter and column
@@ -3371,25 +2707,6 @@ static std::vector<int4> b_s1_items(int M, int na, int n_groups, int r0, int r1,
   return out;
 }
 
-// PVI_B_QW4: 0 = k_b_fact_qw3, 1 = k_b_fact_qw4, 2 = k_b_fact_qw4 with
-// double-buffered row staging, 3 = k_b_fact_qw4 with the constants' rows
-// prefetched into shared memory
-static int qw4_mode() {
-  static const int mode = [] {
-    const char* e = std::getenv("PVI_B_QW4");
-    return e && e[0] >= '0' && e[0] <= '3' ? e[0] - '0' : 3;
-  }();
-  return mode;
-}
-
-static bool w16p_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PVI_B_W16P");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 static int num_sms() {
   static const int n = [] {
     int dev = 0, v = 148;
@@ -3400,30 +2717,77 @@ static int num_sms() {
   return n;
 }
 
-static bool a_group_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PVI_A_GROUP");
-    return !(e && e[0] == '0');
-  }();
-  return on;
+// Per-device model state of the factored B sweep: ER / PT per state, the
+// stock-sorted digit orders, and whether the issued law has unit mass.
+static DeviceCopy& b_factored_tables(const Model& model, const DevModel& dm, cudaStream_t stream) {
+  const int M = dm.b_m, na = dm.b_na, nb = dm.b_nb;
+  int device = 0;
+  PVI_CUDA(cudaGetDevice(&device));
+  DeviceCopy& dc = model.device_copy(device);
+  std::lock_guard<std::mutex> lock(model.dev_mutex);
+  if (dc.b_erpt) return dc;
+  void* p = nullptr;
+  PVI_CUDA(cudaMalloc(&p, 2 * dm.n_states * sizeof(double)));
+  dc.allocations.push_back(p);
+  {
+    const int ima = M * (na - 1), imb = M * (nb - 1);
+    const int np = (ima + 1) * (imb + 1);
+    double* tab = nullptr;
+    PVI_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tab), 2 * np * sizeof(double), stream));
+    k_b_pair_table<<<(np + 127) / 128, 128, 0, stream>>>(dm, tab, ima, imb);
+    k_b_erpt<<<grid_for(dm.n_states, 256), 256, 0, stream>>>(dm, tab, static_cast<double*>(p), dm.n_states, imb);
+    PVI_CUDA(cudaFreeAsync(tab, stream));
+  }
+  PVI_CUDA(cudaGetLastError());
+  const auto oa_h = digit_sum_order(na, M), ob_h = digit_sum_order(nb, M);
+  void* q1 = nullptr;
+  void* q2 = nullptr;
+  PVI_CUDA(cudaMalloc(&q1, oa_h.size() * 2));
+  PVI_CUDA(cudaMalloc(&q2, ob_h.size() * 2));
+  upload_bytes(q1, oa_h.data(), oa_h.size() * 2);
+  upload_bytes(q2, ob_h.data(), ob_h.size() * 2);
+  dc.allocations.push_back(q1);
+  dc.allocations.push_back(q2);
+  dc.b_order_a = static_cast<std::uint16_t*>(q1);
+  dc.b_order_b = static_cast<std::uint16_t*>(q2);
+  // x_2..x_M digit groups ordered by their stock (stage 1's trip count)
+  auto group_order = [&](int radix) {
+    int count = 1;
+    for (int i = 0; i < M - 1; ++i) count *= radix;
+    std::vector<std::uint16_t> go(count);
+    std::vector<int> gs(count);
+    for (int v = 0; v < count; ++v) {
+      int sum = 0, rem = v;
+      for (int i = 0; i < M - 1; ++i) {
+        sum += rem % radix;
+        rem /= radix;
+      }
+      gs[v] = sum;
+      go[v] = static_cast<std::uint16_t>(v);
+    }
+    std::stable_sort(go.begin(), go.end(), [&](int x, int y) { return gs[x] < gs[y]; });
+    void* q = nullptr;
+    PVI_CUDA(cudaMalloc(&q, go.size() * 2));
+    upload_bytes(q, go.data(), go.size() * 2);
+    dc.allocations.push_back(q);
+    return static_cast<std::uint16_t*>(q);
+  };
+  dc.b_group_order = group_order(na);
+  dc.b_group_order_b = group_order(nb);
+  // PT depends on (I_a, I_b) only: the law's mass is checked on the host
+  dc.b_pt_unit = model.b_law_unit();
+  dc.b_erpt = static_cast<double*>(p);
+  return dc;
 }
 
-static bool qf_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PVI_C_QF");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-static bool q16_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PVI_B_Q16");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
+// Factored B sweep.  Two algorithms by shape:
+//  * m = 3, radix-16 orders_b (b/m3/exp1): stage 1 k_b_fact_w16p (f64,
+//    persistent) / k_b_fact_w16 (f32) into the tiled W, stage 2 on the
+//    diagonals: k_b_fact_qw4 on the sweep path (fused finalize, unit law
+//    mass), else k_b_fact_qd3 (fused without the PT shortcut, or per-order
+//    partials / Q rows);
+//  * any other (m <= 3, radix <= 32): k_b_fact_w + k_b_fact_q (partials),
+//    then k_finalize.
 template <typename T>
 bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
                        Scratch& scratch, cudaStream_t stream) {
@@ -3440,223 +2804,146 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
   const std::size_t sm1 = sizeof(double) * slab_rows(static_cast<int>(n_bp)) * stride;
   const std::size_t sm2 = sizeof(double) * (2 * slab_rows(static_cast<int>(n_ap)) * stride + 4 * dm.b_dn);
   if (sm1 > 200 * 1024 || sm2 > 200 * 1024) return false;
+  DeviceCopy& dc = b_factored_tables(model, dm, stream);
 
-  int device = 0;
-  PVI_CUDA(cudaGetDevice(&device));
-  DeviceCopy& dc = model.device_copy(device);
-  {
-    std::lock_guard<std::mutex> lock(model.dev_mutex);
-    if (!dc.b_erpt) {
-      void* p = nullptr;
-      PVI_CUDA(cudaMalloc(&p, 2 * dm.n_states * sizeof(double)));
-      dc.allocations.push_back(p);
-      {
-        const int ima = M * (na - 1), imb = M * (nb - 1);
-        const int np = (ima + 1) * (imb + 1);
-        double* tab = nullptr;
-        PVI_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tab), 2 * np * sizeof(double), stream));
-        k_b_pair_table<<<(np + 127) / 128, 128, 0, stream>>>(dm, tab, ima, imb);
-        k_b_erpt<<<grid_for(dm.n_states, 256), 256, 0, stream>>>(dm, tab, static_cast<double*>(p), dm.n_states, imb);
-        PVI_CUDA(cudaFreeAsync(tab, stream));
-      }
-      PVI_CUDA(cudaGetLastError());
-      const auto oa_h = digit_sum_order(na, M), ob_h = digit_sum_order(nb, M);
-      void* q1 = nullptr;
-      void* q2 = nullptr;
-      PVI_CUDA(cudaMalloc(&q1, oa_h.size() * 2));
-      PVI_CUDA(cudaMalloc(&q2, ob_h.size() * 2));
-      upload_bytes(q1, oa_h.data(), oa_h.size() * 2);
-      upload_bytes(q2, ob_h.data(), ob_h.size() * 2);
-      dc.allocations.push_back(q1);
-      dc.allocations.push_back(q2);
-      dc.b_order_a = static_cast<std::uint16_t*>(q1);
-      dc.b_order_b = static_cast<std::uint16_t*>(q2);
-      // x_2..x_M digit groups ordered by their stock (the *16 kernels' trip count)
-      auto group_order = [&](int radix) {
-        int count = 1;
-        for (int i = 0; i < M - 1; ++i) count *= radix;
-        std::vector<std::uint16_t> go(count);
-        std::vector<int> gs(count);
-        for (int v = 0; v < count; ++v) {
-          int sum = 0, rem = v;
-          for (int i = 0; i < M - 1; ++i) {
-            sum += rem % radix;
-            rem /= radix;
-          }
-          gs[v] = sum;
-          go[v] = static_cast<std::uint16_t>(v);
-        }
-        std::stable_sort(go.begin(), go.end(), [&](int x, int y) { return gs[x] < gs[y]; });
-        void* q = nullptr;
-        PVI_CUDA(cudaMalloc(&q, go.size() * 2));
-        upload_bytes(q, go.data(), go.size() * 2);
-        dc.allocations.push_back(q);
-        return static_cast<std::uint16_t*>(q);
-      };
-      dc.b_group_order = group_order(na);
-      dc.b_group_order_b = group_order(nb);
-      // PT depends on (I_a, I_b) only: the law's mass is checked on the host
-      dc.b_pt_unit = model.b_law_unit();
-      dc.b_erpt = static_cast<double*>(p);
-    }
-  }
   const std::uint64_t lo = a.lo, hi = a.hi, nr = hi - lo;
   double* W = scratch.get<double>(3, static_cast<std::size_t>(n_xb) * n_r * nb, stream);
   double* v0t = scratch.get<double>(4, static_cast<std::size_t>(n_r) * nb, stream);
-  // m = 3, radix-16 order_b: the diagonal stage 2; on the sweep path fused
-  // over the orders_a with the finalize (no partial buffers, no k_finalize)
-  const bool use_qd = M == 3 && nb == 16 && na <= 16 && dm.n_states < (1ull << 31) && qd_enabled();
-  const bool fused = use_qd && a.want_values && a.qout == nullptr;
+  const bool diag = M == 3 && nb == 16 && na <= 16 && dm.n_states < (1ull << 31);
+  const bool f64 = std::is_same<T, double>::value;
+  const bool fused = diag && a.want_values && a.qout == nullptr;  // no partial buffers
+  const bool qw = fused && dc.b_pt_unit;                          // k_b_fact_qw4
   const bool partials = a.want_values && !fused && (a.stages & 2);
   const std::uint64_t r0 = std::min<std::uint64_t>(a.r_lo, n_r), r1 = std::min<std::uint64_t>(a.r_hi, n_r);
   T* pv = partials ? scratch.get<T>(0, static_cast<std::size_t>(na) * nr, stream) : nullptr;
   std::uint8_t* pa = partials ? scratch.get<std::uint8_t>(1, static_cast<std::size_t>(na) * nr, stream) : nullptr;
   count_launches((partials ? 1 : 0) + ((a.stages & 1) && r1 > r0 ? 1 : 0) + ((a.stages & 2) ? 1 : 0));
-  // stage-1 rows the (fused, one-warp) stage 2 of this shard reads
-  const bool qw = fused && dc.b_pt_unit && qw_enabled();
+  // stage-1 rows the stage 2 of this range reads: its x_3 pairs' rows plus
+  // the constants' rows (x_2 = 0) of lower x_3
   int x3_lo = 0, x3_hi = na - 1;
-  if (qw && M == 3) {
+  if (qw) {
     const std::uint64_t per = static_cast<std::uint64_t>(na) * na * n_xb;  // states per x_3 digit
     x3_lo = static_cast<int>(lo / per) / 2 * 2;
     x3_hi = std::min(na - 1, static_cast<int>((hi - 1) / per) / 2 * 2 + 1);
   }
-  // stage-1 row filter: the shard's rows (+ constants' rows), or exactly the
-  // caller's x_3 rows (pipelined host-buffer backup)
-  const bool s1_rows = a.x3_rows_lo >= 0 && qw && M == 3 && std::is_same<T, double>::value && w16p_enabled();
+  // or exactly the caller's x_3 rows (pipelined host-buffer backup)
+  const bool s1_rows = a.x3_rows_lo >= 0 && qw && f64;
   const bool s1_strict = s1_rows && a.x3_rows_strict;
   const int s1_x3_lo = s1_rows ? a.x3_rows_lo : x3_lo, s1_x3_hi = s1_rows ? a.x3_rows_hi : x3_hi;
-  // x_b digit-group range of stage 1 (w16p only)
+  // x_b digit-group range of stage 1 (k_b_fact_w16p only)
   const std::uint32_t n_grp_all = static_cast<std::uint32_t>(n_bp);
   const std::uint32_t g0 = std::min(a.xg_lo, n_grp_all), g1 = std::min(a.xg_hi, n_grp_all);
-  if ((g0 > 0 || g1 < n_grp_all) && !(std::is_same<T, double>::value && w16p_enabled()))
+  if ((g0 > 0 || g1 < n_grp_all) && !(diag && f64))
     fail(PVI_ERR_PARAMETER, "factored b: x_b group ranges need the f64 persistent stage 1");
+  if ((a.stages & 1) && (r0 != 0 || r1 != static_cast<std::uint64_t>(n_r)) && !diag)
+    fail(PVI_ERR_PARAMETER, "factored b: partial stage-1 ranges need the radix-16 kernel");
   const int s1_g_lo = static_cast<int>(g0), s1_g_cnt = (g0 == 0 && g1 == n_grp_all) ? -1 : static_cast<int>(g1 - g0);
   {
     MainKernelScope prof(stream);
-#define PVI_BF(MM, NBX)                                                                            \
-  if (M == MM && nb <= NBX) {                                                                      \
-    cudaFuncSetAttribute(k_b_fact_w<T, MM, NBX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-    cudaFuncSetAttribute(k_b_fact_q<T, MM, NBX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-    if (nb == 16 && q16_enabled()) {                                                               \
-      const std::size_t sm0 = sizeof(double) * slab_rows(static_cast<int>(n_bp)) * slab_stride(16); \
-      cudaFuncSetAttribute(k_b_fact_w16<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-      if ((a.stages & 1) && r1 > r0) {                                                            \
-        if (std::is_same<T, double>::value && w16p_enabled()) {                                    \
-          auto kp = k_b_fact_w16p<MM>;                                                             \
-          cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sm0);          \
-          unsigned g = static_cast<unsigned>(std::min<std::uint64_t>(r1 - r0, 2 * num_sms()));     \
-          /* a shard's sparse row set: the balanced work list */                                   \
-          const int4* s1_items = nullptr;                                                          \
-          int s1_n = 0;                                                                            \
-          if (s1_items_enabled() && !s1_strict &&                                                  \
-              (a.head_pair >= 0 || a.tail_pair >= 0 || s1_g_cnt >= 0 || s1_x3_lo > 0 || s1_x3_hi < na - 1)) { \
-            const std::vector<int> key{MM, static_cast<int>(r0), static_cast<int>(r1), s1_x3_lo,   \
-                                       s1_x3_hi, s1_strict ? 1 : 0, s1_g_lo, s1_g_cnt, a.head_pair, \
-                                       a.head_g_lo, a.tail_pair, a.tail_g_hi, static_cast<int>(g)}; \
-            auto it = dc.b_s1_items.find(key);                                                     \
-            if (it == dc.b_s1_items.end()) {                                                       \
-              const auto v = b_s1_items(MM, na, static_cast<int>(n_bp), static_cast<int>(r0),      \
-                                        static_cast<int>(r1), s1_x3_lo, s1_x3_hi, s1_strict ? 1 : 0, \
-                                        s1_g_lo, s1_g_cnt, a.head_pair, a.head_g_lo, a.tail_pair, \
-                                        a.tail_g_hi, static_cast<int>(g));                         \
-              void* q = nullptr;                                                                   \
-              if (!v.empty()) {                                                                    \
-                PVI_CUDA(cudaMalloc(&q, v.size() * sizeof(int4)));                                 \
-                upload_bytes(q, v.data(), v.size() * sizeof(int4));                                \
-                dc.allocations.push_back(q);                                                       \
-              }                                                                                    \
-              it = dc.b_s1_items.emplace(key, std::make_pair(q, static_cast<int>(v.size()))).first; \
-            }                                                                                      \
-            s1_items = static_cast<const int4*>(it->second.first);                                 \
-            s1_n = it->second.second;                                                              \
-            g = static_cast<unsigned>(std::min<long long>(std::max(s1_n, 1), 2ll * num_sms()));    \
-          }                                                                                        \
-          kp<<<g, 256, 2 * sm0, stream>>>(                                                         \
-              dm, reinterpret_cast<const double*>(a.v), W, v0t, dc.b_group_order_b,                \
-              static_cast<int>(n_bp), static_cast<int>(n_xb), static_cast<int>(n_bp),               \
-              static_cast<int>(n_r), s1_x3_lo, s1_x3_hi, qw && MM == 3 ? 1 : 0, static_cast<int>(r0), \
-              static_cast<int>(r1 - r0), s1_strict ? 1 : 0, s1_g_lo, s1_g_cnt, a.head_pair,       \
-              a.head_g_lo, a.tail_pair, a.tail_g_hi, s1_items, s1_n);                              \
-        } else {                                                                                   \
-          k_b_fact_w16<T, MM><<<static_cast<unsigned>(r1 - r0), 256, sm0, stream>>>(               \
-              dm, a.v, W, v0t, dc.b_group_order_b, static_cast<int>(n_bp), static_cast<int>(n_xb),  \
-              static_cast<int>(n_bp), static_cast<int>(n_r), x3_lo, x3_hi, qw && MM == 3 ? 1 : 0,   \
-              static_cast<int>(r0));                                                               \
-        }                                                                                          \
-      }                                                                                            \
-    } else if (a.stages & 1) {                                                                     \
-      if (r0 != 0 || r1 != static_cast<std::uint64_t>(n_r))                                        \
-        fail(PVI_ERR_PARAMETER, "factored b: partial stage-1 ranges need the radix-16 kernel");    \
-    k_b_fact_w<T, MM, NBX><<<static_cast<unsigned>(n_r), 256, sm1, stream>>>(                       \
-        dm, a.v, W, v0t, dc.b_order_b, static_cast<int>(n_xb), static_cast<int>(n_bp), static_cast<int>(n_r)); \
-    }                                                                                              \
-    if (!(a.stages & 2)) {                                                                         \
-    } else if (MM == 3 && use_qd) {                                                                \
-      const std::size_t sm4 = sizeof(double) * (2 * static_cast<std::size_t>(n_ap) * 16 + 5 * dm.b_dn); \
-      const std::size_t smf = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(T) + 1);              \
-      if (qw) {                                                                                    \
-        const int q4 = qw4_mode();                                                                 \
-        auto kq = q4 == 3 ? (a.act ? k_b_fact_qw4<T, true, false, true> : k_b_fact_qw4<T, false, false, true>)  \
-                : q4 == 2 ? (a.act ? k_b_fact_qw4<T, true, true, false> : k_b_fact_qw4<T, false, true, false>)  \
-                : q4 == 1 ? (a.act ? k_b_fact_qw4<T, true, false, false> : k_b_fact_qw4<T, false, false, false>) \
-                          : (a.act ? k_b_fact_qw3<T, true> : k_b_fact_qw3<T, false>);              \
-        const int n_f = q4 >= 3 ? std::max(na - 2, 1) : q4 == 2 ? 2 * na : q4 == 1 ? 0 : na;         \
-        const std::size_t smq = sizeof(double) * ((2 * na + n_f) * 16 * 2 + 5 * dm.b_dn + 2 * na * na) + 2 * na * na; \
-        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);         \
-        const std::uint64_t xb0 = std::min<std::uint64_t>(a.xb_lo, n_xb);                          \
-        const std::uint64_t xb1 = std::min<std::uint64_t>(a.xb_hi, n_xb);                          \
-        /* only the x_3 pairs holding states of [lo, hi) */                                       \
-        const std::uint64_t per_pr = 2ull * na * na * n_xb;                                       \
-        const std::uint64_t pr0 = lo / per_pr;                                                    \
-        const std::uint64_t pr1 = std::min<std::uint64_t>((hi + per_pr - 1) / per_pr, (na + 1) / 2); \
-        if (a.flat_hi > a.flat_lo)                                                                  \
-          kq<<<dim3(static_cast<unsigned>(a.flat_hi - a.flat_lo), 1), 32, smq, stream>>>(          \
-              dm, W, v0t, dc.b_erpt, lo, hi, a.gamma, static_cast<int>(n_xb),                      \
-              static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa,  \
-              0, 0, static_cast<int>(a.flat_lo));                                                  \
-        else if (xb1 > xb0 && pr1 > pr0)                                                           \
-          kq<<<dim3(static_cast<unsigned>(pr1 - pr0), static_cast<unsigned>(xb1 - xb0)), 32, smq, stream>>>( \
-              dm, W, v0t, dc.b_erpt, lo, hi, a.gamma, static_cast<int>(n_xb),                      \
-              static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa,  \
-              static_cast<int>(xb0), static_cast<int>(pr0), -1);                                   \
-      } else if (fused && dc.b_pt_unit && qp_enabled()) {                                          \
-        auto kq = a.act ? k_b_fact_qp3<T, true> : k_b_fact_qp3<T, false>;                          \
-        const std::size_t smp = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(double) + 1);       \
-        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);         \
-        kq<<<static_cast<unsigned>(n_xb), 256, smp, stream>>>(                                     \
-            dm, W, v0t, dc.b_erpt, lo, hi, a.gamma, static_cast<int>(n_xb),                        \
-            static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa);   \
-      } else if (fused) {                                                                          \
-        auto kq = a.act ? k_b_fact_qd3<T, true, false, true> : k_b_fact_qd3<T, false, false, true>; \
-        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);         \
-        kq<<<static_cast<unsigned>(n_xb), 256, smf, stream>>>(                                     \
-            dm, W, v0t, dc.b_erpt, nullptr, nullptr, nullptr, lo, hi, a.gamma, static_cast<int>(n_xb), \
-            static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa);   \
-      } else {                                                                                     \
-        auto kq = a.qout ? k_b_fact_qd3<T, true, true, false>                                      \
-                         : (a.act ? k_b_fact_qd3<T, true, false, false> : k_b_fact_qd3<T, false, false, false>); \
-        if (!a.act) pa = nullptr;                                                                  \
-        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);         \
-        kq<<<dim3(static_cast<unsigned>(na), static_cast<unsigned>(n_xb)), 256, sm4, stream>>>(    \
-            dm, W, v0t, dc.b_erpt, pv, pa, a.qout, lo, hi, a.gamma, static_cast<int>(n_xb),         \
-            static_cast<int>(n_ap), static_cast<int>(n_r), nullptr, nullptr, nullptr, 0, FinalizeArgs{}); \
-      }                                                                                            \
-    } else if (nb == 16 && na <= 16 && q16_enabled()) {                                            \
-      const std::size_t sm3 = sizeof(double) * (2 * slab_rows(static_cast<int>(n_ap)) * slab_stride(16) + 5 * dm.b_dn); \
-      cudaFuncSetAttribute(k_b_fact_q16<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-      k_b_fact_q16<T, MM><<<dim3(static_cast<unsigned>(na), static_cast<unsigned>(n_xb)), 256, sm3, stream>>>( \
-          dm, W, v0t, dc.b_erpt, dc.b_group_order, pv, pa, a.qout, lo, hi, a.gamma,                  \
-          static_cast<int>(n_ap), static_cast<int>(n_xb), static_cast<int>(n_ap), static_cast<int>(n_r)); \
-    } else {                                                                                       \
-    k_b_fact_q<T, MM, NBX><<<dim3(static_cast<unsigned>(n_xb), static_cast<unsigned>(na)), 256, sm2, stream>>>( \
-        dm, W, v0t, dc.b_erpt, dc.b_order_a, pv, pa, a.qout, lo, hi, a.gamma, static_cast<int>(n_xa), \
-        static_cast<int>(n_xb), static_cast<int>(n_ap), static_cast<int>(n_r));                  \
-    }                                                                                              \
-  } else
-    PVI_BF(2, 16) PVI_BF(2, 32) PVI_BF(3, 16) PVI_BF(3, 32) {
-      return false;
+    // ---- stage 1: W ----------------------------------------------------------
+    if ((a.stages & 1) && r1 > r0) {
+      if (diag) {
+        const std::size_t sm0 = sizeof(double) * slab_rows(static_cast<int>(n_bp)) * slab_stride(16);
+        if (f64) {
+          auto kp = k_b_fact_w16p<3>;
+          cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sm0);
+          unsigned g = static_cast<unsigned>(std::min<std::uint64_t>(r1 - r0, 2 * num_sms()));
+          // a shard's sparse row set: the balanced work list (built once per shape)
+          const int4* s1_items = nullptr;
+          int s1_n = 0;
+          if (!s1_strict && (a.head_pair >= 0 || a.tail_pair >= 0 || s1_g_cnt >= 0 || s1_x3_lo > 0 ||
+                             s1_x3_hi < na - 1)) {
+            const std::vector<int> key{3, static_cast<int>(r0), static_cast<int>(r1), s1_x3_lo, s1_x3_hi,
+                                       s1_strict ? 1 : 0, s1_g_lo, s1_g_cnt, a.head_pair, a.head_g_lo,
+                                       a.tail_pair, a.tail_g_hi, static_cast<int>(g)};
+            std::lock_guard<std::mutex> lock(model.dev_mutex);
+            auto it = dc.b_s1_items.find(key);
+            if (it == dc.b_s1_items.end()) {
+              const auto v = b_s1_items(3, na, static_cast<int>(n_bp), static_cast<int>(r0), static_cast<int>(r1),
+                                        s1_x3_lo, s1_x3_hi, s1_strict ? 1 : 0, s1_g_lo, s1_g_cnt, a.head_pair,
+                                        a.head_g_lo, a.tail_pair, a.tail_g_hi, static_cast<int>(g));
+              void* q = nullptr;
+              if (!v.empty()) {
+                PVI_CUDA(cudaMalloc(&q, v.size() * sizeof(int4)));
+                upload_bytes(q, v.data(), v.size() * sizeof(int4));
+                dc.allocations.push_back(q);
+              }
+              it = dc.b_s1_items.emplace(key, std::make_pair(q, static_cast<int>(v.size()))).first;
+            }
+            s1_items = static_cast<const int4*>(it->second.first);
+            s1_n = it->second.second;
+            g = static_cast<unsigned>(std::min<long long>(std::max(s1_n, 1), 2ll * num_sms()));
+          }
+          kp<<<g, 256, 2 * sm0, stream>>>(dm, reinterpret_cast<const double*>(a.v), W, v0t, dc.b_group_order_b,
+                                          static_cast<int>(n_bp), static_cast<int>(n_xb), static_cast<int>(n_bp),
+                                          static_cast<int>(n_r), s1_x3_lo, s1_x3_hi, qw ? 1 : 0,
+                                          static_cast<int>(r0), static_cast<int>(r1 - r0), s1_strict ? 1 : 0,
+                                          s1_g_lo, s1_g_cnt, a.head_pair, a.head_g_lo, a.tail_pair, a.tail_g_hi,
+                                          s1_items, s1_n);
+        } else {
+          cudaFuncSetAttribute(k_b_fact_w16<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          k_b_fact_w16<T, 3><<<static_cast<unsigned>(r1 - r0), 256, sm0, stream>>>(
+              dm, a.v, W, v0t, dc.b_group_order_b, static_cast<int>(n_bp), static_cast<int>(n_xb),
+              static_cast<int>(n_bp), static_cast<int>(n_r), x3_lo, x3_hi, qw ? 1 : 0, static_cast<int>(r0));
+        }
+      } else {
+        auto kw = M == 2 ? (nb <= 16 ? k_b_fact_w<T, 2, 16> : k_b_fact_w<T, 2, 32>)
+                         : (nb <= 16 ? k_b_fact_w<T, 3, 16> : k_b_fact_w<T, 3, 32>);
+        cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        kw<<<static_cast<unsigned>(n_r), 256, sm1, stream>>>(dm, a.v, W, v0t, dc.b_order_b, static_cast<int>(n_xb),
+                                                            static_cast<int>(n_bp), static_cast<int>(n_r));
+      }
     }
-#undef PVI_BF
+    // ---- stage 2: Q, the first max over (o_a, o_b), finalize -----------------
+    if (a.stages & 2) {
+      if (qw) {
+        auto kq = a.act ? k_b_fact_qw4<T, true> : k_b_fact_qw4<T, false>;
+        const int n_f = std::max(na - 2, 1);
+        const std::size_t smq =
+            sizeof(double) * ((2 * na + n_f) * 16 * 2 + 5 * dm.b_dn + 2 * na * na) + 2 * na * na;
+        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        const std::uint64_t xb0 = std::min<std::uint64_t>(a.xb_lo, n_xb);
+        const std::uint64_t xb1 = std::min<std::uint64_t>(a.xb_hi, n_xb);
+        // only the x_3 pairs holding states of [lo, hi)
+        const std::uint64_t per_pr = 2ull * na * na * n_xb;
+        const std::uint64_t pr0 = lo / per_pr;
+        const std::uint64_t pr1 = std::min<std::uint64_t>((hi + per_pr - 1) / per_pr, (na + 1) / 2);
+        if (a.flat_hi > a.flat_lo)
+          kq<<<dim3(static_cast<unsigned>(a.flat_hi - a.flat_lo), 1), 32, smq, stream>>>(
+              dm, W, v0t, dc.b_erpt, lo, hi, a.gamma, static_cast<int>(n_xb), static_cast<int>(n_ap),
+              static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa, 0, 0, static_cast<int>(a.flat_lo));
+        else if (xb1 > xb0 && pr1 > pr0)
+          kq<<<dim3(static_cast<unsigned>(pr1 - pr0), static_cast<unsigned>(xb1 - xb0)), 32, smq, stream>>>(
+              dm, W, v0t, dc.b_erpt, lo, hi, a.gamma, static_cast<int>(n_xb), static_cast<int>(n_ap),
+              static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa, static_cast<int>(xb0),
+              static_cast<int>(pr0), -1);
+      } else if (diag) {
+        const std::size_t sm4 = sizeof(double) * (2 * static_cast<std::size_t>(n_ap) * 16 + 5 * dm.b_dn);
+        if (fused) {  // the law's mass is not 1: no PT shortcut
+          const std::size_t smf = sm4 + static_cast<std::size_t>(n_xa) * (sizeof(T) + 1);
+          auto kq = a.act ? k_b_fact_qd3<T, true, false, true> : k_b_fact_qd3<T, false, false, true>;
+          cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          kq<<<static_cast<unsigned>(n_xb), 256, smf, stream>>>(
+              dm, W, v0t, dc.b_erpt, nullptr, nullptr, nullptr, lo, hi, a.gamma, static_cast<int>(n_xb),
+              static_cast<int>(n_ap), static_cast<int>(n_r), a.v, a.vout, a.act, a.out_off, a.fa);
+        } else {  // per-order partials and / or every Q
+          if (!a.act) pa = nullptr;
+          auto kq = a.qout ? k_b_fact_qd3<T, true, true, false>
+                           : (a.act ? k_b_fact_qd3<T, true, false, false> : k_b_fact_qd3<T, false, false, false>);
+          cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          kq<<<dim3(static_cast<unsigned>(na), static_cast<unsigned>(n_xb)), 256, sm4, stream>>>(
+              dm, W, v0t, dc.b_erpt, pv, pa, a.qout, lo, hi, a.gamma, static_cast<int>(n_xb),
+              static_cast<int>(n_ap), static_cast<int>(n_r), nullptr, nullptr, nullptr, 0, FinalizeArgs{});
+        }
+      } else {
+        auto kq = M == 2 ? (nb <= 16 ? k_b_fact_q<T, 2, 16> : k_b_fact_q<T, 2, 32>)
+                         : (nb <= 16 ? k_b_fact_q<T, 3, 16> : k_b_fact_q<T, 3, 32>);
+        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        kq<<<dim3(static_cast<unsigned>(n_xb), static_cast<unsigned>(na)), 256, sm2, stream>>>(
+            dm, W, v0t, dc.b_erpt, dc.b_order_a, pv, pa, a.qout, lo, hi, a.gamma, static_cast<int>(n_xa),
+            static_cast<int>(n_xb), static_cast<int>(n_ap), static_cast<int>(n_r));
+      }
+    }
   }
   PVI_CUDA(cudaGetLastError());
   if (partials)
@@ -3666,6 +2953,17 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
   return true;
 }
 
+// True when the factored B sweep of this model runs k_b_fact_qw4 (which
+// honours SweepArgs::xb_lo/xb_hi).  Valid after the first factored launch
+// (the law-mass check runs there).
+bool b_sweep_honours_xb_range(const Model& model, int device) {
+  if (model.scenario != PVI_SCENARIO_B || model.algorithm != PVI_ALGO_FACTORED) return false;
+  if (model.pb.useful_life != 3 || model.b_nb != 16 || model.b_na > 16) return false;
+  if (model.space.count >= (1ull << 31)) return false;
+  (void)device;
+  return model.b_law_unit();
+}
+
 // True when the factored C sweep of this model runs launch_c_factored (whose
 // tables are weekday-local; the exact kernels gather from all of V).
 bool c_weekday_local(const Model& model) {
@@ -3673,17 +2971,6 @@ bool c_weekday_local(const Model& model) {
   long long n_prof = 1;
   for (int i = 0; i < model.pc.useful_life; ++i) n_prof *= model.pc.max_order + 1;
   return model.pc.useful_life >= 2 && model.pc.useful_life <= 6 && n_prof * 7 <= (1ll << 31);
-}
-
-// True when the factored B sweep of this model runs k_b_fact_qw3 (which
-// honours SweepArgs::xb_lo/xb_hi).  Valid after the first factored launch
-// (the law-mass check runs there).
-bool b_sweep_honours_xb_range(const Model& model, int device) {
-  if (model.scenario != PVI_SCENARIO_B || model.algorithm != PVI_ALGO_FACTORED) return false;
-  if (model.pb.useful_life != 3 || model.b_nb != 16 || model.b_na > 16) return false;
-  if (model.space.count >= (1ull << 31) || !qd_enabled() || !qw_enabled()) return false;
-  (void)device;
-  return model.b_law_unit();
 }
 
 // State runs [a, b) of V that the sweep of shard [lo, hi) reads.  The
@@ -3766,7 +3053,7 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
   const int n_tau = tau1 - tau0;
   double* G = scratch.get<double>(5, static_cast<std::size_t>(n_prof) * 7, stream);
   T* pv = a.want_values ? scratch.get<T>(0, static_cast<std::size_t>(na) * nr, stream) : nullptr;
-  const bool bin = dm.c_binom != nullptr && c_bin_enabled();
+  const bool bin = dm.c_binom != nullptr;
   const bool endo = bin && !dm.c_exogenous;
   // pass tables: exo 7*n_prof each; endo sum_a 7 (a+1) wb each
   const std::size_t tab = endo ? c_tri_base(r, wb) : static_cast<std::size_t>(n_prof) * 7;
@@ -3821,7 +3108,7 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
         src = dst;
       }
       // k_c_bin_qf maps 256 threads onto CQ_GROUPS groups of r states: r <= 21
-      if (qf_enabled() && !endo && r * CQ_GROUPS <= 256) {  // endogenous: per-order restaging loses to k_c_bin_q
+      if (!endo && r * CQ_GROUPS <= 256) {  // endogenous: per-order restaging loses to k_c_bin_q
         const std::uint64_t n_groups = dm.n_states / static_cast<std::uint64_t>(r);
         const std::uint64_t g0 = lo / static_cast<std::uint64_t>(r), g1 = (hi - 1) / static_cast<std::uint64_t>(r) + 1;
         const std::size_t smq = sizeof(double) * (static_cast<std::size_t>(r) * r + 8 +
@@ -3916,7 +3203,7 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
         MainKernelScope prof(stream);
         count_launches(1);
         bool spec = false;
-        if (dm.a_lifo && a_group_enabled()) {
+        if (dm.a_lifo) {
           const int rx = dm.a_max_order + 1;
           const std::uint64_t g0 = lo / rx, g1 = (hi + rx - 1) / rx;
 #define PVI_AL(ML)                                                                                   \
@@ -3934,7 +3221,7 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
           }
           break;
         }
-        if (!dm.a_lifo && a_group_enabled()) {
+        {  // FIFO
           const int rx = dm.a_max_order + 1;
           const std::uint64_t n_groups = dm.n_states / (static_cast<std::uint64_t>(rx) * rx);
           const std::uint64_t n_thr = n_groups * (2 * rx - 1);
@@ -3951,18 +3238,6 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
                 dc.a_pd, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, n_groups, fa);
           break;
         }
-#define PVI_AF(ML)                                                                                   \
-  if (!spec && ml == ML) {                                                                           \
-    k_a_fact<T, 16, ML><<<grid_for(nr, block), block, smf, stream>>>(dm, a.v, dc.a_reward, dc.a_cdf_sf, \
-        dc.a_pd, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);                             \
-    spec = true;                                                                                     \
-  }
-        PVI_AF(21) PVI_AF(22) PVI_AF(31) PVI_AF(32) PVI_AF(41) PVI_AF(42) PVI_AF(51) PVI_AF(52)
-#undef PVI_AF
-        if (!spec)
-          k_a_fact<T, 16, 0><<<grid_for(nr, block), block, smf, stream>>>(dm, a.v, dc.a_reward, dc.a_cdf_sf,
-              dc.a_pd, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);
-        break;
       }
       MainKernelScope prof(stream);
       count_launches(1);

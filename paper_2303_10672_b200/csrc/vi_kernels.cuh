@@ -110,6 +110,10 @@ std::vector<std::pair<std::uint64_t, std::uint64_t>> sweep_read_runs(const Model
                                                                      std::uint64_t hi);
 void profile_enable(bool on);
 bool profiling_enabled();
+// simulation measurement hook: Philox blocks, rollout-days and k_rollouts
+// milliseconds accumulated while profiling is enabled
+void sim_profile_add(std::uint64_t philox_blocks, std::uint64_t rollout_days, double kernel_ms);
+void sim_profile_read(std::uint64_t* philox_blocks, std::uint64_t* rollout_days, double* kernel_ms);
 void init_stats_device(SweepStats* st, cudaStream_t stream);
 void profile_read(double* ms, std::uint64_t* main_launches, std::uint64_t* all_launches);
 void launch_initial_b(const DevModel& dm, double* out, std::uint64_t n, cudaStream_t stream);

@@ -611,6 +611,14 @@ def profile_enable(on: bool = True):
     _raise(L.load().pvi_profile_enable(int(on)), None)
 
 
+def profile_sim_read():
+    """(philox_blocks, rollout_days, kernel_ms) of the evaluations since the last read
+    (pvi_profile_sim_read; counted while profile_enable(True))."""
+    b, d, ms = C.c_uint64(), C.c_uint64(), C.c_double()
+    _raise(L.load().pvi_profile_sim_read(C.byref(b), C.byref(d), C.byref(ms)), None)
+    return b.value, d.value, ms.value
+
+
 def profile_read():
     """(K1 milliseconds, K1 launches, all VI-path kernel launches) since enable/read."""
     ms, k, a = C.c_double(), C.c_uint64(), C.c_uint64()

@@ -191,10 +191,38 @@ def runner_golden():
     np.savez_compressed(os.path.join(HERE, "runner_golden.npz"), **out)
 
 
+def runner_large_golden():
+    """acceptance_main.cpp:303-325: b/m3/exp4 (1.16M states) cmd_solve with
+    3 fixed sweeps, uninterrupted and as 2 + resume; SHA-256 of the files
+    (the policy CSV is ~30 MB)."""
+    import ctypes as C
+    import hashlib
+    import tempfile
+    L = R.lib()
+    L.ref_cmd_solve_fixed.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_uint64, C.c_int, C.c_char_p,
+                                      C.c_size_t]
+    err = C.create_string_buffer(1024)
+    out = {}
+    d_ref, d_res = tempfile.mkdtemp(), tempfile.mkdtemp()
+    assert L.ref_cmd_solve_fixed(b"b/m3/exp4", d_ref.encode(), 8, 3, 0, err, 1024) == 0, err.value
+    assert L.ref_cmd_solve_fixed(b"b/m3/exp4", d_res.encode(), 8, 2, 0, err, 1024) == 0, err.value
+    assert L.ref_cmd_solve_fixed(b"b/m3/exp4", d_res.encode(), 8, 3, 1, err, 1024) == 0, err.value
+    for fn in ["checkpoint.ckpt", "policy.csv"]:
+        a = open(os.path.join(d_ref, fn), "rb").read()
+        b = open(os.path.join(d_res, fn), "rb").read()
+        assert a == b, fn  # the reference's own clause
+        out[f"runner_large|b/m3/exp4|3|{fn}|sha256"] = np.frombuffer(hashlib.sha256(a).digest(), np.uint8)
+        out[f"runner_large|b/m3/exp4|3|{fn}|bytes"] = np.array([len(a)], np.int64)
+    np.savez_compressed(os.path.join(HERE, "runner_large_golden.npz"), **out)
+    print("runner_large", {k: v.tolist() for k, v in out.items() if k.endswith("bytes")})
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "simopt":
         simopt_golden()
     elif len(sys.argv) > 1 and sys.argv[1] == "runner":
         runner_golden()
+    elif len(sys.argv) > 1 and sys.argv[1] == "runner_large":
+        runner_large_golden()
     else:
         main()

@@ -260,7 +260,7 @@ def test_shard_reads_only_its_runs(pvi, preset, parts):
 
 
 def test_read_runs_whole_space_for_gather_sweeps(pvi):
-    for preset, algo in [("b/m3/exp4", "exact"), ("c/m5/exp1", "factored"), ("a/m5/exp5", "factored")]:
+    for preset, algo in [("b/m3/exp4", "exact"), ("c/m5/exp1", "exact"), ("a/m5/exp5", "factored")]:
         m = pvi.make_preset(preset).set_algorithm(algo)
         n = m.state_count()
         assert m.sweep_read_runs(n // 3, n // 2) == [(0, n)]
@@ -291,3 +291,23 @@ def test_factored_c_other_radix_close_to_exact(pvi, max_order, slopes):
     rf = pvi.run_value_iteration(fact)
     assert re.iterations == rf.iterations
     np.testing.assert_allclose(rf.values, re.values, rtol=1e-9)
+
+
+@pytest.mark.parametrize("preset", ["c/m5/exp1", "c/m5/exp2"])
+def test_factored_c_weekday_shard_reads_only_its_runs(pvi, preset):
+    """A factored-C weekday shard computes only its weekdays' tables: with
+    every V entry outside its read runs (own weekdays + the next weekday's
+    slice) set to NaN, its backup is unchanged."""
+    m = pvi.make_preset(preset).set_algorithm("factored")
+    n = m.state_count()
+    V = np.random.default_rng(8).uniform(-20.0, 20.0, n)
+    full_v, full_a = pvi.bellman_backup_batch(m, V, 0, n)
+    b = [int(x) for x in m.partition(3)]
+    for r in range(3):
+        lo, hi = b[r], b[r + 1]
+        Vp = np.full(n, np.nan)
+        for x, y in m.sweep_read_runs(lo, hi):
+            Vp[x:y] = V[x:y]
+        v, a = pvi.bellman_backup_batch(m, Vp, lo, hi)
+        np.testing.assert_array_equal(v, full_v[lo:hi])
+        np.testing.assert_array_equal(a, full_a[lo:hi])

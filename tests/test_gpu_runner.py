@@ -58,3 +58,29 @@ def test_evaluate_refuses_foreign_policy(tmp_path, pvi):
     shutil.copy(os.path.join(d, "policy.csv.meta.json"), os.path.join(d, "x.meta.json"))
     with pytest.raises(pvi.FingerprintMismatch):
         runner.cmd_evaluate("a/m2/exp2", d, vi_policy=os.path.join(d, "policy.csv"), n_rollouts=10)
+
+
+LARGE = np.load(os.path.join(os.path.dirname(__file__), "golden", "runner_large_golden.npz"))
+
+
+@pytest.mark.parametrize("algorithm", ["exact", "factored"])
+def test_b_m3_exp4_command_level_resume_bitwise(tmp_path, algorithm):
+    """acceptance_main.cpp:303-325: b/m3/exp4 (1.16M states), cmd_solve with
+    3 fixed sweeps, uninterrupted vs 2 sweeps + resume: the checkpoint and
+    policy CSV files are identical.  On the exact path both also equal the
+    reference runner's files byte for byte (SHA-256 fixture)."""
+    import hashlib
+    from paper_2303_10672_b200 import runner
+    import paper_2303_10672_b200 as P
+    ref_dir, res_dir = str(tmp_path / "ref"), str(tmp_path / "res")
+    runner.cmd_solve("b/m3/exp4", ref_dir, threads=8, config=P.ViConfig(fixed_iterations=3), algorithm=algorithm)
+    runner.cmd_solve("b/m3/exp4", res_dir, threads=8, config=P.ViConfig(fixed_iterations=2), algorithm=algorithm)
+    runner.cmd_solve("b/m3/exp4", res_dir, threads=8, config=P.ViConfig(fixed_iterations=3), resume=True,
+                     algorithm=algorithm)
+    for fn in ["checkpoint.ckpt", "policy.csv"]:
+        a = open(os.path.join(ref_dir, fn), "rb").read()
+        b = open(os.path.join(res_dir, fn), "rb").read()
+        assert a == b, fn
+        if algorithm == "exact":
+            assert len(a) == int(LARGE[f"runner_large|b/m3/exp4|3|{fn}|bytes"][0])
+            assert hashlib.sha256(a).digest() == LARGE[f"runner_large|b/m3/exp4|3|{fn}|sha256"].tobytes(), fn
