@@ -1562,13 +1562,28 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
   double* s_pz = s_ca + dn;
   double* s_cg = s_pz + dn;
   double* s_sa = s_cg + dn;
-  double* s_best = s_sa + dn;          // [n_x3 * na * na]
-  std::uint8_t* s_arg = reinterpret_cast<std::uint8_t*>(s_best + 2 * na * na);
+  // The running first max over (o_a, o_b) per state lives in TENSOR MEMORY:
+  // lane L's 16 states (one per u step) in its TMEM lane, columns 2u and
+  // 2u + 1 (tcgen05.ld / tcgen05.st, 32x32b), 4 KB per CTA that would
+  // otherwise sit in shared memory -- 16 one-warp CTAs per SM instead of 12
+  // (TMEM: 16 x 32 columns = all 512).  Its argmax byte stays in shared memory.
+  std::uint8_t* s_arg = reinterpret_cast<std::uint8_t*>(s_sa + dn);
   const int ilo = static_cast<int>(lo), ihi = static_cast<int>(hi);
   {
     const int s_first = (x3_0 * na * na) * n_xb + xbi;
     const int s_last = ((x3_0 + n_x3) * na * na - 1) * n_xb + xbi;
     if (s_last < ilo || s_first >= ihi) return;  // no state of this CTA in the shard
+  }
+  std::uint32_t taddr = 0;
+  {
+    __shared__ std::uint32_t s_taddr;
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&s_taddr));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(sa) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncwarp();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    taddr = s_taddr;
   }
   int ib = 0;
   {
@@ -1708,6 +1723,10 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
       const double pa = s_pa[ia], pg = s_pz[ia], pb = s_pa[ibb], qb = s_pz[ibb];
       const int xc = min(max(x1, 0), dn - 2);
       const double ca = s_ca[xc], cgx = s_cg[xc + 1];
+      std::uint32_t old_lo = 0, old_hi = 0;
+      // this state's best so far; waited for after the o_b loop
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n"
+                     : "=r"(old_lo), "=r"(old_hi) : "r"(taddr + 2u * u));
       double b0 = 0.0, b1 = 0.0;
       int o0 = 0, o1 = 1;
 #pragma unroll
@@ -1734,11 +1753,18 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
       // first maximum over o_b: the odd chain wins if larger, or equal at a smaller index
       const bool odd = b1 > b0 || (WA && b1 == b0 && o1 < o0);
       const double best = odd ? b1 : b0;
-      if (valid && (oa == 0 || best > s_best[xl])) {
-        s_best[xl] = best;
-        if (WA) s_arg[xl] = static_cast<std::uint8_t>(oa * NB + (odd ? o1 : o0));
+      {
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        const double old = __hiloint2double(static_cast<int>(old_hi), static_cast<int>(old_lo));
+        const bool take = valid && (oa == 0 || best > old);
+        const double nv = take ? best : old;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(taddr + 2u * u),
+                     "r"(__double2loint(nv)), "r"(__double2hiint(nv))
+                     : "memory");
+        if (WA && take) s_arg[xl] = static_cast<std::uint8_t>(oa * NB + (odd ? o1 : o0));
       }
     }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     if (oa + 1 < na) {
       __syncwarp();  // every lane is done with the main rows of oa
       stage(oa + 1, 0);
@@ -1747,15 +1773,26 @@ __global__ void __launch_bounds__(32, 16) k_b_fact_qw4(DevModel dm, const double
   __syncwarp();
   double smx = -DBL_MAX, smn = DBL_MAX;
   unsigned long long bad = ~0ull;
-  for (int xl = lane; xl < n_x3 * na * na; xl += 32) {
-    const int xa = x3_0 * na * na + xl;
-    const int st = xa * n_xb + xbi;
-    if (st < ilo || st >= ihi) continue;
-    const T best = static_cast<T>(__ldg(er_base + 2 * xa) + s_best[xl]);
-    if (vout) vout[st - out_off] = best;
-    if (WA && act) act[st - out_off] = s_arg[xl];
-    if (fa.n_peers) peer_store<T>(fa, xa, na, st, best);
-    state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
+  {  // finalize the lane's own states, read back from its TMEM lane
+    for (int u = 0; u < na; ++u) {
+      std::uint32_t lo32, hi32;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n"
+                   : "=r"(lo32), "=r"(hi32) : "r"(taddr + 2u * u));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      const int x1 = u > L ? L + na - u : L - u;
+      const int xa = x1 + u * na + x3c * na * na;
+      const int st = xa * n_xb + xbi;
+      if (!lane_ok || st < ilo || st >= ihi) continue;
+      const double bv = __hiloint2double(static_cast<int>(hi32), static_cast<int>(lo32));
+      const T best = static_cast<T>(__ldg(er_base + 2 * xa) + bv);
+      if (vout) vout[st - out_off] = best;
+      if (WA && act) act[st - out_off] = s_arg[x1 + u * na + half * na * na];
+      if (fa.n_peers) peer_store<T>(fa, xa, na, st, best);
+      state_stat<T>(fa, static_cast<std::uint64_t>(st), best, V, smx, smn, bad);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(taddr) : "memory");
   }
   reduce_stats_warp(smx, smn, bad, fa);
 }
@@ -2899,8 +2936,9 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
       if (qw) {
         auto kq = a.act ? k_b_fact_qw4<T, true> : k_b_fact_qw4<T, false>;
         const int n_f = std::max(na - 2, 1);
-        const std::size_t smq =
-            sizeof(double) * ((2 * na + n_f) * 16 * 2 + 5 * dm.b_dn + 2 * na * na) + 2 * na * na;
+        // rows + constants' rows + weight tables + the argmax bytes (the
+        // running maxima are in TMEM)
+        const std::size_t smq = sizeof(double) * ((2 * na + n_f) * 16 * 2 + 5 * dm.b_dn) + 2 * na * na;
         cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
         const std::uint64_t xb0 = std::min<std::uint64_t>(a.xb_lo, n_xb);
         const std::uint64_t xb1 = std::min<std::uint64_t>(a.xb_hi, n_xb);
