@@ -2237,6 +2237,89 @@ __global__ void __launch_bounds__(896, 1) k_c_bin_tile_p(const double* __restric
   }
 }
 
+// The same pass by anti-diagonals, with the inputs in registers (round 2).
+// Output (b, d_k) of a pass reads in[b - y][min(d_k + y, cap)] for y <= b:
+// every term lies on the anti-diagonal c = b + d_k once the capped column is
+// read as a virtual extension in_ext[b'][d'] = in[b'][min(d', cap)].  So a
+// thread owns one (c, x_1): it loads the anti-diagonal's inputs
+// in_ext[b'][c - b'] for b' <= min(c, nb - 1) into registers (<= 21
+// doubles; the capped ones are re-read by several threads, L1/L2 hits) and
+// produces all outputs b in [max(0, c - cap), min(c, nb - 1)] of that
+// anti-diagonal from them, the binomial weights being CTA-uniform
+// shared-memory broadcasts.  Each input reaches the FMAs from a register
+// instead of one shared-memory load per FMA (k_c_bin_tile_p is bound by
+// those loads, ncu), there is no staging and no barrier per item, and one
+// CTA per (order a, tau, line) item leaves the overlap of loads and FMAs to
+// the resident CTAs.  Terms in the same order (y = 0..b) as
+// k_c_bin_tile_p / k_c_bin_level: the same bits.
+template <int RC>
+__global__ void __launch_bounds__(448, 2) k_c_bin_diag(const double* __restrict__ Hin,
+                                                      double* __restrict__ Hout,
+                                                      const double* __restrict__ binom_k,
+                                                      std::size_t binom_a_stride, int m, int k,
+                                                      std::uint32_t wb, int endo, int in_is_g, int n_prof,
+                                                      int n_lines, int tau0, int n_tau) {
+  constexpr int R = RC, CAP = RC - 1;
+  __shared__ double s_w[R * R];  // [b][y] = Bin(y; b, q_k(a))
+  const int i = static_cast<int>(blockIdx.x);
+  const int ai = i / (n_tau * n_lines), rem = i % (n_tau * n_lines);
+  const int a = endo ? R - 1 - ai : 0;  // heavy orders first
+  const int nb = endo ? a + 1 : R;
+  const int tau = tau0 + rem / n_lines;
+  std::uint32_t rest0 = 0, wk = 1;
+  {
+    std::uint32_t o = static_cast<std::uint32_t>(rem % n_lines), w = 1;
+    for (int p = 1; p <= m - 1; ++p) {
+      if (p == k) wk = w;
+      if (p != 1 && p != k) {
+        rest0 += (o % static_cast<std::uint32_t>(R)) * w;
+        o /= static_cast<std::uint32_t>(R);
+      }
+      w *= static_cast<std::uint32_t>(R);
+    }
+  }
+  const std::size_t out_base = endo ? c_tri_base(a, wb) + static_cast<std::size_t>(tau) * nb * wb
+                                    : static_cast<std::size_t>(tau) * n_prof;
+  const std::size_t in_base = (endo && !in_is_g) ? out_base : static_cast<std::size_t>(tau) * n_prof;
+  const double* bt = binom_k + a * binom_a_stride;
+  for (int t = threadIdx.x; t < nb * R; t += blockDim.x) s_w[t] = bt[t];
+  __syncthreads();
+  const int n_combo = (CAP + nb) * R;  // anti-diagonals c = 0 .. cap + nb - 1, times x_1
+  // element offsets fit 32 bits (the largest table, endogenous c/m5, has
+  // 3.1e8 entries): one 64-bit pointer per item, 32-bit index arithmetic
+  const double* src = Hin + in_base + rest0;
+  double* dst = Hout + out_base + rest0;
+  const std::uint32_t dwb = wb - wk;  // one step along an uncapped anti-diagonal
+  for (int combo = threadIdx.x; combo < n_combo; combo += blockDim.x) {
+    const int c = combo / R, x1 = combo - (combo / R) * R;
+    const int hi_in = min(c, nb - 1);
+    const int lo_out = max(0, c - CAP);
+    double v[R];
+    // b' < c - cap read the capped column, the rest walk the anti-diagonal
+    std::uint32_t off = static_cast<std::uint32_t>(x1) + static_cast<std::uint32_t>(CAP) * wk;
+#pragma unroll
+    for (int bp = 0; bp < R; ++bp) {
+      if (bp <= hi_in) {
+        const std::uint32_t o = bp < c - CAP ? off : off + static_cast<std::uint32_t>(c - bp - CAP) * wk;
+        v[bp] = __ldg(src + o);
+      }
+      off += wb;
+    }
+    std::uint32_t oo = static_cast<std::uint32_t>(x1) + static_cast<std::uint32_t>(c) * wk;  // b = 0
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      if (b >= lo_out && b <= hi_in) {
+        const double* w = s_w + b * R;
+        double acc = 0.0;
+#pragma unroll
+        for (int y = 0; y <= b; ++y) acc = fma(w[y], v[b - y], acc);
+        dst[oo] = acc;
+      }
+      oo += dwb;
+    }
+  }
+}
+
 // Last pass (k = 1) fused with the Q rows, the first max over the orders and
 // the finalize.  CTA = CQ_GROUPS groups of the A_max+1 states that differ
 // only in x_1; a group's H_2 entries (b, z_1) for b, z_1 in [0, A_max] are one
@@ -3128,11 +3211,17 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
       for (int k = M - 1, i = 0; k >= 2; --k, ++i) {
         wk /= static_cast<std::uint32_t>(r);
         double* dst = Hb[i & 1];
-        if (r <= 21) {
+        if (r == 21) {  // every C preset: the anti-diagonal pass
+          const int n_lines = static_cast<int>(wb / (static_cast<std::uint32_t>(r) * r));
+          const int n_items = (endo ? r : 1) * n_tau * n_lines;
+          k_c_bin_diag<21><<<static_cast<unsigned>(n_items), 448, 0, stream>>>(
+              src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, endo ? a_stride : 0, M, k, wb,
+              endo ? 1 : 0, src == G ? 1 : 0, static_cast<int>(n_prof), n_lines, tau0, n_tau);
+        } else if (r <= 21) {
           const int n_lines = static_cast<int>(wb / (static_cast<std::uint32_t>(r) * r));
           const std::size_t smt = 2 * (static_cast<std::size_t>(r) * r * r + static_cast<std::size_t>(r) * r) * sizeof(double);
           const int n_items = (endo ? r : 1) * n_tau * n_lines;
-          auto kern = r == 21 ? k_c_bin_tile_p<21> : k_c_bin_tile_p<0>;
+          auto kern = k_c_bin_tile_p<0>;  // other radices <= 21
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
           kern<<<static_cast<unsigned>(std::min(n_items, num_sms())), 896, smt, stream>>>(
               src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, endo ? a_stride : 0, r, M, k, wb,
