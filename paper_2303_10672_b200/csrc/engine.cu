@@ -128,6 +128,7 @@ const DevModel& Model::device_view(int device) const {
       d.a_cw = pa.wastage_cost;
       d.a_pmf = upload(*dc, a_pmf);
       d.a_cdf = upload(*dc, a_cdf);
+      d.a_guide = upload(*dc, cdf_guide(a_cdf.data(), pa.max_demand + 1, kGuide));
       break;
     case PVI_SCENARIO_B:
       d.b_m = pb.useful_life;
@@ -153,6 +154,13 @@ const DevModel& Model::device_view(int device) const {
       d.b_pz_cum = upload(*dc, b_pz_cum);
       d.b_cdf_a = upload(*dc, b_cdf_a);
       d.b_cdf_b = upload(*dc, b_cdf_b);
+      d.b_guide_a = upload(*dc, cdf_guide(b_cdf_a.data(), static_cast<int>(b_cdf_a.size()), kGuide));
+      d.b_guide_b = upload(*dc, cdf_guide(b_cdf_b.data(), static_cast<int>(b_cdf_b.size()), kGuide));
+      // trials = demand_b - fill_b <= |support of demand_b| - 1
+      d.b_binom_t = static_cast<int>(b_pmf_b.size()) - 1;
+      d.b_binom_cum = pb.substitution_prob > 0.0 && pb.substitution_prob < 1.0
+                          ? upload(*dc, binomial_cum_table(d.b_binom_t, pb.substitution_prob))
+                          : nullptr;
       d.b_lane_order = upload(*dc, b_lane_order);
       d.b_tile = static_cast<int>(b_lane_order.size());
       break;
@@ -167,6 +175,20 @@ const DevModel& Model::device_view(int device) const {
       d.c_cw = pc.wastage_cost;
       d.c_pmf = upload(*dc, c_pmf);
       d.c_cdf = upload(*dc, c_cdf);
+      {
+        const int dn = pc.max_demand + 1;
+        std::vector<std::int32_t> g;
+        for (int t = 0; t < 7; ++t) {
+          const auto gt = cdf_guide(c_cdf.data() + static_cast<std::size_t>(t) * dn, dn, kGuide);
+          g.insert(g.end(), gt.begin(), gt.end());
+        }
+        d.c_guide = upload(*dc, g);
+        std::vector<double> cum;
+        std::vector<std::int32_t> off;
+        c_receipt_tables(c_receipt.data(), pc.max_order, pc.useful_life, cum, off);
+        d.c_rcpt_cum = upload(*dc, cum);
+        d.c_rcpt_off = upload(*dc, off);
+      }
       d.c_comp = upload(*dc, c_comp);
       d.c_ids = upload(*dc, c_ids);
       d.c_probs = upload(*dc, c_probs);

@@ -54,6 +54,7 @@ struct DevModel {
   double a_cv, a_ch, a_cs, a_cw;
   const double* a_pmf;  // D_max+1
   const double* a_cdf;
+  const std::int32_t* a_guide;  // guide table of a_cdf (kGuide + 1)
 
   // B
   int b_m, b_na, b_nb, b_cap_a, b_cap_b, b_dn;  // b_dn = d_max+1 (pz row length)
@@ -67,6 +68,13 @@ struct DevModel {
   const double* b_pz_cum;
   const double* b_cdf_a;
   const double* b_cdf_b;
+  // rollout sampling tables (sim_tables.cpp): guide tables of the two demand
+  // cdfs, and the substitution binomial's cumulative masses for every trial
+  // count 0..b_binom_t at p = rho (null when rho is 0 or 1)
+  const std::int32_t* b_guide_a;
+  const std::int32_t* b_guide_b;
+  const double* b_binom_cum;
+  int b_binom_t;
   const std::uint16_t* b_lane_order;  // low-digit combos sorted by stock (tile order)
   int b_tile;                          // states per tile (product of the two low radices)
 
@@ -76,6 +84,9 @@ struct DevModel {
   double c_cf, c_ch, c_cs, c_cw;
   const double* c_pmf;        // 7 x (D+1)
   const double* c_cdf;        // 7 x (D+1)
+  const std::int32_t* c_guide;  // 7 x (kGuide + 1) guide tables of c_cdf
+  const double* c_rcpt_cum;     // receipt binomials' cumulative masses (sim_tables.cpp)
+  const std::int32_t* c_rcpt_off;  // (A_max + 1) x (m - 1) offsets into c_rcpt_cum, -1: none
   const std::int8_t* c_comp;  // n_comp x m, freshest first
   const std::uint32_t* c_ids;     // concatenated per action
   const double* c_probs;          // aligned with c_ids
@@ -94,6 +105,13 @@ struct DevModel {
   const double* t_reward;
   const double* t_prob;
 };
+
+// sampling tables of the rollout kernel (sim_tables.cpp)
+constexpr int kGuide = 256;
+std::vector<std::int32_t> cdf_guide(const double* cdf, int size, int G);
+std::vector<double> binomial_cum_table(int T, double p);
+void c_receipt_tables(const double* receipt, int max_order, int m, std::vector<double>& cum,
+                      std::vector<std::int32_t>& offsets);
 
 struct DeviceCopy {
   DevModel dm{};

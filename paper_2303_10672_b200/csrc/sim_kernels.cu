@@ -79,6 +79,23 @@ __device__ __forceinline__ int sample_from_cdf(const double* cdf, int size, doub
   return lo;
 }
 
+// sample_from_cdf through a guide table (sim_tables.cpp cdf_guide): the
+// same index, found by one table load and a short forward scan
+__device__ __forceinline__ int sample_from_cdf_guided(const double* cdf, int size, const std::int32_t* guide,
+                                                      double u) {
+  int i = __ldg(guide + static_cast<int>(u * kGuide));  // u in [0, 1): exact bucket
+  while (i < size - 1 && !(__ldg(cdf + i) > u)) ++i;
+  return i;
+}
+
+// sample_binomial from the precomputed cumulative masses of row `trials`
+// (sim_tables.cpp binomial_cum_table): the same k as the loop below
+__device__ __forceinline__ int sample_binomial_table(int trials, const double* row, double u) {
+  int k = 0;
+  while (k < trials && !(__ldg(row + k) > u)) ++k;
+  return k;
+}
+
 // rng.hpp:76-90
 __device__ __forceinline__ int sample_binomial(int trials, double p, double u) {
   if (trials <= 0 || p <= 0.0) return 0;
@@ -131,7 +148,7 @@ __device__ void step_a(const DevModel& dm, int* state, const int* action, Rng& r
     x[j] = state[lead - 1 + m - j];
     xt += x[j];
   }
-  const int demand = sample_from_cdf(dm.a_cdf, dm.a_dmax + 1, rng.uniform());
+  const int demand = sample_from_cdf_guided(dm.a_cdf, dm.a_dmax + 1, dm.a_guide, rng.uniform());
   const int expired = dm.a_lifo ? age_lifo_s(x, m, demand, aged) : age_fifo_s(x, m, demand, aged);
   const int arriving = lead >= 2 ? state[lead - 2] : order;
   st.reward = -dm.a_cv * order - dm.a_ch * ipos(xt - demand - expired) - dm.a_cs * ipos(demand - xt) -
@@ -158,11 +175,15 @@ __device__ void step_b(const DevModel& dm, int* state, const int* action, Rng& r
     stock_a += xa[j];
     stock_b += xb[j];
   }
-  const int demand_a = sample_from_cdf(dm.b_cdf_a, dm.b_len_a, rng.uniform());
-  const int demand_b = sample_from_cdf(dm.b_cdf_b, dm.b_len_b, rng.uniform());
+  const int demand_a = sample_from_cdf_guided(dm.b_cdf_a, dm.b_len_a, dm.b_guide_a, rng.uniform());
+  const int demand_b = sample_from_cdf_guided(dm.b_cdf_b, dm.b_len_b, dm.b_guide_b, rng.uniform());
   const int own_fill_a = min(demand_a, stock_a);
   const int fill_b = min(demand_b, stock_b);
-  const int accepted = sample_binomial(demand_b - fill_b, dm.b_rho, rng.uniform());
+  const int trials = demand_b - fill_b;
+  const double ub = rng.uniform();
+  const int accepted = dm.b_binom_cum && trials > 0 && trials <= dm.b_binom_t
+                           ? sample_binomial_table(trials, dm.b_binom_cum + trials * (trials + 1) / 2, ub)
+                           : sample_binomial(trials, dm.b_rho, ub);
   const int sub = min(accepted, stock_a - own_fill_a);
   const int h_a = own_fill_a + sub;
   const int h_b = fill_b;
@@ -210,7 +231,10 @@ __device__ void step_c(const DevModel& dm, int* state, const int* action, Rng& r
         continue;
       }
       const double cond = probs[k] / mass_left;
-      counts[k] = sample_binomial(remaining, cond < 1.0 ? cond : 1.0, rng.uniform());
+      const double u = rng.uniform();
+      const int off = dm.c_rcpt_off ? __ldg(dm.c_rcpt_off + order * (m - 1) + k) : -1;
+      counts[k] = off >= 0 ? sample_binomial_table(remaining, dm.c_rcpt_cum + off + remaining * (remaining + 1) / 2, u)
+                           : sample_binomial(remaining, cond < 1.0 ? cond : 1.0, u);
       remaining -= counts[k];
       mass_left -= probs[k];
     }
@@ -219,7 +243,7 @@ __device__ void step_c(const DevModel& dm, int* state, const int* action, Rng& r
   int y[14], x[14], z[14];
   for (int j = 1; j <= m; ++j) y[j] = counts[j - 1];
   const int dn = dm.c_dmax + 1;
-  const int d = sample_from_cdf(dm.c_cdf + tau * dn, dn, rng.uniform());
+  const int d = sample_from_cdf_guided(dm.c_cdf + tau * dn, dn, dm.c_guide + tau * (kGuide + 1), rng.uniform());
   for (int j = 1; j <= m - 1; ++j) x[j] = state[m - j];
   int total = y[m], accepted = y[m];
   for (int j = 1; j <= m - 1; ++j) {

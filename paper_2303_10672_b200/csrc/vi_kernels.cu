@@ -1997,6 +1997,89 @@ __global__ void __launch_bounds__(256) k_c_fact_g(DevModel dm, const T* __restri
   G[static_cast<std::size_t>(tau) * n_prof + gid] = acc;
 }
 
+// G by convolution (round 2).  Along a line of profiles that differ only in
+// z_1 (consecutive indices), every quantity of a (z_1, d) term depends on
+// z_1 and d only through t = z_1 - d: the next-state digits
+// max(min(sp_{j+1} - d, z_{j+1}), 0) with sp_{j+1} = z_1 + q_{j+1}, the
+// stock left total - d = total' + t and the wastage (z_1 - d)^+.  So
+// G[z_1] = sum_d p_d F(z_1 - d) with F(t) = gamma V[idx(t)] + r0(t): one
+// warp per line evaluates the 2 D + 1 = 41 values F(t) (41 index
+// computations and V gathers instead of 441) into shared memory, then lane
+// z_1 folds its 21 demands in order d = 0..D -- the same terms in the same
+// order as k_c_fact_g, hence the same bits.  DN = D + 1 = A_max + 1.
+template <typename T, int M, int DN>
+__global__ void __launch_bounds__(256) k_c_fact_g_conv(DevModel dm, const T* __restrict__ V,
+                                                       double* __restrict__ G, int n_prof, double gamma,
+                                                       int tau0, int n_lines) {
+  constexpr int NRA = M * (DN - 1) + DN, CAP = DN - 1, NT = 2 * DN - 1;  // t in [-(DN-1), DN-1]
+  __shared__ double s_ra[NRA], s_cw[DN], s_pmf[DN];
+  __shared__ double s_f[8][NT + 1];
+  const int tau = tau0 + static_cast<int>(blockIdx.y);
+  for (int i = threadIdx.x; i < NRA; i += blockDim.x) {
+    const int x = i - (DN - 1);
+    s_ra[i] = -dm.c_ch * ipos(x) - dm.c_cs * ipos(-x);
+  }
+  for (int i = threadIdx.x; i < DN; i += blockDim.x) {
+    s_cw[i] = dm.c_cw * i;
+    s_pmf[i] = dm.c_pmf[tau * DN + i];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int line = static_cast<int>(blockIdx.x) * (blockDim.x >> 5) + warp;
+  if (line >= n_lines) return;
+  // the line's digits z_2 .. z_{M-1} and the fresh units y_M (profile index
+  // zi = z_1 + r (z_2 + r (.. + r y_M)))
+  int z[M + 1];
+  {
+    int rem = line;
+#pragma unroll
+    for (int j = 2; j <= M - 1; ++j) {
+      z[j] = rem % DN;
+      rem /= DN;
+    }
+    z[M] = rem;
+  }
+  int q[M + 1];  // q_j = z_2 + .. + z_j
+  q[1] = 0;
+#pragma unroll
+  for (int j = 2; j <= M - 1; ++j) q[j] = q[j - 1] + z[j];
+  const int fresh = z[M];
+  const int total0 = q[M - 1] + fresh;  // total - z_1
+  std::uint32_t w[M + 1];
+  {
+    std::uint32_t wk = 1;
+#pragma unroll
+    for (int j = 1; j <= M - 1; ++j) {
+      w[M - j] = wk;
+      wk *= static_cast<std::uint32_t>(DN);
+    }
+    w[0] = wk;
+  }
+  const std::uint32_t tau_base = static_cast<std::uint32_t>((tau + 1) % 7) * w[0];
+  double* f = s_f[warp];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int ti = lane + 32 * h;
+    if (ti < NT) {
+      const int t = ti - (DN - 1);  // z_1 - d
+      std::uint32_t idx = tau_base;
+#pragma unroll
+      for (int j = 1; j <= M - 2; ++j)
+        idx += static_cast<std::uint32_t>(max(min(q[j + 1] + t, z[j + 1]), 0)) * w[M - j];
+      idx += static_cast<std::uint32_t>(max(min(total0 + t, fresh), 0)) * w[1];
+      const double r0 = s_ra[total0 + t + (DN - 1)] - s_cw[max(t, 0)];
+      f[ti] = fma(gamma, static_cast<double>(__ldg(V + idx)), r0);
+    }
+  }
+  __syncwarp();
+  if (lane <= CAP) {
+    double acc = 0.0;
+#pragma unroll
+    for (int d = 0; d < DN; ++d) acc = fma(s_pmf[d], f[lane - d + (DN - 1)], acc);
+    G[static_cast<std::size_t>(tau) * n_prof + static_cast<std::size_t>(line) * DN + lane] = acc;
+  }
+}
+
 // Stage 2: thread = (state, order); heaviest order first.
 template <typename T, int M>
 __global__ void __launch_bounds__(128) k_c_fact_q(DevModel dm, const double* __restrict__ G,
@@ -3190,9 +3273,11 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     const dim3 ggrid(grid_for(n_prof, 256), static_cast<unsigned>(n_tau));
 #define PVI_CF(MM)                                                                               \
   if (!done && M == MM) {                                                                        \
-    if (dm.c_max_order == 20 && dm.c_dmax == 20)                                                  \
-      k_c_fact_g<T, MM, 21><<<ggrid, 256, 0, stream>>>(dm, a.v, G, static_cast<int>(n_prof), a.gamma, tau0); \
-    else                                                                                           \
+    if (dm.c_max_order == 20 && dm.c_dmax == 20) {                                                \
+      const int n_lines = static_cast<int>(n_prof / 21);                                           \
+      k_c_fact_g_conv<T, MM, 21><<<dim3((n_lines + 7) / 8, static_cast<unsigned>(n_tau)), 256, 0, stream>>>( \
+          dm, a.v, G, static_cast<int>(n_prof), a.gamma, tau0, n_lines);                            \
+    } else                                                                                         \
       k_c_fact_g<T, MM><<<ggrid, 256, 0, stream>>>(dm, a.v, G, static_cast<int>(n_prof), a.gamma, tau0); \
     if (!bin)                                                                                    \
       k_c_fact_q<T, MM><<<dim3(grid_for(nr, 128), na), 128, 0, stream>>>(dm, G, pv, a.qout, lo, hi, static_cast<int>(n_prof)); \
