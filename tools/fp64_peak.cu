@@ -61,6 +61,27 @@ __global__ void __launch_bounds__(256) k_dsetp(double a, double b, int iters, do
   if (s == 12345.678) out[threadIdx.x] = s;
 }
 
+// FP64 tensor-core path (DMMA): mma.sync m8n8k4 f64, CH independent
+// accumulator tiles per warp; 8x8x4 = 256 MACs per warp instruction.
+template <int CH>
+__global__ void __launch_bounds__(256) k_dmma(double a, double b, int iters, double* __restrict__ out) {
+  double acc[CH][2];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) acc[c][0] = acc[c][1] = threadIdx.x * 1e-9 + c;
+  const double fa = a + threadIdx.x * 1e-12, fb = b;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                   : "+d"(acc[c][0]), "+d"(acc[c][1])
+                   : "d"(fa), "d"(fb));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += acc[c][0] + acc[c][1];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
 template <typename K>
 static float best_ms(K kern, int blocks, int iters, double* out) {
   cudaEvent_t e0, e1;
@@ -112,6 +133,14 @@ int main() {
                   "\"fp64_pipe_gops\": %.1f, \"tflops_fma_only\": %.3f}",
                   per_sm, ms, 2.0 * ops / (ms * 1e-3) / 1e9, 2.0 * ops / (ms * 1e-3) / 1e12);
     }
+  }
+  for (int per_sm : {4, 8}) {
+    const int blocks = sms * per_sm;
+    const float ms = best_ms(k_dmma<8>, blocks, iters / 4, out);
+    const double warps = blocks * 8.0;
+    const double fl = 2.0 * 256.0 * warps * (iters / 4) * 8;
+    std::printf(", {\"kernel\": \"dmma m8n8k4\", \"chains\": 8, \"ctas_per_sm\": %d, \"ms\": %.4f, "
+                "\"tflops\": %.3f}", per_sm, ms, fl / (ms * 1e-3) / 1e12);
   }
   std::printf("]}\n");
   return 0;
