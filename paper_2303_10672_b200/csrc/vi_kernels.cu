@@ -3352,15 +3352,17 @@ template <typename T>
 void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
                   Scratch& scratch, cudaStream_t stream) {
   const std::uint64_t lo = a.lo, hi = a.hi, nr = hi - lo;
-  if (nr == 0) return;
-  // a complete sweep (not one stage / row block of a pipelined one) owns
-  // every scratch buffer: poison them all (debug, PVI_POISON=1)
-  if (a.stages == 3 && a.r_lo == 0 && a.r_hi == ~0ull && a.x3_rows_lo < 0) scratch.poison(stream);
   FinalizeArgs fa = a.fa;
+  // the statistics are reset even for an empty range (a rank that owns no
+  // state still contributes its neutral statistics to the all-reduce)
   if (fa.stats && a.init_stats) {
     k_init_stats<<<1, 1, 0, stream>>>(fa.stats);
     count_launches(1);
   }
+  if (nr == 0) return;
+  // a complete sweep (not one stage / row block of a pipelined one) owns
+  // every scratch buffer: poison them all (debug, PVI_POISON=1)
+  if (a.stages == 3 && a.r_lo == 0 && a.r_hi == ~0ull && a.x3_rows_lo < 0) scratch.poison(stream);
   switch (model.scenario) {
     case PVI_SCENARIO_A: {
       const unsigned block = 256;

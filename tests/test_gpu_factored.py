@@ -311,3 +311,26 @@ def test_factored_c_weekday_shard_reads_only_its_runs(pvi, preset):
         v, a = pvi.bellman_backup_batch(m, Vp, lo, hi)
         np.testing.assert_array_equal(v, full_v[lo:hi])
         np.testing.assert_array_equal(a, full_a[lo:hi])
+
+
+@pytest.mark.parametrize("preset,algo", [("c/m5/exp1", "factored"), ("b/m3/exp4", "exact"),
+                                         ("a/m5/exp5", "factored")])
+def test_empty_range_sweep_has_neutral_statistics(pvi, preset, algo):
+    """A rank that owns no state (7 weekdays over 8 ranks) still reports
+    neutral statistics for the MAX all-reduce: -DBL_MAX everywhere, in
+    particular no 'first non-finite state 0' from stale buffers."""
+    import torch
+    m = pvi.make_preset(preset).set_algorithm(algo)
+    n = m.state_count()
+    v = torch.zeros(n, dtype=torch.float64, device="cuda")
+    vn = torch.empty_like(v)
+    st = torch.full((4,), 123.0, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    # poison the rank-local statistics buffer with a real sweep first
+    pvi.sweep_device(m, "f64", m.discount(), v.data_ptr(), vn.data_ptr(), None, 0, min(n, 4096),
+                     "change_span", (), st.data_ptr(), s)
+    pvi.sweep_device(m, "f64", m.discount(), v.data_ptr(), vn.data_ptr(), None, n, n, "change_span", (),
+                     st.data_ptr(), s)
+    torch.cuda.synchronize()
+    got = st.cpu().numpy()
+    assert (got[:3] == -1.7976931348623157e308).all(), got

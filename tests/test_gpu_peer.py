@@ -16,6 +16,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from mp_util import collect
+
 pytestmark = pytest.mark.gpu
 
 
@@ -169,10 +171,7 @@ def test_peer_stores_across_processes_ipc():
     procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    res = collect(procs, q, world, 600)
     for rank, ok_own, ok_peer, untouched, n_from_peers in res:
         assert n_from_peers > 0
         assert ok_own and ok_peer and untouched, (rank, ok_own, ok_peer, untouched)
@@ -217,10 +216,7 @@ def test_sharded_solve_multi_process(pvi, preset, algo, exchange, world):
              for r in range(world)]
     for p in procs:
         p.start()
-    it, conv, values, policy, rbytes = q.get(timeout=900)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    (it, conv, values, policy, rbytes), = collect(procs, q, 1, 900)
     want = pvi.run_value_iteration(pvi.make_preset(preset).set_algorithm(algo))
     assert (it, conv) == (want.iterations, want.converged)
     np.testing.assert_array_equal(values, want.values)
@@ -273,3 +269,27 @@ def test_unit_shards_equal_full_sweep(pvi, parts):
         agg = np.maximum(agg, sts.cpu().numpy()[:3])
     assert (covered == 1).all()  # the shards tile the state space
     np.testing.assert_array_equal(agg, fst.cpu().numpy()[:3])
+
+
+@pytest.mark.parametrize("preset,algo,exchange", [("b/m3/exp1", "factored", "peer"),
+                                                  ("c/m5/exp1", "factored", "runs"),
+                                                  ("b/m3/exp4", "exact", "peer")])
+def test_eight_rank_solve_on_one_gpu(pvi, preset, algo, exchange):
+    """The 8-rank layouts the bench would use on an 8-GPU node, as 8
+    processes sharing this GPU: b/m3/exp1 unit shards with fused peer stores,
+    c/m5/exp1 weekday shards (7 weekdays over 8 ranks: one rank owns no
+    state), b/m3/exp4 exact with broadcast peer stores.  Same iterations,
+    values and policy as one process."""
+    world = 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_solve_worker, args=(r, world, port, preset, algo, exchange, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    (it, conv, values, policy, _), = collect(procs, q, 1, 1500)
+    want = pvi.run_value_iteration(pvi.make_preset(preset).set_algorithm(algo))
+    assert (it, conv) == (want.iterations, want.converged)
+    np.testing.assert_array_equal(values, want.values)
+    np.testing.assert_array_equal(policy, want.policy)

@@ -12,6 +12,8 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from mp_util import collect
+
 pytestmark = pytest.mark.gpu
 GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "simopt_golden.npz"))
 
@@ -59,10 +61,7 @@ def _spawn(world, job):
     procs = [ctx.Process(target=_worker, args=(r, world, port, job, q)) for r in range(world)]
     for p in procs:
         p.start()
-    outs = [q.get(timeout=900) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    outs = collect(procs, q, world, 900)
     return outs
 
 

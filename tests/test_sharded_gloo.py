@@ -17,6 +17,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from mp_util import collect
+
 NEG = -1.7976931348623157e308
 
 
@@ -92,10 +94,7 @@ def test_sharded_solve_matches_single_process(preset, world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, preset, q)) for r in range(world)]
     for p in procs:
         p.start()
-    it, conv, values, policy, bounds = q.get(timeout=600)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    (it, conv, values, policy, bounds), = collect(procs, q, 1, 600)
     want = cport.vi_solve(preset)
     assert (it, conv) == (want.iterations, want.converged)
     np.testing.assert_array_equal(values, want.values)
@@ -173,10 +172,7 @@ def test_read_set_exchange_delivers_every_read(world):
     procs = [ctx.Process(target=_rs_worker, args=(r, world, port, preset, steps, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got = [q.get(timeout=600) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    got = collect(procs, q, world, 600)
     for rank, runs, mine, full, received in got:
         for (a, b), vals in mine.items():
             np.testing.assert_array_equal(vals, want[a:b])
@@ -245,10 +241,7 @@ def test_unit_shard_exchange_delivers_every_read(world):
     procs = [ctx.Process(target=_unit_worker, args=(r, world, port, preset, steps, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got = [q.get(timeout=900) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    got = collect(procs, q, world, 900)
     for rank, mine, full, received in got:
         for (a, b), vals in mine.items():
             np.testing.assert_array_equal(vals, want[a:b])
@@ -306,10 +299,7 @@ def test_peer_setup_falls_back_on_every_rank(fail_where):
              for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted(q.get(timeout=600) for _ in range(world))
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res = sorted(collect(procs, q, world, 600))
     for rank, no_peer, mode, why, opened, closed in res:
         assert no_peer and mode == "runs" and why, (rank, no_peer, mode, why)
         # whatever a healthy rank mapped before the vote is unmapped again

@@ -16,6 +16,8 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from mp_util import collect
+
 
 def _free_port():
     s = socket.socket()
@@ -68,10 +70,7 @@ def _spawn(target, world, *args):
     procs = [ctx.Process(target=target, args=(r, world, port) + args + (q,)) for r in range(world)]
     for p in procs:
         p.start()
-    outs = [q.get(timeout=600) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    outs = collect(procs, q, world, 600)
     return sorted(outs, key=lambda o: o[0])
 
 
