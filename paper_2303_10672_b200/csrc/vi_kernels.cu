@@ -1917,27 +1917,16 @@ __global__ void __launch_bounds__(128) k_sweep_c(DevModel dm, const T* __restric
 // IEEE operations in the same order as the inline expression, so G is
 // bit-identical), instead of three int->double conversions and five FP64
 // operations per term.
-template <typename T, int M, int DN = 0>
+// G[tau][z] = sum_d p_d (r0(z, d) + gamma V[next(tau + 1, z, d)]) for any
+// (A_max, D_max); the A_max = D_max = 20 presets take k_c_fact_g_conv.
+template <typename T, int M>
 __global__ void __launch_bounds__(256) k_c_fact_g(DevModel dm, const T* __restrict__ V,
                                                   double* __restrict__ G, int n_prof,
                                                   double gamma, int tau0) {
-  constexpr int NRA = DN > 0 ? M * (DN - 1) + DN : 1;  // x = total - d in [-(DN-1), M (DN-1)]
-  __shared__ double s_ra[NRA], s_cw[DN > 0 ? DN : 1], s_pmf[DN > 0 ? DN : 1];
   const int tau = tau0 + static_cast<int>(blockIdx.y);  // a shard computes its weekdays' rows only
-  if (DN > 0) {
-    for (int i = threadIdx.x; i < NRA; i += blockDim.x) {
-      const int x = i - (DN - 1);
-      s_ra[i] = -dm.c_ch * ipos(x) - dm.c_cs * ipos(-x);
-    }
-    for (int i = threadIdx.x; i < DN; i += blockDim.x) {
-      s_cw[i] = dm.c_cw * i;
-      s_pmf[i] = dm.c_pmf[tau * DN + i];
-    }
-    __syncthreads();
-  }
   const std::uint64_t gid = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gid >= static_cast<std::uint64_t>(n_prof)) return;
-  const int cap = DN > 0 ? DN - 1 : dm.c_max_order, r = cap + 1, dn = DN > 0 ? DN : dm.c_dmax + 1;
+  const int cap = dm.c_max_order, r = cap + 1, dn = dm.c_dmax + 1;
   // profile digits: zi = y_M r^(M-1) + sum_{j<M} z_j r^(j-1)
   int z[M + 1];
   {
@@ -1970,20 +1959,6 @@ __global__ void __launch_bounds__(256) k_c_fact_g(DevModel dm, const T* __restri
   }
   const std::uint32_t tau_base = static_cast<std::uint32_t>((tau + 1) % 7) * w[0];
   double acc = 0.0;
-  if (DN > 0) {
-#pragma unroll
-    for (int d = 0; d < (DN > 0 ? DN : 1); ++d) {
-      std::uint32_t idx = tau_base;
-#pragma unroll
-      for (int j = 1; j <= M - 2; ++j)
-        idx += static_cast<std::uint32_t>(max(min(sp[j + 1] - d, z[j + 1]), 0)) * w[M - j];
-      idx += static_cast<std::uint32_t>(max(min(total - d, fresh), 0)) * w[1];
-      const double r0 = s_ra[total - d + (DN - 1)] - s_cw[max(z[1] - d, 0)];
-      acc = fma(s_pmf[d], fma(gamma, static_cast<double>(__ldg(V + idx)), r0), acc);
-    }
-    G[static_cast<std::size_t>(tau) * n_prof + gid] = acc;
-    return;
-  }
   const double* pmf = dm.c_pmf + tau * dn;
   for (int d = 0; d < dn; ++d) {
     std::uint32_t idx = tau_base;
