@@ -2378,6 +2378,102 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag(const double* __restrict_
   }
 }
 
+// Endogenous C: the last binomial pass (k = 2) fused with the Q pass (k = 1,
+// only b = a).  An item (order a, tau, x_3..x_{m-1}) of pass 2 produces the
+// whole [b <= a][x_2][x_1] tile of H_2 that the Q of its 441 states
+// (x_2, x_1) reads, so the tile goes to shared memory instead of HBM and the
+// same CTA finishes the states' Q for order a: k_c_bin_q's terms in its
+// order, fixed(a) PD(tau) + sum_y Bin(y; a, q_1(a)) H_2[a - y][x_2][min(x_1 +
+// y, cap)] -- the same bits -- without writing H_2 (2.5 GB for c/m5/exp2)
+// and reading it back.
+template <typename T, int RC>
+__global__ void __launch_bounds__(448, 2) k_c_bin_diag_q(DevModel dm, const double* __restrict__ Hin,
+                                                        const double* __restrict__ binom_k,
+                                                        std::size_t binom_a_stride, int m, std::uint32_t wb,
+                                                        int in_is_g, int n_prof, int n_lines, int tau0,
+                                                        int n_tau, T* __restrict__ part_v, T* __restrict__ qout,
+                                                        std::uint64_t lo, std::uint64_t hi) {
+  constexpr int R = RC, CAP = RC - 1, PLANE = R * R;
+  constexpr int k = 2;
+  __shared__ double s_w[R * R];  // [b][y] = Bin(y; b, q_2(a))
+  __shared__ double s_w1[R];     // Bin(y; a, q_1(a))
+  __shared__ double s_pd;
+  extern __shared__ double s_tile[];  // H_2 [b <= a][x_2][x_1]
+  const int i = static_cast<int>(blockIdx.x);
+  const int ai = i / (n_tau * n_lines), rem = i % (n_tau * n_lines);
+  const int a = R - 1 - ai;  // heavy orders first
+  const int nb = a + 1;
+  const int tau = tau0 + rem / n_lines;
+  std::uint32_t rest0 = 0, wk = 1;
+  {
+    std::uint32_t o = static_cast<std::uint32_t>(rem % n_lines), w = 1;
+    for (int p = 1; p <= m - 1; ++p) {
+      if (p == k) wk = w;
+      if (p != 1 && p != k) {
+        rest0 += (o % static_cast<std::uint32_t>(R)) * w;
+        o /= static_cast<std::uint32_t>(R);
+      }
+      w *= static_cast<std::uint32_t>(R);
+    }
+  }
+  const std::size_t in_base = in_is_g ? static_cast<std::size_t>(tau) * n_prof
+                                      : c_tri_base(a, wb) + static_cast<std::size_t>(tau) * nb * wb;
+  const double* bt = binom_k + a * binom_a_stride;
+  for (int t = threadIdx.x; t < nb * R; t += blockDim.x) s_w[t] = bt[t];
+  if (threadIdx.x < R)  // pass 1's weights of order a: c_binom[a][0][a][y]
+    s_w1[threadIdx.x] = dm.c_binom[(static_cast<std::size_t>(a) * (m - 1) * R + a) * R + threadIdx.x];
+  if (threadIdx.x == 0) {
+    const int dn = dm.c_dmax + 1;
+    double pd = 0.0;
+    for (int d = 0; d < dn; ++d) pd += dm.c_pmf[tau * dn + d];
+    s_pd = pd;
+  }
+  __syncthreads();
+  const int n_combo = (CAP + nb) * R;
+  const double* src = Hin + in_base + rest0;
+  for (int combo = threadIdx.x; combo < n_combo; combo += blockDim.x) {
+    const int c = combo / R, x1 = combo - (combo / R) * R;
+    const int hi_in = min(c, nb - 1);
+    const int lo_out = max(0, c - CAP);
+    double v[R];
+    std::uint32_t off = static_cast<std::uint32_t>(x1) + static_cast<std::uint32_t>(CAP) * wk;
+#pragma unroll
+    for (int bp = 0; bp < R; ++bp) {
+      if (bp <= hi_in) {
+        const std::uint32_t o = bp < c - CAP ? off : off + static_cast<std::uint32_t>(c - bp - CAP) * wk;
+        v[bp] = __ldg(src + o);
+      }
+      off += wb;
+    }
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      if (b >= lo_out && b <= hi_in) {
+        const double* w = s_w + b * R;
+        double acc = 0.0;
+#pragma unroll
+        for (int y = 0; y <= b; ++y) acc = fma(w[y], v[b - y], acc);
+        s_tile[b * PLANE + (c - b) * R + x1] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  // Q of order a for the line's states (x_2, x_1): s = tau wb + rest0 + x_2 r + x_1
+  const std::uint64_t nr = hi - lo;
+  const double fixed = a > 0 ? -dm.c_cf : 0.0;
+  const int na = static_cast<int>(dm.n_actions);
+  for (int t = threadIdx.x; t < PLANE; t += blockDim.x) {
+    const int x2 = t / R, x1 = t - (t / R) * R;
+    const std::uint64_t st = static_cast<std::uint64_t>(tau) * wb + rest0 + static_cast<std::uint32_t>(x2) * wk + x1;
+    if (st < lo || st >= hi) continue;
+    const double* h = s_tile + x2 * R;
+    double acc = 0.0;
+    for (int y = 0; y <= a; ++y) acc = fma(s_w1[y], h[(a - y) * PLANE + min(x1 + y, CAP)], acc);
+    const T qa = static_cast<T>(fma(fixed, s_pd, acc));
+    if (part_v) part_v[static_cast<std::uint64_t>(a) * nr + (st - lo)] = qa;
+    if (qout) qout[(st - lo) * na + a] = qa;
+  }
+}
+
 // Last pass (k = 1) fused with the Q rows, the first max over the orders and
 // the finalize.  CTA = CQ_GROUPS groups of the A_max+1 states that differ
 // only in x_1; a group's H_2 entries (b, z_1) for b, z_1 in [0, A_max] are one
@@ -3241,7 +3337,7 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     Hb[0] = scratch.get<double>(6, tab, stream);
     if (M > 3) Hb[1] = scratch.get<double>(7, tab, stream);
   }
-  bool done = false, qf_done = false;
+  bool done = false, qf_done = false, q_fused = false;
   int launches = 0;
   {
     MainKernelScope prof(stream);
@@ -3271,7 +3367,16 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
       for (int k = M - 1, i = 0; k >= 2; --k, ++i) {
         wk /= static_cast<std::uint32_t>(r);
         double* dst = Hb[i & 1];
-        if (r == 21) {  // every C preset: the anti-diagonal pass
+        if (r == 21 && endo && k == 2) {  // the last pass fused with the Q pass
+          const int n_lines = static_cast<int>(wb / (static_cast<std::uint32_t>(r) * r));
+          const int n_items = r * n_tau * n_lines;
+          const std::size_t smt = static_cast<std::size_t>(r) * r * r * sizeof(double);
+          cudaFuncSetAttribute(k_c_bin_diag_q<T, 21>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+          k_c_bin_diag_q<T, 21><<<static_cast<unsigned>(n_items), 448, smt, stream>>>(
+              dm, src, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, a_stride, M, wb, src == G ? 1 : 0,
+              static_cast<int>(n_prof), n_lines, tau0, n_tau, pv, a.qout, lo, hi);
+          q_fused = true;
+        } else if (r == 21) {  // every C preset: the anti-diagonal pass
           const int n_lines = static_cast<int>(wb / (static_cast<std::uint32_t>(r) * r));
           const int n_items = (endo ? r : 1) * n_tau * n_lines;
           k_c_bin_diag<21><<<static_cast<unsigned>(n_items), 448, 0, stream>>>(
@@ -3306,11 +3411,11 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
             dm, src, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, static_cast<int>(n_prof), wb,
             endo ? 1 : 0, src == G ? 1 : 0, n_groups, g0, a.fa);
         qf_done = true;
-      } else {
+      } else if (!q_fused) {
         k_c_bin_q<T><<<dim3(grid_for(nr, 256), na), 256, 0, stream>>>(
             dm, src, pv, a.qout, lo, hi, static_cast<int>(n_prof), wb, endo ? 1 : 0, src == G ? 1 : 0);
       }
-      launches = M;  // G, m-2 passes, fused pass + Q
+      launches = q_fused ? M - 1 : M;  // G, m-2 passes, fused pass + Q
     }
   }
   if (!done) return false;
