@@ -2474,6 +2474,112 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag_q(DevModel dm, const doub
   }
 }
 
+// Exogenous C: the last binomial pass (k = 2) fused with the Q pass, the
+// first max over the orders and the finalize (what k_c_bin_qf does from H_2
+// in HBM).  The exogenous tables are shared by all orders, so an item (tau,
+// x_3..x_{m-1}) builds the whole [b][x_2][x_1] tile of H_2 in shared memory
+// and its 441 states take Q for every order a from it, in k_c_bin_qf's
+// order and expressions: the same bits, without the 229 MB H_2 round trip.
+template <typename T, int RC>
+__global__ void __launch_bounds__(448, 2) k_c_bin_diag_qf(DevModel dm, const double* __restrict__ Hin,
+                                                         const double* __restrict__ binom_k, int m,
+                                                         std::uint32_t wb, int in_is_g, int n_prof, int n_lines,
+                                                         int tau0, const T* __restrict__ V, T* __restrict__ vout,
+                                                         std::uint32_t* __restrict__ act, T* __restrict__ qout,
+                                                         std::uint64_t lo, std::uint64_t hi, std::uint64_t out_off,
+                                                         FinalizeArgs fa) {
+  constexpr int R = RC, CAP = RC - 1, PLANE = R * R;
+  constexpr int k = 2;
+  __shared__ double s_w[R * R];   // [b][y] = Bin(y; b, q_2)
+  __shared__ double s_w1[R * R];  // [a][y] = Bin(y; a, q_1(a))
+  __shared__ double s_pd;
+  extern __shared__ double s_tile[];  // H_2 [b][x_2][x_1]
+  const int i = static_cast<int>(blockIdx.x);
+  const int tau = tau0 + i / n_lines;
+  std::uint32_t rest0 = 0, wk = 1;
+  {
+    std::uint32_t o = static_cast<std::uint32_t>(i % n_lines), w = 1;
+    for (int p = 1; p <= m - 1; ++p) {
+      if (p == k) wk = w;
+      if (p != 1 && p != k) {
+        rest0 += (o % static_cast<std::uint32_t>(R)) * w;
+        o /= static_cast<std::uint32_t>(R);
+      }
+      w *= static_cast<std::uint32_t>(R);
+    }
+  }
+  const std::size_t in_base = static_cast<std::size_t>(tau) * n_prof;
+  (void)in_is_g;
+  for (int t = threadIdx.x; t < PLANE; t += blockDim.x) {
+    s_w[t] = binom_k[t];
+    const int a = t / R, y = t - (t / R) * R;
+    s_w1[t] = dm.c_binom[(static_cast<std::size_t>(a) * (m - 1) * R + a) * R + y];
+  }
+  if (threadIdx.x == 0) {
+    const int dn = dm.c_dmax + 1;
+    double pd = 0.0;
+    for (int d = 0; d < dn; ++d) pd += dm.c_pmf[tau * dn + d];
+    s_pd = pd;
+  }
+  __syncthreads();
+  constexpr int nb = R;
+  const int n_combo = (CAP + nb) * R;
+  const double* src = Hin + in_base + rest0;
+  for (int combo = threadIdx.x; combo < n_combo; combo += blockDim.x) {
+    const int c = combo / R, x1 = combo - (combo / R) * R;
+    const int hi_in = min(c, nb - 1);
+    const int lo_out = max(0, c - CAP);
+    double v[R];
+    std::uint32_t off = static_cast<std::uint32_t>(x1) + static_cast<std::uint32_t>(CAP) * wk;
+#pragma unroll
+    for (int bp = 0; bp < R; ++bp) {
+      if (bp <= hi_in) {
+        const std::uint32_t o = bp < c - CAP ? off : off + static_cast<std::uint32_t>(c - bp - CAP) * wk;
+        v[bp] = __ldg(src + o);
+      }
+      off += wb;
+    }
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      if (b >= lo_out && b <= hi_in) {
+        const double* w = s_w + b * R;
+        double acc = 0.0;
+#pragma unroll
+        for (int y = 0; y <= b; ++y) acc = fma(w[y], v[b - y], acc);
+        s_tile[b * PLANE + (c - b) * R + x1] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  const int na = static_cast<int>(dm.n_actions);
+  double smx = -DBL_MAX, smn = DBL_MAX;
+  unsigned long long bad = ~0ull;
+  for (int t = threadIdx.x; t < PLANE; t += blockDim.x) {
+    const int x2 = t / R, x1 = t - (t / R) * R;
+    const std::uint64_t st = static_cast<std::uint64_t>(tau) * wb + rest0 + static_cast<std::uint32_t>(x2) * wk + x1;
+    if (st < lo || st >= hi) continue;
+    const double* h = s_tile + x2 * R;
+    T best = T(0);
+    std::uint32_t besta = 0;
+    for (int a = 0; a < na; ++a) {
+      const double* w = s_w1 + a * R;
+      double acc = 0.0;
+      for (int y = 0; y <= a; ++y) acc = fma(w[y], h[(a - y) * PLANE + min(x1 + y, CAP)], acc);
+      const double fixed = a > 0 ? -dm.c_cf : 0.0;
+      const T qa = static_cast<T>(fma(fixed, s_pd, acc));
+      if (a == 0 || qa > best) {
+        best = qa;
+        besta = static_cast<std::uint32_t>(a);
+      }
+      if (qout) qout[(st - lo) * na + a] = qa;
+    }
+    if (vout) vout[st - out_off] = best;
+    if (act) act[st - out_off] = besta;
+    state_stat<T>(fa, st, best, V, smx, smn, bad);
+  }
+  reduce_stats(smx, smn, bad, fa);
+}
+
 // Last pass (k = 1) fused with the Q rows, the first max over the orders and
 // the finalize.  CTA = CQ_GROUPS groups of the A_max+1 states that differ
 // only in x_1; a group's H_2 entries (b, z_1) for b, z_1 in [0, A_max] are one
@@ -3337,7 +3443,7 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
     Hb[0] = scratch.get<double>(6, tab, stream);
     if (M > 3) Hb[1] = scratch.get<double>(7, tab, stream);
   }
-  bool done = false, qf_done = false, q_fused = false;
+  bool done = false, qf_done = false, q_fused = false, qf_fused = false;
   int launches = 0;
   {
     MainKernelScope prof(stream);
@@ -3376,6 +3482,15 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
               dm, src, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, a_stride, M, wb, src == G ? 1 : 0,
               static_cast<int>(n_prof), n_lines, tau0, n_tau, pv, a.qout, lo, hi);
           q_fused = true;
+        } else if (r == 21 && !endo && k == 2 && na == r && dm.n_states < (1ull << 32)) {
+          // the last exogenous pass fused with Q, the max over the orders and the finalize
+          const int n_lines = static_cast<int>(wb / (static_cast<std::uint32_t>(r) * r));
+          const std::size_t smt = static_cast<std::size_t>(r) * r * r * sizeof(double);
+          cudaFuncSetAttribute(k_c_bin_diag_qf<T, 21>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+          k_c_bin_diag_qf<T, 21><<<static_cast<unsigned>(n_tau * n_lines), 448, smt, stream>>>(
+              dm, src, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, M, wb, src == G ? 1 : 0,
+              static_cast<int>(n_prof), n_lines, tau0, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, a.fa);
+          q_fused = qf_fused = true;
         } else if (r == 21) {  // every C preset: the anti-diagonal pass
           const int n_lines = static_cast<int>(wb / (static_cast<std::uint32_t>(r) * r));
           const int n_items = (endo ? r : 1) * n_tau * n_lines;
@@ -3400,7 +3515,9 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
         src = dst;
       }
       // k_c_bin_qf maps 256 threads onto CQ_GROUPS groups of r states: r <= 21
-      if (!endo && r * CQ_GROUPS <= 256) {  // endogenous: per-order restaging loses to k_c_bin_q
+      if (qf_fused) {
+        qf_done = true;
+      } else if (!endo && r * CQ_GROUPS <= 256) {  // endogenous: per-order restaging loses to k_c_bin_q
         const std::uint64_t n_groups = dm.n_states / static_cast<std::uint64_t>(r);
         const std::uint64_t g0 = lo / static_cast<std::uint64_t>(r), g1 = (hi - 1) / static_cast<std::uint64_t>(r) + 1;
         const std::size_t smq = sizeof(double) * (static_cast<std::size_t>(r) * r + 8 +
