@@ -118,21 +118,50 @@ struct Step {
   int demand[2], filled[2], expired[2], received[2], holding[2];
 };
 
-__device__ __forceinline__ int age_fifo_s(const int* x, int m, int demand, int* next) {
+// Geometry of one rollout kernel instantiation (round 2): GM > 0 fixes the
+// scenario's digit counts at compile time (A: 10 m + L, B and C: m) so every
+// per-digit loop unrolls and the state / ageing arrays live in registers
+// (with runtime bounds they were local memory: ~11% of the kernel's
+// instructions were LDL / STL); GM = 0 is the generic instantiation.
+template <int SC, int GM>
+struct Geo {
+  static constexpr int m = GM == 0 ? 0 : SC == PVI_SCENARIO_A ? GM / 10 : GM;
+  static constexpr int lead = SC == PVI_SCENARIO_A && GM > 0 ? GM % 10 : 0;
+  // TupleSpace arity: A m + L - 1, B 2 m, C m (tau + m - 1 stock digits)
+  static constexpr int arity = GM == 0 ? kMaxDigits
+                               : SC == PVI_SCENARIO_A ? m + lead - 1
+                               : SC == PVI_SCENARIO_B ? 2 * m
+                                                      : m;
+  static constexpr int cap = GM == 0 ? 14 : m + 1;  // per-digit array bound (index 1..m)
+};
+
+template <int MC>
+__device__ __forceinline__ int age_fifo_s(const int* x, int m_rt, int demand, int* next) {
+  const int m = MC > 0 ? MC : m_rt;
   const int expired = ipos(x[1] - demand);
   int prefix = 0;
-  for (int j = 1; j <= m - 1; ++j) {
+#pragma unroll
+  for (int j = 1; j <= (MC > 0 ? MC - 1 : 13); ++j) {
+    if (j > m - 1) break;
     prefix += x[j];
     next[j] = ipos(x[j + 1] - ipos(demand - prefix));
   }
   return expired;
 }
 
-__device__ __forceinline__ int age_lifo_s(const int* x, int m, int demand, int* next) {
+template <int MC>
+__device__ __forceinline__ int age_lifo_s(const int* x, int m_rt, int demand, int* next) {
+  const int m = MC > 0 ? MC : m_rt;
   int suffix = 0;
-  for (int j = 2; j <= m; ++j) suffix += x[j];
+#pragma unroll
+  for (int j = 2; j <= (MC > 0 ? MC : 14); ++j) {
+    if (j > m) break;
+    suffix += x[j];
+  }
   const int expired = ipos(x[1] - ipos(demand - suffix));
-  for (int j = 1; j <= m - 1; ++j) {
+#pragma unroll
+  for (int j = 1; j <= (MC > 0 ? MC - 1 : 13); ++j) {
+    if (j > m - 1) break;
     suffix -= x[j + 1];
     next[j] = ipos(x[j + 1] - ipos(demand - suffix));
   }
@@ -140,16 +169,20 @@ __device__ __forceinline__ int age_lifo_s(const int* x, int m, int demand, int* 
 }
 
 // ScenarioA::sample_step (scenario_a.cpp:157-189)
-__device__ void step_a(const DevModel& dm, int* state, const int* action, Rng& rng, Step& st) {
-  const int m = dm.a_m, lead = dm.a_lead, order = action[0];
-  int x[14], aged[14];
+template <int GM>
+__device__ __forceinline__ void step_a(const DevModel& dm, int* state, const int* action, Rng& rng, Step& st) {
+  using G = Geo<PVI_SCENARIO_A, GM>;
+  const int m = GM ? G::m : dm.a_m, lead = GM ? G::lead : dm.a_lead, order = action[0];
+  int x[G::cap], aged[G::cap];
   int xt = 0;
-  for (int j = 1; j <= m; ++j) {
+#pragma unroll
+  for (int j = 1; j < G::cap; ++j) {
+    if (j > m) break;
     x[j] = state[lead - 1 + m - j];
     xt += x[j];
   }
   const int demand = sample_from_cdf_guided(dm.a_cdf, dm.a_dmax + 1, dm.a_guide, rng.uniform());
-  const int expired = dm.a_lifo ? age_lifo_s(x, m, demand, aged) : age_fifo_s(x, m, demand, aged);
+  const int expired = dm.a_lifo ? age_lifo_s<G::m>(x, m, demand, aged) : age_fifo_s<G::m>(x, m, demand, aged);
   const int arriving = lead >= 2 ? state[lead - 2] : order;
   st.reward = -dm.a_cv * order - dm.a_ch * ipos(xt - demand - expired) - dm.a_cs * ipos(demand - xt) -
               dm.a_cw * expired;
@@ -158,18 +191,28 @@ __device__ void step_a(const DevModel& dm, int* state, const int* action, Rng& r
   st.expired[0] = expired;
   st.received[0] = arriving;
   st.holding[0] = ipos(xt - demand - expired);
-  for (int k = lead - 2; k >= 1; --k) state[k] = state[k - 1];
+#pragma unroll
+  for (int k = (GM ? G::lead : 14) - 2; k >= 1; --k)
+    if (k <= lead - 2) state[k] = state[k - 1];
   state[0] = order;
   if (lead >= 2) state[lead - 1] = arriving;
-  for (int j = 1; j <= m - 1; ++j) state[lead + m - 1 - j] = aged[j];
+#pragma unroll
+  for (int j = 1; j < G::cap - 1; ++j) {
+    if (j > m - 1) break;
+    state[lead + m - 1 - j] = aged[j];
+  }
 }
 
 // ScenarioB::sample_step (scenario_b.cpp:332-379)
-__device__ void step_b(const DevModel& dm, int* state, const int* action, Rng& rng, Step& st) {
-  const int m = dm.b_m;
-  int xa[10], xb[10], aa[10], ab[10];
+template <int GM>
+__device__ __forceinline__ void step_b(const DevModel& dm, int* state, const int* action, Rng& rng, Step& st) {
+  using G = Geo<PVI_SCENARIO_B, GM>;
+  const int m = GM ? G::m : dm.b_m;
+  int xa[G::cap], xb[G::cap], aa[G::cap], ab[G::cap];
   int stock_a = 0, stock_b = 0;
-  for (int j = 1; j <= m; ++j) {
+#pragma unroll
+  for (int j = 1; j < G::cap; ++j) {
+    if (j > m) break;
     xa[j] = state[m - j];
     xb[j] = state[2 * m - j];
     stock_a += xa[j];
@@ -187,8 +230,8 @@ __device__ void step_b(const DevModel& dm, int* state, const int* action, Rng& r
   const int sub = min(accepted, stock_a - own_fill_a);
   const int h_a = own_fill_a + sub;
   const int h_b = fill_b;
-  const int exp_a = age_fifo_s(xa, m, h_a, aa);
-  const int exp_b = age_fifo_s(xb, m, h_b, ab);
+  const int exp_a = age_fifo_s<G::m>(xa, m, h_a, aa);
+  const int exp_b = age_fifo_s<G::m>(xb, m, h_b, ab);
   st.reward = -(dm.b_cva * action[0] + dm.b_cvb * action[1]) + dm.b_cra * h_a + dm.b_crb * h_b;
   st.demand[0] = demand_a;
   st.demand[1] = demand_b;
@@ -199,7 +242,9 @@ __device__ void step_b(const DevModel& dm, int* state, const int* action, Rng& r
   st.received[0] = action[0];
   st.received[1] = action[1];
   int hold_a = 0, hold_b = 0;
-  for (int j = 1; j <= m - 1; ++j) {
+#pragma unroll
+  for (int j = 1; j < G::cap - 1; ++j) {
+    if (j > m - 1) break;
     hold_a += aa[j];
     hold_b += ab[j];
   }
@@ -207,7 +252,9 @@ __device__ void step_b(const DevModel& dm, int* state, const int* action, Rng& r
   st.holding[1] = hold_b;
   state[0] = action[0];
   state[m] = action[1];
-  for (int j = 1; j <= m - 1; ++j) {
+#pragma unroll
+  for (int j = 1; j < G::cap - 1; ++j) {
+    if (j > m - 1) break;
     state[m - j] = aa[j];
     state[2 * m - j] = ab[j];
   }
@@ -216,16 +263,20 @@ __device__ void step_b(const DevModel& dm, int* state, const int* action, Rng& r
 // ScenarioC::sample_step (scenario_c.cpp:313-359) with sample_multinomial
 // (rng.hpp:94-110): one uniform per category but the last, skipped once
 // nothing remains.
-__device__ void step_c(const DevModel& dm, int* state, const int* action, Rng& rng, Step& st) {
-  const int m = dm.c_m, cap = dm.c_max_order;
+template <int GM>
+__device__ __forceinline__ void step_c(const DevModel& dm, int* state, const int* action, Rng& rng, Step& st) {
+  using G = Geo<PVI_SCENARIO_C, GM>;
+  const int m = GM ? G::m : dm.c_m, cap = dm.c_max_order;
   const int tau = state[0];
   const int order = action[0];
   const double* probs = dm.c_receipt + static_cast<std::size_t>(order) * m;
-  int counts[13];
+  int counts[G::cap];
   {
     int remaining = order;
     double mass_left = 1.0;
-    for (int k = 0; k + 1 < m; ++k) {
+#pragma unroll
+    for (int k = 0; k + 1 < G::cap - 1; ++k) {
+      if (k + 1 >= m) break;
       if (remaining == 0 || mass_left <= 0.0) {
         counts[k] = 0;
         continue;
@@ -240,19 +291,31 @@ __device__ void step_c(const DevModel& dm, int* state, const int* action, Rng& r
     }
     counts[m - 1] = remaining;
   }
-  int y[14], x[14], z[14];
-  for (int j = 1; j <= m; ++j) y[j] = counts[j - 1];
+  int y[G::cap], x[G::cap], z[G::cap];
+#pragma unroll
+  for (int j = 1; j < G::cap; ++j) {
+    if (j > m) break;
+    y[j] = counts[j - 1];
+  }
   const int dn = dm.c_dmax + 1;
   const int d = sample_from_cdf_guided(dm.c_cdf + tau * dn, dn, dm.c_guide + tau * (kGuide + 1), rng.uniform());
-  for (int j = 1; j <= m - 1; ++j) x[j] = state[m - j];
+#pragma unroll
+  for (int j = 1; j < G::cap - 1; ++j) {
+    if (j > m - 1) break;
+    x[j] = state[m - j];
+  }
   int total = y[m], accepted = y[m];
-  for (int j = 1; j <= m - 1; ++j) {
+#pragma unroll
+  for (int j = 1; j < G::cap - 1; ++j) {
+    if (j > m - 1) break;
     z[j] = min(x[j] + y[j], cap);
     total += z[j];
     accepted += z[j] - x[j];
   }
   int prefix = 0;
-  for (int j = 1; j <= m - 2; ++j) {
+#pragma unroll
+  for (int j = 1; j < G::cap - 2; ++j) {
+    if (j > m - 2) break;
     prefix += z[j];
     state[m - j] = ipos(z[j + 1] - ipos(d - prefix));
   }
@@ -277,12 +340,18 @@ struct DevPolicy {
 
 // policies.hpp:18-82; scenario_a.cpp:191-195; scenario_b.cpp:381-393;
 // scenario_c.cpp:361-370
-template <int SC>
+template <int SC, int GM>
 __device__ __forceinline__ void apply_policy(const DevModel& dm, const DevPolicy& pol, const int* state,
-                                             int arity, int* action) {
+                                             int arity_rt, int* action) {
+  constexpr int AR = Geo<SC, GM>::arity;
+  const int arity = GM ? AR : arity_rt;
   if (pol.kind == 0) {
     std::uint64_t idx = 0;
-    for (int i = 0; i < arity; ++i) idx += static_cast<std::uint64_t>(state[i]) * dm.weight[i];
+#pragma unroll
+    for (int i = 0; i < AR; ++i) {
+      if (i >= arity) break;
+      idx += static_cast<std::uint64_t>(state[i]) * dm.weight[i];
+    }
     const std::uint32_t a = pol.table[idx];
     if (SC == PVI_SCENARIO_B) {
       action[0] = static_cast<int>(a) / dm.b_nb;
@@ -295,15 +364,23 @@ __device__ __forceinline__ void apply_policy(const DevModel& dm, const DevPolicy
   switch (SC) {
     case PVI_SCENARIO_A: {
       int position = 0;
-      for (int i = 0; i < arity; ++i) position += state[i];
+#pragma unroll
+      for (int i = 0; i < AR; ++i) {
+        if (i >= arity) break;
+        position += state[i];
+      }
       action[0] = ipos(pol.params[0] - position);
       return;
     }
     case PVI_SCENARIO_B: {
-      const int m = dm.b_m;
+      const int m = GM ? Geo<SC, GM>::m : dm.b_m;
       int stock_a = 0, stock_b = 0;
-      for (int i = 0; i < m; ++i) stock_a += state[i];
-      for (int i = m; i < 2 * m; ++i) stock_b += state[i];
+#pragma unroll
+      for (int i = 0; i < AR / 2; ++i) {
+        if (i >= m) break;
+        stock_a += state[i];
+        stock_b += state[m + i];
+      }
       const int expiring_a = state[m - 1];
       const int expiring_b = state[2 * m - 1];
       const double waste_a = fmax(0.0, expiring_a - dm.b_mu_a);
@@ -320,7 +397,11 @@ __device__ __forceinline__ void apply_policy(const DevModel& dm, const DevPolicy
         return;
       }
       int stock = 0;
-      for (int i = 1; i < arity; ++i) stock += state[i];
+#pragma unroll
+      for (int i = 1; i < AR; ++i) {
+        if (i >= arity) break;
+        stock += state[i];
+      }
       action[0] = stock > s ? 0 : ipos(S - stock);
       return;
     }
@@ -335,20 +416,26 @@ struct SimError {
   int state[kMaxDigits];
 };
 
-// rollout (sim.hpp:68-124); one instantiation per scenario (SC), so each
-// carries only its own step function and policy arithmetic
-template <int SC, int MINB>
+// rollout (sim.hpp:68-124); one instantiation per scenario (SC) and
+// geometry (GM, see Geo), so each carries only its own step function and
+// policy arithmetic with its digit loops unrolled.  The KPI counts are
+// summed in 32-bit registers and folded into the 64-bit totals every 4096
+// measured days (a day adds at most a few hundred units), the same integers.
+template <int SC, int MINB, int GM>
 __global__ void __launch_bounds__(128, MINB) k_rollouts(DevModel dm, const DevPolicy* __restrict__ pols,
                                                   int n_rollouts, int horizon, int warmup,
-                                                  std::uint64_t base_seed, int arity, int products,
+                                                  std::uint64_t base_seed, int arity_rt, int products,
                                                   double gamma, double* __restrict__ out,
                                                   SimError* err, unsigned long long* blocks_out) {
+  using G = Geo<SC, GM>;
+  const int arity = GM ? G::arity : arity_rt;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int p = blockIdx.y;
   if (i >= n_rollouts) return;
   const DevPolicy pol = pols[p];
-  int state[kMaxDigits];
-  for (int k = 0; k < arity; ++k) state[k] = 0;
+  int state[G::arity];
+#pragma unroll
+  for (int k = 0; k < G::arity; ++k) state[k] = 0;
   int action[2] = {0, 0};
   int bound[2];
   if (SC == PVI_SCENARIO_B) {
@@ -358,14 +445,31 @@ __global__ void __launch_bounds__(128, MINB) k_rollouts(DevModel dm, const DevPo
     bound[0] = bound[1] = static_cast<int>(dm.n_actions) - 1;
   }
   constexpr int action_arity = SC == PVI_SCENARIO_B ? 2 : 1;
+  constexpr int NP = SC == PVI_SCENARIO_B ? 2 : 1;  // products
+  (void)products;
   Rng rng(base_seed, static_cast<std::uint64_t>(i));
   const int total_days = warmup + horizon;
   double ret = 0.0, weight = 1.0;
   unsigned long long blocks = 0;
   long long demand[2] = {0, 0}, filled[2] = {0, 0}, expired[2] = {0, 0}, received[2] = {0, 0},
             holding[2] = {0, 0};
+  int d32[NP], f32[NP], e32[NP], r32[NP], h32[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) d32[k] = f32[k] = e32[k] = r32[k] = h32[k] = 0;
+  auto fold = [&]() {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      demand[k] += d32[k];
+      filled[k] += f32[k];
+      expired[k] += e32[k];
+      received[k] += r32[k];
+      holding[k] += h32[k];
+      d32[k] = f32[k] = e32[k] = r32[k] = h32[k] = 0;
+    }
+  };
   for (int day = 0; day < total_days; ++day) {
-    apply_policy<SC>(dm, pol, state, arity, action);
+    apply_policy<SC, GM>(dm, pol, state, arity, action);
+#pragma unroll
     for (int k = 0; k < action_arity; ++k) {
       if (action[k] < 0 || action[k] > bound[k]) {
         const unsigned long long key = static_cast<unsigned long long>(p) * n_rollouts + i;
@@ -383,29 +487,34 @@ __global__ void __launch_bounds__(128, MINB) k_rollouts(DevModel dm, const DevPo
     rng.begin_day(static_cast<std::uint32_t>(day));
     Step st;
     st.reward = 0.0;
+#pragma unroll
     for (int k = 0; k < 2; ++k)
       st.demand[k] = st.filled[k] = st.expired[k] = st.received[k] = st.holding[k] = 0;
-    if constexpr (SC == PVI_SCENARIO_A) step_a(dm, state, action, rng, st);
-    else if constexpr (SC == PVI_SCENARIO_B) step_b(dm, state, action, rng, st);
-    else step_c(dm, state, action, rng, st);
+    if constexpr (SC == PVI_SCENARIO_A) step_a<GM>(dm, state, action, rng, st);
+    else if constexpr (SC == PVI_SCENARIO_B) step_b<GM>(dm, state, action, rng, st);
+    else step_c<GM>(dm, state, action, rng, st);
     if (day >= warmup) {
       ret += weight * st.reward;
       weight *= gamma;
-      for (int k = 0; k < products; ++k) {
-        demand[k] += st.demand[k];
-        filled[k] += st.filled[k];
-        expired[k] += st.expired[k];
-        received[k] += st.received[k];
-        holding[k] += st.holding[k];
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        d32[k] += st.demand[k];
+        f32[k] += st.filled[k];
+        e32[k] += st.expired[k];
+        r32[k] += st.received[k];
+        h32[k] += st.holding[k];
       }
+      if (((day - warmup) & 4095) == 4095) fold();
     }
   }
+  fold();
   if (blocks_out) atomicAdd(blocks_out, blocks + rng.draw);
   double* o = out + (static_cast<std::size_t>(p) * n_rollouts + i) * 7;
   o[0] = ret;
+#pragma unroll
   for (int k = 0; k < 2; ++k) {
     double svc = 100.0, wst = 0.0, hold = 0.0;
-    if (k < products) {
+    if (k < NP) {
       svc = demand[k] > 0 ? 100.0 * static_cast<double>(filled[k]) / static_cast<double>(demand[k]) : 100.0;
       wst = received[k] > 0 ? 100.0 * static_cast<double>(expired[k]) / static_cast<double>(received[k]) : 0.0;
       hold = horizon > 0 ? static_cast<double>(holding[k]) / horizon : 0.0;
@@ -535,18 +644,26 @@ void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_po
   PVI_CUDA(cudaMemcpyAsync(derr.p, &herr, sizeof(herr), cudaMemcpyHostToDevice, stream));
   const dim3 grid((cfg.n_rollouts + 127) / 128, n_policies);
   // CTAs per SM the register allocation is bounded for (measured per
-  // scenario on a B200: A 3, B 4, C 1; PVI_SIM_MINB overrides)
-  static const int minb_env = [] {
-    const char* e = std::getenv("PVI_SIM_MINB");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int minb = minb_env > 0 ? minb_env
-                   : m.scenario == PVI_SCENARIO_A ? 3 : m.scenario == PVI_SCENARIO_B ? 4 : 1;
-#define PVI_KR(MB)                                                                                   \
-  (m.scenario == PVI_SCENARIO_A ? k_rollouts<PVI_SCENARIO_A, MB>                                    \
-   : m.scenario == PVI_SCENARIO_B ? k_rollouts<PVI_SCENARIO_B, MB> : k_rollouts<PVI_SCENARIO_C, MB>)
-  auto kr = minb >= 5 ? PVI_KR(5) : minb >= 4 ? PVI_KR(4) : minb >= 3 ? PVI_KR(3) : minb >= 2 ? PVI_KR(2) : PVI_KR(1);
+  // scenario on a B200: A 3, B 4, C 1)
+  // geometry of the compiled instantiations (Geo): A 10 m + L, B / C m
+  const int gm = m.scenario == PVI_SCENARIO_A ? 10 * m.pa.useful_life + m.pa.lead_time
+                 : m.scenario == PVI_SCENARIO_B ? m.pb.useful_life
+                                                : m.pc.useful_life;
+  using KR = void (*)(DevModel, const DevPolicy*, int, int, int, std::uint64_t, int, int, double, double*,
+                      SimError*, unsigned long long*);
+  KR kr = nullptr;
+#define PVI_KR(SCN, MB, GMV) \
+  if (!kr && m.scenario == SCN && gm == GMV) kr = k_rollouts<SCN, MB, GMV>;
+  PVI_KR(PVI_SCENARIO_A, 3, 21) PVI_KR(PVI_SCENARIO_A, 3, 22) PVI_KR(PVI_SCENARIO_A, 3, 31)
+  PVI_KR(PVI_SCENARIO_A, 3, 32) PVI_KR(PVI_SCENARIO_A, 3, 41) PVI_KR(PVI_SCENARIO_A, 3, 42)
+  PVI_KR(PVI_SCENARIO_A, 3, 51) PVI_KR(PVI_SCENARIO_A, 3, 52)
+  PVI_KR(PVI_SCENARIO_B, 4, 2) PVI_KR(PVI_SCENARIO_B, 4, 3)
+  PVI_KR(PVI_SCENARIO_C, 1, 3) PVI_KR(PVI_SCENARIO_C, 1, 5)
 #undef PVI_KR
+  if (!kr)
+    kr = m.scenario == PVI_SCENARIO_A ? k_rollouts<PVI_SCENARIO_A, 1, 0>
+         : m.scenario == PVI_SCENARIO_B ? k_rollouts<PVI_SCENARIO_B, 1, 0>
+                                        : k_rollouts<PVI_SCENARIO_C, 1, 0>;
   static const bool trace = [] {
     const char* e = std::getenv("PVI_SIM_TRACE");
     return e && e[0] == '1';
