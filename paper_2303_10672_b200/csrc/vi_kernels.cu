@@ -3655,8 +3655,8 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
           const int rx = dm.a_max_order + 1;
           const std::uint64_t g0 = lo / rx, g1 = (hi + rx - 1) / rx;
 #define PVI_AL(ML)                                                                                   \
-  if (!spec && ml == ML) {                                                                           \
-    k_a_fact_lifo<T, 16, ML><<<grid_for(g1 - g0, 128), 128, smf, stream>>>(dm, a.v, dc.a_reward, dc.a_cdf_sf, \
+  if (!spec && ml == ML && na == 11) {  /* A_max = 10: every preset */                              \
+    k_a_fact_lifo<T, 11, ML><<<grid_for(g1 - g0, 128), 128, smf, stream>>>(dm, a.v, dc.a_reward, dc.a_cdf_sf, \
         dc.a_pd, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, fa);                             \
     spec = true;                                                                                     \
   }
@@ -3674,8 +3674,8 @@ void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
           const std::uint64_t n_groups = dm.n_states / (static_cast<std::uint64_t>(rx) * rx);
           const std::uint64_t n_thr = n_groups * (2 * rx - 1);
 #define PVI_AD(ML)                                                                                   \
-  if (!spec && ml == ML) {                                                                           \
-    k_a_fact_fifo<T, 16, ML><<<grid_for(n_thr, 128), 128, smf, stream>>>(dm, a.v, dc.a_reward, dc.a_cdf_sf, \
+  if (!spec && ml == ML && na == 11) {                                                               \
+    k_a_fact_fifo<T, 11, ML><<<grid_for(n_thr, 128), 128, smf, stream>>>(dm, a.v, dc.a_reward, dc.a_cdf_sf, \
         dc.a_pd, a.vout, a.act, a.qout, lo, hi, a.out_off, a.gamma, n_groups, fa);                   \
     spec = true;                                                                                     \
   }
