@@ -2332,6 +2332,34 @@ __global__ void __launch_bounds__(896, 1) k_c_bin_tile_p(const double* __restric
   }
 }
 
+// One (order a, weekday, line) item of a binomial pass: decoded by one
+// thread and broadcast through shared memory (every warp decoding it was
+// ~17% of k_c_bin_diag's instructions: runtime divisions).
+struct CItem {
+  int a, nb, tau;
+  std::uint32_t rest0, wk;
+};
+__device__ __forceinline__ CItem c_item_decode(int i, int endo, int R, int n_tau, int n_lines, int tau0, int m,
+                                               int k) {
+  CItem it;
+  const int ai = i / (n_tau * n_lines), rem = i % (n_tau * n_lines);
+  it.a = endo ? R - 1 - ai : 0;  // heavy orders first
+  it.nb = endo ? it.a + 1 : R;
+  it.tau = tau0 + rem / n_lines;
+  it.rest0 = 0;
+  it.wk = 1;
+  std::uint32_t o = static_cast<std::uint32_t>(rem % n_lines), w = 1;
+  for (int p = 1; p <= m - 1; ++p) {
+    if (p == k) it.wk = w;
+    if (p != 1 && p != k) {
+      it.rest0 += (o % static_cast<std::uint32_t>(R)) * w;
+      o /= static_cast<std::uint32_t>(R);
+    }
+    w *= static_cast<std::uint32_t>(R);
+  }
+  return it;
+}
+
 // The same pass by anti-diagonals, with the inputs in registers (round 2).
 // Output (b, d_k) of a pass reads in[b - y][min(d_k + y, cap)] for y <= b:
 // every term lies on the anti-diagonal c = b + d_k once the capped column is
@@ -2356,23 +2384,12 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag(const double* __restrict_
                                                       int n_lines, int tau0, int n_tau) {
   constexpr int R = RC, CAP = RC - 1;
   __shared__ double s_w[R * R];  // [b][y] = Bin(y; b, q_k(a))
-  const int i = static_cast<int>(blockIdx.x);
-  const int ai = i / (n_tau * n_lines), rem = i % (n_tau * n_lines);
-  const int a = endo ? R - 1 - ai : 0;  // heavy orders first
-  const int nb = endo ? a + 1 : R;
-  const int tau = tau0 + rem / n_lines;
-  std::uint32_t rest0 = 0, wk = 1;
-  {
-    std::uint32_t o = static_cast<std::uint32_t>(rem % n_lines), w = 1;
-    for (int p = 1; p <= m - 1; ++p) {
-      if (p == k) wk = w;
-      if (p != 1 && p != k) {
-        rest0 += (o % static_cast<std::uint32_t>(R)) * w;
-        o /= static_cast<std::uint32_t>(R);
-      }
-      w *= static_cast<std::uint32_t>(R);
-    }
-  }
+  __shared__ CItem s_item;
+  if (threadIdx.x == 0)
+    s_item = c_item_decode(static_cast<int>(blockIdx.x), endo, R, n_tau, n_lines, tau0, m, k);
+  __syncthreads();
+  const int a = s_item.a, nb = s_item.nb, tau = s_item.tau;
+  const std::uint32_t rest0 = s_item.rest0, wk = s_item.wk;
   const std::size_t out_base = endo ? c_tri_base(a, wb) + static_cast<std::size_t>(tau) * nb * wb
                                     : static_cast<std::size_t>(tau) * n_prof;
   const std::size_t in_base = (endo && !in_is_g) ? out_base : static_cast<std::size_t>(tau) * n_prof;
@@ -2436,23 +2453,11 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag_q(DevModel dm, const doub
   __shared__ double s_w1[R];     // Bin(y; a, q_1(a))
   __shared__ double s_pd;
   extern __shared__ double s_tile[];  // H_2 [b <= a][x_2][x_1]
-  const int i = static_cast<int>(blockIdx.x);
-  const int ai = i / (n_tau * n_lines), rem = i % (n_tau * n_lines);
-  const int a = R - 1 - ai;  // heavy orders first
-  const int nb = a + 1;
-  const int tau = tau0 + rem / n_lines;
-  std::uint32_t rest0 = 0, wk = 1;
-  {
-    std::uint32_t o = static_cast<std::uint32_t>(rem % n_lines), w = 1;
-    for (int p = 1; p <= m - 1; ++p) {
-      if (p == k) wk = w;
-      if (p != 1 && p != k) {
-        rest0 += (o % static_cast<std::uint32_t>(R)) * w;
-        o /= static_cast<std::uint32_t>(R);
-      }
-      w *= static_cast<std::uint32_t>(R);
-    }
-  }
+  __shared__ CItem s_item;
+  if (threadIdx.x == 0) s_item = c_item_decode(static_cast<int>(blockIdx.x), 1, R, n_tau, n_lines, tau0, m, k);
+  __syncthreads();
+  const int a = s_item.a, nb = s_item.nb, tau = s_item.tau;
+  const std::uint32_t rest0 = s_item.rest0, wk = s_item.wk;
   const std::size_t in_base = in_is_g ? static_cast<std::size_t>(tau) * n_prof
                                       : c_tri_base(a, wb) + static_cast<std::size_t>(tau) * nb * wb;
   const double* bt = binom_k + a * binom_a_stride;
@@ -2531,20 +2536,12 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag_qf(DevModel dm, const dou
   __shared__ double s_w1[R * R];  // [a][y] = Bin(y; a, q_1(a))
   __shared__ double s_pd;
   extern __shared__ double s_tile[];  // H_2 [b][x_2][x_1]
-  const int i = static_cast<int>(blockIdx.x);
-  const int tau = tau0 + i / n_lines;
-  std::uint32_t rest0 = 0, wk = 1;
-  {
-    std::uint32_t o = static_cast<std::uint32_t>(i % n_lines), w = 1;
-    for (int p = 1; p <= m - 1; ++p) {
-      if (p == k) wk = w;
-      if (p != 1 && p != k) {
-        rest0 += (o % static_cast<std::uint32_t>(R)) * w;
-        o /= static_cast<std::uint32_t>(R);
-      }
-      w *= static_cast<std::uint32_t>(R);
-    }
-  }
+  __shared__ CItem s_item;
+  if (threadIdx.x == 0) s_item = c_item_decode(static_cast<int>(blockIdx.x), 0, R,
+                                             static_cast<int>(gridDim.x) / n_lines, n_lines, tau0, m, k);
+  __syncthreads();
+  const int tau = s_item.tau;
+  const std::uint32_t rest0 = s_item.rest0, wk = s_item.wk;
   const std::size_t in_base = static_cast<std::size_t>(tau) * n_prof;
   (void)in_is_g;
   for (int t = threadIdx.x; t < PLANE; t += blockDim.x) {
