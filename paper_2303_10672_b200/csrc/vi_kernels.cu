@@ -2432,14 +2432,202 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag(const double* __restrict_
   }
 }
 
+// Passes k >= 3 with x_2 batched beside x_1, on the FP64 tensor cores
+// (round 2).  k_c_bin_diag's items read and write rows of 21 doubles (168 B)
+// scattered at the pass stride.  For k >= 3 the two lowest digits (x_1,
+// x_2) are both outside the pass and adjacent in memory, so a CTA takes one
+// (order a, tau, line without x_1, x_2, x_k) item, half of its 441 (x_2,
+// x_1) columns and a range of anti-diagonals c: every row it reads or
+// writes is contiguous (a copy with this row pattern moves the pass's 5 GB
+// at 6.3 TB/s, tools/c_pattern_peak.cu).  c is CTA-uniform (the item is
+// decoded by every thread from blockIdx), so the row window is a uniform
+// branch.  A scalar version of this kernel (thread = column, the diag
+// kernel's unrolled triangle) ran no faster than k_c_bin_diag (1.33 ms,
+// 1.1e9 instructions: ~10 issue slots per useful multiply-add in row
+// guards, weight broadcasts and addressing).  So the arithmetic goes to
+// DMMA:
+constexpr int C_WIDE_CHUNKS_ENDO = 2;  // anti-diagonal ranges per item
+
+// on one anti-diagonal c the pass is a lower-triangular product out[b] = sum_{b' <=
+// b} L[b][b'] v[b'] (L[b][b'] = Bin(b - b'; b, q_k(a)), v[b'] = in_ext[b'][c
+// - b']) applied to every column, so a warp takes 32 columns (4 n-tiles of
+// mma.sync m8n8k4 f64) per anti-diagonal: 24 B-fragment loads per lane
+// straight from the rows, L's fragments from shared memory (shared by the 4
+// n-tiles), and only the row tiles that meet c's window and the k-steps
+// below them are issued.  DMMA's summation order: within rounding of
+// k_c_bin_diag (the factored contract).
+__device__ __forceinline__ void dmma_884_nv(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+constexpr int C_WMMA_THREADS = 224;  // 7 warps x 32 columns; two CTAs per item cover the 441 columns
+
+template <int RC>
+__global__ void __launch_bounds__(C_WMMA_THREADS, 3) k_c_bin_wide_mma(
+    const double* __restrict__ Hin, double* __restrict__ Hout, const double* __restrict__ binom_k,
+    std::size_t binom_a_stride, int m, int k, std::uint32_t wb, int endo, int in_is_g, int n_prof, int n_lines,
+    int tau0, int n_tau, int n_chunks) {
+  constexpr int R = RC, CAP = RC - 1, PL = RC * RC;
+  constexpr int MT = (R + 7) / 8, KS = (R + 3) / 4, NT = 4;  // 3 row tiles, 6 k-steps, 4 column tiles
+  __shared__ double s_wa[MT * KS * 32];  // [t][s][lane] = L[8 t + lane / 4][4 s + lane % 4]
+  int blk = static_cast<int>(blockIdx.x);
+  const int chunk = blk % n_chunks;
+  blk /= n_chunks;
+  const int half = blk & 1;
+  blk >>= 1;
+  const int ai = blk / (n_tau * n_lines), rem = blk - ai * (n_tau * n_lines);
+  const int a = endo ? R - 1 - ai : 0;  // heavy orders first
+  const int nb = endo ? a + 1 : R;
+  const int tau = tau0 + rem / n_lines;
+  std::uint32_t rest0 = 0, wk = 1;
+  {
+    std::uint32_t o = static_cast<std::uint32_t>(rem % n_lines), w = 1;
+    for (int p = 1; p <= m - 1; ++p) {
+      if (p == k) wk = w;
+      if (p > 2 && p != k) {
+        rest0 += (o % static_cast<std::uint32_t>(R)) * w;
+        o /= static_cast<std::uint32_t>(R);
+      }
+      w *= static_cast<std::uint32_t>(R);
+    }
+  }
+  const std::size_t out_base = endo ? c_tri_base(a, wb) + static_cast<std::size_t>(tau) * nb * wb
+                                    : static_cast<std::size_t>(tau) * n_prof;
+  const std::size_t in_base = (endo && !in_is_g) ? out_base : static_cast<std::size_t>(tau) * n_prof;
+  const double* bt = binom_k + a * binom_a_stride;
+  for (int e = threadIdx.x; e < MT * KS * 32; e += blockDim.x) {
+    const int t = e / (KS * 32), sk = (e / 32) % KS, ln = e & 31;
+    const int b = 8 * t + (ln >> 2), bp = 4 * sk + (ln & 3);
+    s_wa[e] = (bp <= b && b < nb) ? bt[b * R + (b - bp)] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int cb = half * C_WMMA_THREADS + warp * 32;  // this warp's first column
+  if (cb >= PL) return;
+  const double* src = Hin + in_base + rest0;
+  double* dst = Hout + out_base + rest0;
+  const int n_c = CAP + nb;
+  const int per = (n_c + n_chunks - 1) / n_chunks;
+  const int c_lo = chunk * per, c_hi = min(n_c, c_lo + per);
+  const int colb = cb + fr;  // B-fragment column of n-tile 0
+  const int colo = cb + 2 * fc;  // D-fragment column of n-tile 0
+  for (int c = c_lo; c < c_hi; ++c) {
+    const int lo = max(0, c - CAP), hi = min(c, nb - 1);
+    double vb[KS][NT];
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      const int bp = 4 * s + fc;
+      const double* row = src + (static_cast<std::uint32_t>(bp) * wb +
+                                 static_cast<std::uint32_t>(min(c - bp, CAP)) * wk + static_cast<std::uint32_t>(colb));
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        vb[s][j] = 0.0;
+        if (4 * s <= hi && bp <= hi && colb + 8 * j < PL) vb[s][j] = __ldg(row + 8 * j);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      if (8 * t > hi || 8 * t + 7 < lo) continue;  // CTA-uniform
+      double d[NT][2];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) d[j][0] = d[j][1] = 0.0;
+#pragma unroll
+      for (int s = 0; s < KS; ++s)
+        if (4 * s <= 8 * t + 7 && 4 * s <= hi) {
+          const double w = s_wa[(t * KS + s) * 32 + lane];
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma_884_nv(d[j][0], d[j][1], w, vb[s][j]);
+        }
+      const int b = 8 * t + fr;
+      if (b >= lo && b <= hi) {
+        double* o = dst + (static_cast<std::uint32_t>(b) * wb + static_cast<std::uint32_t>(c - b) * wk +
+                           static_cast<std::uint32_t>(colo));
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          if (colo + 8 * j < PL) o[8 * j] = d[j][0];
+          if (colo + 8 * j + 1 < PL) o[8 * j + 1] = d[j][1];
+        }
+      }
+    }
+  }
+}
+
+// The k = 2 pass of an item into its shared-memory tile on the FP64 tensor
+// cores (the same lower-triangular product per anti-diagonal as
+// k_c_bin_wide_mma; for k = 2 the item's input planes [d_2][x_1] are 3.5 KB
+// contiguous).  A warp takes one anti-diagonal c and the 21 columns x_1 as 3
+// n-tiles.  s_wa: L's fragments of this item's order (c_pass_fragments).
+template <int R>
+__device__ __forceinline__ void c_pass_fragments(const double* __restrict__ bt, int nb, double* s_wa) {
+  constexpr int MT = (R + 7) / 8, KS = (R + 3) / 4;
+  for (int e = threadIdx.x; e < MT * KS * 32; e += blockDim.x) {
+    const int t = e / (KS * 32), sk = (e / 32) % KS, ln = e & 31;
+    const int b = 8 * t + (ln >> 2), bp = 4 * sk + (ln & 3);
+    s_wa[e] = (bp <= b && b < nb) ? bt[b * R + (b - bp)] : 0.0;
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void c_pass_tile_mma(const double* __restrict__ src, std::uint32_t wb, std::uint32_t wk,
+                                                int nb, const double* s_wa, double* s_tile) {
+  constexpr int CAP = R - 1, PLANE = R * R;
+  constexpr int MT = (R + 7) / 8, KS = (R + 3) / 4, NG = (R + 7) / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n_warps = blockDim.x >> 5;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int n_c = CAP + nb;
+  for (int c = warp; c < n_c; c += n_warps) {
+    const int lo = max(0, c - CAP), hi = min(c, nb - 1);
+    double vb[KS][NG];
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      const int bp = 4 * s + fc;
+      const double* row = src + (static_cast<std::uint32_t>(bp) * wb +
+                                 static_cast<std::uint32_t>(min(c - bp, CAP)) * wk + static_cast<std::uint32_t>(fr));
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        vb[s][g] = 0.0;
+        if (4 * s <= hi && bp <= hi && 8 * g + fr < R) vb[s][g] = __ldg(row + 8 * g);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      if (8 * t > hi || 8 * t + 7 < lo) continue;  // warp-uniform
+      double d[NG][2];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) d[g][0] = d[g][1] = 0.0;
+#pragma unroll
+      for (int s = 0; s < KS; ++s)
+        if (4 * s <= 8 * t + 7 && 4 * s <= hi) {
+          const double w = s_wa[(t * KS + s) * 32 + lane];
+#pragma unroll
+          for (int g = 0; g < NG; ++g) dmma_884_nv(d[g][0], d[g][1], w, vb[s][g]);
+        }
+      const int b = 8 * t + fr;
+      if (b >= lo && b <= hi) {
+        double* o = s_tile + b * PLANE + (c - b) * R + 2 * fc;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+          const int xo = 8 * g + 2 * fc;
+          if (xo < R) o[8 * g] = d[g][0];
+          if (xo + 1 < R) o[8 * g + 1] = d[g][1];
+        }
+      }
+    }
+  }
+}
+
 // Endogenous C: the last binomial pass (k = 2) fused with the Q pass (k = 1,
 // only b = a).  An item (order a, tau, x_3..x_{m-1}) of pass 2 produces the
 // whole [b <= a][x_2][x_1] tile of H_2 that the Q of its 441 states
 // (x_2, x_1) reads, so the tile goes to shared memory instead of HBM and the
 // same CTA finishes the states' Q for order a: k_c_bin_q's terms in its
 // order, fixed(a) PD(tau) + sum_y Bin(y; a, q_1(a)) H_2[a - y][x_2][min(x_1 +
-// y, cap)] -- the same bits -- without writing H_2 (2.5 GB for c/m5/exp2)
-// and reading it back.
+// y, cap)], without writing H_2 (2.5 GB for c/m5/exp2) and reading it back.
+// The pass itself runs on DMMA (c_pass_tile_mma): 1.52 -> 1.40 ms,
+// 1.0e9 -> 7.9e8 instructions.
 template <typename T, int RC>
 __global__ void __launch_bounds__(448, 2) k_c_bin_diag_q(DevModel dm, const double* __restrict__ Hin,
                                                         const double* __restrict__ binom_k,
@@ -2449,7 +2637,6 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag_q(DevModel dm, const doub
                                                         std::uint64_t lo, std::uint64_t hi) {
   constexpr int R = RC, CAP = RC - 1, PLANE = R * R;
   constexpr int k = 2;
-  __shared__ double s_w[R * R];  // [b][y] = Bin(y; b, q_2(a))
   __shared__ double s_w1[R];     // Bin(y; a, q_1(a))
   __shared__ double s_pd;
   extern __shared__ double s_tile[];  // H_2 [b <= a][x_2][x_1]
@@ -2461,7 +2648,8 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag_q(DevModel dm, const doub
   const std::size_t in_base = in_is_g ? static_cast<std::size_t>(tau) * n_prof
                                       : c_tri_base(a, wb) + static_cast<std::size_t>(tau) * nb * wb;
   const double* bt = binom_k + a * binom_a_stride;
-  for (int t = threadIdx.x; t < nb * R; t += blockDim.x) s_w[t] = bt[t];
+  __shared__ double s_wa[18 * 32];  // L's DMMA fragments (c_pass_fragments)
+  c_pass_fragments<R>(bt, nb, s_wa);
   if (threadIdx.x < R)  // pass 1's weights of order a: c_binom[a][0][a][y]
     s_w1[threadIdx.x] = dm.c_binom[(static_cast<std::size_t>(a) * (m - 1) * R + a) * R + threadIdx.x];
   if (threadIdx.x == 0) {
@@ -2471,33 +2659,8 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag_q(DevModel dm, const doub
     s_pd = pd;
   }
   __syncthreads();
-  const int n_combo = (CAP + nb) * R;
   const double* src = Hin + in_base + rest0;
-  for (int combo = threadIdx.x; combo < n_combo; combo += blockDim.x) {
-    const int c = combo / R, x1 = combo - (combo / R) * R;
-    const int hi_in = min(c, nb - 1);
-    const int lo_out = max(0, c - CAP);
-    double v[R];
-    std::uint32_t off = static_cast<std::uint32_t>(x1) + static_cast<std::uint32_t>(CAP) * wk;
-#pragma unroll
-    for (int bp = 0; bp < R; ++bp) {
-      if (bp <= hi_in) {
-        const std::uint32_t o = bp < c - CAP ? off : off + static_cast<std::uint32_t>(c - bp - CAP) * wk;
-        v[bp] = __ldg(src + o);
-      }
-      off += wb;
-    }
-#pragma unroll
-    for (int b = 0; b < R; ++b) {
-      if (b >= lo_out && b <= hi_in) {
-        const double* w = s_w + b * R;
-        double acc = 0.0;
-#pragma unroll
-        for (int y = 0; y <= b; ++y) acc = fma(w[y], v[b - y], acc);
-        s_tile[b * PLANE + (c - b) * R + x1] = acc;
-      }
-    }
-  }
+  c_pass_tile_mma<R>(src, wb, wk, nb, s_wa, s_tile);
   __syncthreads();
   // Q of order a for the line's states (x_2, x_1): s = tau wb + rest0 + x_2 r + x_1
   const std::uint64_t nr = hi - lo;
@@ -2557,8 +2720,8 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag_qf(DevModel dm, const dou
   }
   __syncthreads();
   constexpr int nb = R;
-  const int n_combo = (CAP + nb) * R;
   const double* src = Hin + in_base + rest0;
+  const int n_combo = (CAP + nb) * R;
   for (int combo = threadIdx.x; combo < n_combo; combo += blockDim.x) {
     const int c = combo / R, x1 = combo - (combo / R) * R;
     const int hi_in = min(c, nb - 1);
@@ -3511,8 +3674,9 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
           const int n_lines = static_cast<int>(wb / (static_cast<std::uint32_t>(r) * r));
           const int n_items = r * n_tau * n_lines;
           const std::size_t smt = static_cast<std::size_t>(r) * r * r * sizeof(double);
-          cudaFuncSetAttribute(k_c_bin_diag_q<T, 21>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-          k_c_bin_diag_q<T, 21><<<static_cast<unsigned>(n_items), 448, smt, stream>>>(
+          auto kq = k_c_bin_diag_q<T, 21>;
+          cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+          kq<<<static_cast<unsigned>(n_items), 448, smt, stream>>>(
               dm, src, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, a_stride, M, wb, src == G ? 1 : 0,
               static_cast<int>(n_prof), n_lines, tau0, n_tau, pv, a.qout, lo, hi);
           q_fused = true;
@@ -3520,14 +3684,22 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
           // the last exogenous pass fused with Q, the max over the orders and the finalize
           const int n_lines = static_cast<int>(wb / (static_cast<std::uint32_t>(r) * r));
           const std::size_t smt = static_cast<std::size_t>(r) * r * r * sizeof(double);
-          cudaFuncSetAttribute(k_c_bin_diag_qf<T, 21>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-          k_c_bin_diag_qf<T, 21><<<static_cast<unsigned>(n_tau * n_lines), 448, smt, stream>>>(
+          auto kqf = k_c_bin_diag_qf<T, 21>;  // (a DMMA pass here measured no faster: 0.633 vs 0.629 ms/sweep)
+          cudaFuncSetAttribute(kqf, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+          kqf<<<static_cast<unsigned>(n_tau * n_lines), 448, smt, stream>>>(
               dm, src, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, M, wb, src == G ? 1 : 0,
               static_cast<int>(n_prof), n_lines, tau0, a.v, a.vout, a.act, a.qout, lo, hi, a.out_off, a.fa);
           q_fused = qf_fused = true;
         } else if (r == 21) {  // every C preset: the anti-diagonal pass
           const int n_lines = static_cast<int>(wb / (static_cast<std::uint32_t>(r) * r));
           const int n_items = (endo ? r : 1) * n_tau * n_lines;
+          if (endo && k >= 3) {  // x_2 batched beside x_1, DMMA
+            const int n_lines2 = n_lines / r;
+            k_c_bin_wide_mma<21><<<static_cast<unsigned>(r * n_tau * n_lines2 * 2 * C_WIDE_CHUNKS_ENDO),
+                                   C_WMMA_THREADS, 0, stream>>>(
+                src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, a_stride, M, k, wb, 1,
+                src == G ? 1 : 0, static_cast<int>(n_prof), n_lines2, tau0, n_tau, C_WIDE_CHUNKS_ENDO);
+          } else  // exogenous passes: measured faster than the wide kernel (0.63 vs 0.65 ms per c/m5/exp1 sweep)
           k_c_bin_diag<21><<<static_cast<unsigned>(n_items), 448, 0, stream>>>(
               src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, endo ? a_stride : 0, M, k, wb,
               endo ? 1 : 0, src == G ? 1 : 0, static_cast<int>(n_prof), n_lines, tau0, n_tau);
