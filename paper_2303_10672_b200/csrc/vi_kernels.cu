@@ -561,6 +561,8 @@ __global__ void __launch_bounds__(256) k_a_reward(DevModel dm, double* __restric
   out[s] = acc;
 }
 
+__host__ __device__ constexpr std::uint64_t a_pow(std::uint64_t r, int e) { return e <= 0 ? 1 : r * a_pow(r, e - 1); }
+
 // LIFO: the carried stock's fate does not depend on the oldest bucket x_1
 // (it is used last and expires anyway), so U(s, .) is shared by the
 // A_max + 1 states that differ only in x_1 -- consecutive indices, since x_1
@@ -581,7 +583,10 @@ __global__ void __launch_bounds__(128) k_a_fact_lifo(DevModel dm, const T* __res
   for (int i = threadIdx.x; i < dn; i += blockDim.x) s_pmf[i] = dm.a_pmf[i];
   for (int i = threadIdx.x; i <= dn; i += blockDim.x) s_sf[i] = cdf_sf[dn + i];
   __syncthreads();
-  const int rx = dm.a_max_order + 1;  // radix of x_1
+  // ML != 0: launched with na == NA == A_max + 1, the radix of every digit,
+  // so the action count, the digit weights and the order stride are constants
+  constexpr bool FIXED = ML != 0;
+  const int rx = FIXED ? NA : dm.a_max_order + 1;  // radix of x_1
   const std::uint64_t g = lo / rx + static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   double smax = -DBL_MAX, smin = DBL_MAX;
   unsigned long long bad = ~0ull;
@@ -589,8 +594,9 @@ __global__ void __launch_bounds__(128) k_a_fact_lifo(DevModel dm, const T* __res
   if (s0 < hi) {
     constexpr int MC = ML / 10, LC = ML % 10;
     const int m = ML ? MC : dm.a_m, lead = ML ? LC : dm.a_lead;
-    const int na = static_cast<int>(dm.n_actions);
+    const int na = FIXED ? NA : static_cast<int>(dm.n_actions);
     constexpr int ND = ML ? MC + LC - 1 : kMaxDigits;
+    auto wgt = [&](int k) -> std::uint64_t { return FIXED ? a_pow(NA, ND - 1 - k) : dm.weight[k]; };
     int st[ND];
     if (ML) {
       const std::uint32_t r = static_cast<std::uint32_t>(rx);
@@ -612,16 +618,16 @@ __global__ void __launch_bounds__(128) k_a_fact_lifo(DevModel dm, const T* __res
     }
     std::uint64_t base_static = 0;
 #pragma unroll
-    for (int k = 1; k <= lead - 2; ++k) base_static += st[k - 1] * dm.weight[k];
-    if (lead >= 2) base_static += st[lead - 2] * dm.weight[lead - 1];
-    const std::uint64_t w0 = dm.weight[0];
+    for (int k = 1; k <= lead - 2; ++k) base_static += st[k - 1] * wgt(k);
+    if (lead >= 2) base_static += st[lead - 2] * wgt(lead - 1);
+    const std::uint64_t w0 = wgt(0);
     double u[NA];
 #pragma unroll
     for (int a = 0; a < NA; ++a) u[a] = 0.0;
     for (int d = 0; d <= carried; ++d) {
       age_lifo(x, m, d, aged);
       std::uint64_t base = base_static;
-      for (int j = 1; j <= m - 1; ++j) base += aged[j] * dm.weight[lead + m - 1 - j];
+      for (int j = 1; j <= m - 1; ++j) base += aged[j] * wgt(lead + m - 1 - j);
       const double w = d < carried ? s_pmf[d] : s_sf[carried];
       const T* vb = V + base;
 #pragma unroll
@@ -659,7 +665,10 @@ __global__ void __launch_bounds__(128) k_a_fact_lifo(DevModel dm, const T* __res
 // where K(S2) collects the demands that reach x_3.. (d > S2) and does not
 // depend on how S2 splits.  Thread = one diagonal (S2, x_3.., pipeline),
 // walking x_2 = u with the middle sum as a running sum.  Warp = 32 digit
-// groups with the same S2 (uniform trip counts).
+// groups with the same S2 (uniform trip counts).  Round 2: constant
+// geometry (FIXED) and the next R(u) row loaded ahead: a/m5/exp6 168 -> 128
+// us per sweep.  (A warp per digit group, lane = S2, makes every gather row
+// warp-uniform but measured slower in the solve: 155 vs 134 us per sweep.)
 template <typename T, int NA, int ML>
 __global__ void __launch_bounds__(128) k_a_fact_fifo(DevModel dm, const T* __restrict__ V,
                                                      const double* __restrict__ reward,
@@ -681,7 +690,8 @@ __global__ void __launch_bounds__(128) k_a_fact_fifo(DevModel dm, const T* __res
   }
   for (int i = threadIdx.x; i <= dn; i += blockDim.x) s_sf[i] = cdf_sf[dn + i];
   __syncthreads();
-  const int rx = dm.a_max_order + 1;
+  constexpr bool FIXED = ML != 0;  // na == NA == A_max + 1 (see k_a_fact_lifo)
+  const int rx = FIXED ? NA : dm.a_max_order + 1;
   const std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int S2 = static_cast<int>(t / n_groups);
   const std::uint64_t g = t % n_groups;   // digits above x_2
@@ -691,8 +701,9 @@ __global__ void __launch_bounds__(128) k_a_fact_fifo(DevModel dm, const T* __res
   if (S2 <= 2 * (rx - 1) && s0 < hi && s0 + rx * rx > lo) {
     constexpr int MC = ML / 10, LC = ML % 10;
     const int m = ML ? MC : dm.a_m, lead = ML ? LC : dm.a_lead;
-    const int na = static_cast<int>(dm.n_actions);
+    const int na = FIXED ? NA : static_cast<int>(dm.n_actions);
     constexpr int ND = ML ? MC + LC - 1 : kMaxDigits;
+    auto wgt = [&](int k) -> std::uint64_t { return FIXED ? a_pow(NA, ND - 1 - k) : dm.weight[k]; };
     int st[ND];
     if (ML) {
       const std::uint32_t r = static_cast<std::uint32_t>(rx);
@@ -714,18 +725,19 @@ __global__ void __launch_bounds__(128) k_a_fact_fifo(DevModel dm, const T* __res
     }
     std::uint64_t base_static = 0;
 #pragma unroll
-    for (int k = 1; k <= lead - 2; ++k) base_static += st[k - 1] * dm.weight[k];
-    if (lead >= 2) base_static += st[lead - 2] * dm.weight[lead - 1];
-    const std::uint64_t w0 = dm.weight[0];
+    for (int k = 1; k <= lead - 2; ++k) base_static += st[k - 1] * wgt(k);
+    if (lead >= 2) base_static += st[lead - 2] * wgt(lead - 1);
+    const std::uint64_t w0 = wgt(0);
     auto base_of = [&]() {
       std::uint64_t b = base_static;
-      for (int j = 1; j <= m - 1; ++j) b += aged[j] * dm.weight[lead + m - 1 - j];
+      for (int j = 1; j <= m - 1; ++j) b += aged[j] * wgt(lead + m - 1 - j);
       return b;
     };
     // K(S2): demands S2 + k, k >= 1, consume x_3.. (x_1 = x_2 = 0 in x here)
     double acc[NA];
 #pragma unroll
     for (int a = 0; a < NA; ++a) acc[a] = 0.0;
+#pragma unroll 2
     for (int k = 1; k <= max(above, 1); ++k) {
       age_fifo(x, m, k, aged);
       const double w = k < above ? s_pmf[min(S2 + k, dn - 1)] : s_sf[min(S2 + k, dn)];
@@ -735,13 +747,21 @@ __global__ void __launch_bounds__(128) k_a_fact_fifo(DevModel dm, const T* __res
         if (a < na) acc[a] = fma(w, static_cast<double>(__ldg(vb + a * w0)), acc[a]);
     }
     const int ulast = min(S2, rx - 1);
-    for (int u = 0; u <= ulast; ++u) {
+    // R(u) is one gather row per step; the next step's row is loaded before
+    // this step's outputs so two rows of loads are in flight
+    auto load_row = [&](int u, double (&rv)[NA]) {
       x[2] = u;  // R(u): next stock (u, x_3, .., x_m)
       age_fifo(x, m, 0, aged);
       const T* vb = V + base_of();
-      double rv[NA];
 #pragma unroll
       for (int a = 0; a < NA; ++a) rv[a] = a < na ? static_cast<double>(__ldg(vb + a * w0)) : 0.0;
+    };
+    double rv[NA], rvn[NA];
+    load_row(0, rvn);
+    for (int u = 0; u <= ulast; ++u) {
+#pragma unroll
+      for (int a = 0; a < NA; ++a) rv[a] = rvn[a];
+      if (u < ulast) load_row(u + 1, rvn);
       const int x1 = S2 - u;
       const std::uint64_t s = s0 + static_cast<std::uint64_t>(u) * rx + x1;
       if (x1 < rx && s >= lo && s < hi) {
