@@ -177,6 +177,10 @@ const DevModel& Model::device_view(int device) const {
       d.c_cdf = upload(*dc, c_cdf);
       {
         const int dn = pc.max_demand + 1;
+        std::vector<double> pd(7, 0.0);  // the kernels' former per-CTA loop, same order
+        for (int t = 0; t < 7; ++t)
+          for (int dd = 0; dd < dn; ++dd) pd[t] += c_pmf[static_cast<std::size_t>(t) * dn + dd];
+        d.c_pd = upload(*dc, pd);
         std::vector<std::int32_t> g;
         for (int t = 0; t < 7; ++t) {
           const auto gt = cdf_guide(c_cdf.data() + static_cast<std::size_t>(t) * dn, dn, kGuide);

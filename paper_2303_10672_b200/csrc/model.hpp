@@ -83,6 +83,7 @@ struct DevModel {
   std::uint32_t c_n_comp;
   double c_cf, c_ch, c_cs, c_cw;
   const double* c_pmf;        // 7 x (D+1)
+  const double* c_pd;         // 7: PD(tau) = sum_d pmf[tau][d], summed in d order
   const double* c_cdf;        // 7 x (D+1)
   const std::int32_t* c_guide;  // 7 x (kGuide + 1) guide tables of c_cdf
   const double* c_rcpt_cum;     // receipt binomials' cumulative masses (sim_tables.cpp)

@@ -2452,6 +2452,11 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag(const double* __restrict_
   }
 }
 
+// B-fragment rows past an anti-diagonal's last input read this instead of
+// being zeroed per element (their weights are exact zeros; a finite source
+// keeps 0 x v = 0)
+__device__ const double g_zero_row[32] = {};
+
 // Passes k >= 3 with x_2 batched beside x_1, on the FP64 tensor cores
 // (round 2).  k_c_bin_diag's items read and write rows of 21 doubles (168 B)
 // scattered at the pass stride.  For k >= 3 the two lowest digits (x_1,
@@ -2537,6 +2542,8 @@ __global__ void __launch_bounds__(C_WMMA_THREADS, 3) k_c_bin_wide_mma(
   for (int c = c_lo; c < c_hi; ++c) {
     const int lo = max(0, c - CAP), hi = min(c, nb - 1);
     double vb[KS][NT];
+    // (reading zeros from g_zero_row instead of zeroing here saves 6% of the
+    // instructions but spills at 80 registers: no faster, 1.10-1.12 ms)
 #pragma unroll
     for (int s = 0; s < KS; ++s) {
       const int bp = 4 * s + fc;
@@ -2598,19 +2605,22 @@ __device__ __forceinline__ void c_pass_tile_mma(const double* __restrict__ src, 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n_warps = blockDim.x >> 5;
   const int fr = lane >> 2, fc = lane & 3;
   const int n_c = CAP + nb;
+  // columns past x_1 = R - 1 read a clamped column: their outputs are not stored
+  int cofs[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) cofs[g] = min(8 * g + fr, R - 1);
   for (int c = warp; c < n_c; c += n_warps) {
     const int lo = max(0, c - CAP), hi = min(c, nb - 1);
     double vb[KS][NG];
 #pragma unroll
     for (int s = 0; s < KS; ++s) {
+      if (4 * s > hi) break;  // warp-uniform: these k-steps are not issued
       const int bp = 4 * s + fc;
-      const double* row = src + (static_cast<std::uint32_t>(bp) * wb +
-                                 static_cast<std::uint32_t>(min(c - bp, CAP)) * wk + static_cast<std::uint32_t>(fr));
+      const double* row = bp <= hi ? src + (static_cast<std::uint32_t>(bp) * wb +
+                                            static_cast<std::uint32_t>(min(c - bp, CAP)) * wk)
+                                   : g_zero_row;
 #pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        vb[s][g] = 0.0;
-        if (4 * s <= hi && bp <= hi && 8 * g + fr < R) vb[s][g] = __ldg(row + 8 * g);
-      }
+      for (int g = 0; g < NG; ++g) vb[s][g] = __ldg(row + cofs[g]);
     }
 #pragma unroll
     for (int t = 0; t < MT; ++t) {
@@ -2672,12 +2682,7 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag_q(DevModel dm, const doub
   c_pass_fragments<R>(bt, nb, s_wa);
   if (threadIdx.x < R)  // pass 1's weights of order a: c_binom[a][0][a][y]
     s_w1[threadIdx.x] = dm.c_binom[(static_cast<std::size_t>(a) * (m - 1) * R + a) * R + threadIdx.x];
-  if (threadIdx.x == 0) {
-    const int dn = dm.c_dmax + 1;
-    double pd = 0.0;
-    for (int d = 0; d < dn; ++d) pd += dm.c_pmf[tau * dn + d];
-    s_pd = pd;
-  }
+  if (threadIdx.x == 0) s_pd = dm.c_pd[tau];  // (a serial 21-load loop here cost every CTA ~4 us)
   __syncthreads();
   const double* src = Hin + in_base + rest0;
   c_pass_tile_mma<R>(src, wb, wk, nb, s_wa, s_tile);
@@ -2732,12 +2737,7 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag_qf(DevModel dm, const dou
     const int a = t / R, y = t - (t / R) * R;
     s_w1[t] = dm.c_binom[(static_cast<std::size_t>(a) * (m - 1) * R + a) * R + y];
   }
-  if (threadIdx.x == 0) {
-    const int dn = dm.c_dmax + 1;
-    double pd = 0.0;
-    for (int d = 0; d < dn; ++d) pd += dm.c_pmf[tau * dn + d];
-    s_pd = pd;
-  }
+  if (threadIdx.x == 0) s_pd = dm.c_pd[tau];  // (a serial 21-load loop here cost every CTA ~4 us)
   __syncthreads();
   constexpr int nb = R;
   const double* src = Hin + in_base + rest0;
