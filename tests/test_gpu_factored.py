@@ -134,10 +134,11 @@ def test_factored_shards_equal_full_sweep(pvi, preset, parts):
 
 @pytest.mark.parametrize("preset", ["c/m5/exp1", "c/m5/exp2"])
 def test_factored_c_full_sweep_close_to_exact(pvi, preset):
-    """Whole-space backup: c/m5/exp1 has an exogenous receipt law and runs
-    the sequential-binomial passes (k_c_exo_level); exp2 is endogenous and
-    runs the composition gather (k_c_fact_q).  Both agree with the exact
-    (reference-order) sweep to rounding."""
+    """Whole-space backup: c/m5/exp1 has an exogenous receipt law (scalar
+    anti-diagonal passes k_c_bin_diag + the fused k_c_bin_diag_qf); exp2 is
+    endogenous (the DMMA passes k_c_bin_wide_mma + the fused pass-2/Q
+    k_c_bin_diag_q).  Both agree with the exact (reference-order) sweep to
+    rounding."""
     exact = pvi.make_preset(preset)
     fact = pvi.make_preset(preset).set_algorithm("factored")
     n = exact.state_count()
@@ -156,7 +157,7 @@ def test_factored_c_full_sweep_close_to_exact(pvi, preset):
 def test_factored_b_full_sweep_close_to_exact(pvi, preset):
     """Whole-space backup against the exact (reference-order) sweep: every
     x_a digit pattern goes through the diagonal stage-2 kernel
-    (k_b_fact_qd3 on b/m3/exp1)."""
+    (k_b_fact_qw4 on b/m3/exp1)."""
     exact = pvi.make_preset(preset)
     fact = pvi.make_preset(preset).set_algorithm("factored")
     n = exact.state_count()
