@@ -1079,7 +1079,7 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_q(DevModel dm, const double* 
   }
 }
 
-// Stage 1, register-blocked the same way as k_b_fact_q16 (order_b radix 16):
+// Stage 1, register-blocked for order_b radix 16:
 // the 16 x_b states of a group (same x_2..x_M, x_1 = 0..15) walk the same
 // aged-B-profile path, so each slab element read feeds 8 states' FMAs.
 // Stage-1 work of one r (the r-slab of V staged in shared memory as
@@ -1172,7 +1172,7 @@ __device__ __forceinline__ void w16_row(const double* __restrict__ slab, double*
       for (int i = 0; i < S8; ++i) {
         const int xbi = grp * NB + x1b + i;
         // tiled layout [x_b / 16][r][x_b % 16][o_b]: the 16 x_1 of a group form
-        // one 2 KB run per r (k_b_fact_qw3 reads it); else [x_b][r][o_b]
+        // one 2 KB run per r (k_b_fact_qw4 reads it); else [x_b][r][o_b]
         double* out = tiled ? W + ((static_cast<std::size_t>(grp) * n_r + r) * NB + x1b + i) * NB + ob0
                             : W + (static_cast<std::size_t>(xbi) * n_r + r) * NB + ob0;
         // one 32-byte store per lane (4 lanes write a 128-byte row)
@@ -1197,7 +1197,7 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16(DevModel dm, const T* __r
   const int r = r_base + static_cast<int>(blockIdx.x);
   if (M == 3) {
     // a state shard only reads the W rows of its own x_3 digits and the
-    // R(0, j) rows of the diagonal constants (k_b_fact_qw3)
+    // R(0, j) rows of the diagonal constants (k_b_fact_qw4)
     const int na = dm.b_na, ap = r % (na * na), x2r = ap % na, x3r = ap / na;
     if ((x3r < x3_lo || x3r > x3_hi) && !(x2r == 0 && x3r <= x3_hi)) return;
   }
@@ -1339,7 +1339,7 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16p(DevModel dm, const doubl
 // with u = x_2 = 0, 1, .. carries it as a running sum, and the last two
 // lines are constant along the diagonal (I_a = S2 + x_3): one accumulator per
 // order_b holds all of it.  ~6 FP64 ops per (state, order) instead of
-// ~2 (I_a - x_1 + 1) FMAs in k_b_fact_q16.  Warp = one x_3, lane = one
+// ~2 (I_a - x_1 + 1) FMAs per state and order.  Warp = one x_3, lane = one
 // diagonal S2 with all 16 orders_b in registers (no cross-lane max): at
 // every step the lanes read the same R row (shared-memory broadcast), the
 // weights are consecutive table entries and the lanes' ER/PT are contiguous.
