@@ -64,6 +64,41 @@ struct Rng {
   __device__ __forceinline__ double uniform() {
     return static_cast<double>(next_u64() >> 11) * 0x1.0p-53;
   }
+  // the next N uniforms (draws draw .. draw + N - 1), their Philox blocks
+  // interleaved round by round: N independent multiply chains in flight
+  // instead of one (a block's 10 rounds are a serial dependency chain)
+  template <int N>
+  __device__ __forceinline__ void uniforms(double (&u)[N]) {
+    std::uint32_t c[N][4];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      c[i][0] = day;
+      c[i][1] = draw + i;
+      c[i][2] = 0x7F4A7C15u;
+      c[i][3] = 0u;
+    }
+    draw += N;
+    std::uint32_t a0 = k0, a1 = k1;
+#pragma unroll
+    for (int round = 0; round < 10; ++round) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const std::uint32_t hi0 = __umulhi(0xD2511F53u, c[i][0]);
+        const std::uint32_t lo0 = 0xD2511F53u * c[i][0];
+        const std::uint32_t hi1 = __umulhi(0xCD9E8D57u, c[i][2]);
+        const std::uint32_t lo1 = 0xCD9E8D57u * c[i][2];
+        c[i][0] = hi1 ^ c[i][1] ^ a0;
+        c[i][1] = lo1;
+        c[i][2] = hi0 ^ c[i][3] ^ a1;
+        c[i][3] = lo0;
+      }
+      a0 += 0x9E3779B9u;
+      a1 += 0xBB67AE85u;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      u[i] = static_cast<double>(((static_cast<std::uint64_t>(c[i][0]) << 32) | c[i][1]) >> 11) * 0x1.0p-53;
+  }
 };
 
 // rng.hpp:63-73
@@ -218,12 +253,16 @@ __device__ __forceinline__ void step_b(const DevModel& dm, int* state, const int
     stock_a += xa[j];
     stock_b += xb[j];
   }
-  const int demand_a = sample_from_cdf_guided(dm.b_cdf_a, dm.b_len_a, dm.b_guide_a, rng.uniform());
-  const int demand_b = sample_from_cdf_guided(dm.b_cdf_b, dm.b_len_b, dm.b_guide_b, rng.uniform());
+  // every day draws exactly three uniforms (scenario_b.cpp:332-379): demand
+  // A, demand B, the substitution binomial -- generated together
+  double u3[3];
+  rng.uniforms(u3);
+  const int demand_a = sample_from_cdf_guided(dm.b_cdf_a, dm.b_len_a, dm.b_guide_a, u3[0]);
+  const int demand_b = sample_from_cdf_guided(dm.b_cdf_b, dm.b_len_b, dm.b_guide_b, u3[1]);
   const int own_fill_a = min(demand_a, stock_a);
   const int fill_b = min(demand_b, stock_b);
   const int trials = demand_b - fill_b;
-  const double ub = rng.uniform();
+  const double ub = u3[2];
   const int accepted = dm.b_binom_cum && trials > 0 && trials <= dm.b_binom_t
                            ? sample_binomial_table(trials, dm.b_binom_cum + trials * (trials + 1) / 2, ub)
                            : sample_binomial(trials, dm.b_rho, ub);
