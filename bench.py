@@ -133,16 +133,43 @@ def work_from_reference(preset: str) -> Work:
 
 
 class Clocks:
+    """SM clock and clock-event reasons sampled DURING the timed region.
+
+    NVML in a thread every 10 ms (no process start-up: a 20-step headline
+    region lasts ~0.1 s, shorter than nvidia-smi's first line); nvidia-smi
+    -lms 200 only when NVML is unavailable."""
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int = 0):
         self.index = index
         self.proc = None
         self.lines = []
+        self.nv = None
+        self.handle = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            try:  # the torch device's physical GPU (CUDA_VISIBLE_DEVICES may remap)
+                import torch
+                pr = torch.cuda.get_device_properties(index)
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                self.handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.handle = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.nv = pynvml
+        except Exception:
+            self.nv = None
 
     def start(self):
+        self.samples, self.reason_bits = [], 0
+        if self.nv is not None:
+            self.stop_flag = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
@@ -153,11 +180,40 @@ class Clocks:
         except FileNotFoundError:
             self.proc = None
 
+    def _poll(self):
+        nv, h = self.nv, self.handle
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons",
+                              getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons", None))
+        while not self.stop_flag.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                if get_reasons is not None:
+                    self.reason_bits |= int(get_reasons(h))
+            except Exception:
+                pass
+            self.stop_flag.wait(0.01)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nv is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=2)
+            nv = self.nv
+            bits = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+                    "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+                    "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+                    "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
+            reasons = sorted(nm for nm, c in bits.items() if self.reason_bits & int(getattr(nv, c, 0)))
+            try:
+                smax = float(nv.nvmlDeviceGetMaxClockInfo(self.handle, nv.NVML_CLOCK_SM))
+            except Exception:
+                smax = None
+            return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                    "sm_max_mhz": smax, "reasons": reasons, "samples": len(self.samples),
+                    "source": "nvml, 10 ms"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -166,7 +222,6 @@ class Clocks:
         except Exception:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
@@ -176,11 +231,11 @@ class Clocks:
                 smax = float(parts[2])
             except ValueError:
                 continue
-            for nm, val in zip(names, parts[5:9]):
+            for nm, val in zip(self.NAMES, parts[5:9]):
                 if val.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi -lms 200"}
 
 
 # ---------------------------------------------------------------------------
