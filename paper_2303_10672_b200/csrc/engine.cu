@@ -478,6 +478,119 @@ void initial_values_host(const Model& m, double* out) {
 
 namespace {
 
+// Device -> host copy into the caller's memory at pinned-copy speed.  A
+// run_value_iteration caller (a std::vector, a numpy array) hands pageable
+// memory, which the driver copies at ~21 GB/s through its own staging; here
+// the copy goes through a pinned ring in 8 MB chunks, each landed chunk
+// moved to the caller by a small persistent host pool while the next chunks
+// are in flight (~45 GB/s measured on the B200 host, tools/pageable_probe.py).
+// Pinned (page-locked or registered) destinations take one cudaMemcpyAsync.
+class BounceCopier {
+ public:
+  static BounceCopier& get() {
+    static BounceCopier b;
+    return b;
+  }
+  void copy(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return;
+    cudaPointerAttributes at{};
+    const bool pinned = cudaPointerGetAttributes(&at, dst) == cudaSuccess &&
+                        (at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeManaged);
+    cudaGetLastError();  // an unregistered pointer is not an error here
+    if (pinned || bytes <= kChunk) {
+      PVI_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+      PVI_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    std::lock_guard<std::mutex> lock(use_mu_);
+    ensure_ring();
+    const std::size_t n_chunks = (bytes + kChunk - 1) / kChunk;
+    auto issue = [&](std::size_t i) {
+      const std::size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+      PVI_CUDA(cudaMemcpyAsync(ring_[i % kSlots], static_cast<const char*>(src) + off, len,
+                               cudaMemcpyDeviceToHost, s));
+      PVI_CUDA(cudaEventRecord(ev_[i % kSlots], s));
+    };
+    for (std::size_t i = 0; i < std::min<std::size_t>(kSlots, n_chunks); ++i) issue(i);
+    for (std::size_t i = 0; i < n_chunks; ++i) {
+      PVI_CUDA(cudaEventSynchronize(ev_[i % kSlots]));
+      const std::size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+      parallel_memcpy(static_cast<char*>(dst) + off, ring_[i % kSlots], len);
+      if (i + kSlots < n_chunks) issue(i + kSlots);
+    }
+  }
+
+ private:
+  static constexpr std::size_t kChunk = 8u << 20;
+  static constexpr int kSlots = 3, kThreads = 4;
+  BounceCopier() {
+    for (int t = 0; t < kThreads; ++t) pool_.emplace_back([this, t] { worker(t); });
+  }
+  ~BounceCopier() {
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& th : pool_) th.join();
+  }
+  void ensure_ring() {
+    if (ring_[0]) return;
+    for (int k = 0; k < kSlots; ++k) {
+      PVI_CUDA(cudaHostAlloc(&ring_[k], kChunk, cudaHostAllocDefault));
+      PVI_CUDA(cudaEventCreateWithFlags(&ev_[k], cudaEventDisableTiming));
+    }
+  }
+  void parallel_memcpy(char* dst, const char* src, std::size_t len) {
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      job_dst_ = dst;
+      job_src_ = src;
+      job_len_ = len;
+      pending_ = kThreads;
+      ++gen_;
+    }
+    cv_.notify_all();
+    std::unique_lock<std::mutex> l(mu_);
+    done_cv_.wait(l, [&] { return pending_ == 0; });
+  }
+  void worker(int t) {
+    std::uint64_t seen = 0;
+    for (;;) {
+      char* d;
+      const char* sr;
+      std::size_t len;
+      {
+        std::unique_lock<std::mutex> l(mu_);
+        cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        d = job_dst_;
+        sr = job_src_;
+        len = job_len_;
+      }
+      const std::size_t per = (len / kThreads + 63) & ~std::size_t(63);
+      const std::size_t a = std::min(len, per * t), b = std::min(len, per * (t + 1));
+      if (b > a) std::memcpy(d + a, sr + a, b - a);
+      {
+        std::lock_guard<std::mutex> l(mu_);
+        if (--pending_ == 0) done_cv_.notify_one();
+      }
+    }
+  }
+  std::mutex use_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  std::vector<std::thread> pool_;
+  bool stop_ = false;
+  std::uint64_t gen_ = 0;
+  int pending_ = 0;
+  char* job_dst_ = nullptr;
+  const char* job_src_ = nullptr;
+  std::size_t job_len_ = 0;
+  char* ring_[kSlots] = {};
+  cudaEvent_t ev_[kSlots] = {};
+};
+
 bool evaluate_test(int test, double hi, double lo, double epsilon, std::uint64_t iteration) {
   switch (test) {
     case PVI_TEST_VALUE_SPAN:
@@ -959,8 +1072,7 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
     PVI_CUDA(cudaEventRecord(ev1, stream.s));
     if (out_values) {
       PVI_CUDA(cudaStreamWaitEvent(side->s, ev_wide, 0));
-      PVI_CUDA(cudaMemcpyAsync(out_values, wide->p, n * 8, cudaMemcpyDeviceToHost, side->s));
-      PVI_CUDA(cudaStreamSynchronize(side->s));
+      BounceCopier::get().copy(out_values, wide->p, n * 8, side->s);
       cudaEventDestroy(ev_wide);
     }
     PVI_CUDA(cudaStreamSynchronize(stream.s));
@@ -971,10 +1083,7 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
   }
   wide.reset();  // freed on the solve stream, after the side copy completed
   if (writer) writer->finish();  // every checkpoint on disk before returning
-  if (out_policy) {
-    PVI_CUDA(cudaMemcpyAsync(out_policy, policy.p, n * 4, cudaMemcpyDeviceToHost, stream.s));
-    PVI_CUDA(cudaStreamSynchronize(stream.s));
-  }
+  if (out_policy) BounceCopier::get().copy(out_policy, policy.p, n * 4, stream.s);
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   if (loop_trace())
