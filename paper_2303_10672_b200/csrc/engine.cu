@@ -1382,10 +1382,10 @@ void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t
     }
     c_lo = c_hi;
   }
-  if (chunks == 1) {
-    if (out_values) PVI_CUDA(cudaMemcpyAsync(out_values, vo, nr * sizeof(T), cudaMemcpyDeviceToHost, st));
-    if (out_actions) PVI_CUDA(cudaMemcpyAsync(out_actions, ao, nr * 4, cudaMemcpyDeviceToHost, st));
-    if (out_q) PVI_CUDA(cudaMemcpyAsync(out_q, qo, nr * m.n_actions * sizeof(T), cudaMemcpyDeviceToHost, st));
+  if (chunks == 1) {  // pageable caller buffers go through the pinned ring
+    if (out_values) BounceCopier::get().copy(out_values, vo, nr * sizeof(T), st);
+    if (out_actions) BounceCopier::get().copy(out_actions, ao, nr * 4, st);
+    if (out_q) BounceCopier::get().copy(out_q, qo, nr * m.n_actions * sizeof(T), st);
   }
   PVI_CUDA(cudaStreamSynchronize(st));
   PVI_CUDA(cudaStreamSynchronize(ws.copy));
