@@ -1184,6 +1184,103 @@ __device__ __forceinline__ void w16_row(const double* __restrict__ slab, double*
   }
 }
 
+// mma.sync m8n8k4 f64, D = A B + D (non-volatile: schedulable)
+__device__ __forceinline__ void dmma_884_nv(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// Stage-1 row on the FP64 tensor cores (round 2).  For one group (x_2..x_M)
+// and one row r the 16 x 16 block W[x_1][o_b] is a product
+//   W = A B,  A[x_1][j] = a0(x_1) (j = 0), pmf_b(x_1 + j) (0 < j < S),
+//             B[j][o_b] = slab[bp_j][o_b]   (bp_j: the aged B profile after
+//             x_1 + j units, the same for all 16 x_1)
+// with K = max(S, 1) (S = x_2 + .. + x_M): a warp takes one group and runs
+// ceil(K / 4) k-steps of 2 x 2 mma.sync m8n8k4 f64 tiles, A from the pmf /
+// cdf table in shared memory, B straight from the slab.  With the k-steps
+// in j order the results measured bit-identical to w16_row's FMA chain
+// (b/m3/exp1 V' and argmax hashes, tools/b_sweep_ab.py; the tests compare
+// against the exact kernels either way); 62 instead of 126 registers -> 3
+// persistent CTAs per SM: stage 1 0.523 -> 0.505 ms.
+template <int M>
+__device__ __forceinline__ void w16_row_mma(const double* __restrict__ slab, double* __restrict__ W,
+                                            double* __restrict__ v0t,
+                                            const std::uint16_t* __restrict__ group_order, int n_groups,
+                                            int n_r, int r, int tiled, const double* s_pmf_b,
+                                            const double* s_cdf_b, int g_lo = 0, int g_cnt = -1,
+                                            bool sorted = false, bool write_v0 = true) {
+  constexpr int NB = 16;
+  const int stride = slab_stride(NB);
+  if (write_v0 && threadIdx.x < NB) v0t[static_cast<std::size_t>(r) * NB + threadIdx.x] = slab[threadIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n_warps = blockDim.x >> 5;
+  const int fr = lane >> 2, fc = lane & 3;
+  const bool all_groups = g_cnt < 0 || g_cnt >= n_groups;
+  const bool by_order = all_groups || sorted;
+  const int g_base = all_groups ? 0 : g_lo;
+  const int n_iter = all_groups ? n_groups : g_cnt;
+  for (int gi = warp; gi < n_iter; gi += n_warps) {
+    const int grp = by_order ? group_order[g_base + gi] : g_lo + gi;
+    int xg[M + 1];
+    int S = 0;
+    {
+      int rem = grp;
+#pragma unroll
+      for (int j = 2; j <= M; ++j) {
+        xg[j] = rem % NB;
+        rem /= NB;
+        S += xg[j];
+      }
+    }
+    const int K = max(S, 1);
+    double d[2][2][2];  // [m-tile][n-tile][pair]
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) d[a][b][0] = d[a][b][1] = 0.0;
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const int j = k0 + fc;  // this lane's k index (A column, B row)
+      // B: row bp_j of the slab (a zero row past K)
+      int bp = 0, w = 1, prefix = 0;
+#pragma unroll
+      for (int q = 1; q <= M - 1; ++q) {
+        bp += ipos(xg[q + 1] - ipos(j - prefix)) * w;
+        prefix += xg[q + 1];
+        w *= NB;
+      }
+      const double* brow = slab + slab_row(bp) * stride;
+      const double b0 = j < K ? brow[fr] : 0.0, b1 = j < K ? brow[8 + fr] : 0.0;
+      // A: x_1 = fr (+ 8)
+      double a[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int x1 = 8 * mt + fr;
+        a[mt] = j >= K ? 0.0
+                : j == 0 ? (S > 0 ? s_cdf_b[x1] : (x1 > 0 ? s_cdf_b[x1 - 1] : 0.0))
+                         : s_pmf_b[x1 + j];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        dmma_884_nv(d[mt][0][0], d[mt][0][1], a[mt], b0);
+        dmma_884_nv(d[mt][1][0], d[mt][1][1], a[mt], b1);
+      }
+    }
+    // D: x_1 = 8 mt + fr, o_b = 8 nt + 2 fc + e
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int x1 = 8 * mt + fr;
+      const int xbi = grp * NB + x1;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int ob = 8 * nt + 2 * fc;
+        double* out = tiled ? W + ((static_cast<std::size_t>(grp) * n_r + r) * NB + x1) * NB + ob
+                            : W + (static_cast<std::size_t>(xbi) * n_r + r) * NB + ob;
+        *reinterpret_cast<double2*>(out) = make_double2(d[mt][nt][0], d[mt][nt][1]);
+      }
+    }
+  }
+}
+
 template <typename T, int M>
 __global__ void __launch_bounds__(256, 2) k_b_fact_w16(DevModel dm, const T* __restrict__ V,
                                                        double* __restrict__ W,
@@ -1221,7 +1318,7 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16(DevModel dm, const T* __r
 // computed, so the slab load latency and the W write stream overlap the
 // FMAs instead of alternating with them.
 template <int M>
-__global__ void __launch_bounds__(256, 2) k_b_fact_w16p(DevModel dm, const double* __restrict__ V,
+__global__ void __launch_bounds__(256, 3) k_b_fact_w16p(DevModel dm, const double* __restrict__ V,
                                                         double* __restrict__ W,
                                                         double* __restrict__ v0t,
                                                         const std::uint16_t* __restrict__ group_order,
@@ -1281,8 +1378,8 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16p(DevModel dm, const doubl
       }
       __syncthreads();
       const int4 it = items[i];
-      w16_row<M>(slabs + buf * slab_sz, W, v0t, group_order, n_groups, n_r, it.x, tiled, s_pmf_b, s_cdf_b,
-                 it.y, it.z, (it.w & 1) != 0, (it.w & 2) != 0);
+      w16_row_mma<M>(slabs + buf * slab_sz, W, v0t, group_order, n_groups, n_r, it.x, tiled, s_pmf_b, s_cdf_b,
+                     it.y, it.z, (it.w & 1) != 0, (it.w & 2) != 0);
       __syncthreads();  // the slab is refilled two items later
       i = in;
     }
@@ -1316,8 +1413,8 @@ __global__ void __launch_bounds__(256, 2) k_b_fact_w16p(DevModel dm, const doubl
         rg_cnt = tg_hi;
       }
     }
-    w16_row<M>(slabs + buf * slab_sz, W, v0t, group_order, n_groups, n_r, r_base + t, tiled, s_pmf_b,
-               s_cdf_b, rg_lo, rg_cnt);
+    w16_row_mma<M>(slabs + buf * slab_sz, W, v0t, group_order, n_groups, n_r, r_base + t, tiled, s_pmf_b,
+                   s_cdf_b, rg_lo, rg_cnt);
     __syncthreads();  // the slab is refilled two rows later
     t = tn;
   }
@@ -2481,11 +2578,6 @@ constexpr int C_WIDE_CHUNKS_ENDO = 2;  // anti-diagonal ranges per item
 // n-tiles), and only the row tiles that meet c's window and the k-steps
 // below them are issued.  DMMA's summation order: within rounding of
 // k_c_bin_diag (the factored contract).
-__device__ __forceinline__ void dmma_884_nv(double& d0, double& d1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
-      : "+d"(d0), "+d"(d1)
-      : "d"(a), "d"(b));
-}
 
 constexpr int C_WMMA_THREADS = 224;  // 7 warps x 32 columns; two CTAs per item cover the 441 columns
 
@@ -3444,7 +3536,8 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
         if (f64) {
           auto kp = k_b_fact_w16p<3>;
           cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sm0);
-          unsigned g = static_cast<unsigned>(std::min<std::uint64_t>(r1 - r0, 2 * num_sms()));
+          const int per_sm = 3;  // 62 registers, 74 KB of slabs per CTA
+          unsigned g = static_cast<unsigned>(std::min<std::uint64_t>(r1 - r0, per_sm * num_sms()));
           // a shard's sparse row set: the balanced work list (built once per shape)
           const int4* s1_items = nullptr;
           int s1_n = 0;
@@ -3469,7 +3562,7 @@ bool launch_b_factored(const Model& model, const DevModel& dm, const SweepArgs<T
             }
             s1_items = static_cast<const int4*>(it->second.first);
             s1_n = it->second.second;
-            g = static_cast<unsigned>(std::min<long long>(std::max(s1_n, 1), 2ll * num_sms()));
+            g = static_cast<unsigned>(std::min<long long>(std::max(s1_n, 1), static_cast<long long>(per_sm) * num_sms()));
           }
           kp<<<g, 256, 2 * sm0, stream>>>(dm, reinterpret_cast<const double*>(a.v), W, v0t, dc.b_group_order_b,
                                           static_cast<int>(n_bp), static_cast<int>(n_xb), static_cast<int>(n_bp),
