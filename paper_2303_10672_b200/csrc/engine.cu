@@ -503,19 +503,22 @@ class BounceCopier {
       return;
     }
     std::lock_guard<std::mutex> lock(use_mu_);
-    ensure_ring();
+    int device = 0;
+    PVI_CUDA(cudaGetDevice(&device));
+    if (device < 0 || device >= kMaxDevices) fail(PVI_ERR_DEVICE, "device ordinal out of range");
+    Ring& rg = ring(device);  // events belong to the stream's device
     const std::size_t n_chunks = (bytes + kChunk - 1) / kChunk;
     auto issue = [&](std::size_t i) {
       const std::size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
-      PVI_CUDA(cudaMemcpyAsync(ring_[i % kSlots], static_cast<const char*>(src) + off, len,
+      PVI_CUDA(cudaMemcpyAsync(rg.buf[i % kSlots], static_cast<const char*>(src) + off, len,
                                cudaMemcpyDeviceToHost, s));
-      PVI_CUDA(cudaEventRecord(ev_[i % kSlots], s));
+      PVI_CUDA(cudaEventRecord(rg.ev[i % kSlots], s));
     };
     for (std::size_t i = 0; i < std::min<std::size_t>(kSlots, n_chunks); ++i) issue(i);
     for (std::size_t i = 0; i < n_chunks; ++i) {
-      PVI_CUDA(cudaEventSynchronize(ev_[i % kSlots]));
+      PVI_CUDA(cudaEventSynchronize(rg.ev[i % kSlots]));
       const std::size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
-      parallel_memcpy(static_cast<char*>(dst) + off, ring_[i % kSlots], len);
+      parallel_memcpy(static_cast<char*>(dst) + off, rg.buf[i % kSlots], len);
       if (i + kSlots < n_chunks) issue(i + kSlots);
     }
   }
@@ -534,12 +537,19 @@ class BounceCopier {
     cv_.notify_all();
     for (auto& th : pool_) th.join();
   }
-  void ensure_ring() {
-    if (ring_[0]) return;
+  struct Ring {
+    char* buf[kSlots] = {};
+    cudaEvent_t ev[kSlots] = {};
+  };
+  static constexpr int kMaxDevices = 64;
+  Ring& ring(int device) {  // pinned (portable) slots and events of one device, made on first use
+    Ring& rg = rings_[device];
+    if (rg.buf[0]) return rg;
     for (int k = 0; k < kSlots; ++k) {
-      PVI_CUDA(cudaHostAlloc(&ring_[k], kChunk, cudaHostAllocDefault));
-      PVI_CUDA(cudaEventCreateWithFlags(&ev_[k], cudaEventDisableTiming));
+      PVI_CUDA(cudaHostAlloc(&rg.buf[k], kChunk, cudaHostAllocPortable));
+      PVI_CUDA(cudaEventCreateWithFlags(&rg.ev[k], cudaEventDisableTiming));
     }
+    return rg;
   }
   void parallel_memcpy(char* dst, const char* src, std::size_t len) {
     {
@@ -587,8 +597,7 @@ class BounceCopier {
   char* job_dst_ = nullptr;
   const char* job_src_ = nullptr;
   std::size_t job_len_ = 0;
-  char* ring_[kSlots] = {};
-  cudaEvent_t ev_[kSlots] = {};
+  Ring rings_[kMaxDevices];
 };
 
 bool evaluate_test(int test, double hi, double lo, double epsilon, std::uint64_t iteration) {
