@@ -2870,12 +2870,21 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag_qf(DevModel dm, const dou
     const double* h = s_tile + x2 * R;
     T best = T(0);
     std::uint32_t besta = 0;
-    for (int a = 0; a < na; ++a) {
+    // the launcher guarantees na == R: the triangle (a, y <= a) unrolls with
+    // each term one shared-memory load at a register column + an immediate
+    // row offset (the columns min(x_1 + y, cap) are computed once per state)
+    int col[R];
+#pragma unroll
+    for (int y = 0; y < R; ++y) col[y] = min(x1 + y, CAP);
+    const double cf = -dm.c_cf, pd = s_pd;
+#pragma unroll
+    for (int a = 0; a < R; ++a) {
       const double* w = s_w1 + a * R;
       double acc = 0.0;
-      for (int y = 0; y <= a; ++y) acc = fma(w[y], h[(a - y) * PLANE + min(x1 + y, CAP)], acc);
-      const double fixed = a > 0 ? -dm.c_cf : 0.0;
-      const T qa = static_cast<T>(fma(fixed, s_pd, acc));
+#pragma unroll
+      for (int y = 0; y <= a; ++y) acc = fma(w[y], h[(a - y) * PLANE + col[y]], acc);
+      const double fixed = a > 0 ? cf : 0.0;
+      const T qa = static_cast<T>(fma(fixed, pd, acc));
       if (a == 0 || qa > best) {
         best = qa;
         besta = static_cast<std::uint32_t>(a);
