@@ -200,6 +200,25 @@ const DevModel& Model::device_view(int device) const {
       d.c_receipt = upload(*dc, c_receipt);
       d.c_exogenous = c_exogenous ? 1 : 0;
       d.c_binom = c_binom.empty() ? nullptr : upload(*dc, c_binom);
+      d.c_frag = nullptr;
+      if (!c_binom.empty() && !c_exogenous && pc.max_order == 20) {
+        // [t][s][lane] = L[8 t + lane / 4][4 s + lane % 4], L[b][b'] =
+        // Bin(b - b'; b, q_k(a)) for b' <= b < a + 1 (c_pass_fragments' layout)
+        constexpr int R = 21, NF = 3 * 6 * 32;
+        const int life = pc.useful_life;
+        std::vector<double> fr(static_cast<std::size_t>(R) * (life - 1) * NF, 0.0);
+        for (int a = 0; a < R; ++a)
+          for (int k = 1; k <= life - 1; ++k) {
+            const double* bt = &c_binom[(static_cast<std::size_t>(a) * (life - 1) + (k - 1)) * R * R];
+            double* out = &fr[(static_cast<std::size_t>(a) * (life - 1) + (k - 1)) * NF];
+            for (int e = 0; e < NF; ++e) {
+              const int t = e / (6 * 32), sk = (e / 32) % 6, ln = e & 31;
+              const int b = 8 * t + (ln >> 2), bp = 4 * sk + (ln & 3);
+              out[e] = (bp <= b && b < a + 1) ? bt[b * R + (b - bp)] : 0.0;
+            }
+          }
+        d.c_frag = upload(*dc, fr);
+      }
       break;
     default:
       d.t_outcomes = n_outcomes;

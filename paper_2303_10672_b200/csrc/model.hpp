@@ -99,6 +99,10 @@ struct DevModel {
   // does not depend on a (all c_receipt rows equal).
   int c_exogenous;
   const double* c_binom;
+  // endogenous law, A_max = 20: the DMMA A fragments of every pass's
+  // lower-triangular matrix, c_frag[a][k-1][576] (k_c_bin_wide_mma,
+  // k_c_bin_diag_q), built once on the host instead of per CTA
+  const double* c_frag;
 
   // tabular
   std::uint64_t t_outcomes;

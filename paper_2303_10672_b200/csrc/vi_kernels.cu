@@ -2585,7 +2585,7 @@ template <int RC>
 __global__ void __launch_bounds__(C_WMMA_THREADS, 3) k_c_bin_wide_mma(
     const double* __restrict__ Hin, double* __restrict__ Hout, const double* __restrict__ binom_k,
     std::size_t binom_a_stride, int m, int k, std::uint32_t wb, int endo, int in_is_g, int n_prof, int n_lines,
-    int tau0, int n_tau, int n_chunks) {
+    int tau0, int n_tau, int n_chunks, const double* __restrict__ frag) {
   constexpr int R = RC, CAP = RC - 1, PL = RC * RC;
   constexpr int MT = (R + 7) / 8, KS = (R + 3) / 4, NT = 4;  // 3 row tiles, 6 k-steps, 4 column tiles
   __shared__ double s_wa[MT * KS * 32];  // [t][s][lane] = L[8 t + lane / 4][4 s + lane % 4]
@@ -2613,12 +2613,11 @@ __global__ void __launch_bounds__(C_WMMA_THREADS, 3) k_c_bin_wide_mma(
   const std::size_t out_base = endo ? c_tri_base(a, wb) + static_cast<std::size_t>(tau) * nb * wb
                                     : static_cast<std::size_t>(tau) * n_prof;
   const std::size_t in_base = (endo && !in_is_g) ? out_base : static_cast<std::size_t>(tau) * n_prof;
-  const double* bt = binom_k + a * binom_a_stride;
-  for (int e = threadIdx.x; e < MT * KS * 32; e += blockDim.x) {
-    const int t = e / (KS * 32), sk = (e / 32) % KS, ln = e & 31;
-    const int b = 8 * t + (ln >> 2), bp = 4 * sk + (ln & 3);
-    s_wa[e] = (bp <= b && b < nb) ? bt[b * R + (b - bp)] : 0.0;
-  }
+  // L's fragments of (a, k), precomputed per model (DevModel::c_frag)
+  (void)binom_k;
+  (void)binom_a_stride;
+  const double* fsrc = frag + (static_cast<std::size_t>(a) * (m - 1) + (k - 1)) * (MT * KS * 32);
+  for (int e = threadIdx.x; e < MT * KS * 32; e += blockDim.x) s_wa[e] = __ldg(fsrc + e);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int fr = lane >> 2, fc = lane & 3;
@@ -2678,17 +2677,7 @@ __global__ void __launch_bounds__(C_WMMA_THREADS, 3) k_c_bin_wide_mma(
 // cores (the same lower-triangular product per anti-diagonal as
 // k_c_bin_wide_mma; for k = 2 the item's input planes [d_2][x_1] are 3.5 KB
 // contiguous).  A warp takes one anti-diagonal c and the 21 columns x_1 as 3
-// n-tiles.  s_wa: L's fragments of this item's order (c_pass_fragments).
-template <int R>
-__device__ __forceinline__ void c_pass_fragments(const double* __restrict__ bt, int nb, double* s_wa) {
-  constexpr int MT = (R + 7) / 8, KS = (R + 3) / 4;
-  for (int e = threadIdx.x; e < MT * KS * 32; e += blockDim.x) {
-    const int t = e / (KS * 32), sk = (e / 32) % KS, ln = e & 31;
-    const int b = 8 * t + (ln >> 2), bp = 4 * sk + (ln & 3);
-    s_wa[e] = (bp <= b && b < nb) ? bt[b * R + (b - bp)] : 0.0;
-  }
-}
-
+// n-tiles.  s_wa: L's fragments of this item's order (DevModel::c_frag).
 template <int R>
 __device__ __forceinline__ void c_pass_tile_mma(const double* __restrict__ src, std::uint32_t wb, std::uint32_t wk,
                                                 int nb, const double* s_wa, double* s_tile) {
@@ -2770,8 +2759,12 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag_q(DevModel dm, const doub
   const std::size_t in_base = in_is_g ? static_cast<std::size_t>(tau) * n_prof
                                       : c_tri_base(a, wb) + static_cast<std::size_t>(tau) * nb * wb;
   const double* bt = binom_k + a * binom_a_stride;
-  __shared__ double s_wa[18 * 32];  // L's DMMA fragments (c_pass_fragments)
-  c_pass_fragments<R>(bt, nb, s_wa);
+  __shared__ double s_wa[18 * 32];  // L's DMMA fragments of (a, k = 2), precomputed (DevModel::c_frag)
+  {
+    const double* fsrc = dm.c_frag + (static_cast<std::size_t>(a) * (m - 1) + 1) * (18 * 32);
+    for (int e = threadIdx.x; e < 18 * 32; e += blockDim.x) s_wa[e] = __ldg(fsrc + e);
+  }
+  (void)bt;
   if (threadIdx.x < R)  // pass 1's weights of order a: c_binom[a][0][a][y]
     s_w1[threadIdx.x] = dm.c_binom[(static_cast<std::size_t>(a) * (m - 1) * R + a) * R + threadIdx.x];
   if (threadIdx.x == 0) s_pd = dm.c_pd[tau];  // (a serial 21-load loop here cost every CTA ~4 us)
@@ -3820,7 +3813,7 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
             k_c_bin_wide_mma<21><<<static_cast<unsigned>(r * n_tau * n_lines2 * 2 * C_WIDE_CHUNKS_ENDO),
                                    C_WMMA_THREADS, 0, stream>>>(
                 src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, a_stride, M, k, wb, 1,
-                src == G ? 1 : 0, static_cast<int>(n_prof), n_lines2, tau0, n_tau, C_WIDE_CHUNKS_ENDO);
+                src == G ? 1 : 0, static_cast<int>(n_prof), n_lines2, tau0, n_tau, C_WIDE_CHUNKS_ENDO, dm.c_frag);
           } else  // exogenous passes: measured faster than the wide kernel (0.63 vs 0.65 ms per c/m5/exp1 sweep)
           k_c_bin_diag<21><<<static_cast<unsigned>(n_items), 448, 0, stream>>>(
               src, dst, dm.c_binom + static_cast<std::size_t>(k - 1) * per_k, endo ? a_stride : 0, M, k, wb,
