@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <cstdlib>
@@ -11,6 +12,17 @@
 #include "model.hpp"
 
 namespace pvi_b200 {
+
+// NVTX range (header-only NVTX3: a no-op unless a profiler such as nsys or
+// ncu --nvtx is attached): per-sweep, solve-phase, backup-pipeline and
+// rollout ranges for timeline tools (SURVEY §5 tracing).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 #define PVI_CUDA(call)                                                                     \
   do {                                                                                     \

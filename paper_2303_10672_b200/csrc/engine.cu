@@ -853,6 +853,7 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
   const bool use_graph = graph_possible && (cfg.loop == 1 || (cfg.loop < 0 && hist_cap == 2));
   std::uint64_t graph_sweeps = 0;
   const auto t_loop_start = std::chrono::steady_clock::now();
+  auto nvtx_loop = std::make_unique<NvtxRange>("pvi solve loop");
   while (true) {
     if (cfg.fixed_iterations > 0) {
       if (iteration >= cfg.fixed_iterations) {
@@ -1071,7 +1072,9 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
     if (converged) break;
   }
 
+  nvtx_loop.reset();
   const auto t_loop_end = std::chrono::steady_clock::now();
+  NvtxRange nvtx_extraction("pvi policy extraction + read-back");
   // Policy extraction (vi.hpp:267-280): one more argmax sweep.
   const T* vfinal = ring[order.back()]->as<T>();
   // The value read-back overlaps the extraction sweep (which only reads
@@ -1174,6 +1177,7 @@ int backup_chunks() {
 template <typename T>
 void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t lo,
                  std::uint64_t hi, void* out_values, std::uint32_t* out_actions, void* out_q) {
+  NvtxRange nvtx_range("pvi backup (host buffers)");
   const std::uint64_t n = m.space.count;
   if (lo > hi || hi > n) fail(PVI_ERR_PARAMETER, "state range out of bounds");
   const int device = select_device(-1);

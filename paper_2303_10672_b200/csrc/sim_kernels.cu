@@ -636,6 +636,7 @@ void fill_evaluations(const double* stat, std::uint32_t n_policies, int n_rollou
 void sim_evaluate(const Model& m, const pvi_policy* policies, std::uint32_t n_policies,
                   const pvi_rollout_config& cfg, pvi_rollout_summary* per_rollout,
                   pvi_evaluation* evals) {
+  NvtxRange nvtx_range("pvi rollouts");
   if (cfg.n_rollouts < 1) fail(PVI_ERR_PARAMETER, "evaluation needs at least one rollout");
   if (m.scenario == PVI_TABULAR) fail(PVI_ERR_PARAMETER, "tabular models have no simulator");
   if (n_policies == 0) return;

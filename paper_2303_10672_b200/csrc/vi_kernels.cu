@@ -3869,6 +3869,7 @@ bool launch_c_factored(const Model& model, const DevModel& dm, const SweepArgs<T
 template <typename T>
 void launch_sweep(const Model& model, const DevModel& dm, const SweepArgs<T>& a,
                   Scratch& scratch, cudaStream_t stream) {
+  NvtxRange nvtx_range("pvi sweep");
   const std::uint64_t lo = a.lo, hi = a.hi, nr = hi - lo;
   FinalizeArgs fa = a.fa;
   // the statistics are reset even for an empty range (a rank that owns no
