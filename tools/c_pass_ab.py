@@ -1,8 +1,9 @@
-"""A/B of the factored-C binomial pass kernels (PVI_C_DIAG=1: k_c_bin_diag,
-0: k_c_bin_tile_p): full c/m5 sweeps, K1 time from the measurement hook and
-a hash of the results (the two must be bit-identical).
+"""Factored-C sweeps for A/B of kernel versions: full c/m5 (and c/m3/exp2)
+sweeps on a seeded V, K1 time from the measurement hook and a SHA-256 of
+V' + argmax (bit-identical versions print the same hash).  Compare builds
+with tools/with_lib.py.
 
-    PVI_C_DIAG=1 python tools/c_pass_ab.py
+    python tools/c_pass_ab.py
 """
 import hashlib
 import os
@@ -25,4 +26,4 @@ for preset in ["c/m5/exp1", "c/m5/exp2", "c/m3/exp2"]:
     ms, kl, al = P.profile_read()
     P.profile_enable(False)
     h = hashlib.sha256(v.tobytes() + a.tobytes()).hexdigest()[:16]
-    print(f"{preset} diag={os.environ.get('PVI_C_DIAG', '1')} K1 {ms / reps:.3f} ms/sweep hash {h}")
+    print(f"{preset} K1 {ms / reps:.3f} ms/sweep hash {h}")

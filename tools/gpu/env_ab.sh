@@ -1,5 +1,5 @@
 # A/B of one env switch on the default bench step (+ optional test file):
-#   VAR=PVI_B_W16P VALS="0 1" TESTVALS=1 TESTS=tests/test_gpu_factored.py bash tools/gpu/env_ab.sh
+#   VAR=PVI_E2E_PAIRS VALS="0 1" TESTVALS=1 TESTS=tests/test_gpu_factored.py bash tools/gpu/env_ab.sh
 mkdir -p gpurun_out
 B="python bench.py --no-alt --no-simopt --no-solve --no-cpu-baseline --steps 10 ${EXTRA:-}"
 for v in $VALS; do env $VAR=$v timeout 300 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err; done
