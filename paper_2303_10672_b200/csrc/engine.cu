@@ -668,7 +668,7 @@ struct LoopState {
   int pad;
 };
 
-__device__ bool loop_decide(LoopState* ls, const SweepStats* st) {
+__device__ bool loop_decide(LoopState* ls, SweepStats* st) {
   LoopState s = *ls;
   s.iteration += 1;
   bool stop = false;
@@ -696,10 +696,16 @@ __device__ bool loop_decide(LoopState* ls, const SweepStats* st) {
     }
   }
   *ls = s;
+  // reset the statistics for the next sweep (the graph's sweeps skip their
+  // own k_init_stats launch: one kernel fewer per sweep)
+  st->max_key = 0ull;
+  st->min_key = ~0ull;
+  st->first_bad = ~0ull;
+  st->pad = 0;
   return stop;
 }
 
-__global__ void k_loop_decide(LoopState* ls, const SweepStats* st, cudaGraphConditionalHandle h_while,
+__global__ void k_loop_decide(LoopState* ls, SweepStats* st, cudaGraphConditionalHandle h_while,
                               cudaGraphConditionalHandle h_if, int set_if) {
   const bool stop = loop_decide(ls, st);
   cudaGraphSetConditional(h_while, stop ? 0u : 1u);
@@ -709,7 +715,7 @@ __global__ void k_loop_decide(LoopState* ls, const SweepStats* st, cudaGraphCond
 // Eight-slot ring (periodic span): the WHILE body is a chain of eight IF
 // nodes, one per ring phase; IF k sweeps into slot k of the rotation, then
 // clears its own condition and arms IF k+1 (IF 0 in the next iteration).
-__global__ void k_loop_decide_phase(LoopState* ls, const SweepStats* st, cudaGraphConditionalHandle h_while,
+__global__ void k_loop_decide_phase(LoopState* ls, SweepStats* st, cudaGraphConditionalHandle h_while,
                                     cudaGraphConditionalHandle h_self, cudaGraphConditionalHandle h_next) {
   const bool stop = loop_decide(ls, st);
   cudaGraphSetConditional(h_while, stop ? 0u : 1u);
@@ -904,6 +910,7 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
         a.fa.test = h.test;
         a.fa.gamma = gamma;
         a.fa.stats = dstats.as<SweepStats>();
+        a.init_stats = false;  // reset by the decision kernel after every sweep
         return a;
       };
       cudaStream_t cs = stream.s;
@@ -985,6 +992,7 @@ void solve_impl(const Model& m, const pvi_vi_config& cfg, const double* resume_v
       }
       const auto tr2 = std::chrono::steady_clock::now();
       PVI_CUDA(cudaEventRecord(ev0, cs));
+      init_stats_device(dstats.as<SweepStats>(), cs);  // the first graph sweep's statistics
       PVI_CUDA(cudaGraphLaunch(exec, cs));
       PVI_CUDA(cudaEventRecord(ev1, cs));
       PVI_CUDA(cudaMemcpyAsync(&h, dls.p, sizeof(h), cudaMemcpyDeviceToHost, cs));
