@@ -568,7 +568,7 @@ __host__ __device__ constexpr std::uint64_t a_pow(std::uint64_t r, int e) { retu
 // A_max + 1 states that differ only in x_1 -- consecutive indices, since x_1
 // is the least significant digit.  One thread per such group.
 template <typename T, int NA, int ML>
-__global__ void __launch_bounds__(128) k_a_fact_lifo(DevModel dm, const T* __restrict__ V,
+__global__ void __launch_bounds__(128, ML ? 9 : 1) k_a_fact_lifo(DevModel dm, const T* __restrict__ V,
                                                      const double* __restrict__ reward,
                                                      const double* __restrict__ cdf_sf, double pd,
                                                      T* __restrict__ vout,
