@@ -57,7 +57,7 @@ struct Workspace {
   cudaStream_t up = nullptr;    // host-to-device pieces (the other PCIe direction)
   cudaStream_t s2[2] = {};      // stage 2 of consecutive x_3 pairs, overlapping
   cudaEvent_t done[kChunkEvents] = {};
-  cudaEvent_t ev[3 * kChunkEvents] = {};
+  cudaEvent_t ev[4 * kChunkEvents] = {};
   Workspace() {
     // `stream` carries the pipelined backup's stage-1 pieces: highest
     // priority, so they are scheduled ahead of the stage-2 grids they feed
@@ -1298,19 +1298,22 @@ void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t
     // (512 rows of 2,048 states) goes back with one 2-D copy as it finishes
     const std::uint64_t xa_rows = 2ull * na * na;
     for (int p = 0; p < pairs; ++p) {
-      for (int h = 0; h < 2; ++h) {
+      // the last pair in quarters: the copy-back that trails the last grid
+      // is a quarter of a pair instead of a half
+      const int hs = p == pairs - 1 ? 4 : 2;
+      for (int h = 0; h < hs; ++h) {
         cudaStream_t cs = ws.s2[(2 * p + h) % 2];
         PVI_CUDA(cudaStreamWaitEvent(cs, ws.ev[p], 0));
         a.stages = 2;
         a.x3_rows_lo = a.x3_rows_hi = -1;
         a.lo = p * per_pair;
         a.hi = (p + 1) * per_pair;
-        a.xb_lo = h * n_xb / 2;
-        a.xb_hi = (h + 1) * n_xb / 2;
+        a.xb_lo = h * n_xb / hs;
+        a.xb_hi = (h + 1) * n_xb / hs;
         launch_sweep<T>(m, dm, a, ws.scratch, cs);
         mark(cs);
-        PVI_CUDA(cudaEventRecord(ws.ev[20 + 2 * p + h], cs));
-        PVI_CUDA(cudaStreamWaitEvent(ws.copy, ws.ev[20 + 2 * p + h], 0));
+        PVI_CUDA(cudaEventRecord(ws.ev[20 + 4 * p + h], cs));
+        PVI_CUDA(cudaStreamWaitEvent(ws.copy, ws.ev[20 + 4 * p + h], 0));
         const std::uint64_t o = a.lo + a.xb_lo, w = a.xb_hi - a.xb_lo;
         if (out_values)
           PVI_CUDA(cudaMemcpy2DAsync(static_cast<T*>(out_values) + o, n_xb * sizeof(T), vo + o, n_xb * sizeof(T),
