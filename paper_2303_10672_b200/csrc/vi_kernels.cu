@@ -2712,7 +2712,7 @@ __device__ __forceinline__ void c_pass_tile_mma(const double* __restrict__ src, 
 #pragma unroll
       for (int s = 0; s < KS; ++s)
         if (4 * s <= 8 * t + 7 && 4 * s <= hi) {
-          const double w = s_wa[(t * KS + s) * 32 + lane];
+          const double w = __ldg(s_wa + (t * KS + s) * 32 + lane);
 #pragma unroll
           for (int g = 0; g < NG; ++g) dmma_884_nv(d[g][0], d[g][1], w, vb[s][g]);
         }
@@ -2759,11 +2759,10 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag_q(DevModel dm, const doub
   const std::size_t in_base = in_is_g ? static_cast<std::size_t>(tau) * n_prof
                                       : c_tri_base(a, wb) + static_cast<std::size_t>(tau) * nb * wb;
   const double* bt = binom_k + a * binom_a_stride;
-  __shared__ double s_wa[18 * 32];  // L's DMMA fragments of (a, k = 2), precomputed (DevModel::c_frag)
-  {
-    const double* fsrc = dm.c_frag + (static_cast<std::size_t>(a) * (m - 1) + 1) * (18 * 32);
-    for (int e = threadIdx.x; e < 18 * 32; e += blockDim.x) s_wa[e] = __ldg(fsrc + e);
-  }
+  // L's DMMA fragments of (a, k = 2), precomputed (DevModel::c_frag), read
+  // by the DMMA loop straight from L1 (a shared-memory copy per CTA was 8%
+  // of this kernel's instructions)
+  const double* s_wa = dm.c_frag + (static_cast<std::size_t>(a) * (m - 1) + 1) * (18 * 32);
   (void)bt;
   if (threadIdx.x < R)  // pass 1's weights of order a: c_binom[a][0][a][y]
     s_w1[threadIdx.x] = dm.c_binom[(static_cast<std::size_t>(a) * (m - 1) * R + a) * R + threadIdx.x];
