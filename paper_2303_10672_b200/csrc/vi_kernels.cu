@@ -2781,7 +2781,15 @@ __global__ void __launch_bounds__(448, 2) k_c_bin_diag_q(DevModel dm, const doub
     if (st < lo || st >= hi) continue;
     const double* h = s_tile + x2 * R;
     double acc = 0.0;
-    for (int y = 0; y <= a; ++y) acc = fma(s_w1[y], h[(a - y) * PLANE + min(x1 + y, CAP)], acc);
+    {
+      const double* hp = h + a * PLANE;  // row b = a - y, one plane down per y
+      int col = x1;
+#pragma unroll 4
+      for (int y = 0; y <= a; ++y, hp -= PLANE) {
+        acc = fma(s_w1[y], hp[col], acc);
+        col = min(col + 1, CAP);
+      }
+    }
     const T qa = static_cast<T>(fma(fixed, s_pd, acc));
     if (part_v) part_v[static_cast<std::uint64_t>(a) * nr + (st - lo)] = qa;
     if (qout) qout[(st - lo) * na + a] = qa;
