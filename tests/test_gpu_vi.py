@@ -263,9 +263,9 @@ def test_sharded_driver_world1_equals_solver(pvi, preset):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("preset,algo", [("c/m5/exp1", "factored"), ("a/m5/exp5", "factored"),
-                                         ("b/m2/exp1", "exact")])
-def test_pageable_and_pinned_readback_identical(pvi, preset, algo):
+@pytest.mark.parametrize("preset,algo,prec", [("c/m5/exp1", "factored", "f64"), ("a/m5/exp5", "factored", "f64"),
+                                              ("b/m2/exp1", "exact", "f64"), ("b/m3/exp1", "factored", "f32")])
+def test_pageable_and_pinned_readback_identical(pvi, preset, algo, prec):
     """Result buffers in pageable memory go through the engine's pinned ring
     and host copy pool (several 8 MB chunks here), pinned ones take one
     direct copy: the same bytes either way, and the same as a range split."""
@@ -273,16 +273,19 @@ def test_pageable_and_pinned_readback_identical(pvi, preset, algo):
     m = pvi.make_preset(preset).set_algorithm(algo)
     n = m.state_count()
     V = np.random.default_rng(21).uniform(-10.0, 10.0, n)
-    v_pg, a_pg = pvi.bellman_backup_batch(m, V, 0, n)  # numpy: pageable
-    ov = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+    tdt = torch.float32 if prec == "f32" else torch.float64
+    v_pg, a_pg = pvi.bellman_backup_batch(m, V, 0, n, precision=prec)  # numpy: pageable
+    ov = torch.empty(n, dtype=tdt).pin_memory().numpy()
     oa = torch.empty(n, dtype=torch.int32).pin_memory().numpy().view(np.uint32)
-    v_pn, a_pn = pvi.bellman_backup_batch(m, V, 0, n, out_values=ov, out_actions=oa)
+    v_pn, a_pn = pvi.bellman_backup_batch(m, V, 0, n, precision=prec, out_values=ov, out_actions=oa)
     np.testing.assert_array_equal(v_pg, v_pn)
     np.testing.assert_array_equal(a_pg, a_pn)
     half = n // 2 + 7
-    v1, a1 = pvi.bellman_backup_batch(m, V, 0, half)
+    v1, a1 = pvi.bellman_backup_batch(m, V, 0, half, precision=prec)
     np.testing.assert_array_equal(v1, v_pg[:half])
     np.testing.assert_array_equal(a1, a_pg[:half])
+    if prec == "f32":
+        return
     # the solve's read-back (pageable numpy result) equals three backups
     res = pvi.run_value_iteration(m, pvi.ViConfig(fixed_iterations=3))
     v = np.asarray(m.initial_values(), np.float64)
