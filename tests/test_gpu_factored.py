@@ -335,3 +335,30 @@ def test_empty_range_sweep_has_neutral_statistics(pvi, preset, algo):
     torch.cuda.synchronize()
     got = st.cpu().numpy()
     assert (got[:3] == -1.7976931348623157e308).all(), got
+
+
+@pytest.mark.parametrize("slopes", [[0.0, 0.0, 0.0], [0.4, -0.2, 0.1]])
+def test_factored_c_m4_radix21_close_to_exact(pvi, slopes):
+    """useful_life = 4 at A_max = D_max = 20: the r = 21 kernels with other
+    line shapes than the presets -- the DMMA G convolution for M = 4, the
+    wide DMMA pass for k = 3 with a single x_2-batched line per weekday and
+    order (endogenous law, slopes != 0) or the scalar anti-diagonal pass
+    (exogenous), then the fused last pass + Q."""
+    kw = dict(useful_life=4, max_order=20, max_demand=20, life_slopes=slopes)
+    exact = pvi.ScenarioC(**kw)
+    fact = pvi.ScenarioC(**kw).set_algorithm("factored")
+    n = exact.state_count()
+    V = np.random.default_rng(29).uniform(-30.0, 30.0, n)
+    ve, ae = pvi.bellman_backup_batch(exact, V, 0, n)
+    vf, af = pvi.bellman_backup_batch(fact, V, 0, n)
+    np.testing.assert_allclose(vf, ve, rtol=1e-12, atol=1e-10)
+    for s in np.nonzero(af != ae)[0]:
+        q = pvi.q_rows(exact, V, int(s), int(s) + 1)[0]
+        assert abs(q[af[s]] - q[ae[s]]) <= 1e-9 * max(1.0, abs(q[ae[s]]))
+    qe = pvi.q_rows(exact, V, n // 3, n // 3 + 200)
+    qf = pvi.q_rows(fact, V, n // 3, n // 3 + 200)
+    np.testing.assert_allclose(qf, qe, rtol=1e-12, atol=1e-10)
+    re = pvi.run_value_iteration(exact)
+    rf = pvi.run_value_iteration(fact)
+    assert re.iterations == rf.iterations
+    np.testing.assert_allclose(rf.values, re.values, rtol=1e-9)
