@@ -201,6 +201,30 @@ const DevModel& Model::device_view(int device) const {
       d.c_exogenous = c_exogenous ? 1 : 0;
       d.c_binom = c_binom.empty() ? nullptr : upload(*dc, c_binom);
       d.c_frag = nullptr;
+      d.c_gband = d.c_ra = d.c_cwt = nullptr;
+      if (pc.max_order == 20 && pc.max_demand == 20) {
+        constexpr int DN = 21, CAP = 20, NT = 2 * DN - 1, NF = 3 * 7 * 32;
+        std::vector<double> band(7 * static_cast<std::size_t>(NF), 0.0);
+        for (int t = 0; t < 7; ++t)
+          for (int e = 0; e < NF; ++e) {
+            const int i = e / (7 * 32), j = (e / 32) % 7, ln = e % 32;
+            const int row = 8 * i + (ln >> 2), col = 4 * (2 * i + j) + (ln & 3);  // T[z_1][t]
+            const int dd = row - col + CAP;
+            band[static_cast<std::size_t>(t) * NF + e] =
+                (row < DN && col < NT && dd >= 0 && dd <= CAP) ? c_pmf[static_cast<std::size_t>(t) * DN + dd] : 0.0;
+          }
+        const int nra = pc.useful_life * (DN - 1) + DN;
+        std::vector<double> ra(nra), cw(DN);
+        for (int i = 0; i < nra; ++i) {
+          const int x = i - (DN - 1);
+          ra[i] = -pc.holding_cost * static_cast<double>(std::max(x, 0)) -
+                  pc.shortage_cost * static_cast<double>(std::max(-x, 0));
+        }
+        for (int i = 0; i < DN; ++i) cw[i] = pc.wastage_cost * static_cast<double>(i);
+        d.c_gband = upload(*dc, band);
+        d.c_ra = upload(*dc, ra);
+        d.c_cwt = upload(*dc, cw);
+      }
       if (!c_binom.empty() && !c_exogenous && pc.max_order == 20) {
         // [t][s][lane] = L[8 t + lane / 4][4 s + lane % 4], L[b][b'] =
         // Bin(b - b'; b, q_k(a)) for b' <= b < a + 1 (c_pass_fragments' layout)

@@ -103,6 +103,12 @@ struct DevModel {
   // lower-triangular matrix, c_frag[a][k-1][576] (k_c_bin_wide_mma,
   // k_c_bin_diag_q), built once on the host instead of per CTA
   const double* c_frag;
+  // A_max = D_max = 20: k_c_fact_g_mma's per-model tables -- the demand
+  // band's DMMA fragments per weekday [7][3 * 7 * 32], the shortage /
+  // holding reward RA[total - d + D] (m D + D + 1) and C_w w (D + 1)
+  const double* c_gband;
+  const double* c_ra;
+  const double* c_cwt;
 
   // tabular
   std::uint64_t t_outcomes;

@@ -2121,21 +2121,16 @@ __global__ void __launch_bounds__(256) k_c_fact_g_mma(DevModel dm, const T* __re
   constexpr int NRA = M * (DN - 1) + DN, CAP = DN - 1, NT = 2 * DN - 1;  // t in [0, 2 D]
   constexpr int MT = (DN + 7) / 8, KS = (NT + 3) / 4;                   // 3 row tiles, 11 k-steps
   static_assert(DN == 21, "band tiling assumes D = 20");
-  __shared__ double s_ra[NRA], s_cw[DN];
-  __shared__ double s_t[MT * 7 * 32];  // A fragments: [tile i][band step j][lane]
+  (void)NRA;
   const int tau = tau0 + static_cast<int>(blockIdx.y);
-  for (int i = threadIdx.x; i < NRA; i += blockDim.x) {
-    const int x = i - (DN - 1);
-    s_ra[i] = -dm.c_ch * ipos(x) - dm.c_cs * ipos(-x);
-  }
-  for (int i = threadIdx.x; i < DN; i += blockDim.x) s_cw[i] = dm.c_cw * i;
-  for (int e = threadIdx.x; e < MT * 7 * 32; e += blockDim.x) {
-    const int i = e / (7 * 32), j = (e / 32) % 7, ln = e % 32;
-    const int row = 8 * i + (ln >> 2), col = 4 * (2 * i + j) + (ln & 3);  // T[z_1][t]
-    const int d = row - col + CAP;
-    s_t[e] = (row < DN && col < NT && d >= 0 && d <= CAP) ? dm.c_pmf[tau * DN + d] : 0.0;
-  }
-  __syncthreads();
+  // per-model tables (engine.cu, DevModel::c_gband / c_ra / c_cwt), read
+  // through L1: rebuilding them per CTA was ~30% of this kernel's
+  // instructions.  s_t = T's band fragments [tile i][band step j][lane],
+  // T[z_1][t] = pmf(tau, z_1 - t + D); s_ra[total - d + D] = -C_h
+  // (total - d)^+ - C_s (d - total)^+; s_cw[w] = C_w w.
+  const double* __restrict__ s_t = dm.c_gband + static_cast<std::size_t>(tau) * (MT * 7 * 32);
+  const double* __restrict__ s_ra = dm.c_ra;
+  const double* __restrict__ s_cw = dm.c_cwt;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int line0 = (static_cast<int>(blockIdx.x) * (blockDim.x >> 5) + warp) * 8;
@@ -2182,7 +2177,7 @@ __global__ void __launch_bounds__(256) k_c_fact_g_mma(DevModel dm, const T* __re
       for (int j = 1; j <= M - 2; ++j)
         idx += static_cast<std::uint32_t>(max(min(qs[j + 1] + t, z[j + 1]), 0)) * w[M - j];
       idx += static_cast<std::uint32_t>(max(min(total0 + t, fresh), 0)) * w[1];
-      const double r0 = s_ra[total0 + t + CAP] - s_cw[max(t, 0)];
+      const double r0 = __ldg(s_ra + total0 + t + CAP) - __ldg(s_cw + max(t, 0));
       bf[kk] = fma(gamma, static_cast<double>(__ldg(V + idx)), r0);
     }
   }
@@ -2193,7 +2188,7 @@ __global__ void __launch_bounds__(256) k_c_fact_g_mma(DevModel dm, const T* __re
 #pragma unroll
     for (int j = 0; j < 7; ++j) {
       const int kk = 2 * i + j;
-      if (kk < KS) dmma_884(acc[i], s_t[(i * 7 + j) * 32 + lane], bf[kk]);
+      if (kk < KS) dmma_884(acc[i], __ldg(s_t + (i * 7 + j) * 32 + lane), bf[kk]);
     }
   }
   // D: row z_1 = 8 i + g, columns (lines) line0 + 2 q + e
