@@ -158,9 +158,13 @@ const DevModel& Model::device_view(int device) const {
       d.b_guide_b = upload(*dc, cdf_guide(b_cdf_b.data(), static_cast<int>(b_cdf_b.size()), kGuide));
       // trials = demand_b - fill_b <= |support of demand_b| - 1
       d.b_binom_t = static_cast<int>(b_pmf_b.size()) - 1;
-      d.b_binom_cum = pb.substitution_prob > 0.0 && pb.substitution_prob < 1.0
-                          ? upload(*dc, binomial_cum_table(d.b_binom_t, pb.substitution_prob))
-                          : nullptr;
+      d.b_binom_cum = nullptr;
+      d.b_binom_guide = nullptr;
+      if (pb.substitution_prob > 0.0 && pb.substitution_prob < 1.0) {
+        const auto cum = binomial_cum_table(d.b_binom_t, pb.substitution_prob);
+        d.b_binom_cum = upload(*dc, cum);
+        d.b_binom_guide = upload(*dc, binomial_guide_table(cum, d.b_binom_t, kBinGuide));
+      }
       d.b_lane_order = upload(*dc, b_lane_order);
       d.b_tile = static_cast<int>(b_lane_order.size());
       break;

@@ -74,6 +74,7 @@ struct DevModel {
   const std::int32_t* b_guide_a;
   const std::int32_t* b_guide_b;
   const double* b_binom_cum;
+  const std::int32_t* b_binom_guide;  // per trial count t, kBinGuide + 1 start indices into row t
   int b_binom_t;
   const std::uint16_t* b_lane_order;  // low-digit combos sorted by stock (tile order)
   int b_tile;                          // states per tile (product of the two low radices)
@@ -121,6 +122,8 @@ struct DevModel {
 constexpr int kGuide = 256;
 std::vector<std::int32_t> cdf_guide(const double* cdf, int size, int G);
 std::vector<double> binomial_cum_table(int T, double p);
+constexpr int kBinGuide = 64;
+std::vector<std::int32_t> binomial_guide_table(const std::vector<double>& cum, int T, int G);
 void c_receipt_tables(const double* receipt, int max_order, int m, std::vector<double>& cum,
                       std::vector<std::int32_t>& offsets);
 

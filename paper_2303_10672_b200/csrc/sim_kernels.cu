@@ -131,6 +131,15 @@ __device__ __forceinline__ int sample_binomial_table(int trials, const double* r
   return k;
 }
 
+// the same k through the row's guide table (sim_tables.cpp
+// binomial_guide_table): start at the sample of floor(u G) / G
+__device__ __forceinline__ int sample_binomial_guided(int trials, const double* row, const std::int32_t* guide,
+                                                      double u) {
+  int k = __ldg(guide + static_cast<int>(u * kBinGuide));  // u in [0, 1): exact bucket
+  while (k < trials && !(__ldg(row + k) > u)) ++k;
+  return k;
+}
+
 // rng.hpp:76-90
 __device__ __forceinline__ int sample_binomial(int trials, double p, double u) {
   if (trials <= 0 || p <= 0.0) return 0;
@@ -264,7 +273,8 @@ __device__ __forceinline__ void step_b(const DevModel& dm, int* state, const int
   const int trials = demand_b - fill_b;
   const double ub = u3[2];
   const int accepted = dm.b_binom_cum && trials > 0 && trials <= dm.b_binom_t
-                           ? sample_binomial_table(trials, dm.b_binom_cum + trials * (trials + 1) / 2, ub)
+                           ? sample_binomial_guided(trials, dm.b_binom_cum + trials * (trials + 1) / 2,
+                                                    dm.b_binom_guide + trials * (kBinGuide + 1), ub)
                            : sample_binomial(trials, dm.b_rho, ub);
   const int sub = min(accepted, stock_a - own_fill_a);
   const int h_a = own_fill_a + sub;

@@ -50,6 +50,25 @@ std::vector<double> binomial_cum_table(int T, double p) {
   return out;
 }
 
+// Guide tables of the rows of a binomial_cum_table (the cdf_guide idea per
+// trial count): row t's entry j is the sample for u = j / G -- the first
+// k < t with cum_k > u, else t -- so the kernel's scan for u in [j/G,
+// (j+1)/G) starts there (a larger u only moves the answer up): the same k
+// after ~1 comparison instead of a scan from 0.
+std::vector<std::int32_t> binomial_guide_table(const std::vector<double>& cum, int T, int G) {
+  std::vector<std::int32_t> g(static_cast<std::size_t>(T + 1) * (G + 1));
+  for (int t = 0; t <= T; ++t) {
+    const double* row = cum.data() + static_cast<std::size_t>(t) * (t + 1) / 2;
+    int k = 0;
+    for (int j = 0; j <= G; ++j) {
+      const double u = static_cast<double>(j) / G;  // exact: G is a power of two
+      while (k < t && !(row[k] > u)) ++k;
+      g[static_cast<std::size_t>(t) * (G + 1) + j] = k;
+    }
+  }
+  return g;
+}
+
 // Scenario C's receipt sampler (scenario_c.cpp sample_step: the age split of
 // an order of a units as m - 1 sequential binomials with p_k = probs[k] /
 // mass_left, mass_left = 1 - probs[0] - .. - probs[k-1] while units remain):
