@@ -196,6 +196,19 @@ const DevModel& Model::device_view(int device) const {
         c_receipt_tables(c_receipt.data(), pc.max_order, pc.useful_life, cum, off);
         d.c_rcpt_cum = upload(*dc, cum);
         d.c_rcpt_off = upload(*dc, off);
+        // each (a, k) table's guide rows at a parallel offset
+        std::vector<std::int32_t> goff(off.size(), -1), guide;
+        for (std::size_t i = 0; i < off.size(); ++i) {
+          if (off[i] < 0) continue;
+          const int a = static_cast<int>(i / (pc.useful_life - 1));
+          const std::vector<double> tab(cum.begin() + off[i],
+                                        cum.begin() + off[i] + static_cast<std::ptrdiff_t>(a + 1) * (a + 2) / 2);
+          const auto gt = binomial_guide_table(tab, a, kBinGuide);
+          goff[i] = static_cast<std::int32_t>(guide.size());
+          guide.insert(guide.end(), gt.begin(), gt.end());
+        }
+        d.c_rcpt_goff = upload(*dc, goff);
+        d.c_rcpt_guide = guide.empty() ? nullptr : upload(*dc, guide);
       }
       d.c_comp = upload(*dc, c_comp);
       d.c_ids = upload(*dc, c_ids);

@@ -89,6 +89,8 @@ struct DevModel {
   const std::int32_t* c_guide;  // 7 x (kGuide + 1) guide tables of c_cdf
   const double* c_rcpt_cum;     // receipt binomials' cumulative masses (sim_tables.cpp)
   const std::int32_t* c_rcpt_off;  // (A_max + 1) x (m - 1) offsets into c_rcpt_cum, -1: none
+  const std::int32_t* c_rcpt_guide;  // binomial guide rows of those tables (kBinGuide + 1 per trial count)
+  const std::int32_t* c_rcpt_goff;   // (A_max + 1) x (m - 1) offsets into c_rcpt_guide, -1: none
   const std::int8_t* c_comp;  // n_comp x m, freshest first
   const std::uint32_t* c_ids;     // concatenated per action
   const double* c_probs;          // aligned with c_ids
