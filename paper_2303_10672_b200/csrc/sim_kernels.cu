@@ -325,14 +325,17 @@ __device__ __forceinline__ void step_c(const DevModel& dm, int* state, const int
         counts[k] = 0;
         continue;
       }
-      const double cond = probs[k] / mass_left;
       const double u = rng.uniform();
       const int off = dm.c_rcpt_off ? __ldg(dm.c_rcpt_off + order * (m - 1) + k) : -1;
-      counts[k] = off >= 0 ? sample_binomial_guided(remaining, dm.c_rcpt_cum + off + remaining * (remaining + 1) / 2,
-                                                    dm.c_rcpt_guide + __ldg(dm.c_rcpt_goff + order * (m - 1) + k) +
-                                                        remaining * (kBinGuide + 1),
-                                                    u)
-                           : sample_binomial(remaining, cond < 1.0 ? cond : 1.0, u);
+      if (off >= 0) {
+        counts[k] = sample_binomial_guided(remaining, dm.c_rcpt_cum + off + remaining * (remaining + 1) / 2,
+                                           dm.c_rcpt_guide + __ldg(dm.c_rcpt_goff + order * (m - 1) + k) +
+                                               remaining * (kBinGuide + 1),
+                                           u);
+      } else {  // no table (p_k = 0 or 1, or a = 0): the reference's sampler, its division only here
+        const double cond = probs[k] / mass_left;
+        counts[k] = sample_binomial(remaining, cond < 1.0 ? cond : 1.0, u);
+      }
       remaining -= counts[k];
       mass_left -= probs[k];
     }
