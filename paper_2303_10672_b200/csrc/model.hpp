@@ -121,7 +121,7 @@ struct DevModel {
 };
 
 // sampling tables of the rollout kernel (sim_tables.cpp)
-constexpr int kGuide = 256;
+constexpr int kGuide = 1024;  // cdf guide buckets (sim_tables.cpp cdf_guide)
 std::vector<std::int32_t> cdf_guide(const double* cdf, int size, int G);
 std::vector<double> binomial_cum_table(int T, double p);
 constexpr int kBinGuide = 64;

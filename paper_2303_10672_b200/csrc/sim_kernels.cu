@@ -118,7 +118,9 @@ __device__ __forceinline__ int sample_from_cdf(const double* cdf, int size, doub
 // same index, found by one table load and a short forward scan
 __device__ __forceinline__ int sample_from_cdf_guided(const double* cdf, int size, const std::int32_t* guide,
                                                       double u) {
-  int i = __ldg(guide + static_cast<int>(u * kGuide));  // u in [0, 1): exact bucket
+  const int e = __ldg(guide + static_cast<int>(u * kGuide));  // u in [0, 1): exact bucket
+  if (e >= 0) return e;  // no cdf boundary inside the bucket
+  int i = -e - 1;
   while (i < size - 1 && !(__ldg(cdf + i) > u)) ++i;
   return i;
 }

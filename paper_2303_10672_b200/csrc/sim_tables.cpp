@@ -16,6 +16,12 @@ namespace pvi_b200 {
 // the answer is >= g[j] (a larger u only removes candidates), so a forward
 // scan from g[j] finds it -- about one comparison instead of log2(size)
 // dependent loads.
+//
+// Buckets whose two ends give the same index hold no cdf boundary: every u
+// in them samples that index, so the entry is stored as is and the kernel
+// returns it without touching the cdf; the other entries are stored as
+// -(start + 1) and the kernel scans from start.  With G = 1024 almost every
+// bucket is exact (a 101-value demand law has at most 100 boundaries).
 std::vector<std::int32_t> cdf_guide(const double* cdf, int size, int G) {
   std::vector<std::int32_t> g(G + 1);
   int i = 0;
@@ -24,7 +30,9 @@ std::vector<std::int32_t> cdf_guide(const double* cdf, int size, int G) {
     while (i < size - 1 && !(cdf[i] > u)) ++i;
     g[j] = i;
   }
-  return g;
+  std::vector<std::int32_t> out(G + 1);
+  for (int j = 0; j <= G; ++j) out[j] = (j < G && g[j] == g[j + 1]) ? g[j] : -(g[j] + 1);
+  return out;
 }
 
 // Cumulative masses of sample_binomial (rng.hpp:76-90) for every trial count
