@@ -124,7 +124,7 @@ struct DevModel {
 constexpr int kGuide = 1024;  // cdf guide buckets (sim_tables.cpp cdf_guide)
 std::vector<std::int32_t> cdf_guide(const double* cdf, int size, int G);
 std::vector<double> binomial_cum_table(int T, double p);
-constexpr int kBinGuide = 64;
+constexpr int kBinGuide = 256;  // binomial guide buckets (sim_tables.cpp binomial_guide_table)
 std::vector<std::int32_t> binomial_guide_table(const std::vector<double>& cum, int T, int G);
 void c_receipt_tables(const double* receipt, int max_order, int m, std::vector<double>& cum,
                       std::vector<std::int32_t>& offsets);

@@ -132,7 +132,9 @@ __device__ __forceinline__ int sample_from_cdf_guided(const double* cdf, int siz
 // comparison instead of a scan from 0: B rollouts -13%, C -26%)
 __device__ __forceinline__ int sample_binomial_guided(int trials, const double* row, const std::int32_t* guide,
                                                       double u) {
-  int k = __ldg(guide + static_cast<int>(u * kBinGuide));  // u in [0, 1): exact bucket
+  const int e = __ldg(guide + static_cast<int>(u * kBinGuide));  // u in [0, 1): exact bucket
+  if (e >= 0) return e;  // no boundary inside the bucket
+  int k = -e - 1;
   while (k < trials && !(__ldg(row + k) > u)) ++k;
   return k;
 }

@@ -64,15 +64,19 @@ std::vector<double> binomial_cum_table(int T, double p) {
 // (j+1)/G) starts there (a larger u only moves the answer up): the same k
 // after ~1 comparison instead of a scan from 0.
 std::vector<std::int32_t> binomial_guide_table(const std::vector<double>& cum, int T, int G) {
+  // (exact buckets stored as is, the others as -(start + 1): cdf_guide)
   std::vector<std::int32_t> g(static_cast<std::size_t>(T + 1) * (G + 1));
+  std::vector<std::int32_t> r(G + 1);
   for (int t = 0; t <= T; ++t) {
     const double* row = cum.data() + static_cast<std::size_t>(t) * (t + 1) / 2;
     int k = 0;
     for (int j = 0; j <= G; ++j) {
       const double u = static_cast<double>(j) / G;  // exact: G is a power of two
       while (k < t && !(row[k] > u)) ++k;
-      g[static_cast<std::size_t>(t) * (G + 1) + j] = k;
+      r[j] = k;
     }
+    for (int j = 0; j <= G; ++j)
+      g[static_cast<std::size_t>(t) * (G + 1) + j] = (j < G && r[j] == r[j + 1]) ? r[j] : -(r[j] + 1);
   }
   return g;
 }
