@@ -54,6 +54,7 @@ struct Workspace {
   Scratch io;       // 0: V, 1: V' slice, 2: argmax slice, 3: Q rows
   cudaStream_t stream = nullptr;
   cudaStream_t copy = nullptr;  // device-to-host results of finished chunks
+  cudaStream_t copy2 = nullptr;  // the argmax half of them (a second copy queue)
   cudaStream_t up = nullptr;    // host-to-device pieces (the other PCIe direction)
   cudaStream_t s2[2] = {};      // stage 2 of consecutive x_3 pairs, overlapping
   cudaEvent_t done[kChunkEvents] = {};
@@ -65,6 +66,7 @@ struct Workspace {
     PVI_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     PVI_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, greatest));
     PVI_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    PVI_CUDA(cudaStreamCreateWithFlags(&copy2, cudaStreamNonBlocking));
     PVI_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
     for (auto& x : s2) PVI_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
     for (auto& e : done) PVI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -78,6 +80,7 @@ struct Workspace {
     for (auto& x : s2)
       if (x) cudaStreamDestroy(x);
     if (copy) cudaStreamDestroy(copy);
+    if (copy2) cudaStreamDestroy(copy2);
     if (up) cudaStreamDestroy(up);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -1355,13 +1358,14 @@ void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t
         mark(cs);
         PVI_CUDA(cudaEventRecord(ws.ev[20 + 4 * p + h], cs));
         PVI_CUDA(cudaStreamWaitEvent(ws.copy, ws.ev[20 + 4 * p + h], 0));
+        PVI_CUDA(cudaStreamWaitEvent(ws.copy2, ws.ev[20 + 4 * p + h], 0));
         const std::uint64_t o = a.lo + a.xb_lo, w = a.xb_hi - a.xb_lo;
         if (out_values)
           PVI_CUDA(cudaMemcpy2DAsync(static_cast<T*>(out_values) + o, n_xb * sizeof(T), vo + o, n_xb * sizeof(T),
                                      w * sizeof(T), xa_rows, cudaMemcpyDeviceToHost, ws.copy));
         if (out_actions)
           PVI_CUDA(cudaMemcpy2DAsync(out_actions + o, n_xb * 4, ao + o, n_xb * 4, w * 4, xa_rows,
-                                     cudaMemcpyDeviceToHost, ws.copy));
+                                     cudaMemcpyDeviceToHost, ws.copy2));
         mark(ws.copy);
       }
     }
@@ -1370,6 +1374,7 @@ void backup_impl(const Model& m, double gamma, const void* values, std::uint64_t
     PVI_CUDA(cudaStreamSynchronize(st));
     for (auto x : ws.s2) PVI_CUDA(cudaStreamSynchronize(x));
     PVI_CUDA(cudaStreamSynchronize(ws.copy));
+    PVI_CUDA(cudaStreamSynchronize(ws.copy2));
     PVI_CUDA(cudaStreamSynchronize(ws.up));
     if (!tev.empty()) {
       // order: t0, up[0..P), s1[0..P), then per pair: s2 done, d2h done
